@@ -1,0 +1,181 @@
+/* ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU implementation of the fast fermion sampling (FFS)
+ * algorithm of arXiv 2109.07358 exactly as the paper states it: a random permutation m
+ * (PAPER.md:69), then for k = 1..N the conditional P(x_k | x_1..x_{k-1}; m) ∝ |u_{x_k}^T h|^2
+ * with h the unit normal vector of u_{x_1..x_{k-1}} (Eq. 3), h obtained by the
+ * iterative Gaussian elimination of Supp S1, and an inverse-CDF draw.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+ * load this library. It shares no code, header, table or helper with the CUDA path
+ * (paper_2109_07358_b200/csrc); the CUDA path never calls it.
+ *
+ * fp64 throughout; complex U as C99 double _Complex (interleaved re,im — identical bytes to the
+ * ABI's C128 layout). OpenMP only across independent samples.
+ *
+ * Build: gcc -O2 -fopenmp -shared -fPIC -o libffs_ref.so ffs_ref.c -lm
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define FFS_REF_F64 0
+#define FFS_REF_C128 1
+
+/* ---- real instantiation ---- */
+#define SCALAR double
+#define ABS2(z) ((z) * (z))
+#define SFX(name) name##_f64
+#include "ffs_ref_core.h"
+#undef SCALAR
+#undef ABS2
+#undef SFX
+
+/* ---- complex instantiation ---- */
+static inline double abs2_c(double _Complex z) { return creal(z) * creal(z) + cimag(z) * cimag(z); }
+#define SCALAR double _Complex
+#define ABS2(z) abs2_c(z)
+#define SFX(name) name##_c128
+#include "ffs_ref_core.h"
+#undef SCALAR
+#undef ABS2
+#undef SFX
+
+/* Permutation draw ("generate a vector m as a random permutation of n"; reading Q6):
+ * forward partial Fisher-Yates over the first Np slots:
+ *   m = (0..N-1); for j = 0..Np-1: n = N-j; r = j + min(n-1, floor(u[j]*n)); swap(m[j], m[r]). */
+void ffs_ref_permutation(const double* u, int64_t N, int64_t Np, int32_t* m)
+{
+    for (int64_t j = 0; j < N; ++j) m[j] = (int32_t)j;
+    for (int64_t j = 0; j < Np; ++j) {
+        int64_t n = N - j;
+        int64_t r = (int64_t)floor(u[j] * (double)n);
+        if (r > n - 1) r = n - 1;
+        r += j;
+        int32_t t = m[j];
+        m[j] = m[r];
+        m[r] = t;
+    }
+}
+
+static int check_args(const double* U, int64_t L, int64_t N, int dtype, int64_t Np)
+{
+    if (!U || L < 1 || N < 1 || N > L || Np < 1 || Np > N) return -1;
+    if (dtype != FFS_REF_F64 && dtype != FFS_REF_C128) return -1;
+    return 0;
+}
+
+static size_t scratch_bytes(int64_t L, int64_t N, int64_t Np, int dtype)
+{
+    size_t es = dtype == FFS_REF_C128 ? 16 : 8;
+    return es * (size_t)(Np * Np + Np) + 8 * (size_t)L + (size_t)L + 4 * (size_t)N + 64;
+}
+
+static int run_one(const double* U, int64_t L, int64_t N, int dtype, int64_t Np, const double* urow,
+                   const int32_t* forced_m, const int32_t* forced_x, int32_t* x_out, double* w_trace,
+                   double* hn2, double* tot, char* buf)
+{
+    size_t es = dtype == FFS_REF_C128 ? 16 : 8;
+    char* p = buf;
+    void* R = p;            p += es * (size_t)(Np * Np);
+    void* h = p;            p += es * (size_t)Np;
+    double* w = (double*)p; p += 8 * (size_t)L;
+    char* chosen = p;       p += (size_t)L;
+    int32_t* m = (int32_t*)(((uintptr_t)p + 3) & ~(uintptr_t)3);
+    if (forced_m) memcpy(m, forced_m, 4 * (size_t)N);
+    else ffs_ref_permutation(urow, N, Np, m);
+    const double* usel = urow ? urow + Np : NULL;
+    if (dtype == FFS_REF_F64)
+        return sample_chain_f64(U, L, N, Np, m, usel, forced_x, x_out, w_trace, hn2, tot,
+                                (double*)R, (double*)h, w, chosen);
+    return sample_chain_c128((const double _Complex*)U, L, N, Np, m, usel, forced_x, x_out, w_trace,
+                             hn2, tot, (double _Complex*)R, (double _Complex*)h, w, chosen);
+}
+
+/* ffs_ref_sample_marginal: M independent samples of Np steps (Np = N: full sampling).
+ * uniforms [M][2Np] (perm draws | selection draws), positions [M][Np], flags [M] or NULL.
+ * nthreads <= 0: OpenMP default. Returns 0, or -1 on bad arguments. */
+int ffs_ref_sample_marginal(const double* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np,
+                            const double* uniforms, int32_t* positions, int32_t* flags, int nthreads)
+{
+    if (M == 0) return 0;
+    if (check_args(U, L, N, dtype, Np) || !uniforms || !positions) return -1;
+    size_t sb = scratch_bytes(L, N, Np, dtype);
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        char* buf = (char*)malloc(sb);
+        if (!buf) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = 1;
+        } else {
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 16)
+#endif
+            for (int64_t i = 0; i < M; ++i) {
+                int f = run_one(U, L, N, dtype, Np, uniforms + i * 2 * Np, NULL, NULL,
+                                positions + i * Np, NULL, NULL, NULL, buf);
+                if (flags) flags[i] = f;
+            }
+            free(buf);
+        }
+    }
+    return bad ? -2 : 0;
+}
+
+int ffs_ref_sample(const double* U, int64_t L, int64_t N, int dtype, int64_t M,
+                   const double* uniforms, int32_t* positions, int32_t* flags, int nthreads)
+{
+    return ffs_ref_sample_marginal(U, L, N, dtype, M, N, uniforms, positions, flags, nthreads);
+}
+
+/* ffs_ref_weights: the first S samples of ffs_ref_sample_marginal, also returning the normalised
+ * conditional weight vectors [S][Np][L] along the oracle's own path. */
+int ffs_ref_weights(const double* U, int64_t L, int64_t N, int dtype, int64_t S, int64_t Np,
+                    const double* uniforms, int32_t* positions, double* weights)
+{
+    if (S == 0) return 0;
+    if (check_args(U, L, N, dtype, Np) || !uniforms || !positions || !weights) return -1;
+    char* buf = (char*)malloc(scratch_bytes(L, N, Np, dtype));
+    if (!buf) return -2;
+    for (int64_t i = 0; i < S; ++i)
+        run_one(U, L, N, dtype, Np, uniforms + i * 2 * Np, NULL, NULL, positions + i * Np,
+                weights + i * Np * L, NULL, NULL, buf);
+    free(buf);
+    return 0;
+}
+
+/* ffs_ref_chain: teacher-forced chain for a given permutation m [N] and positions x [Np]:
+ * weights [Np][L] normalised conditionals P(. | x_1..x_{k-1}; m), hnorm2 [Np] = |h'|^2 with
+ * h'[k-1] = 1, totals [Np] = sum_x |u_x^T h|^2 with unit h (any may be NULL except weights). */
+int ffs_ref_chain(const double* U, int64_t L, int64_t N, int dtype, int64_t Np, const int32_t* m,
+                  const int32_t* x, double* weights, double* hnorm2, double* totals)
+{
+    if (check_args(U, L, N, dtype, Np) || !m || !x || !weights) return -1;
+    char* buf = (char*)malloc(scratch_bytes(L, N, Np, dtype));
+    if (!buf) return -2;
+    int32_t* xo = (int32_t*)malloc(4 * (size_t)Np);
+    int r = run_one(U, L, N, dtype, Np, NULL, m, x, xo, weights, hnorm2, totals, buf);
+    free(xo);
+    free(buf);
+    return r;
+}
+
+int ffs_ref_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,118 @@
+/* ORACLE CORE — TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+ *
+ * One FFS sample, written step by step in the paper's order and notation.
+ * This file is #included twice by ffs_ref.c: once with SCALAR = double (real U, dtype F64)
+ * and once with SCALAR = double _Complex (complex U, dtype C128). The macros
+ *   SCALAR, ABS2(z) = |z|^2, SFX(name) = name-suffix
+ * are defined by the includer. Nothing here is shared with the CUDA path.
+ *
+ * Notation (Supp S1 PAPER.md:242-256):
+ *   U       : L x N, orthonormal columns, row-major, U[x*N + c]
+ *   m       : random permutation of (0..N-1); only m[0..Np) is used
+ *   u_x     : the k-dimensional row vector U_{x,(m_1..m_k)}
+ *   R       : the iteratively Gauss-eliminated rows of u_{x_1..x_{k-1}}, kept in the permuted
+ *             column order over ncols columns ("always carry out Gaussian elimination in the full
+ *             N-dimensional space"; ncols = Np, reading R2 in DESIGN.md)
+ *   h       : k-dim unit normal vector, perpendicular to u_{x_1..x_{k-1}} (Eq. 3)
+ *   w(x)    : |u_x^T h|^2  (Eq. 3; bilinear u^T h, no conjugation: reading Q3)
+ */
+
+/* Unit normal vector h of step k (1-based) from the k-1 reduced rows R (PAPER.md:255:
+ * "the normal vector h can be determined with another k(k-1)/2 additions and summations"):
+ * back-substitution of R[0:k-1, 0:k] h = 0 with the free component h[k-1] = 1, then normalise.
+ * Returns |h'|^2 of the un-normalised h' (h'[k-1] = 1) through *hnorm2. */
+static void SFX(normal_vector)(const SCALAR* R, int64_t ncols, int64_t k, SCALAR* h, double* hnorm2)
+{
+    h[k - 1] = 1.0;
+    for (int64_t i = k - 2; i >= 0; --i) {
+        SCALAR acc = 0.0;
+        for (int64_t j = i + 1; j <= k - 1; ++j) acc += R[i * ncols + j] * h[j];
+        h[i] = -acc / R[i * ncols + i];
+    }
+    double n2 = 0.0;
+    for (int64_t j = 0; j < k; ++j) n2 += ABS2(h[j]);
+    *hnorm2 = n2;
+    double inv = 1.0 / sqrt(n2);
+    for (int64_t j = 0; j < k; ++j) h[j] *= inv;
+}
+
+/* advance_elimination: append the row u_{x_{k-1}} (all ncols permuted columns)
+ * as R[k-2], eliminating its first k-2 entries against the k-2 rows already stored. */
+static void SFX(advance_elimination)(const SCALAR* U, int64_t N, const int32_t* m, int64_t x,
+                                     SCALAR* R, int64_t ncols, int64_t k)
+{
+    SCALAR* row = R + (k - 2) * ncols;
+    for (int64_t j = 0; j < ncols; ++j) row[j] = U[x * N + m[j]];
+    for (int64_t i = 0; i <= k - 3; ++i) {
+        SCALAR f = row[i] / R[i * ncols + i];
+        row[i] = 0.0;
+        for (int64_t j = i + 1; j < ncols; ++j) row[j] -= f * R[i * ncols + j];
+    }
+}
+
+/* One sample of Np sequential steps ("the fermion position x_k is drawn
+ * according to the conditional probability distribution, with the index k iteratively increased
+ * from 1 to N step by step"; marginal N_< = Np < N stops the loop early).
+ *
+ *   m        : permutation (already drawn), length >= Np
+ *   u_sel    : Np selection uniforms in [0,1)
+ *   forced   : if non-NULL, teacher forcing: x_k := forced[k-1] (weights still computed)
+ *   x_out    : Np positions (0-based, sampling order)
+ *   w_trace  : if non-NULL, [Np][L] normalised conditional weights w/T
+ *   hn2_out  : if non-NULL, [Np] |h'|^2 (un-normalised normal vector with h'[k-1]=1)
+ *   tot_out  : if non-NULL, [Np] T = sum_x w(x) with unit h
+ *   scratch  : R (Np*Np SCALAR) + h (Np SCALAR) + w (L double) + chosen (L char) — caller-provided
+ * Returns flags: bit0 = a step had a non-finite or non-positive total T,
+ *                bit1 = a selected normalised weight was < 1e-12.                            */
+static int SFX(sample_chain)(const SCALAR* U, int64_t L, int64_t N, int64_t Np, const int32_t* m,
+                             const double* u_sel, const int32_t* forced, int32_t* x_out,
+                             double* w_trace, double* hn2_out, double* tot_out,
+                             SCALAR* R, SCALAR* h, double* w, char* chosen)
+{
+    const int64_t ncols = Np;
+    int flags = 0;
+    memset(chosen, 0, (size_t)L);
+    for (int64_t k = 1; k <= Np; ++k) {
+        if (k >= 2) SFX(advance_elimination)(U, N, m, x_out[k - 2], R, ncols, k);
+        double hn2;
+        SFX(normal_vector)(R, ncols, k, h, &hn2);
+        /* conditional weights for all L candidates ("Calculating the inner product
+         * u_{x_k}^T h for all x_k"); already-chosen sites forced to 0 (reading Q5/SPEC.md:211) */
+        double T = 0.0;
+        for (int64_t x = 0; x < L; ++x) {
+            double wx = 0.0;
+            if (!chosen[x]) {
+                SCALAR s = 0.0;
+                for (int64_t j = 0; j < k; ++j) s += U[x * N + m[j]] * h[j];
+                wx = ABS2(s);
+            }
+            w[x] = wx;
+            T += wx;
+        }
+        /* inverse-CDF draw (reading Q4/Q5): x_k = min{x : C(x) > u*T}, C the inclusive prefix
+         * sum in index order; if none, the largest x with w(x) > 0. */
+        int64_t sel = -1;
+        if (!(T > 0.0) || !isfinite(T)) {
+            flags |= 1;
+            for (int64_t x = 0; x < L; ++x) if (!chosen[x]) { sel = x; break; }
+        } else if (!forced) {
+            double t = u_sel[k - 1] * T, C = 0.0;
+            for (int64_t x = 0; x < L; ++x) {
+                C += w[x];
+                if (C > t) { sel = x; break; }
+            }
+            if (sel < 0)
+                for (int64_t x = L - 1; x >= 0; --x) if (w[x] > 0.0) { sel = x; break; }
+        }
+        if (forced) sel = forced[k - 1];
+        if (sel < 0) sel = 0; /* unreachable for L >= N: some unchosen site always exists */
+        if (T > 0.0 && w[sel] / T < 1e-12) flags |= 2;
+        x_out[k - 1] = (int32_t)sel;
+        chosen[sel] = 1;
+        if (w_trace)
+            for (int64_t x = 0; x < L; ++x) w_trace[(k - 1) * L + x] = (T > 0.0) ? w[x] / T : 0.0;
+        if (hn2_out) hn2_out[k - 1] = hn2;
+        if (tot_out) tot_out[k - 1] = T;
+    }
+    return flags;
+}

@@ -1,0 +1,188 @@
+"""Seeded synthetic inputs for the FFS hot path: orbital matrices U and Philox uniforms.
+
+This module is shared by the CUDA path's tests/bench AND by the oracle's tests. It holds
+NO arithmetic of the sampling method itself (no elimination, no weights, no selection):
+only the construction of the one-body problems whose N lowest orbitals form U (setup,
+never timed), and the counter-based uniforms the method consumes.
+
+Recipes follow BASELINE.json `configs` and SURVEY.md §8(d) (readings Q14/Q15 in DESIGN.md):
+
+* C1 tiny     : U = Q of reduced QR of a seeded 16x4 N(0,1) matrix.
+* C2 dw       : open chain L=256, t=1, V(x)=4((x-128)^2/64^2-1)^2; N=32 lowest.
+* C3 anderson : open chain L=1024, t=1, eps_x ~ U[-2,2] (seed 0); N=128 lowest; marginal N'=16.
+* C4 peierls  : 64x64 torus, site 64*x+y, Landau gauge (x-bonds -1, y-bonds -exp(i 2 pi phi x)),
+                phi=1/16, + U[-1,1] disorder; complex128; N=512 lowest.
+* C5 dpp      : B = diag(q) G, G ~ N(0,1)^{16384x1024}, q = exp(0.5 z), z ~ N(0,1) (G drawn first);
+                U = Q of reduced QR (projection DPP with every eigenvector of C = B B^T kept,
+                PAPER.md:178-180); N=1024; marginal N'=64.
+
+Uniform rows (reading Q6/Q7): uniforms[i, 0:N'] drive the permutation draw,
+uniforms[i, N':2N'] drive the N' inverse-CDF selections.
+"""
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+import os
+from typing import Optional
+
+import numpy as np
+
+F64 = 0
+C128 = 1
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    L: int
+    N: int
+    M: int
+    Nprime: int           # steps per sample (== N for full sampling)
+    dtype: int            # F64 or C128
+    index: int            # BASELINE.json configs[] index (uniform seed = 1000 + index)
+    recipe: str           # which U builder
+    marginal_M: Optional[int] = None  # extra marginal workload (BASELINE.json) if any
+    marginal_Np: Optional[int] = None
+
+    @property
+    def uniform_seed(self) -> int:
+        return 1000 + self.index
+
+
+CONFIGS = {
+    "tiny": Config("tiny", 16, 4, 200000, 4, F64, 0, "qr_gauss"),
+    "dw": Config("dw", 256, 32, 65536, 32, F64, 1, "double_well"),
+    "anderson": Config("anderson", 1024, 128, 16384, 128, F64, 2, "anderson",
+                       marginal_M=16384, marginal_Np=16),
+    "peierls": Config("peierls", 4096, 512, 4096, 512, C128, 3, "peierls"),
+    "dpp": Config("dpp", 16384, 1024, 1024, 1024, F64, 4, "dpp",
+                  marginal_M=8192, marginal_Np=64),
+}
+
+
+def lowest_orbitals(H: np.ndarray, N: int) -> np.ndarray:
+    """N lowest eigenvectors of a Hermitian one-body Hamiltonian (setup, not timed)."""
+    w, v = np.linalg.eigh(H)
+    return np.ascontiguousarray(v[:, :N])
+
+
+def chain_hamiltonian(onsite: np.ndarray, t: float = 1.0) -> np.ndarray:
+    """Open-boundary nearest-neighbour chain: H = -t sum (c+_x c_{x+1} + h.c.) + sum v_x n_x."""
+    L = onsite.shape[0]
+    H = np.diag(onsite.astype(np.float64))
+    idx = np.arange(L - 1)
+    H[idx, idx + 1] = -t
+    H[idx + 1, idx] = -t
+    return H
+
+
+def build_u_qr_gauss(L: int, N: int, seed: int = 0) -> np.ndarray:
+    G = np.random.default_rng(seed).standard_normal((L, N))
+    Q, _ = np.linalg.qr(G)
+    return np.ascontiguousarray(Q)
+
+
+def build_u_double_well(L: int = 256, N: int = 32) -> np.ndarray:
+    x = np.arange(L, dtype=np.float64)
+    V = 4.0 * ((x - L / 2) ** 2 / (L / 4) ** 2 - 1.0) ** 2
+    return lowest_orbitals(chain_hamiltonian(V), N)
+
+
+def build_u_anderson(L: int = 1024, N: int = 128, W: float = 2.0, seed: int = 0) -> np.ndarray:
+    eps = np.random.default_rng(seed).uniform(-W, W, L)
+    return lowest_orbitals(chain_hamiltonian(eps), N)
+
+
+def build_u_peierls(Lx: int = 64, Ly: int = 64, N: int = 512, phi: float = 1.0 / 16,
+                    W: float = 1.0, seed: int = 0) -> np.ndarray:
+    L = Lx * Ly
+    H = np.zeros((L, L), dtype=np.complex128)
+    site = lambda x, y: (x % Lx) * Ly + (y % Ly)
+    for x in range(Lx):
+        for y in range(Ly):
+            s = site(x, y)
+            sx = site(x + 1, y)
+            H[s, sx] += -1.0
+            H[sx, s] += -1.0
+            sy = site(x, y + 1)
+            ph = np.exp(2j * np.pi * phi * x)
+            H[s, sy] += -ph
+            H[sy, s] += -np.conj(ph)
+    eps = np.random.default_rng(seed).uniform(-W, W, L)
+    H[np.arange(L), np.arange(L)] += eps
+    return lowest_orbitals(H, N)
+
+
+def build_u_dpp(L: int = 16384, N: int = 1024, seed: int = 0) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    G = rng.standard_normal((L, N))
+    q = np.exp(0.5 * rng.standard_normal(L))
+    Q, _ = np.linalg.qr(q[:, None] * G)
+    return np.ascontiguousarray(Q)
+
+
+def random_orthonormal(L: int, N: int, seed: int, complex_: bool = False) -> np.ndarray:
+    """Random L x N matrix with orthonormal columns (Fig. 3B-style inputs; small test cases)."""
+    rng = np.random.default_rng(seed)
+    G = rng.standard_normal((L, N))
+    if complex_:
+        G = G + 1j * rng.standard_normal((L, N))
+    Q, _ = np.linalg.qr(G)
+    return np.ascontiguousarray(Q)
+
+
+_CACHE_DIR = os.environ.get("FFS_INPUT_CACHE",
+                            os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                         ".input_cache"))
+
+
+def build_u(cfg: Config) -> np.ndarray:
+    """U for a registered config; cached on disk (git-ignored) because C4's eigh takes ~1 min."""
+    path = os.path.join(_CACHE_DIR, f"U_{cfg.name}.npy")
+    if os.path.exists(path):
+        try:
+            return np.load(path)
+        except Exception:
+            pass
+    if cfg.recipe == "qr_gauss":
+        U = build_u_qr_gauss(cfg.L, cfg.N, 0)
+    elif cfg.recipe == "double_well":
+        U = build_u_double_well(cfg.L, cfg.N)
+    elif cfg.recipe == "anderson":
+        U = build_u_anderson(cfg.L, cfg.N)
+    elif cfg.recipe == "peierls":
+        U = build_u_peierls(64, 64, cfg.N)
+    elif cfg.recipe == "dpp":
+        U = build_u_dpp(cfg.L, cfg.N)
+    else:
+        raise ValueError(cfg.recipe)
+    try:
+        os.makedirs(_CACHE_DIR, exist_ok=True)
+        tmp = path + f".tmp{os.getpid()}"
+        np.save(tmp, U)
+        os.replace(tmp + ".npy" if not tmp.endswith(".npy") else tmp, path)
+    except OSError:
+        pass
+    return U
+
+
+def u_sha256(U: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(U).tobytes()).hexdigest()
+
+
+def uniforms(M: int, Nprime: int, seed: int) -> np.ndarray:
+    """[M][2N'] fp64 uniforms in [0,1) from numpy's counter-based Philox generator."""
+    return np.random.Generator(np.random.Philox(seed)).random((M, 2 * Nprime))
+
+
+def u_as_f64_view(U: np.ndarray) -> np.ndarray:
+    """Interleaved (re,im) float64 view for complex U (ABI dtype C128); real U unchanged."""
+    U = np.ascontiguousarray(U)
+    if np.iscomplexobj(U):
+        return U.view(np.float64).reshape(U.shape[0], U.shape[1] * 2)
+    return U.astype(np.float64, copy=False)
+
+
+def dtype_of(U: np.ndarray) -> int:
+    return C128 if np.iscomplexobj(U) else F64

@@ -1,0 +1,277 @@
+"""T0 — pins of the CPU oracle (oracle/) against what PAPER.md and the mathematics fix.
+
+Every check compares the oracle with something other than itself: hand-derived values
+(tests/golden), the Eq. 1 / Eq. 2 determinant definitions (numpy det), the Eq. 3 null-vector
+definition (numpy SVD), closed forms of projection DPPs (K = U U^dagger), brute-force
+enumeration and chi-square sampling tests. No GPU.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import exact, ref
+from paper_2109_07358_b200 import inputs
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand_u(L, N, seed, cplx=False):
+    return inputs.random_orthonormal(L, N, seed, complex_=cplx)
+
+
+# ---------------------------------------------------------------- hand-derived worked example
+def test_golden_worked_example():
+    g = json.load(open(os.path.join(GOLDEN, "worked_example_l3n2.json")))
+    U = np.array(g["U"])
+    for c in g["cases"]:
+        u = np.array(c["uniforms"])[None, :]
+        m = ref.permutation(u[0, :2], 2)
+        assert list(m) == c["m"]
+        pos, w = ref.weights(U, u)
+        assert list(pos[0]) == c["positions"]
+        np.testing.assert_allclose(w[0], np.array(c["weights"]), atol=1e-15)
+        _, hn2, tot = ref.chain(U, m, pos[0])
+        np.testing.assert_allclose(hn2, c["hnorm2"], rtol=1e-14)
+        np.testing.assert_allclose(tot, 1.0, rtol=1e-14)
+        # chain determinant (Eq. 2 numerator): prod_k |u_{x_k}^T h'_k|^2 = |det U_{x,(m)}|^2
+        prod = np.prod([w[0][k, pos[0][k]] * tot[k] * hn2[k] for k in range(2)])
+        assert abs(prod - c["det2_chosen"]) < 1e-15
+
+
+# ---------------------------------------------------------------- permutation rule (Q6)
+def test_permutation_is_uniform_n4():
+    from scipy import stats
+    M = 48000
+    u = inputs.uniforms(M, 4, 7)[:, :4]
+    counts = {}
+    for i in range(M):
+        counts[tuple(ref.permutation(u[i], 4))] = counts.get(tuple(ref.permutation(u[i], 4)), 0) + 1
+    assert len(counts) == 24
+    obs = np.array(list(counts.values()))
+    assert stats.chisquare(obs).pvalue > 1e-3
+
+
+def test_partial_permutation_prefix_uniform():
+    from scipy import stats
+    M = 40000
+    u = inputs.uniforms(M, 2, 8)[:, :2]
+    counts = {}
+    for i in range(M):
+        k = tuple(ref.permutation(u[i], 5, 2)[:2])
+        counts[k] = counts.get(k, 0) + 1
+    assert len(counts) == 20  # all ordered pairs of 5 columns
+    assert stats.chisquare(np.array(list(counts.values()))).pvalue > 1e-3
+
+
+def test_identity_U_follows_permutation():
+    # U = I (L = N): column m_k has its single nonzero at row m_k, so x_k = m_k exactly.
+    N = 6
+    U = np.eye(N)
+    uni = inputs.uniforms(200, N, 3)
+    pos = ref.sample(U, uni)
+    for i in range(200):
+        assert list(pos[i]) == list(ref.permutation(uni[i, :N], N))
+
+
+# ---------------------------------------------------------------- selection rule (Q5)
+def test_selection_rule_strict_index_order():
+    U = np.full((4, 1), 0.5)  # w = 0.25 each, exactly; T = 1 exactly
+    for us, want in [(0.0, 0), (0.2499999, 0), (0.25, 1), (0.5, 2), (0.74999, 2), (0.75, 3),
+                     (0.9999999999999999, 3)]:
+        pos = ref.sample(U, np.array([[0.3, us]]))
+        assert pos[0, 0] == want, (us, pos)
+
+
+# ---------------------------------------------------------------- conditionals vs definitions
+@pytest.mark.parametrize("cplx", [False, True])
+def test_conditional_equals_determinant_ratio(cplx):
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        L, N = 7, 4
+        U = _rand_u(L, N, 100 + trial, cplx)
+        m = rng.permutation(N).astype(np.int32)
+        x = rng.choice(L, N, replace=False).astype(np.int32)
+        w, _, _ = ref.chain(U, m, x)
+        for k in range(N):
+            want = exact.det_conditional(U, m, list(x[:k]))
+            np.testing.assert_allclose(w[k], want, atol=1e-13, rtol=0)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_conditional_equals_nullvector_definition(cplx):
+    L, N = 64, 16
+    U = _rand_u(L, N, 5, cplx)
+    uni = inputs.uniforms(3, N, 21)
+    pos, w = ref.weights(U, uni)
+    for i in range(3):
+        m = ref.permutation(uni[i, :N], N)
+        for k in range(N):
+            want = exact.nullvec_conditional(U, m, list(pos[i, :k]))
+            assert np.max(np.abs(w[i, k] - want)) <= 1e-12 * np.max(want)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_mixture_identity_eq2(cplx):
+    # Eq. 2: sum_m prod_k P(x_k | x_<k; m) = |det U_{x,n}|^2 for every ordered x.
+    L, N = 5, 3
+    U = _rand_u(L, N, 17, cplx)
+    perms = [np.array(p, dtype=np.int32) for p in itertools.permutations(range(N))]
+    worst = 0.0
+    for x in itertools.permutations(range(L), N):
+        x = np.array(x, dtype=np.int32)
+        s = 0.0
+        for m in perms:
+            w, _, _ = ref.chain(U, m, x)
+            s += np.prod([w[k, x[k]] for k in range(N)])
+        worst = max(worst, abs(s - abs(np.linalg.det(U[x, :])) ** 2))
+    assert worst < 1e-13
+
+
+def test_k1_weights_are_column_moduli():
+    U = _rand_u(20, 5, 2, True)
+    m = np.array([3, 1, 4, 0, 2], dtype=np.int32)
+    w, _, _ = ref.chain(U, m, np.array([0], dtype=np.int32))
+    np.testing.assert_allclose(w[0], np.abs(U[:, 3]) ** 2, atol=1e-15)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_normalisation_and_chain_determinant(cplx):
+    # U^dagger U = 1 => sum_x |u_x^T h|^2 = |h|^2 = 1 (unit h); prod_k |u_{x_k}^T h'_k|^2 = |det V_{X,1..N}|^2
+    L, N = 32, 8
+    U = _rand_u(L, N, 23, cplx)
+    uni = inputs.uniforms(5, N, 4)
+    pos, w = ref.weights(U, uni)
+    for i in range(5):
+        m = ref.permutation(uni[i, :N], N)
+        wc, hn2, tot = ref.chain(U, m, pos[i])
+        np.testing.assert_allclose(tot, 1.0, atol=1e-13)
+        np.testing.assert_allclose(w[i].sum(axis=1), 1.0, atol=1e-13)
+        prod = np.prod([wc[k, pos[i, k]] * tot[k] * hn2[k] for k in range(N)])
+        det2 = abs(np.linalg.det(U[np.ix_(pos[i], m)])) ** 2
+        assert abs(prod - det2) <= 1e-10 * det2
+
+
+# ---------------------------------------------------------------- special cases
+def test_point_mass():
+    U = np.zeros((5, 1))
+    U[2, 0] = 1.0
+    pos = ref.sample(U, inputs.uniforms(100, 1, 5))
+    assert (pos[:, 0] == 2).all()
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_full_filling(cplx):
+    U = _rand_u(3, 3, 9, cplx)
+    pos = ref.sample(U, inputs.uniforms(500, 3, 6))
+    assert all(sorted(p) == [0, 1, 2] for p in pos.tolist())
+
+
+def test_pauli_exclusion_and_range():
+    U = _rand_u(40, 12, 1)
+    pos = ref.sample(U, inputs.uniforms(2000, 12, 2))
+    assert pos.min() >= 0 and pos.max() < 40
+    assert all(len(set(p)) == 12 for p in pos.tolist())
+
+
+def test_marginal_np_equal_n_is_full():
+    U = _rand_u(30, 6, 12)
+    uni = inputs.uniforms(300, 6, 13)
+    a = ref.sample(U, uni)
+    b = ref.sample(U, uni, Np=6)
+    assert (a == b).all()
+
+
+# ---------------------------------------------------------------- output law (Eq. 1)
+def test_chisquare_tiny_config_against_bruteforce():
+    # BASELINE configs[0]: L=16, N=4, M=200000; histogram vs |det U_S|^2 over all 1820 sets.
+    cfg = inputs.CONFIGS["tiny"]
+    U = inputs.build_u(cfg)
+    subsets, p = exact.set_probabilities(U)
+    assert abs(p.sum() - 1.0) < 1e-13  # Cauchy-Binet
+    pos = ref.sample(U, inputs.uniforms(cfg.M, cfg.N, cfg.uniform_seed))
+    index = {s: i for i, s in enumerate(subsets)}
+    obs = np.bincount([index[tuple(sorted(r))] for r in pos.tolist()], minlength=len(subsets))
+    stat, dof, pval, nb = exact.pooled_chisquare(obs, p * cfg.M)
+    assert pval > 1e-3, (stat, dof, pval)
+    # (TV over 1820 bins at M=2e5 has a sampling floor of ~0.02, so only the chi-square is asserted)
+
+
+def test_chisquare_complex_small():
+    U = _rand_u(6, 3, 31, True)
+    subsets, p = exact.set_probabilities(U)
+    M = 60000
+    pos = ref.sample(U, inputs.uniforms(M, 3, 32))
+    index = {s: i for i, s in enumerate(subsets)}
+    obs = np.bincount([index[tuple(sorted(r))] for r in pos.tolist()], minlength=len(subsets))
+    assert exact.pooled_chisquare(obs, p * M)[2] > 1e-3
+
+
+# ---------------------------------------------------------------- marginal
+@pytest.mark.parametrize("cplx", [False, True])
+def test_marginal_exact_enumeration(cplx):
+    # E_m[P(x_1|m) P(x_2|x_1;m)] over all N! permutations equals det K[x,x] (N-N')!/N!.
+    L, N, Np = 6, 3, 2
+    U = _rand_u(L, N, 41, cplx)
+    perms = [np.array(p, dtype=np.int32) for p in itertools.permutations(range(N))]
+    for xs in itertools.permutations(range(L), Np):
+        xs = np.array(xs, dtype=np.int32)
+        s = 0.0
+        for m in perms:
+            w, _, _ = ref.chain(U, m, xs)
+            s += w[0, xs[0]] * w[1, xs[1]]
+        s /= math.factorial(N)
+        assert abs(s - exact.ordered_marginal_probability(U, xs)) < 1e-14
+
+
+def test_marginal_sampling_chisquare():
+    L, N, Np = 6, 3, 2
+    U = _rand_u(L, N, 43)
+    M = 60000
+    pos = ref.sample(U, inputs.uniforms(M, Np, 44), Np=Np)
+    pairs = list(itertools.permutations(range(L), Np))
+    expected = np.array([exact.ordered_marginal_probability(U, q) for q in pairs]) * M
+    idx = {q: i for i, q in enumerate(pairs)}
+    obs = np.bincount([idx[tuple(r)] for r in pos.tolist()], minlength=len(pairs))
+    assert abs(expected.sum() - M) < 1e-6 * M
+    assert exact.pooled_chisquare(obs, expected)[2] > 1e-3
+
+
+def test_marginal_one_step_is_kxx_over_n():
+    U = _rand_u(12, 4, 45)
+    M = 80000
+    pos = ref.sample(U, inputs.uniforms(M, 1, 46), Np=1)
+    K = np.sum(np.abs(U) ** 2, axis=1)
+    from scipy import stats
+    obs = np.bincount(pos[:, 0], minlength=12)
+    assert stats.chisquare(obs, K / 4 * M).pvalue > 1e-3
+
+
+# ---------------------------------------------------------------- mid-size config: occupations
+def test_occupation_double_well_config():
+    # <n_x> = K_xx (projection DPP), z-test with Bonferroni over sites.
+    cfg = inputs.CONFIGS["dw"]
+    U = inputs.build_u(cfg)
+    M = 8000
+    pos = ref.sample(U, inputs.uniforms(M, cfg.N, cfg.uniform_seed)[:M])
+    occ = np.bincount(pos.ravel(), minlength=cfg.L) / M
+    K = np.sum(U ** 2, axis=1)
+    se = np.sqrt(np.maximum(K * (1 - K), 1e-12) / M)
+    z = np.abs(occ - K) / se
+    assert z.max() < 4.5
+    assert abs(occ.sum() - cfg.N) < 1e-9
+
+
+# ---------------------------------------------------------------- argument handling
+def test_bad_arguments_rejected():
+    L = ref.lib()
+    U = np.zeros((4, 2))
+    uni = np.zeros((1, 4))
+    pos = np.zeros((1, 2), dtype=np.int32)
+    assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 5, 0, 1, 2, uni.ctypes.data, pos.ctypes.data, None, 1) == -1
+    assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 2, 0, 1, 3, uni.ctypes.data, pos.ctypes.data, None, 1) == -1
+    assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 2, 7, 1, 2, uni.ctypes.data, pos.ctypes.data, None, 1) == -1
+    assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 2, 0, 0, 2, None, None, None, 1) == 0
