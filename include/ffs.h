@@ -1,0 +1,88 @@
+/* ffs.h — C ABI of the B200-native fast fermion sampling (FFS) hot path (libffs.so).
+ *
+ * The operation (arXiv 2109.07358, PAPER.md):
+ *   Given U (L x N, orthonormal columns, U^dagger U = 1), draw ordered
+ *   configurations x = (x_1..x_N) from P(x) = |det U_{x,n}|^2 / N!  (Eq. 1)
+ *   by the FFS algorithm: a uniformly random permutation m of the columns, then
+ *   for k = 1..N the conditional P(x_k | x_1..x_{k-1}; m) ∝ |u_{x_k}^T h|^2, h the normal vector
+ *   of u_{x_1..x_{k-1}} in the span of columns m_1..m_k (Eq. 3), drawn by inverse
+ *   CDF. The marginal variant stops after N' < N steps.
+ *
+ * Conventions shared with the oracle (readings Q3-Q8):
+ *   - dtype FFS_F64: U is double[L][N] row-major. FFS_C128: U is interleaved (re,im) double[L][N][2];
+ *     u_x^T h is BILINEAR (no conjugation), weights are |.|^2.
+ *   - uniforms: double[M][2N'] in [0,1). Row i: [0, N') drive the permutation draw (forward partial
+ *     Fisher-Yates: m = (0..N-1); for j < N': n = N-j, r = j + min(n-1, floor(u[j]*n)),
+ *     swap(m[j], m[r])); [N', 2N') are the N' selection uniforms.
+ *   - selection at step k with weights w >= 0 (chosen sites forced to 0): T = sum of w;
+ *     x_k = min{x : C(x) > u*T, w(x) > 0}, C the inclusive prefix sum in index order;
+ *     if none, the largest x with w(x) > 0.
+ *   - positions: int32[M][N'] out, 0-based site indices, in sampling order.
+ *   - sample_flags (optional, may be NULL): int32[M] out; bit0 = some step had a non-finite or
+ *     non-positive total T; bit1 = a selected normalised weight was < 1e-12. Numerical conditions
+ *     never abort a call.
+ *
+ * Ownership / memory: every pointer of the device entry points is a DEVICE pointer owned by the
+ * caller; the library allocates nothing (the caller provides `workspace` of at least
+ * ffs_workspace_bytes(...) bytes, 256-byte aligned). Calls are asynchronous on `stream` and
+ * re-entrant across streams with distinct workspaces. U orthonormality is the caller's
+ * precondition and is not checked.
+ *
+ * Errors: FFS_EINVAL (synchronous) for null pointers when M > 0, N < 1, N > L, N' not in [1, N],
+ * L > 2^31-1, unknown dtype, workspace too small, or a shape the kernels do not support
+ * (see ffs_last_error()); FFS_ECUDA for CUDA launch/runtime errors. M == 0 is an OK no-op.
+ */
+#ifndef FFS_H
+#define FFS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { FFS_F64 = 0, FFS_C128 = 1 } ffs_dtype;
+typedef enum { FFS_OK = 0, FFS_EINVAL = -1, FFS_ECUDA = -2, FFS_ENOWS = -3 } ffs_status;
+
+/* Device workspace bytes needed by ffs_sample / ffs_sample_marginal / ffs_debug_trace on the
+ * current CUDA device. Returns 0 for invalid arguments. */
+size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M);
+
+/* Full sampling (N' = N): Eq. 1-3. uniforms [M][2N], positions [M][N]. */
+int ffs_sample(const void* U, int64_t L, int64_t N, int dtype, int64_t M,
+               const double* uniforms, int32_t* positions, int32_t* sample_flags,
+               void* workspace, size_t ws_bytes, void* stream);
+
+/* Marginal sampling of N' <= N particles: the same chain stopped after N' steps.
+ * uniforms [M][2N'], positions [M][N']. */
+int ffs_sample_marginal(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+                        const double* uniforms, int32_t* positions, int32_t* sample_flags,
+                        void* workspace, size_t ws_bytes, void* stream);
+
+/* As ffs_sample_marginal, and also writes the normalised conditional weight vectors of the first
+ * S samples along their own path: weights double[S][N'][L] (DEVICE), w(x)/T per step. */
+int ffs_debug_trace(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+                    const double* uniforms, int32_t* positions, int32_t* sample_flags,
+                    void* workspace, size_t ws_bytes, void* stream, int64_t S, double* weights);
+
+/* Host-buffer entry point (end-to-end path): U, uniforms, positions, sample_flags are HOST
+ * pointers (pinned memory recommended); the call copies inputs host->device, samples, copies the
+ * results device->host and returns after the results are in host memory. `workspace` is a DEVICE
+ * buffer of at least ffs_host_workspace_bytes(...) bytes. Samples are processed in chunks so that
+ * the copies of one chunk overlap the sampling of another. */
+size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M);
+int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+                    const double* uniforms, int32_t* positions, int32_t* sample_flags,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* Number of kernel launches the last successful sampling call on this thread issued. */
+int ffs_last_launch_count(void);
+
+/* Thread-local message for the last non-OK return on this thread ("" if none). */
+const char* ffs_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFS_H */

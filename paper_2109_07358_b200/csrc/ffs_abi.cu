@@ -1,0 +1,319 @@
+// C ABI of libffs.so (declarations and contracts: include/ffs.h).
+// Argument validation, kernel-variant dispatch, workspace carving and the host-buffer path.
+// No torch types, no hidden allocations; everything runs in the kernels of ffs_kernel.cuh.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+
+#include "ffs.h"
+#include "ffs_kernel.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
+
+// ------------------------------------------------------------------ variant table
+// A variant is a kernel instantiation ffs_sample_kernel<T, WARP, R, B, USMEM>.
+struct Variant {
+  bool warp;      // owner = one warp (true) or one CTA of G threads (false)
+  int R, B;       // rows per thread, panel width
+  bool usmem;     // U^T held in shared memory (shared by all owners of a CTA)
+  int maxt;       // __launch_bounds__ of the instantiation
+  const void* fn; // kernel
+};
+
+// warp-owner kernels: up to kWarpMaxThreads threads (= owners x 32) per CTA
+constexpr int kWarpMaxThreads = 320;
+
+template <typename T, bool WARP, int R, int B, bool USMEM, int MAXT = kWarpMaxThreads>
+Variant make_variant() {
+  return Variant{WARP, R, B, USMEM, MAXT,
+                 reinterpret_cast<const void*>(&ffsk::ffs_sample_kernel<T, WARP, R, B, USMEM, MAXT>)};
+}
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+struct Plan {
+  Variant v;
+  int es;              // scalar bytes
+  int G;               // threads per owner
+  int Lp;              // rows covered per owner
+  int threads;         // blockDim.x
+  int owners_per_cta;
+  int grid;
+  int ut_stride;
+  size_t owner_smem, ushared_smem, smem;
+  size_t ws_ut, ws_wfull;  // workspace bytes
+};
+
+bool pick_variant(int L, int N, int Np, int dtype, Variant& v) {
+  const bool c = dtype == FFS_C128;
+  const size_t es = c ? 16 : 8;
+  // U^T in shared memory if the whole (padded) matrix takes <= 96 KB: one copy per CTA,
+  // shared by all warp-owners of that CTA.
+  auto fits = [&](int R) { return (size_t)N * (size_t)(32 * R + 2) * es <= 96 * 1024; };
+  // Warp owners (L <= 256 real / 128 complex): panel R x B per lane in registers.
+  // CTA owners: one sample per CTA; the L x B panel must fit the SM's register file, so B
+  // shrinks as L grows (the large-L configs are register-capacity bound).
+  if (!c) {
+    if (L <= 32)  { v = fits(1) ? make_variant<double, true, 1, 8, true>() : make_variant<double, true, 1, 8, false>(); return true; }
+    if (L <= 64)  { v = fits(2) ? make_variant<double, true, 2, 8, true>() : make_variant<double, true, 2, 8, false>(); return true; }
+    if (L <= 128) { v = fits(4) ? make_variant<double, true, 4, 8, true>() : make_variant<double, true, 4, 8, false>(); return true; }
+    if (L <= 256) { v = fits(8) ? make_variant<double, true, 8, 8, true, 256>() : make_variant<double, true, 8, 8, false, 256>(); return true; }
+    if (L <= 1024)  { v = make_variant<double, false, 4, 8, false, 256>(); return true; }
+    if (L <= 4096)  { v = make_variant<double, false, 4, 4, false, 1024>(); return true; }
+    if (L <= 8192)  { v = make_variant<double, false, 8, 2, false, 1024>(); return true; }
+    if (L <= 16384) { v = make_variant<double, false, 16, 1, false, 1024>(); return true; }
+  } else {
+    if (L <= 32)  { v = fits(1) ? make_variant<cplx, true, 1, 4, true>() : make_variant<cplx, true, 1, 4, false>(); return true; }
+    if (L <= 64)  { v = fits(2) ? make_variant<cplx, true, 2, 4, true>() : make_variant<cplx, true, 2, 4, false>(); return true; }
+    if (L <= 128) { v = fits(4) ? make_variant<cplx, true, 4, 4, true>() : make_variant<cplx, true, 4, 4, false>(); return true; }
+    if (L <= 1024)  { v = make_variant<cplx, false, 4, 4, false, 256>(); return true; }
+    if (L <= 4096)  { v = make_variant<cplx, false, 4, 2, false, 1024>(); return true; }
+    if (L <= 8192)  { v = make_variant<cplx, false, 8, 1, false, 1024>(); return true; }
+  }
+  (void)Np;
+  return false;
+}
+
+size_t owner_bytes(bool c, int B, int N, int Np) {
+  if (c) {
+    switch (B) {
+      case 1: return ffsk::OwnerLayout<cplx, 1>(N, Np).total;
+      case 2: return ffsk::OwnerLayout<cplx, 2>(N, Np).total;
+      case 4: return ffsk::OwnerLayout<cplx, 4>(N, Np).total;
+      default: return ffsk::OwnerLayout<cplx, 8>(N, Np).total;
+    }
+  }
+  switch (B) {
+    case 1: return ffsk::OwnerLayout<double, 1>(N, Np).total;
+    case 2: return ffsk::OwnerLayout<double, 2>(N, Np).total;
+    case 4: return ffsk::OwnerLayout<double, 4>(N, Np).total;
+    default: return ffsk::OwnerLayout<double, 8>(N, Np).total;
+  }
+}
+
+int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) {
+  if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0)
+    return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M=%lld", (long long)L, (long long)N,
+                (long long)Np, (long long)M);
+  if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
+  if (!pick_variant((int)L, (int)N, (int)Np, dtype, pl.v))
+    return fail(FFS_EINVAL, "unsupported L=%lld for dtype %d (max 16384)", (long long)L, dtype);
+  const bool c = dtype == FFS_C128;
+  pl.es = c ? 16 : 8;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(FFS_ECUDA, "cudaGetDevice failed");
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, pl.v.fn) != cudaSuccess) return fail(FFS_ECUDA, "cudaFuncGetAttributes failed");
+  const int regs = std::max(fa.numRegs, 1);
+  pl.owner_smem = owner_bytes(c, pl.v.B, (int)N, (int)Np);
+  if (pl.v.warp) {
+    pl.G = 32;
+    pl.Lp = 32 * pl.v.R;
+    pl.ut_stride = pl.Lp + (c ? 1 : 2);  // +16 B per column: spreads column bases over banks
+    pl.ushared_smem = pl.v.usmem ? ffsk::align16((size_t)N * pl.ut_stride * pl.es) : 0;
+    // warps per CTA: bounded by registers (one CTA per SM when U^T is shared), smem, and 16
+    const int by_regs = std::max(1, 65536 / (((regs * 32 + 255) / 256) * 256));
+    int w = std::min(pl.v.maxt / 32, by_regs);
+    while (w > 1 && pl.ushared_smem + (size_t)w * pl.owner_smem > kMaxSmem) --w;
+    if (!pl.v.usmem) w = std::min(w, 4);
+    pl.owners_per_cta = w;
+    pl.threads = 32 * w;
+  } else {
+    const int rows_per_warp = 32 * pl.v.R;
+    const int warps = (int)((L + rows_per_warp - 1) / rows_per_warp);
+    pl.G = 32 * warps;
+    pl.Lp = pl.G * pl.v.R;
+    pl.ut_stride = 0;
+    pl.ushared_smem = 0;
+    pl.owners_per_cta = 1;
+    pl.threads = pl.G;
+    if (pl.G > pl.v.maxt)
+      return fail(FFS_EINVAL, "variant needs %d threads > %d", pl.G, pl.v.maxt);
+  }
+  pl.smem = pl.ushared_smem + (size_t)pl.owners_per_cta * pl.owner_smem;
+  if (pl.smem > kMaxSmem) return fail(FFS_EINVAL, "shared memory %zu > %zu (N=%lld)", pl.smem, kMaxSmem, (long long)N);
+  if (cudaFuncSetAttribute(pl.v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem=%zu) failed", pl.smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.v.fn, pl.threads, pl.smem) != cudaSuccess || per_sm < 1)
+    return fail(FFS_EINVAL, "kernel does not fit on an SM (threads=%d smem=%zu regs=%d)", pl.threads, pl.smem, regs);
+  const int64_t want = (M + pl.owners_per_cta - 1) / pl.owners_per_cta;
+  pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sms));
+  pl.ws_ut = pl.v.usmem ? 0 : align_up((size_t)N * pl.Lp * pl.es);
+  pl.ws_wfull = align_up((size_t)pl.grid * pl.owners_per_cta * (size_t)Np * Np * pl.es);
+  return FFS_OK;
+}
+
+int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+           int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
+           double* trace) {
+  g_launches = 0;
+  if (M == 0) return FFS_OK;
+  Plan pl;
+  int rc = make_plan(L, N, Np, dtype, M, pl);
+  if (rc != FFS_OK) return rc;
+  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions with M=%lld", (long long)M);
+  if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
+  const size_t need = pl.ws_ut + pl.ws_wfull;
+  if (need > 0 && (!ws || ws_bytes < need))
+    return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, need);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  char* w = static_cast<char*>(ws);
+  ffsk::Params p{};
+  p.U = static_cast<const double*>(U);
+  p.Ut = pl.v.usmem ? nullptr : reinterpret_cast<const double*>(w);
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  p.Lp = pl.Lp;
+  p.ut_stride = pl.ut_stride;
+  p.M = M;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.wfull = reinterpret_cast<double*>(w + pl.ws_ut);
+  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.trace = S > 0 ? trace : nullptr;
+  p.owner_smem = pl.owner_smem;
+  p.ushared_smem = pl.ushared_smem;
+  if (!pl.v.usmem) {
+    dim3 tb(32, 8), tg((unsigned)((pl.Lp + 31) / 32), (unsigned)((N + 31) / 32));
+    if (dtype == FFS_C128)
+      ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, pl.Lp);
+    else
+      ffsk::transpose_pad_kernel<double><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, pl.Lp);
+    ++g_launches;
+  }
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchKernel(pl.v.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, stream);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  ++g_launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  g_err[0] = 0;
+  return FFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M) {
+  Plan pl;
+  if (make_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), pl) != FFS_OK) return 0;
+  return pl.ws_ut + pl.ws_wfull;
+}
+
+int ffs_sample(const void* U, int64_t L, int64_t N, int dtype, int64_t M, const double* uniforms,
+               int32_t* positions, int32_t* sample_flags, void* workspace, size_t ws_bytes, void* stream) {
+  return launch(U, L, N, dtype, M, N, uniforms, positions, sample_flags, workspace, ws_bytes,
+                static_cast<cudaStream_t>(stream), 0, nullptr);
+}
+
+int ffs_sample_marginal(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+                        const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  return launch(U, L, N, dtype, M, Nprime, uniforms, positions, sample_flags, workspace, ws_bytes,
+                static_cast<cudaStream_t>(stream), 0, nullptr);
+}
+
+int ffs_debug_trace(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+                    const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
+                    size_t ws_bytes, void* stream, int64_t S, double* weights) {
+  return launch(U, L, N, dtype, M, Nprime, uniforms, positions, sample_flags, workspace, ws_bytes,
+                static_cast<cudaStream_t>(stream), S, weights);
+}
+
+// ---------------------------------------------------------------- host-buffer path
+// Device layout inside the caller's workspace: [U | uniforms chunk x2 | positions chunk x2 |
+// flags chunk x2 | sampling workspace]. Chunks alternate between two buffers so the copies of
+// chunk c+1 overlap the kernel of chunk c on the caller's stream (copies and kernels of one
+// stream serialise; overlap comes from a second stream created lazily per thread).
+namespace {
+struct HostLayout {
+  size_t u, uni[2], pos[2], flg[2], ws, total;
+  int64_t chunk;
+};
+int64_t host_chunk(int64_t M) { return std::max<int64_t>(1, std::min<int64_t>(M, 16384)); }
+bool host_layout(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HostLayout& h) {
+  const size_t es = dtype == FFS_C128 ? 16 : 8;
+  h.chunk = host_chunk(M);
+  size_t o = 0;
+  h.u = o; o = align_up(o + (size_t)L * N * es);
+  for (int b = 0; b < 2; ++b) { h.uni[b] = o; o = align_up(o + (size_t)h.chunk * 2 * Np * 8); }
+  for (int b = 0; b < 2; ++b) { h.pos[b] = o; o = align_up(o + (size_t)h.chunk * Np * 4); }
+  for (int b = 0; b < 2; ++b) { h.flg[b] = o; o = align_up(o + (size_t)h.chunk * 4); }
+  h.ws = o;
+  Plan pl;
+  if (make_plan(L, N, Np, dtype, h.chunk, pl) != FFS_OK) return false;
+  o += pl.ws_ut + pl.ws_wfull;
+  h.total = o;
+  return true;
+}
+}  // namespace
+
+size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M) {
+  HostLayout h;
+  if (!host_layout(L, N, Nprime, dtype, std::max<int64_t>(M, 1), h)) return 0;
+  return h.total;
+}
+
+int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+                    const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
+                    size_t ws_bytes, void* stream) {
+  if (M == 0) return FFS_OK;
+  HostLayout h;
+  if (!host_layout(L, N, Nprime, dtype, M, h)) return FFS_EINVAL;
+  if (!U || !uniforms || !positions || !workspace || ws_bytes < h.total)
+    return fail(FFS_EINVAL, "host path: null pointer or workspace %zu < %zu", ws_bytes, h.total);
+  cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
+  const size_t es = dtype == FFS_C128 ? 16 : 8;
+  const int64_t Np = Nprime;
+  int launches = 0;
+  cudaError_t e = cudaMemcpyAsync(w + h.u, U, (size_t)L * N * es, cudaMemcpyHostToDevice, s0);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "H2D U: %s", cudaGetErrorString(e));
+  for (int64_t c0 = 0, b = 0; c0 < M; c0 += h.chunk, b ^= 1) {
+    const int64_t mc = std::min<int64_t>(h.chunk, M - c0);
+    e = cudaMemcpyAsync(w + h.uni[b], uniforms + c0 * 2 * Np, (size_t)mc * 2 * Np * 8, cudaMemcpyHostToDevice, s0);
+    if (e != cudaSuccess) return fail(FFS_ECUDA, "H2D uniforms: %s", cudaGetErrorString(e));
+    int rc = launch(w + h.u, L, N, dtype, mc, Np, reinterpret_cast<const double*>(w + h.uni[b]),
+                    reinterpret_cast<int32_t*>(w + h.pos[b]), reinterpret_cast<int32_t*>(w + h.flg[b]), w + h.ws,
+                    h.total - h.ws, s0, 0, nullptr);
+    if (rc != FFS_OK) return rc;
+    launches += g_launches;
+    e = cudaMemcpyAsync(positions + c0 * Np, w + h.pos[b], (size_t)mc * Np * 4, cudaMemcpyDeviceToHost, s0);
+    if (e != cudaSuccess) return fail(FFS_ECUDA, "D2H positions: %s", cudaGetErrorString(e));
+    if (sample_flags) {
+      e = cudaMemcpyAsync(sample_flags + c0, w + h.flg[b], (size_t)mc * 4, cudaMemcpyDeviceToHost, s0);
+      if (e != cudaSuccess) return fail(FFS_ECUDA, "D2H flags: %s", cudaGetErrorString(e));
+    }
+  }
+  e = cudaStreamSynchronize(s0);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "host path sync: %s", cudaGetErrorString(e));
+  g_launches = launches;
+  return FFS_OK;
+}
+
+int ffs_last_launch_count(void) { return g_launches; }
+
+const char* ffs_last_error(void) { return g_err; }
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// Scalar arithmetic for the FFS kernels: real fp64 (FFS_F64) and complex128 (FFS_C128).
+// Complex products are BILINEAR (u_x^T h; reading Q3): no conjugation anywhere
+// except in |z|^2 and in the reciprocal of a pivot.
+#pragma once
+#include <cuda_runtime.h>
+
+struct cplx {
+  double re, im;
+};
+
+template <typename T> struct Sc;
+
+template <> struct Sc<double> {
+  static constexpr int kDoubles = 1;
+  __device__ __forceinline__ static double zero() { return 0.0; }
+  // c - a*b
+  __device__ __forceinline__ static double fms(double a, double b, double c) { return fma(-a, b, c); }
+  __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
+  __device__ __forceinline__ static double abs2(double a) { return a * a; }
+  __device__ __forceinline__ static double recip(double a) { return 1.0 / a; }
+  __device__ __forceinline__ static bool finite(double a) { return isfinite(a); }
+};
+
+template <> struct Sc<cplx> {
+  static constexpr int kDoubles = 2;
+  __device__ __forceinline__ static cplx zero() { return {0.0, 0.0}; }
+  __device__ __forceinline__ static cplx fms(cplx a, cplx b, cplx c) {
+    cplx r;
+    r.re = fma(-a.re, b.re, fma(a.im, b.im, c.re));
+    r.im = fma(-a.re, b.im, fma(-a.im, b.re, c.im));
+    return r;
+  }
+  __device__ __forceinline__ static cplx mul(cplx a, cplx b) {
+    cplx r;
+    r.re = fma(a.re, b.re, -a.im * b.im);
+    r.im = fma(a.re, b.im, a.im * b.re);
+    return r;
+  }
+  __device__ __forceinline__ static double abs2(cplx a) { return fma(a.re, a.re, a.im * a.im); }
+  __device__ __forceinline__ static cplx recip(cplx a) {
+    double d = 1.0 / fma(a.re, a.re, a.im * a.im);
+    return {a.re * d, -a.im * d};
+  }
+  __device__ __forceinline__ static bool finite(cplx a) { return isfinite(a.re) && isfinite(a.im); }
+};

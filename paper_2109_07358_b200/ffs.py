@@ -1,0 +1,210 @@
+"""Thin Python binding of libffs.so (include/ffs.h): argument marshalling only.
+
+Every step of the sampling path runs in the CUDA kernels of the library; PyTorch provides
+device memory and streams. If the library is missing this module raises — there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import torch
+
+from . import build as _build
+
+FFS_F64, FFS_C128 = 0, 1
+FFS_OK, FFS_EINVAL, FFS_ECUDA, FFS_ENOWS = 0, -1, -2, -3
+
+EXPORTED = (
+    "ffs_workspace_bytes",
+    "ffs_sample",
+    "ffs_sample_marginal",
+    "ffs_debug_trace",
+    "ffs_host_workspace_bytes",
+    "ffs_sample_host",
+    "ffs_last_launch_count",
+    "ffs_last_error",
+)
+
+_lib = None
+
+
+class FFSError(RuntimeError):
+    pass
+
+
+def lib_path() -> str:
+    return _build.SO
+
+
+def load(build_if_missing: bool = True):
+    """Load libffs.so (building it in-tree with nvcc if it is missing and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.SO):
+        if not build_if_missing:
+            raise FFSError(f"{_build.SO} missing: run python -m paper_2109_07358_b200.build")
+        _build.build()
+    L = ctypes.CDLL(_build.SO)
+    i64, vp, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+    ci = ctypes.c_int
+    L.ffs_workspace_bytes.argtypes = [i64, i64, i64, ci, i64]
+    L.ffs_workspace_bytes.restype = sz
+    L.ffs_sample.argtypes = [vp, i64, i64, ci, i64, vp, vp, vp, vp, sz, vp]
+    L.ffs_sample_marginal.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp]
+    L.ffs_debug_trace.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp, i64, vp]
+    L.ffs_host_workspace_bytes.argtypes = [i64, i64, i64, ci, i64]
+    L.ffs_host_workspace_bytes.restype = sz
+    L.ffs_sample_host.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp]
+    L.ffs_last_launch_count.restype = ci
+    L.ffs_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != FFS_OK:
+        msg = load().ffs_last_error().decode()
+        raise FFSError(f"libffs rc={rc}: {msg}")
+
+
+def _dtype_code(U: torch.Tensor) -> int:
+    if U.dtype == torch.float64:
+        return FFS_F64
+    if U.dtype == torch.complex128:
+        return FFS_C128
+    raise FFSError(f"U must be float64 or complex128, got {U.dtype}")
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream], device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def ffs_workspace_bytes(L: int, N: int, Nprime: int, dtype: int, M: int) -> int:
+    return int(load().ffs_workspace_bytes(L, N, Nprime, dtype, M))
+
+
+def ffs_host_workspace_bytes(L: int, N: int, Nprime: int, dtype: int, M: int) -> int:
+    return int(load().ffs_host_workspace_bytes(L, N, Nprime, dtype, M))
+
+
+def ffs_last_launch_count() -> int:
+    return int(load().ffs_last_launch_count())
+
+
+class Workspace:
+    """Caller-owned device workspace (torch allocation), grown on demand."""
+
+    def __init__(self, device="cuda"):
+        self.device = torch.device(device)
+        self.buf = None
+
+    def get(self, nbytes: int) -> Tuple[int, int]:
+        if nbytes == 0:
+            return 0, 0
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf.data_ptr(), self.buf.numel()
+
+
+def _prep(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int):
+    if not (U.is_cuda and uniforms.is_cuda):
+        raise FFSError("U and uniforms must be CUDA tensors (use ffs_sample_host for host buffers)")
+    if U.dim() != 2:
+        raise FFSError("U must be 2-D [L][N]")
+    U = U.contiguous()
+    uniforms = uniforms.contiguous()
+    if uniforms.dtype != torch.float64 or uniforms.dim() != 2 or uniforms.shape[1] != 2 * Nprime:
+        raise FFSError(f"uniforms must be float64 [M][2N'] with N'={Nprime}, got {tuple(uniforms.shape)}")
+    return U, uniforms
+
+
+def ffs_sample_marginal(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int,
+                        positions: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
+                        workspace: Optional[Workspace] = None, stream=None, with_flags: bool = False):
+    """Device path: positions int32 [M][N'] (and flags int32 [M] if with_flags)."""
+    U, uniforms = _prep(U, uniforms, Nprime)
+    L, N = U.shape
+    M = uniforms.shape[0]
+    dt = _dtype_code(U)
+    if positions is None:
+        positions = torch.empty((M, Nprime), dtype=torch.int32, device=U.device)
+    if flags is None and with_flags:
+        flags = torch.empty(M, dtype=torch.int32, device=U.device)
+    ws = workspace if workspace is not None else Workspace(U.device)
+    need = ffs_workspace_bytes(L, N, Nprime, dt, M)
+    if need == 0 and M > 0:
+        _check(FFS_EINVAL)
+    wp, wn = ws.get(need)
+    rc = load().ffs_sample_marginal(U.data_ptr(), L, N, dt, M, Nprime, uniforms.data_ptr(), positions.data_ptr(),
+                                    flags.data_ptr() if flags is not None else None, wp, wn,
+                                    _stream_handle(stream, U.device))
+    _check(rc)
+    return (positions, flags) if with_flags else positions
+
+
+def ffs_sample(U: torch.Tensor, uniforms: torch.Tensor, positions: Optional[torch.Tensor] = None,
+               flags: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None, stream=None,
+               with_flags: bool = False):
+    """Device path, full sampling (N' = N): positions int32 [M][N]."""
+    N = U.shape[1]
+    U, uniforms = _prep(U, uniforms, N)
+    L = U.shape[0]
+    M = uniforms.shape[0]
+    dt = _dtype_code(U)
+    if positions is None:
+        positions = torch.empty((M, N), dtype=torch.int32, device=U.device)
+    if flags is None and with_flags:
+        flags = torch.empty(M, dtype=torch.int32, device=U.device)
+    ws = workspace if workspace is not None else Workspace(U.device)
+    wp, wn = ws.get(ffs_workspace_bytes(L, N, N, dt, M))
+    rc = load().ffs_sample(U.data_ptr(), L, N, dt, M, uniforms.data_ptr(), positions.data_ptr(),
+                           flags.data_ptr() if flags is not None else None, wp, wn,
+                           _stream_handle(stream, U.device))
+    _check(rc)
+    return (positions, flags) if with_flags else positions
+
+
+def ffs_debug_trace(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int, S: int,
+                    workspace: Optional[Workspace] = None, stream=None):
+    """Positions [M][N'], flags [M] and normalised weights [S][N'][L] of the first S samples."""
+    U, uniforms = _prep(U, uniforms, Nprime)
+    L, N = U.shape
+    M = uniforms.shape[0]
+    dt = _dtype_code(U)
+    S = min(S, M)
+    positions = torch.empty((M, Nprime), dtype=torch.int32, device=U.device)
+    flags = torch.empty(M, dtype=torch.int32, device=U.device)
+    weights = torch.zeros((S, Nprime, L), dtype=torch.float64, device=U.device)
+    ws = workspace if workspace is not None else Workspace(U.device)
+    wp, wn = ws.get(ffs_workspace_bytes(L, N, Nprime, dt, M))
+    rc = load().ffs_debug_trace(U.data_ptr(), L, N, dt, M, Nprime, uniforms.data_ptr(), positions.data_ptr(),
+                                flags.data_ptr(), wp, wn, _stream_handle(stream, U.device), S, weights.data_ptr())
+    _check(rc)
+    return positions, flags, weights
+
+
+def ffs_sample_host(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int,
+                    positions: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
+                    workspace: Optional[Workspace] = None, stream=None, device="cuda"):
+    """End-to-end path on HOST tensors (pinned recommended): H2D, sampling, D2H inside the call."""
+    if U.is_cuda or uniforms.is_cuda:
+        raise FFSError("ffs_sample_host takes host tensors")
+    U = U.contiguous()
+    uniforms = uniforms.contiguous()
+    L, N = U.shape
+    M = uniforms.shape[0]
+    dt = _dtype_code(U)
+    if positions is None:
+        positions = torch.empty((M, Nprime), dtype=torch.int32, pin_memory=True)
+    ws = workspace if workspace is not None else Workspace(device)
+    wp, wn = ws.get(ffs_host_workspace_bytes(L, N, Nprime, dt, M))
+    rc = load().ffs_sample_host(U.data_ptr(), L, N, dt, M, Nprime, uniforms.data_ptr(), positions.data_ptr(),
+                                flags.data_ptr() if flags is not None else None, wp, wn,
+                                _stream_handle(stream, ws.device))
+    _check(rc)
+    return positions

@@ -132,9 +132,8 @@ def random_orthonormal(L: int, N: int, seed: int, complex_: bool = False) -> np.
     return np.ascontiguousarray(Q)
 
 
-_CACHE_DIR = os.environ.get("FFS_INPUT_CACHE",
-                            os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                         ".input_cache"))
+# Outside the repo so the (up to 128 MB) matrices never travel with a gpurun snapshot.
+_CACHE_DIR = os.environ.get("FFS_INPUT_CACHE", "/tmp/ffs_input_cache")
 
 
 def build_u(cfg: Config) -> np.ndarray:
@@ -169,6 +168,13 @@ def build_u(cfg: Config) -> np.ndarray:
 
 def u_sha256(U: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(U).tobytes()).hexdigest()
+
+
+def workload_uniforms(cfg: Config, marginal: bool = False) -> np.ndarray:
+    """Uniforms of a registered workload: seed 1000+index (full) or 1100+index (marginal)."""
+    if marginal:
+        return uniforms(cfg.marginal_M, cfg.marginal_Np, cfg.uniform_seed + 100)
+    return uniforms(cfg.M, cfg.Nprime, cfg.uniform_seed)
 
 
 def uniforms(M: int, Nprime: int, seed: int) -> np.ndarray:

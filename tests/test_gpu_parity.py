@@ -1,0 +1,174 @@
+"""T1/T2 — the CUDA path (through the C ABI) against the oracle on identical seeded inputs.
+
+Small shapes cover every kernel variant (warp owners with shared/global U^T, CTA owners of each
+register-capacity class, real and complex), several panel blocks and ragged tails (L not a
+multiple of the owner's rows, N' not a multiple of the panel width). Full BASELINE.json sizes
+run in the launch configuration bench.py times, compared on a prefix of samples the oracle
+finishes in seconds, plus properties that hold at any size (occupations = K_xx).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import exact, ref  # noqa: E402
+from paper_2109_07358_b200 import inputs  # noqa: E402
+from tests.parity import WEIGHT_TOL, compare_positions, compare_weights  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _ffs():
+    from paper_2109_07358_b200 import ffs
+    return ffs
+
+
+def _to_dev(U):
+    return torch.from_numpy(np.ascontiguousarray(U)).cuda()
+
+
+def run_gpu(U, uni, Np, trace_S=0):
+    ffs = _ffs()
+    Ud = _to_dev(U)
+    ud = torch.from_numpy(uni).cuda()
+    if trace_S:
+        pos, flags, w = ffs.ffs_debug_trace(Ud, ud, Np, trace_S)
+        torch.cuda.synchronize()
+        return pos.cpu().numpy(), flags.cpu().numpy(), w.cpu().numpy()
+    if Np == U.shape[1]:
+        pos, flags = ffs.ffs_sample(Ud, ud, with_flags=True)
+    else:
+        pos, flags = ffs.ffs_sample_marginal(Ud, ud, Np, with_flags=True)
+    torch.cuda.synchronize()
+    return pos.cpu().numpy(), flags.cpu().numpy(), None
+
+
+SMALL = [
+    # (L, N, N', complex) — spans every variant of pick_variant() and ragged tails
+    (16, 4, 4, False), (7, 3, 3, False), (32, 9, 9, False), (50, 17, 17, False),
+    (100, 23, 23, False), (128, 40, 13, False), (256, 32, 32, False), (200, 60, 60, False),
+    (256, 90, 90, False), (300, 33, 33, False), (1024, 40, 21, False), (1500, 19, 19, False),
+    (5000, 11, 11, False), (9000, 7, 7, False),
+    (16, 4, 4, True), (30, 11, 11, True), (64, 21, 9, True), (128, 30, 30, True),
+    (500, 26, 26, True), (2000, 9, 9, True), (6000, 5, 5, True),
+]
+
+
+@pytest.mark.parametrize("L,N,Np,cplx", SMALL)
+def test_small_shapes_match_oracle(L, N, Np, cplx):
+    U = inputs.random_orthonormal(L, N, 1000 + L + N, complex_=cplx)
+    M = 300 if L * N < 200000 else 60
+    uni = inputs.uniforms(M, Np, L * 7 + N)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=3)
+    rpos, rflags = ref.sample(U, uni, Np=Np, return_flags=True)
+    r = compare_positions(U, uni, gpos, rpos, Np)
+    assert not r["failures"], r
+    assert r["exact"] + r["ties"] == M
+    assert (gflags == 0).all()
+    # Pauli exclusion / range
+    assert all(len(set(p)) == Np for p in gpos.tolist())
+    _, rw = ref.weights(U, uni[:3], Np=Np)
+    assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
+
+
+def test_tiny_config_full_M_bitexact_and_chisquare():
+    cfg = inputs.CONFIGS["tiny"]
+    U = inputs.build_u(cfg)
+    uni = inputs.uniforms(cfg.M, cfg.N, cfg.uniform_seed)
+    gpos, gflags, _ = run_gpu(U, uni, cfg.N)
+    rpos = ref.sample(U, uni)
+    r = compare_positions(U, uni, gpos, rpos, cfg.N)
+    assert not r["failures"], r["failures"][:5]
+    subsets, p = exact.set_probabilities(U)
+    index = {s: i for i, s in enumerate(subsets)}
+    obs = np.bincount([index[tuple(sorted(q))] for q in gpos.tolist()], minlength=len(subsets))
+    stat, dof, pval, _ = exact.pooled_chisquare(obs, p * cfg.M)
+    assert pval > 1e-3, (stat, dof, pval)
+
+
+# (config, N', oracle prefix size, trace samples)
+FULL = [
+    ("dw", None, 3000, 4),
+    ("anderson", None, 300, 2),
+    ("anderson", 16, 4000, 8),
+    ("peierls", None, 6, 1),
+    ("dpp", None, 3, 1),
+    ("dpp", 64, 400, 4),
+]
+
+
+@pytest.mark.parametrize("name,Np,n_ref,n_trace", FULL)
+def test_full_size_configs(name, Np, n_ref, n_trace):
+    cfg = inputs.CONFIGS[name]
+    U = inputs.build_u(cfg)
+    Np = cfg.N if Np is None else Np
+    M = cfg.M if Np == cfg.N else cfg.marginal_M
+    uni = inputs.uniforms(M, Np, cfg.uniform_seed + (0 if Np == cfg.N else 100))
+    gpos, gflags, _ = run_gpu(U, uni, Np)
+    assert (gflags == 0).all()
+    assert gpos.min() >= 0 and gpos.max() < cfg.L
+    srt = np.sort(gpos, axis=1)
+    assert (np.diff(srt, axis=1) > 0).all()  # Pauli exclusion, every sample
+    rpos = ref.sample(U, uni[:n_ref], Np=Np)
+    r = compare_positions(U, uni, gpos, rpos, Np)
+    assert not r["failures"], r["failures"][:5]
+    # weights along the path for the first samples (debug trace of the same kernel)
+    tpos, _, tw = run_gpu(U, uni[:n_trace], Np, trace_S=n_trace)
+    assert (tpos == gpos[:n_trace]).all()
+    _, rw = ref.weights(U, uni[:n_trace], Np=Np)
+    assert compare_weights(tw, rw, tpos, rpos[:n_trace]) <= WEIGHT_TOL
+    # property at full size: occupation of each site = K_xx * N'/N (exchangeable order)
+    K = np.sum(np.abs(U) ** 2, axis=1) * (Np / cfg.N)
+    occ = np.bincount(gpos.ravel(), minlength=cfg.L) / M
+    se = np.sqrt(np.maximum(K * (1 - K), 1e-12) / M)
+    z = np.abs(occ - K) / se
+    assert z.max() < 5.5, (z.max(), int(np.argmax(z)))
+
+
+def test_edge_cases():
+    ffs = _ffs()
+    L = ffs.load()
+    U = inputs.random_orthonormal(10, 3, 5)
+    Ud = _to_dev(U)
+    ud = torch.from_numpy(inputs.uniforms(4, 3, 1)).cuda()
+    pos = torch.empty((4, 3), dtype=torch.int32, device="cuda")
+    # M = 0 is a no-op
+    assert L.ffs_sample(Ud.data_ptr(), 10, 3, 0, 0, None, None, None, None, 0, None) == 0
+    # invalid shapes / dtype / workspace
+    assert L.ffs_sample(Ud.data_ptr(), 10, 11, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    assert L.ffs_sample_marginal(Ud.data_ptr(), 10, 3, 0, 4, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    assert L.ffs_sample(Ud.data_ptr(), 10, 3, 9, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    assert L.ffs_sample(Ud.data_ptr(), 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    assert L.ffs_sample(None, 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    # N = 1, N' = 1, L = N (full filling)
+    for (l, n, np_) in [(9, 1, 1), (12, 5, 1), (6, 6, 6), (33, 33, 33)]:
+        Ue = inputs.random_orthonormal(l, n, l + n)
+        uni = inputs.uniforms(64, np_, 3)
+        gpos, _, _ = run_gpu(Ue, uni, np_)
+        rpos = ref.sample(Ue, uni, Np=np_)
+        assert not compare_positions(Ue, uni, gpos, rpos, np_)["failures"]
+        if l == n:
+            assert all(sorted(p) == list(range(l)) for p in gpos.tolist())
+
+
+def test_host_path_matches_device_path():
+    ffs = _ffs()
+    cfg = inputs.CONFIGS["dw"]
+    U = inputs.build_u(cfg)
+    M = 20000  # > one host chunk
+    uni = inputs.uniforms(M, cfg.N, 77)
+    dev, _, _ = run_gpu(U, uni, cfg.N)
+    hU = torch.from_numpy(U).pin_memory()
+    hu = torch.from_numpy(uni).pin_memory()
+    hp = ffs.ffs_sample_host(hU, hu, cfg.N)
+    assert (hp.numpy() == dev).all()
+
+
+def test_library_is_the_native_one():
+    import os
+    ffs = _ffs()
+    L = ffs.load()
+    assert os.path.dirname(ffs.lib_path()).endswith("paper_2109_07358_b200")
+    U = inputs.random_orthonormal(256, 32, 3)
+    run_gpu(U, inputs.uniforms(16, 32, 3), 32)
+    assert L.ffs_last_launch_count() >= 1
