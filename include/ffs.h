@@ -79,6 +79,13 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, i
 /* Number of kernel launches the last successful sampling call on this thread issued. */
 int ffs_last_launch_count(void);
 
+/* Measurement hooks (bench.py): when enabled, each device sampling call records CUDA events on
+ * its stream immediately before and after its dominant kernel (the per-sample sampling kernel);
+ * ffs_last_kernel_ms() waits for the last call's end event and returns the elapsed milliseconds
+ * (-1 if none). Per calling thread. */
+int ffs_profile_enable(int on);
+float ffs_last_kernel_ms(void);
+
 /* Thread-local message for the last non-OK return on this thread ("" if none). */
 const char* ffs_last_error(void);
 

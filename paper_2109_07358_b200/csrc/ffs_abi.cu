@@ -4,15 +4,38 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <algorithm>
 
 #include "ffs.h"
 #include "ffs_kernel.cuh"
+#include "ffs_warp_kernel.cuh"
 
 namespace {
 
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
+
+// Optional CUDA-event timing of the dominant (sampling) kernel of each call, on the launch stream.
+thread_local bool g_prof = false;
+thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
+thread_local bool g_ev_pending = false;
+
+cudaError_t launch_timed(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+  if (g_prof) {
+    if (!g_ev0) {
+      cudaEventCreate(&g_ev0);
+      cudaEventCreate(&g_ev1);
+    }
+    cudaEventRecord(g_ev0, s);
+  }
+  cudaError_t e = cudaLaunchKernel(fn, grid, block, args, smem, s);
+  if (g_prof && e == cudaSuccess) {
+    cudaEventRecord(g_ev1, s);
+    g_ev_pending = true;
+  }
+  return e;
+}
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -161,11 +184,132 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
   return FFS_OK;
 }
 
+// ------------------------------------------------------------------ fast warp-owner path
+// Real U, L <= 256, N' <= kMaxNpWarp, U^T small enough for shared memory: ffs_warp_kernel
+// (one CTA per SM, warps = sample owners) after ffs_permute_kernel.
+struct WarpPlan {
+  const void* fn;
+  int R, B, S, maxt, warps, grid, Lp, ut_stride;
+  size_t ushared, owner, smem, ws_perm;
+  int perm_tpb;
+  size_t perm_smem;
+};
+
+template <int R, int B, int S, int MAXREG>
+void warp_fn_r(WarpPlan& w) {
+  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_warp_kernel_r<R, B, S, MAXREG>);
+  w.R = R;
+  w.B = B;
+  w.S = S;
+  w.maxt = 4 * 32 * (16384 / (32 * MAXREG));  // per-SMSP register file: 16K regs
+}
+
+template <int R, int B, int S, int MAXT>
+void warp_fn(WarpPlan& w) {
+  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_warp_kernel<R, B, S, MAXT>);
+  w.R = R;
+  w.B = B;
+  w.S = S;
+  w.maxt = MAXT;
+}
+
+bool warp_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
+  if (dtype != FFS_F64 || L > 256 || Np > ffsk::kMaxNpWarp || N > 4096) return false;
+  const int R = L <= 64 ? 2 : (L <= 128 ? 4 : 8);
+  return (size_t)N * (32 * R + 2) * 8 <= 100 * 1024;
+}
+
+int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
+  const char* var = getenv("FFS_WARP_VARIANT");  // development: "b6" selects B=6 for R=8
+  if (L <= 64) warp_fn<2, 8, 1, 384>(w);
+  else if (L <= 128) warp_fn<4, 8, 1, 384>(w);
+  else if (var && strcmp(var, "b8") == 0) warp_fn<8, 8, 1, 256>(w);
+  else if (var && strcmp(var, "b8r168") == 0) warp_fn_r<8, 8, 1, 168>(w);
+  else if (var && strcmp(var, "s2") == 0) warp_fn<8, 4, 2, 256>(w);
+  else warp_fn<8, 4, 1, 512>(w);  // fastest measured on B200 (profiles/)
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(FFS_ECUDA, "cudaGetDevice failed");
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, w.fn) != cudaSuccess) return fail(FFS_ECUDA, "cudaFuncGetAttributes failed");
+  w.Lp = 32 * w.R;
+  w.ut_stride = w.Lp + 2;
+  w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
+  w.owner = ffsk::WarpLayout((int)Np, w.B).total;  // per sample; a warp holds S slices
+  // registers are allocated per SM sub-partition (4 x 16K); warps are spread round-robin
+  const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
+  int warps = std::min(w.maxt / 32, by_regs);
+  while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
+  w.warps = warps;
+  w.smem = w.ushared + (size_t)warps * w.S * w.owner;
+  if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
+  const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
+  w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
+  w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
+  w.perm_tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
+  w.perm_smem = (size_t)w.perm_tpb * N * 4;
+  return FFS_OK;
+}
+
+int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, const double* uniforms,
+                int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
+                double* trace) {
+  WarpPlan w;
+  int rc = make_warp_plan(L, N, Np, M, w);
+  if (rc != FFS_OK) return rc;
+  if (!ws || ws_bytes < w.ws_perm) return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, w.ws_perm);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  int32_t* perm = static_cast<int32_t*>(ws);
+  const int64_t pgrid = (M + w.perm_tpb - 1) / w.perm_tpb;
+  ffsk::ffs_permute_kernel<<<(unsigned)pgrid, w.perm_tpb, w.perm_smem, stream>>>(uniforms, perm, M, (int)N, (int)Np);
+  ++g_launches;
+  if (cudaFuncSetAttribute(w.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.smem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem=%zu) failed", w.smem);
+  ffsk::WarpParams p{};
+  p.U = static_cast<const double*>(U);
+  p.perm = perm;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.M = M;
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  p.Lp = w.Lp;
+  p.ut_stride = w.ut_stride;
+  p.ushared = w.ushared;
+  p.owner_bytes = w.owner;
+  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.trace = S > 0 ? trace : nullptr;
+  void* args[] = {&p};
+  cudaError_t e = launch_timed(w.fn, dim3(w.grid), dim3(32 * w.warps), args, w.smem, stream);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  ++g_launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  g_err[0] = 0;
+  return FFS_OK;
+}
+
+bool use_warp_path(int64_t L, int64_t N, int64_t Np, int dtype) {
+  const char* g = getenv("FFS_FORCE_GENERIC");
+  if (g && g[0] == '1') return false;
+  return warp_eligible(L, N, Np, dtype);
+}
+
 int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
            int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
            double* trace) {
   g_launches = 0;
   if (M == 0) return FFS_OK;
+  if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0)
+    return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M=%lld", (long long)L, (long long)N,
+                (long long)Np, (long long)M);
+  if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
+  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions with M=%lld", (long long)M);
+  if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
+  if (use_warp_path(L, N, Np, dtype))
+    return launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   Plan pl;
   int rc = make_plan(L, N, Np, dtype, M, pl);
   if (rc != FFS_OK) return rc;
@@ -202,7 +346,7 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
     ++g_launches;
   }
   void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(pl.v.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, stream);
+  cudaError_t e = launch_timed(pl.v.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, stream);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
   ++g_launches;
   e = cudaGetLastError();
@@ -216,6 +360,11 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
 extern "C" {
 
 size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M) {
+  if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && use_warp_path(L, N, Nprime, dtype)) {
+    WarpPlan w;
+    if (make_warp_plan(L, N, Nprime, std::max<int64_t>(M, 1), w) != FFS_OK) return 0;
+    return w.ws_perm;
+  }
   Plan pl;
   if (make_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), pl) != FFS_OK) return 0;
   return pl.ws_ut + pl.ws_wfull;
@@ -261,9 +410,9 @@ bool host_layout(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HostLay
   for (int b = 0; b < 2; ++b) { h.pos[b] = o; o = align_up(o + (size_t)h.chunk * Np * 4); }
   for (int b = 0; b < 2; ++b) { h.flg[b] = o; o = align_up(o + (size_t)h.chunk * 4); }
   h.ws = o;
-  Plan pl;
-  if (make_plan(L, N, Np, dtype, h.chunk, pl) != FFS_OK) return false;
-  o += pl.ws_ut + pl.ws_wfull;
+  const size_t need = ffs_workspace_bytes(L, N, Np, dtype, h.chunk);
+  if (need == 0) return false;
+  o += need;
   h.total = o;
   return true;
 }
@@ -313,6 +462,20 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, i
 }
 
 int ffs_last_launch_count(void) { return g_launches; }
+
+int ffs_profile_enable(int on) {
+  g_prof = on != 0;
+  g_ev_pending = false;
+  return FFS_OK;
+}
+
+float ffs_last_kernel_ms(void) {
+  if (!g_ev_pending) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventSynchronize(g_ev1) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, g_ev0, g_ev1) != cudaSuccess) return -1.0f;
+  return ms;
+}
 
 const char* ffs_last_error(void) { return g_err; }
 

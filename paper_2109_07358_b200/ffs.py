@@ -25,6 +25,8 @@ EXPORTED = (
     "ffs_host_workspace_bytes",
     "ffs_sample_host",
     "ffs_last_launch_count",
+    "ffs_profile_enable",
+    "ffs_last_kernel_ms",
     "ffs_last_error",
 )
 
@@ -60,6 +62,8 @@ def load(build_if_missing: bool = True):
     L.ffs_host_workspace_bytes.restype = sz
     L.ffs_sample_host.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp]
     L.ffs_last_launch_count.restype = ci
+    L.ffs_profile_enable.argtypes = [ci]
+    L.ffs_last_kernel_ms.restype = ctypes.c_float
     L.ffs_last_error.restype = ctypes.c_char_p
     _lib = L
     return L
@@ -94,6 +98,14 @@ def ffs_host_workspace_bytes(L: int, N: int, Nprime: int, dtype: int, M: int) ->
 
 def ffs_last_launch_count() -> int:
     return int(load().ffs_last_launch_count())
+
+
+def ffs_profile_enable(on: bool = True) -> None:
+    load().ffs_profile_enable(1 if on else 0)
+
+
+def ffs_last_kernel_ms() -> float:
+    return float(load().ffs_last_kernel_ms())
 
 
 class Workspace:
