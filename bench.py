@@ -260,7 +260,7 @@ def run_gpu(args):
             "weight_gflops": value * weight_flops(cfg.L, Np, cplx) / 1e9,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                         "kernel": "ffs_warp_kernel" if ffs_uses_warp(cfg, Np, cplx) else "ffs_sample_kernel",
+                         "kernel": "ffs_seg_kernel" if ffs_uses_warp(cfg, Np, cplx) else "ffs_sample_kernel",
                          "kernel_ms": kms, "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"},
             "gpu_launches": launches,
             "sample_flags_nonzero": flags_bad,

@@ -20,6 +20,7 @@ thread_local int g_launches = 0;
 thread_local bool g_prof = false;
 thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
 thread_local bool g_ev_pending = false;
+unsigned long long* g_timing = nullptr;  // development: device counters for FFS_DEBUG_SKIP bit3
 
 cudaError_t launch_timed(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
   if (g_prof) {
@@ -189,11 +190,21 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
 // (one CTA per SM, warps = sample owners) after ffs_permute_kernel.
 struct WarpPlan {
   const void* fn;
-  int R, B, S, maxt, warps, grid, Lp, ut_stride;
+  int R, B, S, G = 32, maxt, warps, grid, Lp, ut_stride;
   size_t ushared, owner, smem, ws_perm;
   int perm_tpb;
   size_t perm_smem;
 };
+
+template <int R, int B, int G, int MAXT, bool TIMING = false>
+void warp_fn_seg(WarpPlan& w) {
+  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_seg_kernel<R, B, G, MAXT, TIMING>);
+  w.R = R;
+  w.B = B;
+  w.S = 32 / G;  // samples per warp (one per G-lane segment)
+  w.G = G;
+  w.maxt = MAXT;
+}
 
 template <int R, int B, int S, int MAXREG>
 void warp_fn_r(WarpPlan& w) {
@@ -215,24 +226,37 @@ void warp_fn(WarpPlan& w) {
 
 bool warp_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   if (dtype != FFS_F64 || L > 256 || Np > ffsk::kMaxNpWarp || N > 4096) return false;
-  const int R = L <= 64 ? 2 : (L <= 128 ? 4 : 8);
-  return (size_t)N * (32 * R + 2) * 8 <= 100 * 1024;
+  return (size_t)N * (256 + 2) * 8 <= 100 * 1024;  // padded U^T fits shared memory
 }
 
 int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   const char* var = getenv("FFS_WARP_VARIANT");  // development: "b6" selects B=6 for R=8
-  if (L <= 64) warp_fn<2, 8, 1, 384>(w);
+  const bool legacy = var && strncmp(var, "w", 1) == 0;  // "w..." = whole-warp owner variants
+  if (!legacy) {
+    if (L <= 16) warp_fn_seg<2, 4, 8, 512>(w);
+    else if (L <= 32) warp_fn_seg<4, 4, 8, 512>(w);
+    else if (L <= 64) warp_fn_seg<8, 4, 8, 512>(w);
+    else if (L <= 128) warp_fn_seg<8, 4, 16, 512>(w);
+    else if (var && strcmp(var, "seg16b4r168") == 0) warp_fn_seg<16, 4, 16, 384>(w);
+    else if (var && strcmp(var, "seg16b4r128") == 0) warp_fn_seg<16, 4, 16, 512>(w);
+    else if (var && strcmp(var, "seg32b4") == 0) warp_fn_seg<8, 4, 32, 512>(w);
+    else if (var && strcmp(var, "seg32b4r168") == 0) warp_fn_seg<8, 4, 32, 384>(w);
+    else if (var && strcmp(var, "seg32b8") == 0) warp_fn_seg<8, 8, 32, 256>(w);
+    else if (var && strcmp(var, "seg32b4t") == 0) warp_fn_seg<8, 4, 32, 512, true>(w);
+    else if (var && strcmp(var, "seg16b4t") == 0) warp_fn_seg<16, 4, 16, 256, true>(w);
+    else warp_fn_seg<8, 4, 32, 384>(w);  // 12 sample-owning warps/SM, 164 regs (profiles/)
+  } else if (L <= 64) warp_fn<2, 8, 1, 384>(w);
   else if (L <= 128) warp_fn<4, 8, 1, 384>(w);
-  else if (var && strcmp(var, "b8") == 0) warp_fn<8, 8, 1, 256>(w);
-  else if (var && strcmp(var, "b8r168") == 0) warp_fn_r<8, 8, 1, 168>(w);
-  else if (var && strcmp(var, "s2") == 0) warp_fn<8, 4, 2, 256>(w);
+  else if (var && strcmp(var, "wb8") == 0) warp_fn<8, 8, 1, 256>(w);
+  else if (var && strcmp(var, "wb8r168") == 0) warp_fn_r<8, 8, 1, 168>(w);
+  else if (var && strcmp(var, "ws2") == 0) warp_fn<8, 4, 2, 256>(w);
   else warp_fn<8, 4, 1, 512>(w);  // fastest measured on B200 (profiles/)
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(FFS_ECUDA, "cudaGetDevice failed");
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, w.fn) != cudaSuccess) return fail(FFS_ECUDA, "cudaFuncGetAttributes failed");
-  w.Lp = 32 * w.R;
+  w.Lp = w.G * w.R;
   w.ut_stride = w.Lp + 2;
   w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
   w.owner = ffsk::WarpLayout((int)Np, w.B).total;  // per sample; a warp holds S slices
@@ -240,6 +264,7 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
   int warps = std::min(w.maxt / 32, by_regs);
   while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
+  if (const char* fw = getenv("FFS_WARPS")) warps = std::max(1, std::min(warps, atoi(fw)));  // development
   w.warps = warps;
   w.smem = w.ushared + (size_t)warps * w.S * w.owner;
   if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
@@ -281,6 +306,9 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   p.owner_bytes = w.owner;
   p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
   p.trace = S > 0 ? trace : nullptr;
+  const char* dbg = getenv("FFS_DEBUG_SKIP");  // development only: bits 0-2 break the results
+  p.dbg = dbg ? atoi(dbg) : 0;
+  p.timing = g_timing;
   void* args[] = {&p};
   cudaError_t e = launch_timed(w.fn, dim3(w.grid), dim3(32 * w.warps), args, w.smem, stream);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
@@ -400,7 +428,7 @@ struct HostLayout {
   size_t u, uni[2], pos[2], flg[2], ws, total;
   int64_t chunk;
 };
-int64_t host_chunk(int64_t M) { return std::max<int64_t>(1, std::min<int64_t>(M, 16384)); }
+int64_t host_chunk(int64_t M) { return std::max<int64_t>(1, std::min<int64_t>(M, M > 32768 ? 16384 : M)); }
 bool host_layout(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HostLayout& h) {
   const size_t es = dtype == FFS_C128 ? 16 : 8;
   h.chunk = host_chunk(M);
@@ -424,6 +452,32 @@ size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype,
   return h.total;
 }
 
+// Three-stage pipeline over sample chunks, double-buffered in the workspace: copy-in stream
+// (U once, then uniforms of chunk c) -> caller's stream (sampling of chunk c) -> copy-out stream
+// (positions/flags of chunk c). Chunk c+1's upload and chunk c-1's download overlap chunk c's
+// kernels. Streams/events are created once per host thread (no device memory is allocated).
+namespace {
+struct HostPipe {
+  cudaStream_t ci = nullptr, co = nullptr;
+  cudaEvent_t entry, in_ready[2], done[2], out_done[2];
+  bool ok = false;
+  bool init() {
+    if (ok) return true;
+    if (cudaStreamCreateWithFlags(&ci, cudaStreamNonBlocking) != cudaSuccess) return false;
+    if (cudaStreamCreateWithFlags(&co, cudaStreamNonBlocking) != cudaSuccess) return false;
+    if (cudaEventCreateWithFlags(&entry, cudaEventDisableTiming) != cudaSuccess) return false;
+    for (int b = 0; b < 2; ++b) {
+      if (cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming) != cudaSuccess) return false;
+      if (cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) return false;
+      if (cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming) != cudaSuccess) return false;
+    }
+    ok = true;
+    return true;
+  }
+};
+thread_local HostPipe g_pipe;
+}  // namespace
+
 int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
                     const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
                     size_t ws_bytes, void* stream) {
@@ -432,36 +486,62 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, i
   if (!host_layout(L, N, Nprime, dtype, M, h)) return FFS_EINVAL;
   if (!U || !uniforms || !positions || !workspace || ws_bytes < h.total)
     return fail(FFS_EINVAL, "host path: null pointer or workspace %zu < %zu", ws_bytes, h.total);
+  if (!g_pipe.init()) return fail(FFS_ECUDA, "host path: stream/event creation failed");
   cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+  HostPipe& hp = g_pipe;
   char* w = static_cast<char*>(workspace);
   const size_t es = dtype == FFS_C128 ? 16 : 8;
   const int64_t Np = Nprime;
   int launches = 0;
-  cudaError_t e = cudaMemcpyAsync(w + h.u, U, (size_t)L * N * es, cudaMemcpyHostToDevice, s0);
-  if (e != cudaSuccess) return fail(FFS_ECUDA, "H2D U: %s", cudaGetErrorString(e));
-  for (int64_t c0 = 0, b = 0; c0 < M; c0 += h.chunk, b ^= 1) {
+  cudaError_t e = cudaSuccess;
+#define FFS_CK(x, what) do { e = (x); if (e != cudaSuccess) return fail(FFS_ECUDA, "%s: %s", what, cudaGetErrorString(e)); } while (0)
+  FFS_CK(cudaEventRecord(hp.entry, s0), "record");          // prior work on the caller's stream
+  FFS_CK(cudaStreamWaitEvent(hp.ci, hp.entry, 0), "wait");
+  FFS_CK(cudaMemcpyAsync(w + h.u, U, (size_t)L * N * es, cudaMemcpyHostToDevice, hp.ci), "H2D U");
+  const int64_t nchunks = (M + h.chunk - 1) / h.chunk;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t c0 = c * h.chunk;
     const int64_t mc = std::min<int64_t>(h.chunk, M - c0);
-    e = cudaMemcpyAsync(w + h.uni[b], uniforms + c0 * 2 * Np, (size_t)mc * 2 * Np * 8, cudaMemcpyHostToDevice, s0);
-    if (e != cudaSuccess) return fail(FFS_ECUDA, "H2D uniforms: %s", cudaGetErrorString(e));
+    if (c >= 2) FFS_CK(cudaStreamWaitEvent(hp.ci, hp.done[b], 0), "wait");  // uniforms[b] consumed
+    FFS_CK(cudaMemcpyAsync(w + h.uni[b], uniforms + c0 * 2 * Np, (size_t)mc * 2 * Np * 8, cudaMemcpyHostToDevice,
+                           hp.ci), "H2D uniforms");
+    FFS_CK(cudaEventRecord(hp.in_ready[b], hp.ci), "record");
+    FFS_CK(cudaStreamWaitEvent(s0, hp.in_ready[b], 0), "wait");
+    if (c >= 2) FFS_CK(cudaStreamWaitEvent(s0, hp.out_done[b], 0), "wait");  // positions[b] drained
     int rc = launch(w + h.u, L, N, dtype, mc, Np, reinterpret_cast<const double*>(w + h.uni[b]),
                     reinterpret_cast<int32_t*>(w + h.pos[b]), reinterpret_cast<int32_t*>(w + h.flg[b]), w + h.ws,
                     h.total - h.ws, s0, 0, nullptr);
     if (rc != FFS_OK) return rc;
     launches += g_launches;
-    e = cudaMemcpyAsync(positions + c0 * Np, w + h.pos[b], (size_t)mc * Np * 4, cudaMemcpyDeviceToHost, s0);
-    if (e != cudaSuccess) return fail(FFS_ECUDA, "D2H positions: %s", cudaGetErrorString(e));
-    if (sample_flags) {
-      e = cudaMemcpyAsync(sample_flags + c0, w + h.flg[b], (size_t)mc * 4, cudaMemcpyDeviceToHost, s0);
-      if (e != cudaSuccess) return fail(FFS_ECUDA, "D2H flags: %s", cudaGetErrorString(e));
-    }
+    FFS_CK(cudaEventRecord(hp.done[b], s0), "record");
+    FFS_CK(cudaStreamWaitEvent(hp.co, hp.done[b], 0), "wait");
+    FFS_CK(cudaMemcpyAsync(positions + c0 * Np, w + h.pos[b], (size_t)mc * Np * 4, cudaMemcpyDeviceToHost, hp.co),
+           "D2H positions");
+    if (sample_flags)
+      FFS_CK(cudaMemcpyAsync(sample_flags + c0, w + h.flg[b], (size_t)mc * 4, cudaMemcpyDeviceToHost, hp.co),
+             "D2H flags");
+    FFS_CK(cudaEventRecord(hp.out_done[b], hp.co), "record");
   }
-  e = cudaStreamSynchronize(s0);
-  if (e != cudaSuccess) return fail(FFS_ECUDA, "host path sync: %s", cudaGetErrorString(e));
+  FFS_CK(cudaStreamSynchronize(hp.co), "host path sync");
+  FFS_CK(cudaStreamSynchronize(s0), "host path sync");
+#undef FFS_CK
   g_launches = launches;
   return FFS_OK;
 }
 
 int ffs_last_launch_count(void) { return g_launches; }
+
+// development only (not in ffs.h): per-phase clock64 sums of the segmented warp kernel
+int ffs_dev_timing(unsigned long long* host8, int reset) {
+  if (!g_timing) {
+    if (cudaMalloc(&g_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return FFS_ECUDA;
+    cudaMemset(g_timing, 0, 8 * sizeof(unsigned long long));
+  }
+  if (host8) cudaMemcpy(host8, g_timing, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (reset) cudaMemset(g_timing, 0, 8 * sizeof(unsigned long long));
+  return FFS_OK;
+}
 
 int ffs_profile_enable(int on) {
   g_prof = on != 0;

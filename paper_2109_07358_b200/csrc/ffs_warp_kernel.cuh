@@ -24,7 +24,7 @@ namespace ffsk {
 constexpr int kMaxNpWarp = 48;
 
 struct WarpLayout {
-  size_t perm, pos, usel, row, pinv, wf, vnt, total;
+  size_t perm, pos, usel, row, pinv, wf, vnt, dump, total;
   int ldw;  // row stride of W: Np + B rounded to even; columns [Np, ldw) stay zero
   __host__ __device__ WarpLayout(int Np, int B) {
     ldw = (Np + B + 1) & ~1;
@@ -36,6 +36,7 @@ struct WarpLayout {
     pinv = o; o = align16(o + sizeof(double) * B);
     wf = o;   o = align16(o + sizeof(double) * (size_t)Np * ldw);
     vnt = o;  o = align16(o + sizeof(double) * (size_t)Np * B);
+    dump = o; o = align16(o + sizeof(double) * 16 * 8);  // owner lane's R x B panel (R<=16, B<=8)
     total = o;
   }
 };
@@ -51,6 +52,9 @@ struct WarpParams {
   size_t ushared, owner_bytes;
   int64_t S;
   double* trace;          // [S][Np][L] or null
+  int dbg;                // development: bit0 skip GEMM, bit1 trivial draws, bit2 skip GJ (WRONG results),
+                          // bit3 per-phase clock64 accounting into timing[0..7]
+  unsigned long long* timing;
 };
 
 // Result of the branch-free part of a draw.
@@ -456,6 +460,439 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_warp_kernel(const WarpParams p) {
 template <int R, int B, int S, int MAXREG>
 __global__ void __maxnreg__(MAXREG) ffs_warp_kernel_r(const WarpParams p) {
   ffs_warp_body<R, B, S>(p);
+}
+
+
+// =====================================================================================
+// Segmented warp kernel: a warp is split into 32/G segments of G lanes, one sample per segment.
+// Warp-wide instructions (scan levels, ballots, broadcasts, shared loads, the reciprocal of the
+// pivot) then serve 32/G samples at once, and the register file holds 32/G panels per warp.
+// Lane s of a segment owns rows s*R .. s*R+R-1 of its sample (index order = scan order).
+// =====================================================================================
+// 1/a to ~1 ulp: hardware approximation + two Newton steps (no slow path; pivots are normal)
+__device__ __forceinline__ double fast_rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+template <int G>
+struct SegOps {
+  static constexpr unsigned kUpC = (unsigned)(32 - G) << 8;         // shfl.up segment control
+  static constexpr unsigned kIdxC = ((unsigned)(32 - G) << 8) | 31u;  // shfl.idx segment control
+  // v + (value of segment lane - d) for segment lanes >= d
+  __device__ __forceinline__ static double scan_level(double v, int d) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, ylo, yhi;\n\t.reg .f64 y;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "shfl.sync.up.b32 ylo|p, lo, %1, %2, -1;\n\t"
+        "shfl.sync.up.b32 yhi, hi, %1, %2, -1;\n\t"
+        "mov.b64 y, {ylo, yhi};\n\t"
+        "@p add.f64 %0, %0, y;\n\t}"
+        : "+d"(v) : "r"(d), "r"(kUpC));
+    return v;
+  }
+  // value of segment lane - 1, 0 for the first segment lane
+  __device__ __forceinline__ static double prev(double v) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, ylo, yhi;\n\t"
+        "mov.b64 {lo, hi}, %1;\n\t"
+        "shfl.sync.up.b32 ylo|p, lo, 1, %2, -1;\n\t"
+        "shfl.sync.up.b32 yhi, hi, 1, %2, -1;\n\t"
+        "mov.b64 %0, {ylo, yhi};\n\t"
+        "@!p mov.f64 %0, 0d0000000000000000;\n\t}"
+        : "=d"(r) : "d"(v), "r"(kUpC));
+    return r;
+  }
+  // value of the last lane of the segment
+  __device__ __forceinline__ static double last(double v) {
+    double r;
+    asm("{\n\t.reg .b32 lo, hi, ylo, yhi;\n\t"
+        "mov.b64 {lo, hi}, %1;\n\t"
+        "shfl.sync.idx.b32 ylo, lo, %2, %3, -1;\n\t"
+        "shfl.sync.idx.b32 yhi, hi, %2, %3, -1;\n\t"
+        "mov.b64 %0, {ylo, yhi};\n\t}"
+        : "=d"(r) : "d"(v), "r"(G - 1), "r"(kIdxC));
+    return r;
+  }
+};
+
+// Branch-free part of a draw for one segment (see draw_part1): returns the crossing lanes of
+// this lane's segment (bit i = segment lane i), the crossing row in this lane, and T.
+template <int R, int G>
+__device__ __forceinline__ Draw seg_draw(const double (&col)[R], double u, int seg) {
+  // Pass 1: lane total of w_r = col_r^2 (index order; for R > 8 two parallel half chains).
+  constexpr int H = R > 8 ? R / 2 : R;
+  double h1 = col[0] * col[0];
+#pragma unroll
+  for (int r = 1; r < H; ++r) h1 = fma(col[r], col[r], h1);
+  double tot = h1;
+  double h2 = 0.0;
+  if constexpr (R > 8) {
+    h2 = col[H] * col[H];
+#pragma unroll
+    for (int r = H + 1; r < R; ++r) h2 = fma(col[r], col[r], h2);
+    tot = h1 + h2;
+  }
+  double incl = tot;
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) incl = SegOps<G>::scan_level(incl, d);
+  const double excl = SegOps<G>::prev(incl);
+  Draw d;
+  d.T = SegOps<G>::last(incl);
+  const bool ok = (d.T > 0.0) && (d.T < INFINITY);
+  // crossing threshold relative to this lane's exclusive prefix, clamped at 0 so that a lane
+  // whose rounded prefix already passed u*T still lands on its first positive weight
+  const double tp = fmax(fma(u, d.T, -excl), 0.0);
+  const unsigned b = __ballot_sync(0xffffffffu, ok && (tot > tp));
+  d.ball = (G == 32) ? b : ((b >> (seg * G)) & ((1u << G) - 1u));
+  // Pass 2: the same partial sums again (bit-identical), count rows with C_r <= tp (r < R-1).
+  unsigned m = 0;
+  double a = col[0] * col[0];
+  m |= (a <= tp) ? 1u : 0u;
+#pragma unroll
+  for (int r = 1; r < H && r < R - 1; ++r) {
+    a = fma(col[r], col[r], a);
+    m |= (a <= tp) ? (1u << r) : 0u;
+  }
+  if constexpr (R > 8) {
+    double bb = col[H] * col[H];
+    m |= (h1 + bb <= tp) ? (1u << H) : 0u;
+#pragma unroll
+    for (int r = H + 1; r < R - 1; ++r) {
+      bb = fma(col[r], col[r], bb);
+      m |= (h1 + bb <= tp) ? (1u << r) : 0u;
+    }
+  }
+  d.rsel = __popc(m);
+  return d;
+}
+
+// Rare paths for one segment; every lane of the warp calls it (segments may differ).
+template <int R, int G>
+__device__ __noinline__ int seg_fallback(const double* col, double T, uint32_t chosen, int L, int sl, int seg) {
+  const bool ok = (T > 0.0) && isfinite(T);
+  int rl = -1, rf = R;
+  for (int r = 0; r < R; ++r) {
+    if (col[r] * col[r] > 0.0) rl = r;
+    if (rf == R && sl * R + r < L && !((chosen >> r) & 1u)) rf = r;
+  }
+  const unsigned mseg = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (seg * G));
+  const unsigned bl = __ballot_sync(0xffffffffu, rl >= 0) & mseg;
+  const unsigned bf = __ballot_sync(0xffffffffu, rf < R) & mseg;
+  int ln, rr;
+  if (ok && bl) {  // largest x with w(x) > 0
+    ln = 31 - __clz(bl);
+    rr = __shfl_sync(0xffffffffu, rl, ln);
+  } else {         // smallest unchosen site
+    ln = __ffs(bf) - 1;
+    rr = __shfl_sync(0xffffffffu, rf, ln);
+  }
+  return (ln - seg * G) * R + rr;
+}
+
+template <int R, int B, int G, bool TIMING>
+__device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using Sw = Swz<double, R>;
+  constexpr int SEGS = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int seg = lane / G, sl = lane % G;
+  const int L = p.L, N = p.N, Np = p.Np;
+  const int stride = p.ut_stride;
+
+  // ---- U^T into shared memory (swizzled 16-byte chunks; rows >= L zero)
+  double* Uts = reinterpret_cast<double*>(smem);
+  for (int idx = threadIdx.x; idx < N * p.Lp; idx += blockDim.x) {
+    const int x = idx / N, c = idx % N;
+    Uts[(size_t)c * stride + Sw::phys(x)] = (x < L) ? p.U[(size_t)x * N + c] : 0.0;
+  }
+  __syncthreads();
+
+  const WarpLayout lay(Np, B);
+  const int ldw = lay.ldw;
+  unsigned char* ob = smem + p.ushared + (size_t)(wid * SEGS + seg) * p.owner_bytes;
+  int* perm = reinterpret_cast<int*>(ob + lay.perm);
+  int* pos = reinterpret_cast<int*>(ob + lay.pos);
+  double* usel = reinterpret_cast<double*>(ob + lay.usel);
+  double* Row = reinterpret_cast<double*>(ob + lay.row);
+  double* Pinv = reinterpret_cast<double*>(ob + lay.pinv);
+  double* Wf = reinterpret_cast<double*>(ob + lay.wf);
+  double* VnT = reinterpret_cast<double*>(ob + lay.vnt);
+  double* Dump = reinterpret_cast<double*>(ob + lay.dump);
+  const int sw = Sw::sw(sl);
+  const double* Ucol0 = Uts + sl * R;
+  int qoff[R / 2];  // swizzled 16-byte chunk offsets of this lane's rows within a column
+#pragma unroll
+  for (int q = 0; q < R / 2; ++q) qoff[q] = (q ^ sw) << 1;
+  for (int idx = sl; idx < Np * ldw; idx += G) Wf[idx] = 0.0;  // padding columns stay 0
+  for (int idx = sl; idx < B * B; idx += G) Row[idx] = 0.0;
+  __syncwarp();
+
+  const int64_t ngroups = (p.M + SEGS - 1) / SEGS;
+  long long tacc[TIMING ? 8 : 1] = {0};  // development timing
+  for (int64_t g = (int64_t)blockIdx.x * nwarps + wid; g < ngroups; g += (int64_t)gridDim.x * nwarps) {
+    const int64_t id = g * SEGS + seg;
+    const int64_t i = id < p.M ? id : p.M - 1;  // a short last group recomputes a sample
+    for (int j = sl; j < Np; j += G) {
+      perm[j] = p.perm[i * Np + j];
+      usel[j] = p.uniforms[i * 2 * (int64_t)Np + Np + j];
+    }
+    __syncwarp();
+    uint32_t chosen = 0;
+    int flag = 0;
+    constexpr bool tm = TIMING;  // development: per-phase clock64 accounting (separate instance)
+    long long tA = 0;
+    if constexpr (tm) tA = clock64();
+
+    for (int k0 = 0; k0 < Np; k0 += B) {
+      const int nb = min(B, Np - k0);
+      // ---- a3 panel: P = V[:, k0:k0+B] - V[:, 0:k0] Wb  (Wb = Wf[0:k0][k0:k0+B], smem)
+      double P[R][B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const double* cb = Ucol0 + perm[min(k0 + c, Np - 1)] * stride;
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) {
+          const double2 d = *reinterpret_cast<const double2*>(cb + qoff[q]);
+          P[2 * q][c] = (c < nb) ? d.x : 0.0;
+          P[2 * q + 1][c] = (c < nb) ? d.y : 0.0;
+        }
+      }
+      {
+        const int kend = (p.dbg & 1) ? 0 : k0;
+        const double* wrow = Wf + k0;
+#pragma unroll 2
+        for (int ii = 0; ii < kend; ++ii, wrow += ldw) {
+          const double* cb = Ucol0 + perm[ii] * stride;
+          double wb[B];
+#pragma unroll
+          for (int c = 0; c < B; c += 2) {
+            const double2 d = *reinterpret_cast<const double2*>(wrow + c);
+            wb[c] = d.x;
+            wb[c + 1] = d.y;
+          }
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            const double2 d = *reinterpret_cast<const double2*>(cb + qoff[q]);
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+              P[2 * q][c] = fma(-d.x, wb[c], P[2 * q][c]);
+              P[2 * q + 1][c] = fma(-d.y, wb[c], P[2 * q + 1][c]);
+            }
+          }
+        }
+      }
+      // rows drawn in earlier blocks: exactly zero (the contraction leaves O(eps) residues)
+      // rows drawn earlier get weight exactly 0: mask the column of the next draw (only that
+      // column is ever squared; the contraction leaves O(eps) residues in drawn rows)
+#pragma unroll
+      for (int r = 0; r < R; ++r) P[r][0] = ((chosen >> r) & 1u) ? 0.0 : P[r][0];
+      if constexpr (tm) {
+        const long long t = clock64();
+        tacc[0] += (t - tA);
+        tA = t;
+      }
+
+      // ---- a4/a5: nb sequential draws on the panel, one-column lookahead
+      Draw dr;
+      {
+        double col0[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) col0[r] = P[r][0];
+        if (p.dbg & 2) { dr.ball = 1u; dr.rsel = (k0 / B) % R; dr.T = 1.0; }
+        else dr = seg_draw<R, G>(col0, usel[k0], seg);
+      }
+      static_for<0, B>([&](auto rrc) {
+        constexpr int rr = decltype(rrc)::value;
+        if (rr < nb) {
+          const int k = k0 + rr;
+          long long ts0 = 0;
+          if constexpr (tm) ts0 = clock64();
+          int own, orow;  // owner lane within the segment, row within the owner
+          if (__all_sync(0xffffffffu, dr.ball != 0u)) {
+            own = __ffs(dr.ball) - 1;
+            orow = __shfl_sync(0xffffffffu, dr.rsel, seg * G + own);
+          } else {
+            // rare: some segment has u*T at/after its last partial sum, or T not finite/positive
+            int o = 0, rw = 0;
+            if (dr.ball != 0u) {
+              o = __ffs(dr.ball) - 1;
+            }
+            rw = __shfl_sync(0xffffffffu, dr.rsel, seg * G + o);
+            double colr[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) colr[r] = P[r][rr];
+            const int xf = seg_fallback<R, G>(colr, dr.T, chosen, L, sl, seg);
+            own = dr.ball != 0u ? o : xf / R;
+            orow = dr.ball != 0u ? rw : xf % R;
+          }
+          if constexpr (tm) {
+            const long long t = clock64() + (long long)orow * 0;
+            tacc[3] += (t - ts0);
+            ts0 = t;
+          }
+          if (!((dr.T > 0.0) && isfinite(dr.T))) flag |= 1;
+          if (p.trace != nullptr && id < p.S) {
+            const double inv = dr.T > 0.0 ? 1.0 / dr.T : 0.0;
+            double* tr = p.trace + (id * Np + k) * (int64_t)L;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (sl * R + r < L) tr[sl * R + r] = P[r][rr] * P[r][rr] * inv;
+          }
+          // pivot row: every lane selects row `rs` of its own R x B block with a branch-free
+          // select tree (rs = its crossing row, or orow on the rare fallback path); the owner
+          // lane's selection is then broadcast to its segment with shuffles (no smem, no branch)
+          const double Tk = dr.T;
+          const int rs = dr.ball != 0u ? dr.rsel : orow;
+          double prow[B];
+#pragma unroll
+          for (int c = 0; c < B; ++c) {
+            double t[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) t[r] = P[r][c];
+#pragma unroll
+            for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+              for (int i = 0; i < R; i += 2 * w) t[i] = (rs & w) ? t[i + w] : t[i];
+            prow[c] = __shfl_sync(0xffffffffu, t[0], seg * G + own);
+          }
+          chosen |= (sl == own) ? (1u << orow) : 0u;
+          if (prow[rr] * prow[rr] < 1e-12 * Tk) flag |= 2;
+          if (sl == 0) {
+            pos[k] = own * R + orow;
+#pragma unroll
+            for (int c = 0; c < B; c += 2)
+              *reinterpret_cast<double2*>(Row + rr * B + c) = make_double2(prow[c], prow[c + 1]);
+          }
+          if constexpr (tm) {
+            const long long t = clock64() + (long long)(prow[0] * 0.0);
+            tacc[4] += (t - ts0);
+            ts0 = t;
+          }
+          const double ip = fast_rcp(prow[rr]);
+          if constexpr (tm) {
+            const long long t = clock64() + (long long)(ip * 0.0);
+            tacc[5] += (t - ts0);
+            ts0 = t;
+          }
+          if (sl == 0) Pinv[rr] = ip;
+          if constexpr (rr + 1 < B) {
+            double sp[B];  // pivot row scaled by 1/pivot
+#pragma unroll
+            for (int c = 0; c < B; c += 2) {
+              const double2 d = *reinterpret_cast<const double2*>(Row + rr * B + c);
+              sp[c] = d.x * ip;
+              sp[c + 1] = d.y * ip;
+            }
+            // column rr+1 first, then the next draw, then the remaining columns
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              P[r][rr + 1] = ((chosen >> r) & 1u) ? 0.0 : fma(-P[r][rr], sp[rr + 1], P[r][rr + 1]);
+            if (rr + 1 < nb) {
+              double cn[R];
+#pragma unroll
+              for (int r = 0; r < R; ++r) cn[r] = P[r][rr + 1];
+              if (p.dbg & 2) { dr.ball = 1u << ((k + 1) % G); dr.rsel = (k + 1) / G % R; dr.T = 1.0 + cn[0] * 1e-300; }
+              else dr = seg_draw<R, G>(cn, usel[k + 1], seg);
+              if constexpr (tm) {
+                const long long t = clock64() + (long long)(dr.T * 0.0) + dr.rsel * 0;
+                tacc[6] += (t - ts0);
+                ts0 = t;
+              }
+            }
+#pragma unroll
+            for (int c = rr + 2; c < B; ++c)
+#pragma unroll
+              for (int r = 0; r < R; ++r) P[r][c] = fma(-P[r][rr], sp[c], P[r][c]);
+          }
+        }
+      });
+
+      if constexpr (tm) {
+        const long long t = clock64();
+        tacc[1] += (t - tA);
+        tA = t;
+      }
+      // ---- Gauss-Jordan update of W with the nb new rows (only if later columns remain)
+      if (k0 + nb < Np && !(p.dbg & 4)) {
+        __syncwarp();
+        for (int idx = sl; idx < Np * B; idx += G) {
+          const int ii = idx / B, tt = idx % B;
+          VnT[idx] = (tt < nb) ? Uts[perm[ii] * stride + Sw::phys(pos[k0 + tt])] : 0.0;
+        }
+        __syncwarp();
+        for (int j = k0 + nb + sl; j < Np; j += G) {
+          double z[B];
+#pragma unroll
+          for (int tt = 0; tt < B; ++tt) z[tt] = VnT[j * B + tt];
+#pragma unroll 2
+          for (int ii = 0; ii < k0; ++ii) {
+            const double wij = Wf[ii * ldw + j];
+#pragma unroll
+            for (int tt = 0; tt < B; tt += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(VnT + ii * B + tt);
+              z[tt] = fma(-v.x, wij, z[tt]);
+              z[tt + 1] = fma(-v.y, wij, z[tt + 1]);
+            }
+          }
+          double ipv[B];
+#pragma unroll
+          for (int t2 = 0; t2 < B; ++t2) ipv[t2] = (t2 < nb) ? Pinv[t2] : 0.0;
+#pragma unroll
+          for (int tt = 1; tt < B; ++tt)
+#pragma unroll
+            for (int t2 = 0; t2 < tt; ++t2) z[tt] = fma(-(Row[tt * B + t2] * ipv[t2]), z[t2], z[tt]);
+#pragma unroll
+          for (int tt = B - 1; tt >= 0; --tt) {
+#pragma unroll
+            for (int t2 = tt + 1; t2 < B; ++t2) z[tt] = fma(-Row[tt * B + t2], z[t2], z[tt]);
+            z[tt] *= ipv[tt];
+          }
+#pragma unroll 2
+          for (int ii = 0; ii < k0; ++ii) {
+            double a = Wf[ii * ldw + j];
+#pragma unroll
+            for (int tt = 0; tt < B; tt += 2) {
+              const double2 wbv = *reinterpret_cast<const double2*>(Wf + ii * ldw + k0 + tt);
+              a = fma(-wbv.x, z[tt], a);
+              a = fma(-wbv.y, z[tt + 1], a);
+            }
+            Wf[ii * ldw + j] = a;
+          }
+#pragma unroll
+          for (int tt = 0; tt < B; ++tt)
+            if (tt < nb) Wf[(k0 + tt) * ldw + j] = z[tt];
+        }
+        __syncwarp();
+      }
+      if constexpr (tm) {
+        const long long t = clock64();
+        tacc[2] += (t - tA);
+        tA = t;
+      }
+    }
+    // ---- a6: positions and flags
+    unsigned fl = __reduce_or_sync(0xffffffffu, (unsigned)flag << (seg * 2));
+    if (id < p.M) {
+      for (int j = sl; j < Np; j += G) p.positions[id * Np + j] = pos[j];
+      if (sl == 0 && p.flags != nullptr) p.flags[id] = (fl >> (seg * 2)) & 3u;
+    }
+    __syncwarp();
+  }
+  if constexpr (TIMING) {
+    if (p.timing != nullptr && lane == 0)
+      for (int q = 0; q < 8; ++q) atomicAdd(p.timing + q, (unsigned long long)tacc[q]);
+  }
+}
+
+template <int R, int B, int G, int MAXT, bool TIMING = false>
+__global__ void __launch_bounds__(MAXT, 1) ffs_seg_kernel(const WarpParams p) {
+  ffs_seg_body<R, B, G, TIMING>(p);
 }
 
 }  // namespace ffsk
