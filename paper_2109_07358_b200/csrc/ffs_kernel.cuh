@@ -318,7 +318,7 @@ ffs_sample_kernel(const Params p) {
 #pragma unroll
         for (int r = 0; r < R; ++r) P[r][c] = v[r];
       }
-#pragma unroll 2
+#pragma unroll 4
       for (int ii = 0; ii < k0; ++ii) {
         T v[R];
         load_col<T, R, USMEM>(p, Uts, perm[ii], t, v);
@@ -391,7 +391,19 @@ ffs_sample_kernel(const Params p) {
           T z[B];
 #pragma unroll
           for (int tt = 0; tt < B; ++tt) z[tt] = tt < nb ? Vnew[tt * Np + j] : S::zero();
-          for (int ii = 0; ii < k0; ++ii) {
+          // R_new = V[X_new, j] - V[X_new, 0:k0] W[0:k0, j]; 8 independent W loads in flight
+          int ii = 0;
+          for (; ii + 8 <= k0; ii += 8) {
+            T w8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w8[u] = Wf[(size_t)(ii + u) * Np + j];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+              for (int tt = 0; tt < B; ++tt)
+                if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii + u], w8[u], z[tt]);
+          }
+          for (; ii < k0; ++ii) {
             const T wij = Wf[(size_t)ii * Np + j];
 #pragma unroll
             for (int tt = 0; tt < B; ++tt)
@@ -416,7 +428,21 @@ ffs_sample_kernel(const Params p) {
 #pragma unroll
           for (int tt = 0; tt < B; ++tt)
             if (tt < nb) Wf[(size_t)(k0 + tt) * Np + j] = z[tt];
-          for (int ii = 0; ii < k0; ++ii) {
+          // W[0:k0, j] -= Wb Z[:, j]; 8 rows per batch (independent loads, then stores)
+          ii = 0;
+          for (; ii + 8 <= k0; ii += 8) {
+            T a8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a8[u] = Wf[(size_t)(ii + u) * Np + j];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+#pragma unroll
+              for (int tt = 0; tt < B; ++tt)
+                if (tt < nb) a8[u] = S::fms(Wb[(ii + u) * B + tt], z[tt], a8[u]);
+              Wf[(size_t)(ii + u) * Np + j] = a8[u];
+            }
+          }
+          for (; ii < k0; ++ii) {
             T a = Wf[(size_t)ii * Np + j];
 #pragma unroll
             for (int tt = 0; tt < B; ++tt)
