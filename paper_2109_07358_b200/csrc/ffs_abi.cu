@@ -10,6 +10,7 @@
 #include "ffs.h"
 #include "ffs_kernel.cuh"
 #include "ffs_warp_kernel.cuh"
+#include "ffs_pc_kernel.cuh"
 
 namespace {
 
@@ -191,7 +192,9 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
 struct WarpPlan {
   const void* fn;
   int R, B, S, G = 32, maxt, warps, grid, Lp, ut_stride;
-  size_t ushared, owner, smem, ws_perm;
+  bool pc = false;  // producer/consumer kernel (owner = consumer+producer warp pair, 2 slots)
+  bool wsmem = false;  // pc kernel keeps W in shared memory
+  size_t ushared, owner, smem, ws_perm, ws_w = 0;
   int perm_tpb;
   size_t perm_smem;
 };
@@ -204,6 +207,18 @@ void warp_fn_seg(WarpPlan& w) {
   w.S = 32 / G;  // samples per warp (one per G-lane segment)
   w.G = G;
   w.maxt = MAXT;
+}
+
+template <int R, int B, int MAXT, bool WSMEM, bool TIMING = false>
+void warp_fn_pc(WarpPlan& w) {
+  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_pc_kernel<R, B, MAXT, WSMEM, TIMING>);
+  w.wsmem = WSMEM;
+  w.R = R;
+  w.B = B;
+  w.S = 1;
+  w.G = 32;
+  w.maxt = MAXT;
+  w.pc = true;
 }
 
 template <int R, int B, int S, int MAXREG>
@@ -241,6 +256,11 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
     else if (var && strcmp(var, "seg16b4r128") == 0) warp_fn_seg<16, 4, 16, 512>(w);
     else if (var && strcmp(var, "seg32b4") == 0) warp_fn_seg<8, 4, 32, 512>(w);
     else if (var && strcmp(var, "seg32b4r168") == 0) warp_fn_seg<8, 4, 32, 384>(w);
+    else if (var && strcmp(var, "pc512") == 0) warp_fn_pc<8, 4, 512, false>(w);
+    else if (var && strcmp(var, "pc384") == 0) warp_fn_pc<8, 4, 384, false>(w);
+    else if (var && strcmp(var, "pcs") == 0) warp_fn_pc<8, 4, 512, true>(w);
+    else if (var && strcmp(var, "pcs256") == 0) warp_fn_pc<8, 4, 256, true>(w);
+    else if (var && strcmp(var, "pcs256t") == 0) warp_fn_pc<8, 4, 256, true, true>(w);
     else if (var && strcmp(var, "seg32b8") == 0) warp_fn_seg<8, 8, 32, 256>(w);
     else if (var && strcmp(var, "seg32b4t") == 0) warp_fn_seg<8, 4, 32, 512, true>(w);
     else if (var && strcmp(var, "seg16b4t") == 0) warp_fn_seg<16, 4, 16, 256, true>(w);
@@ -259,18 +279,34 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   w.Lp = w.G * w.R;
   w.ut_stride = w.Lp + 2;
   w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
-  w.owner = ffsk::WarpLayout((int)Np, w.B).total;  // per sample; a warp holds S slices
+  w.owner = w.pc ? ffsk::pc_pair_bytes((int)Np, w.B, w.R, w.wsmem)  // per consumer/producer pair
+                 : ffsk::WarpLayout((int)Np, w.B).total;         // per sample; a warp holds S slices
   // registers are allocated per SM sub-partition (4 x 16K); warps are spread round-robin
   const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
   int warps = std::min(w.maxt / 32, by_regs);
-  while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
-  if (const char* fw = getenv("FFS_WARPS")) warps = std::max(1, std::min(warps, atoi(fw)));  // development
-  w.warps = warps;
-  w.smem = w.ushared + (size_t)warps * w.S * w.owner;
-  if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
-  const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
-  w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
-  w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
+  if (w.pc) {
+    // warps come in (consumer, producer) pairs; each pair owns two sample slots
+    int pairs = std::max(1, warps / 2);
+    while (pairs > 1 && w.ushared + (size_t)pairs * w.owner > kMaxSmem) --pairs;
+    if (const char* fw = getenv("FFS_WARPS")) pairs = std::max(1, std::min(pairs, atoi(fw) / 2));
+    w.warps = 2 * pairs;
+    w.smem = w.ushared + (size_t)pairs * w.owner;
+    if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "pc path smem %zu too large", w.smem);
+    const int64_t ctas = (M + 2LL * pairs - 1) / (2LL * pairs);
+    w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
+    const int ldw = (int)((Np + w.B + 1) & ~1);
+    w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
+    w.ws_w = w.wsmem ? 0 : align_up((size_t)w.grid * pairs * 2 * Np * ldw * 8);
+  } else {
+    while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
+    if (const char* fw = getenv("FFS_WARPS")) warps = std::max(1, std::min(warps, atoi(fw)));  // development
+    w.warps = warps;
+    w.smem = w.ushared + (size_t)warps * w.S * w.owner;
+    if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
+    const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
+    w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
+    w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
+  }
   w.perm_tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
   w.perm_smem = (size_t)w.perm_tpb * N * 4;
   return FFS_OK;
@@ -282,7 +318,8 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   WarpPlan w;
   int rc = make_warp_plan(L, N, Np, M, w);
   if (rc != FFS_OK) return rc;
-  if (!ws || ws_bytes < w.ws_perm) return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, w.ws_perm);
+  if (!ws || ws_bytes < w.ws_perm + w.ws_w)
+    return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, w.ws_perm + w.ws_w);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   int32_t* perm = static_cast<int32_t*>(ws);
   const int64_t pgrid = (M + w.perm_tpb - 1) / w.perm_tpb;
@@ -304,6 +341,7 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   p.ut_stride = w.ut_stride;
   p.ushared = w.ushared;
   p.owner_bytes = w.owner;
+  p.wfull = w.pc ? reinterpret_cast<double*>(static_cast<char*>(ws) + w.ws_perm) : nullptr;
   p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
   p.trace = S > 0 ? trace : nullptr;
   const char* dbg = getenv("FFS_DEBUG_SKIP");  // development only: bits 0-2 break the results
@@ -391,7 +429,7 @@ size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int6
   if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && use_warp_path(L, N, Nprime, dtype)) {
     WarpPlan w;
     if (make_warp_plan(L, N, Nprime, std::max<int64_t>(M, 1), w) != FFS_OK) return 0;
-    return w.ws_perm;
+    return w.ws_perm + w.ws_w;
   }
   Plan pl;
   if (make_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), pl) != FFS_OK) return 0;

@@ -55,6 +55,7 @@ struct WarpParams {
   int dbg;                // development: bit0 skip GEMM, bit1 trivial draws, bit2 skip GJ (WRONG results),
                           // bit3 per-phase clock64 accounting into timing[0..7]
   unsigned long long* timing;
+  double* wfull;          // producer/consumer kernel: per (pair, slot) W [N'][ldw] in global memory
 };
 
 // Result of the branch-free part of a draw.

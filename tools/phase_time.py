@@ -19,5 +19,8 @@ L.ffs_dev_timing(buf, 1)
 ms = e0.elapsed_time(e1)
 tot = sum(buf[:3])
 sps = cfg.M * cfg.N
-print(f"{os.environ.get('FFS_WARP_VARIANT','default')}: {ms:.3f} ms; per warp-sample-step cycles (lane-0 sums / sample-steps / segs):",
-      {k: round(buf[i] / sps, 1) for i, k in enumerate(["gemm+init", "steps", "gj", "finish", "switch+sync", "rcp", "col+nextdraw"])})
+names = ["gemm+init", "steps", "gj", "finish", "switch+sync", "rcp", "col+nextdraw"]
+if os.environ.get("FFS_WARP_VARIANT", "").startswith("pc"):
+    names = ["prod_wait", "prod_gj", "prod_gemm", "cons_wait", "cons_steps"]
+print(f"{os.environ.get('FFS_WARP_VARIANT','default')}: {ms:.3f} ms; cycles per sample-step (sum over warps / sample-steps):",
+      {k: round(buf[i] / sps, 1) for i, k in enumerate(names)})
