@@ -11,6 +11,7 @@
 #include "ffs_kernel.cuh"
 #include "ffs_warp_kernel.cuh"
 #include "ffs_pc_kernel.cuh"
+#include "ffs_cluster_kernel.cuh"
 
 namespace {
 
@@ -357,6 +358,132 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   return FFS_OK;
 }
 
+
+// ------------------------------------------------------------------ cluster-owner path
+// Large L (>= 2048): one thread-block cluster of CS CTAs per sample (ffs_cluster_kernel), the
+// L x B panel spread over the cluster; B = 8.
+struct ClusterPlan {
+  const void* fn;
+  int R, B, threads, CS, Lc, Lpt, grid, es;
+  size_t smem, ws_ut, ws_w;
+};
+
+template <typename T, int R, int B, int MAXT>
+void cluster_fn(ClusterPlan& c) {
+  c.fn = reinterpret_cast<const void*>(&ffsk::ffs_cluster_kernel<T, R, B, MAXT>);
+  c.R = R;
+  c.B = B;
+  c.threads = MAXT;
+}
+
+bool cluster_eligible(int64_t L, int dtype) {
+  const char* g = getenv("FFS_NO_CLUSTER");
+  if (g && g[0] == '1') return false;
+  return L >= 2048 && L <= (dtype == FFS_C128 ? 16 * 512 * 2 : 16 * 512 * 4);
+}
+
+int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, ClusterPlan& c) {
+  const bool cx = dtype == FFS_C128;
+  if (cx) cluster_fn<cplx, 2, 8, 512>(c);
+  else cluster_fn<double, 4, 8, 512>(c);
+  c.es = cx ? 16 : 8;
+  const int rows_per_cta = c.threads * c.R;
+  c.CS = (int)((L + rows_per_cta - 1) / rows_per_cta);
+  if (c.CS < 2) c.CS = 2;
+  if (c.CS > 8) c.CS = 16;
+  c.Lc = rows_per_cta;
+  c.Lpt = c.CS * c.Lc;
+  c.smem = cx ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np).total : ffsk::ClusterLayout<double, 8>((int)N, (int)Np).total;
+  if (c.smem > kMaxSmem) return fail(FFS_EINVAL, "cluster path smem %zu > %zu (N'=%lld)", c.smem, kMaxSmem, (long long)Np);
+  if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem) failed");
+  if (c.CS > 8 && cudaFuncSetAttribute(c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return fail(FFS_ECUDA, "non-portable cluster size not allowed");
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = c.CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(c.threads);
+  cfg.gridDim = dim3(c.CS);
+  cfg.dynamicSmemBytes = c.smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int maxcl = 0;
+  if (cudaOccupancyMaxActiveClusters(&maxcl, c.fn, &cfg) != cudaSuccess || maxcl < 1)
+    return fail(FFS_EINVAL, "cluster of %d CTAs does not fit", c.CS);
+  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(M, maxcl));
+  c.grid = (int)(ncl * c.CS);
+  c.ws_ut = align_up((size_t)N * c.Lpt * c.es);
+  c.ws_w = align_up((size_t)ncl * Np * Np * c.es);
+  return FFS_OK;
+}
+
+int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+                   int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
+                   double* trace) {
+  ClusterPlan c;
+  int rc = make_cluster_plan(L, N, Np, dtype, M, c);
+  if (rc != FFS_OK) return rc;
+  if (!ws || ws_bytes < c.ws_ut + c.ws_w)
+    return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, c.ws_ut + c.ws_w);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  char* w = static_cast<char*>(ws);
+  ffsk::ClusterParams p{};
+  p.U = static_cast<const double*>(U);
+  p.Ut = reinterpret_cast<const double*>(w);
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  p.Lc = c.Lc;
+  p.Lpt = c.Lpt;
+  p.M = M;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.wfull = reinterpret_cast<double*>(w + c.ws_ut);
+  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.trace = S > 0 ? trace : nullptr;
+  dim3 tb(32, 8), tg((unsigned)((c.Lpt + 31) / 32), (unsigned)((N + 31) / 32));
+  if (dtype == FFS_C128)
+    ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, c.Lpt);
+  else
+    ffsk::transpose_pad_kernel<double><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, c.Lpt);
+  ++g_launches;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = c.CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(c.threads);
+  cfg.gridDim = dim3(c.grid);
+  cfg.dynamicSmemBytes = c.smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&p};
+  if (g_prof) {
+    if (!g_ev0) {
+      cudaEventCreate(&g_ev0);
+      cudaEventCreate(&g_ev1);
+    }
+    cudaEventRecord(g_ev0, stream);
+  }
+  cudaError_t e = cudaLaunchKernelExC(&cfg, c.fn, args);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "cluster launch failed: %s", cudaGetErrorString(e));
+  if (g_prof) {
+    cudaEventRecord(g_ev1, stream);
+    g_ev_pending = true;
+  }
+  ++g_launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  g_err[0] = 0;
+  return FFS_OK;
+}
+
 bool use_warp_path(int64_t L, int64_t N, int64_t Np, int dtype) {
   const char* g = getenv("FFS_FORCE_GENERIC");
   if (g && g[0] == '1') return false;
@@ -376,6 +503,8 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
   if (use_warp_path(L, N, Np, dtype))
     return launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
+  if (cluster_eligible(L, dtype))
+    return launch_cluster(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   Plan pl;
   int rc = make_plan(L, N, Np, dtype, M, pl);
   if (rc != FFS_OK) return rc;
@@ -430,6 +559,11 @@ size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int6
     WarpPlan w;
     if (make_warp_plan(L, N, Nprime, std::max<int64_t>(M, 1), w) != FFS_OK) return 0;
     return w.ws_perm + w.ws_w;
+  }
+  if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && cluster_eligible(L, dtype)) {
+    ClusterPlan c;
+    if (make_cluster_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), c) != FFS_OK) return 0;
+    return c.ws_ut + c.ws_w;
   }
   Plan pl;
   if (make_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), pl) != FFS_OK) return 0;

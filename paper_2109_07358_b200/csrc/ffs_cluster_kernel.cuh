@@ -1,0 +1,426 @@
+// Cluster-owner FFS kernel for large L (the C4 2D lattice and the C5 DPP-shaped workloads).
+//
+// Same mathematics as ffs_kernel.cuh (blocked left-looking randomized-pivot LU),
+// but one sample is owned by a thread-block CLUSTER of CS CTAs (one per SM): CTA `rank` holds
+// rows [rank*Lc, (rank+1)*Lc) of the L x B panel in registers (Lc = threads * R). The panel
+// width B -- the reuse factor of every V element gathered from U in the contraction a3 -- is
+// therefore bounded by the register files of CS SMs instead of one, which is what makes the
+// contraction compute-bound for L = 4096..16384.
+// Per draw (a4): CTA-local weights / prefix / totals, then each CTA publishes its total and
+// fallback candidates into every CTA's shared memory (DSMEM stores) and the cluster barrier
+// makes them visible; every CTA derives the same crossing CTA; the crossing CTA finds x_k and
+// pushes the pivot row to all CTAs (DSMEM) before the second cluster barrier.
+// W = A^{-1} V[X, later columns] lives in global memory (per cluster); its Gauss-Jordan update
+// after each block is split over the cluster's CTAs by column.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ffs_kernel.cuh"
+
+namespace ffsk {
+
+constexpr int kMaxCS = 16;
+
+struct ClusterParams {
+  const double* U;         // [L][N] row-major scalars (complex interleaved)
+  const double* Ut;        // [N][Lpt] transposed, zero-padded (workspace)
+  int L, N, Np, Lc, Lpt;   // Lc rows per CTA, Lpt = CS * Lc
+  int64_t M;
+  const double* uniforms;  // [M][2Np]
+  int32_t* positions;      // [M][Np]
+  int32_t* flags;
+  double* wfull;           // per cluster [Np][Np] scalars
+  int64_t S;
+  double* trace;           // [S][Np][L] or null
+};
+
+template <typename T, int B>
+struct ClusterLayout {
+  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, total;
+  __host__ __device__ ClusterLayout(int N, int Np) {
+    size_t o = 0;
+    perm = o; o = align16(o + sizeof(int) * N);
+    pos = o;  o = align16(o + sizeof(int) * Np);
+    usel = o; o = align16(o + sizeof(double) * Np);
+    row = o;  o = align16(o + sizeof(T) * B * B);
+    pinv = o; o = align16(o + sizeof(T) * B);
+    wb = o;   o = align16(o + sizeof(T) * (size_t)Np * B);
+    vnew = o; o = align16(o + sizeof(T) * (size_t)Np * B);
+    red = o;  o = align16(o + sizeof(double) * 64 + sizeof(int) * 96);
+    xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + sizeof(T) * B + 64);  // cluster exchange
+    total = o;
+  }
+};
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned nclusters_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store to the same shared-memory variable in CTA `rank` of this cluster
+__device__ __forceinline__ void st_remote_f64(void* local_ptr, unsigned rank, double v) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local_ptr)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_remote_s32(void* local_ptr, unsigned rank, int v) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local_ptr)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
+template <typename T, int R, int B, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using S = Sc<T>;
+  constexpr int kD = S::kDoubles;
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const int nw = blockDim.x >> 5;
+  const unsigned rank = cluster_rank();
+  const unsigned CS = cluster_size();
+  const int L = p.L, N = p.N, Np = p.Np, Lc = p.Lc;
+  const int row0 = (int)rank * Lc + t * R;  // first global row of this thread
+
+  const ClusterLayout<T, B> lay(N, Np);
+  int* perm = reinterpret_cast<int*>(smem + lay.perm);
+  int* pos = reinterpret_cast<int*>(smem + lay.pos);
+  double* usel = reinterpret_cast<double*>(smem + lay.usel);
+  T* Row = reinterpret_cast<T*>(smem + lay.row);
+  T* Pinv = reinterpret_cast<T*>(smem + lay.pinv);
+  T* Wb = reinterpret_cast<T*>(smem + lay.wb);
+  T* Vnew = reinterpret_cast<T*>(smem + lay.vnew);
+  double* red = reinterpret_cast<double*>(smem + lay.red);
+  int* redi = reinterpret_cast<int*>(smem + lay.red + sizeof(double) * 64);
+  double* xtot = reinterpret_cast<double*>(smem + lay.xch);  // [CS] CTA totals
+  int* xlast = reinterpret_cast<int*>(xtot + kMaxCS);        // [CS] last positive row (global) or -1
+  int* xfree = xlast + kMaxCS;                                 // [CS] first unchosen row or INT_MAX
+  int* xsel = xfree + kMaxCS;                                  // selected row (global)
+  T* xrow = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(xsel) + 16);  // [B] pivot row
+
+  const int64_t cid = cluster_id_x();
+  const int64_t ncl = nclusters_x();
+  T* Wf = reinterpret_cast<T*>(p.wfull) + cid * (int64_t)Np * Np;
+  const T* Ug = reinterpret_cast<const T*>(p.U);
+  const T* Utg = reinterpret_cast<const T*>(p.Ut);
+  constexpr int kNone = 0x7fffffff;
+
+  for (int64_t i = cid; i < p.M; i += ncl) {
+    const double* urow = p.uniforms + i * 2 * (int64_t)Np;
+    // ---- a1 permutation (every CTA computes the same one)
+    for (int j = t; j < N; j += blockDim.x) perm[j] = j;
+    for (int j = t; j < Np; j += blockDim.x) usel[j] = urow[Np + j];
+    __syncthreads();
+    if (t == 0) {
+      for (int j = 0; j < Np; ++j) {
+        const int n = N - j;
+        int r = (int)floor(urow[j] * (double)n);
+        r = (r > n - 1 ? n - 1 : r) + j;
+        const int a = perm[j];
+        perm[j] = perm[r];
+        perm[r] = a;
+      }
+    }
+    __syncthreads();
+    uint32_t chosen = 0;
+    int flag = 0;
+
+    for (int k0 = 0; k0 < Np; k0 += B) {
+      const int nb = min(B, Np - k0);
+      // W (global) is final for rows < k0 after the previous block's update + cluster barrier
+      for (int idx = t; idx < k0 * B; idx += blockDim.x) {
+        const int ii = idx / B, c = idx % B;
+        Wb[idx] = c < nb ? Wf[(size_t)ii * Np + k0 + c] : S::zero();
+      }
+      __syncthreads();
+      // ---- a3 panel for this CTA's rows
+      T P[R][B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const T* base = Utg + (size_t)perm[min(k0 + c, Np - 1)] * p.Lpt + row0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
+      }
+#pragma unroll 4
+      for (int ii = 0; ii < k0; ++ii) {
+        const T* base = Utg + (size_t)perm[ii] * p.Lpt + row0;
+        T v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = base[r];
+        T wb[B];
+#pragma unroll
+        for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];
+#pragma unroll
+        for (int c = 0; c < B; ++c)
+#pragma unroll
+          for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
+      }
+      // rows drawn earlier: exactly zero weight in the first column of this block
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((chosen >> r) & 1u) P[r][0] = S::zero();
+
+      // ---- a4/a5: nb sequential draws
+      static_for<0, B>([&](auto rrc) {
+        constexpr int rr = decltype(rrc)::value;
+        if (rr < nb) {
+          const int k = k0 + rr;
+          double w[R], c[R];
+          double acc = 0.0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            w[r] = S::abs2(P[r][rr]);
+            acc += w[r];
+            c[r] = acc;
+          }
+          // CTA-level inclusive scan of thread totals
+          double incl = warp_incl_scan(acc, lane);
+          if (lane == 31) red[warp] = incl;
+          // local fallback candidates
+          int rl = -1, rf = kNone;
+#pragma unroll
+          for (int r = R - 1; r >= 0; --r) {
+            if (row0 + r < L && !((chosen >> r) & 1u)) rf = row0 + r;
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (w[r] > 0.0) rl = row0 + r;
+          const int wl = __reduce_max_sync(0xffffffffu, rl);
+          const int wf = __reduce_min_sync(0xffffffffu, rf);
+          if (lane == 0) {
+            redi[warp] = wl;
+            redi[32 + warp] = wf;
+          }
+          __syncthreads();
+          double woff = 0.0, Tc;
+          {
+            const double wt = lane < nw ? red[lane] : 0.0;
+            const double ws = warp_incl_scan(wt, lane);
+            woff = warp > 0 ? __shfl_sync(0xffffffffu, ws, warp - 1) : 0.0;
+            Tc = __shfl_sync(0xffffffffu, ws, 31);
+          }
+          double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+          if (lane == 0) excl = 0.0;
+          excl += woff;
+          // publish this CTA's total and fallback candidates to every CTA of the cluster
+          if (t == 0) {
+            int cl = -1, cf = kNone;
+            for (int q = 0; q < nw; ++q) {
+              cl = max(cl, redi[q]);
+              cf = min(cf, redi[32 + q]);
+            }
+            for (unsigned q = 0; q < CS; ++q) {
+              st_remote_f64(&xtot[rank], q, Tc);
+              st_remote_s32(&xlast[rank], q, cl);
+              st_remote_s32(&xfree[rank], q, cf);
+            }
+          }
+          cluster_sync_all();
+          // cluster-uniform: total, this CTA's offset, crossing CTA, fallback row
+          double Ttot = 0.0, off = 0.0;
+          int owner_cta = -1, fb_last = -1, fb_free = kNone;
+          const double u = usel[k];
+          {
+            double run = 0.0;
+            for (unsigned q = 0; q < CS; ++q) {
+              if (q == rank) off = run;
+              run += xtot[q];
+              fb_last = max(fb_last, xlast[q]);
+              fb_free = min(fb_free, xfree[q]);
+            }
+            Ttot = run;
+          }
+          const bool ok = (Ttot > 0.0) && isfinite(Ttot);
+          const double thr = u * Ttot;
+          {
+            double run = 0.0;
+            for (unsigned q = 0; q < CS; ++q) {
+              const double tq = xtot[q];
+              if (owner_cta < 0 && tq > 0.0 && run + tq > thr) owner_cta = (int)q;
+              run += tq;
+            }
+          }
+          // the selected row: fallbacks are cluster-uniform; a regular crossing is resolved by the
+          // crossing CTA (first local row with C(x) > u*T, w > 0; clamped threshold as elsewhere)
+          int xs = -1;
+          if (!ok) {
+            xs = fb_free;
+            flag |= 1;
+          } else if (owner_cta < 0) {
+            xs = fb_last;
+          } else if (owner_cta == (int)rank) {
+            const double tp = fmax(thr - off - excl, 0.0);
+            int rs = R;
+#pragma unroll
+            for (int r = R - 1; r >= 0; --r)
+              if (w[r] > 0.0 && c[r] > tp) rs = r;
+            const unsigned bal = __ballot_sync(0xffffffffu, rs < R);
+            int cand = kNone;
+            if (bal) {
+              const int ln = __ffs(bal) - 1;
+              cand = (int)rank * Lc + (warp * 32 + ln) * R + __shfl_sync(0xffffffffu, rs, ln);
+            }
+            if (lane == 0) redi[64 + warp] = cand;
+            __syncthreads();
+            int best = kNone;
+            for (int q = 0; q < nw; ++q) best = min(best, redi[64 + q]);
+            xs = best != kNone ? best : xlast[rank];  // rounding corner: last positive row here
+          }
+          // the CTA that holds the selected row publishes it (index + pivot row) to all CTAs
+          if (xs >= 0 && (unsigned)(xs / Lc) == rank) {
+            const int own = (xs - (int)rank * Lc) / R, orow = (xs - (int)rank * Lc) % R;
+            if (t == own) {
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+                if (r == orow) {
+                  for (unsigned q = 0; q < CS; ++q) {
+#pragma unroll
+                    for (int cc = 0; cc < B; ++cc) {
+                      const double* src = reinterpret_cast<const double*>(&P[r][cc]);
+                      double* dst = reinterpret_cast<double*>(&xrow[cc]);
+#pragma unroll
+                      for (int h = 0; h < kD; ++h) st_remote_f64(dst + h, q, src[h]);
+                    }
+                    st_remote_s32(xsel, q, xs);
+                  }
+                  if (ok && w[r] < 1e-12 * Ttot) flag |= 2;
+                  chosen |= 1u << r;
+                }
+            }
+          }
+          if (p.trace != nullptr && i < p.S) {
+            const double inv = Ttot > 0.0 ? 1.0 / Ttot : 0.0;
+            double* tr = p.trace + (i * Np + k) * (int64_t)L;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (row0 + r < L) tr[row0 + r] = w[r] * inv;
+          }
+          cluster_sync_all();
+          const int xsel_k = *xsel;
+          if (t == 0) pos[k] = xsel_k;
+#pragma unroll
+          for (int cc = 0; cc < B; ++cc)
+            if (t == 0) Row[rr * B + cc] = xrow[cc];
+          const T piv = xrow[rr];
+          const T ip = S::recip(piv);
+          if (t == 0) Pinv[rr] = ip;
+          // rank-1 update of the remaining panel columns; the drawn row becomes exactly zero
+          T lmul[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) lmul[r] = S::mul(P[r][rr], ip);
+#pragma unroll
+          for (int cc = rr + 1; cc < B; ++cc) {
+            const T pc = xrow[cc];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              P[r][cc] = ((chosen >> r) & 1u) ? S::zero() : S::fms(lmul[r], pc, P[r][cc]);
+          }
+          __syncthreads();
+        }
+      });
+
+      // ---- Gauss-Jordan update of W with the nb new rows, columns split over the cluster
+      if (k0 + nb < Np) {
+        for (int idx = t; idx < nb * Np; idx += blockDim.x) {
+          const int tt = idx / Np, j = idx % Np;
+          Vnew[idx] = Ug[(size_t)pos[k0 + tt] * N + perm[j]];
+        }
+        __syncthreads();
+        for (int j = k0 + nb + (int)rank * blockDim.x + t; j < Np; j += (int)CS * blockDim.x) {
+          T z[B];
+#pragma unroll
+          for (int tt = 0; tt < B; ++tt) z[tt] = tt < nb ? Vnew[tt * Np + j] : S::zero();
+          int ii = 0;
+          for (; ii + 8 <= k0; ii += 8) {
+            T w8[8];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu) w8[uu] = Wf[(size_t)(ii + uu) * Np + j];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu)
+#pragma unroll
+              for (int tt = 0; tt < B; ++tt)
+                if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii + uu], w8[uu], z[tt]);
+          }
+          for (; ii < k0; ++ii) {
+            const T wij = Wf[(size_t)ii * Np + j];
+#pragma unroll
+            for (int tt = 0; tt < B; ++tt)
+              if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii], wij, z[tt]);
+          }
+#pragma unroll
+          for (int tt = 1; tt < B; ++tt)
+            if (tt < nb) {
+#pragma unroll
+              for (int s2 = 0; s2 < tt; ++s2) z[tt] = S::fms(S::mul(Row[tt * B + s2], Pinv[s2]), z[s2], z[tt]);
+            }
+#pragma unroll
+          for (int tt = B - 1; tt >= 0; --tt)
+            if (tt < nb) {
+#pragma unroll
+              for (int s2 = tt + 1; s2 < B; ++s2)
+                if (s2 < nb) z[tt] = S::fms(Row[tt * B + s2], z[s2], z[tt]);
+              z[tt] = S::mul(z[tt], Pinv[tt]);
+            }
+#pragma unroll
+          for (int tt = 0; tt < B; ++tt)
+            if (tt < nb) Wf[(size_t)(k0 + tt) * Np + j] = z[tt];
+          ii = 0;
+          for (; ii + 8 <= k0; ii += 8) {
+            T a8[8];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu) a8[uu] = Wf[(size_t)(ii + uu) * Np + j];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu) {
+#pragma unroll
+              for (int tt = 0; tt < B; ++tt)
+                if (tt < nb) a8[uu] = S::fms(Wb[(ii + uu) * B + tt], z[tt], a8[uu]);
+              Wf[(size_t)(ii + uu) * Np + j] = a8[uu];
+            }
+          }
+          for (; ii < k0; ++ii) {
+            T a = Wf[(size_t)ii * Np + j];
+#pragma unroll
+            for (int tt = 0; tt < B; ++tt)
+              if (tt < nb) a = S::fms(Wb[ii * B + tt], z[tt], a);
+            Wf[(size_t)ii * Np + j] = a;
+          }
+        }
+        __threadfence();
+        cluster_sync_all();  // W visible to every CTA before the next block's Wb load
+      }
+    }
+    // ---- a6: positions (rank 0) and flags (OR over the cluster, collected in rank 0)
+    const int fcta = (__syncthreads_or(flag & 1) ? 1 : 0) | (__syncthreads_or(flag & 2) ? 2 : 0);
+    if (rank == 0)
+      for (int j = t; j < Np; j += blockDim.x) p.positions[i * Np + j] = pos[j];
+    if (t == 0) st_remote_s32(&xfree[rank], 0, fcta);
+    cluster_sync_all();
+    if (rank == 0 && t == 0 && p.flags != nullptr) {
+      int f = 0;
+      for (unsigned q = 0; q < CS; ++q) f |= xfree[q];
+      p.flags[i] = f;
+    }
+    cluster_sync_all();
+  }
+}
+
+}  // namespace ffsk
