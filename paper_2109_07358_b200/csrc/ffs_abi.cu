@@ -393,7 +393,8 @@ int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Cl
   if (c.CS > 8) c.CS = 16;
   c.Lc = rows_per_cta;
   c.Lpt = c.CS * c.Lc;
-  c.smem = cx ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np).total : ffsk::ClusterLayout<double, 8>((int)N, (int)Np).total;
+  c.smem = cx ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np, c.threads, c.R).total
+              : ffsk::ClusterLayout<double, 8>((int)N, (int)Np, c.threads, c.R).total;
   if (c.smem > kMaxSmem) return fail(FFS_EINVAL, "cluster path smem %zu > %zu (N'=%lld)", c.smem, kMaxSmem, (long long)Np);
   if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem) failed");

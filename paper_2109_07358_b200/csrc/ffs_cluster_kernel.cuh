@@ -35,10 +35,12 @@ struct ClusterParams {
   double* trace;           // [S][Np][L] or null
 };
 
+constexpr int kRingDepth = 4;  // per-thread cp.async pipeline depth of the contraction
+
 template <typename T, int B>
 struct ClusterLayout {
-  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, total;
-  __host__ __device__ ClusterLayout(int N, int Np) {
+  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, ring, total;
+  __host__ __device__ ClusterLayout(int N, int Np, int threads = 0, int R = 0) {
     size_t o = 0;
     perm = o; o = align16(o + sizeof(int) * N);
     pos = o;  o = align16(o + sizeof(int) * Np);
@@ -49,6 +51,7 @@ struct ClusterLayout {
     vnew = o; o = align16(o + sizeof(T) * (size_t)Np * B);
     red = o;  o = align16(o + sizeof(double) * 64 + sizeof(int) * 96);
     xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + sizeof(T) * B + 64);  // cluster exchange
+    ring = o; o = align16(o + (size_t)kRingDepth * threads * R * sizeof(T));  // [stage][chunk][thread]
     total = o;
   }
 };
@@ -101,7 +104,10 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   const int L = p.L, N = p.N, Np = p.Np, Lc = p.Lc;
   const int row0 = (int)rank * Lc + t * R;  // first global row of this thread
 
-  const ClusterLayout<T, B> lay(N, Np);
+  const ClusterLayout<T, B> lay(N, Np, blockDim.x, R);
+  constexpr int kChunks = R * kD / 2;  // 16-byte chunks per thread per column
+  double2* ring = reinterpret_cast<double2*>(smem + lay.ring);
+  auto ring_at = [&](int d, int q) { return ring + ((size_t)(d * kChunks + q) * blockDim.x + t); };
   int* perm = reinterpret_cast<int*>(smem + lay.perm);
   int* pos = reinterpret_cast<int*>(smem + lay.pos);
   double* usel = reinterpret_cast<double*>(smem + lay.usel);
@@ -160,12 +166,37 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 #pragma unroll
         for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
       }
-#pragma unroll 4
+      // contraction over the k0 earlier columns; this thread's R rows of column perm[ii] are
+      // copied global->shared with cp.async kRingDepth columns ahead (private ring: no barrier)
+      auto issue = [&](int ii) {
+        const double2* src = reinterpret_cast<const double2*>(Utg + (size_t)perm[ii] * p.Lpt + row0);
+#pragma unroll
+        for (int q = 0; q < kChunks; ++q) {
+          const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ring_at(ii % kRingDepth, q)));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + q) : "memory");
+        }
+      };
+#pragma unroll
+      for (int d = 0; d < kRingDepth; ++d) {
+        if (d < k0) issue(d);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
       for (int ii = 0; ii < k0; ++ii) {
-        const T* base = Utg + (size_t)perm[ii] * p.Lpt + row0;
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRingDepth - 1) : "memory");
         T v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = base[r];
+        for (int q = 0; q < kChunks; ++q) {
+          const double2 d2 = *ring_at(ii % kRingDepth, q);
+          if constexpr (kD == 1) {
+            reinterpret_cast<double*>(v)[2 * q] = d2.x;
+            reinterpret_cast<double*>(v)[2 * q + 1] = d2.y;
+          } else {
+            v[q].re = d2.x;
+            v[q].im = d2.y;
+          }
+        }
+        if (ii + kRingDepth < k0) issue(ii + kRingDepth);
+        asm volatile("cp.async.commit_group;" ::: "memory");
         T wb[B];
 #pragma unroll
         for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];

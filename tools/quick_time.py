@@ -10,6 +10,9 @@ for name in names:
     cfg = inputs.CONFIGS[name.split(":")[0]]
     U = inputs.build_u(cfg)
     uni = inputs.workload_uniforms(cfg, marg)
+    import os
+    if os.environ.get("FFS_QT_M"):
+        uni = uni[: int(os.environ["FFS_QT_M"])]
     Np = cfg.marginal_Np if marg else cfg.N
     Ud = torch.from_numpy(U).cuda(); ud = torch.from_numpy(uni).cuda()
     ws = ffs.Workspace()
