@@ -36,6 +36,7 @@ struct ClusterParams {
 };
 
 constexpr int kRingDepth = 4;  // per-thread cp.async pipeline depth of the contraction
+constexpr bool kUseRing = false;  // measured slower on C4/C5 (profiles/r01_ncu_summary.md)
 
 template <typename T, int B>
 struct ClusterLayout {
@@ -166,6 +167,22 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 #pragma unroll
         for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
       }
+      if constexpr (!kUseRing) {
+#pragma unroll 4
+        for (int ii = 0; ii < k0; ++ii) {
+          const T* base = Utg + (size_t)perm[ii] * p.Lpt + row0;
+          T v[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[r] = base[r];
+          T wb[B];
+#pragma unroll
+          for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];
+#pragma unroll
+          for (int c = 0; c < B; ++c)
+#pragma unroll
+            for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
+        }
+      } else {
       // contraction over the k0 earlier columns; this thread's R rows of column perm[ii] are
       // copied global->shared with cp.async kRingDepth columns ahead (private ring: no barrier)
       auto issue = [&](int ii) {
@@ -205,6 +222,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 #pragma unroll
           for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
       }
+      }  // kUseRing
       // rows drawn earlier: exactly zero weight in the first column of this block
 #pragma unroll
       for (int r = 0; r < R; ++r)
