@@ -522,8 +522,49 @@ struct SegOps {
 
 // Branch-free part of a draw for one segment (see draw_part1): returns the crossing lanes of
 // this lane's segment (bit i = segment lane i), the crossing row in this lane, and T.
+// Whole-warp draw (G = 32, R <= 8) with a shorter dependency chain: the local inclusive prefix is
+// kept (no second pass), and the 32-lane scan runs as a 3-level scan inside 8-lane groups plus
+// the group offsets read from the group-final lanes (one shuffle round instead of two levels).
+// Every prefix value compared against the threshold is computed exactly as the previous lane's
+// inclusive value would be, so the crossing lane and row are consistent (reading Q5).
+template <int R>
+__device__ __forceinline__ Draw warp_draw_fast(const double (&col)[R], double u, int lane) {
+  double c[R];
+  c[0] = col[0] * col[0];
+#pragma unroll
+  for (int r = 1; r < R; ++r) c[r] = fma(col[r], col[r], c[r - 1]);
+  const double tot = c[R - 1];
+  double li = tot;
+  li = SegOps<8>::scan_level(li, 1);
+  li = SegOps<8>::scan_level(li, 2);
+  li = SegOps<8>::scan_level(li, 4);
+  const double le = SegOps<8>::prev(li);
+  const double g0 = __shfl_sync(0xffffffffu, li, 7);
+  const double g1 = __shfl_sync(0xffffffffu, li, 15);
+  const double g2 = __shfl_sync(0xffffffffu, li, 23);
+  const double g3 = __shfl_sync(0xffffffffu, li, 31);
+  const double o1 = g0, o2 = o1 + g1, o3 = o2 + g2;
+  Draw d;
+  d.T = o3 + g3;
+  const int grp = lane >> 3;
+  const double off = grp == 0 ? 0.0 : (grp == 1 ? o1 : (grp == 2 ? o2 : o3));
+  const double excl = off + le;
+  const bool ok = (d.T > 0.0) && (d.T < INFINITY);
+  const double tq = fma(u, d.T, -excl);
+  const double tp = tq > 0.0 ? tq : 0.0;
+  d.ball = __ballot_sync(0xffffffffu, ok && (tot > tp));
+  unsigned m = 0;
+#pragma unroll
+  for (int r = 0; r < R - 1; ++r) m |= (c[r] <= tp) ? (1u << r) : 0u;
+  d.rsel = __popc(m);
+  return d;
+}
+
 template <int R, int G>
 __device__ __forceinline__ Draw seg_draw(const double (&col)[R], double u, int seg) {
+  if constexpr (false && G == 32 && R <= 8) {  // measured slower (646 vs 544 cycles/draw)
+    return warp_draw_fast<R>(col, u, threadIdx.x & 31);
+  }
   // Pass 1: lane total of w_r = col_r^2 (index order; for R > 8 two parallel half chains).
   constexpr int H = R > 8 ? R / 2 : R;
   double h1 = col[0] * col[0];
