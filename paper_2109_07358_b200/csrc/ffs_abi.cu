@@ -379,13 +379,20 @@ void cluster_fn(ClusterPlan& c) {
 bool cluster_eligible(int64_t L, int dtype) {
   const char* g = getenv("FFS_NO_CLUSTER");
   if (g && g[0] == '1') return false;
-  return L >= 2048 && L <= (dtype == FFS_C128 ? 16 * 512 * 2 : 16 * 512 * 4);
+  return L >= 2048 && L <= (dtype == FFS_C128 ? 16 * 512 * 1 : 16 * 512 * 2);
 }
 
 int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, ClusterPlan& c) {
   const bool cx = dtype == FFS_C128;
-  if (cx) cluster_fn<cplx, 2, 8, 512>(c);
-  else cluster_fn<double, 4, 8, 512>(c);
+  const char* cv = getenv("FFS_CLUSTER_VARIANT");  // development: "b16" selects B=16 (slower)
+  const bool b8 = !(cv && strcmp(cv, "b16") == 0);
+  if (cx) {
+    if (b8) cluster_fn<cplx, 2, 8, 512>(c);
+    else cluster_fn<cplx, 1, 16, 512>(c);
+  } else {
+    if (b8) cluster_fn<double, 4, 8, 512>(c);
+    else cluster_fn<double, 2, 16, 512>(c);
+  }
   c.es = cx ? 16 : 8;
   const int rows_per_cta = c.threads * c.R;
   c.CS = (int)((L + rows_per_cta - 1) / rows_per_cta);
@@ -393,8 +400,12 @@ int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Cl
   if (c.CS > 8) c.CS = 16;
   c.Lc = rows_per_cta;
   c.Lpt = c.CS * c.Lc;
-  c.smem = cx ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np, c.threads, c.R).total
-              : ffsk::ClusterLayout<double, 8>((int)N, (int)Np, c.threads, c.R).total;
+  if (cx)
+    c.smem = c.B == 8 ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np, c.threads, c.R).total
+                      : ffsk::ClusterLayout<cplx, 16>((int)N, (int)Np, c.threads, c.R).total;
+  else
+    c.smem = c.B == 8 ? ffsk::ClusterLayout<double, 8>((int)N, (int)Np, c.threads, c.R).total
+                      : ffsk::ClusterLayout<double, 16>((int)N, (int)Np, c.threads, c.R).total;
   if (c.smem > kMaxSmem) return fail(FFS_EINVAL, "cluster path smem %zu > %zu (N'=%lld)", c.smem, kMaxSmem, (long long)Np);
   if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem) failed");

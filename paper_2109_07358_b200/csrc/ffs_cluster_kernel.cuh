@@ -36,6 +36,7 @@ struct ClusterParams {
 };
 
 constexpr int kRingDepth = 4;  // per-thread cp.async pipeline depth of the contraction
+constexpr int kKC = 64;        // rows of W (or columns of the new rows) staged per chunk
 constexpr bool kUseRing = false;  // measured slower on C4/C5 (profiles/r01_ncu_summary.md)
 
 template <typename T, int B>
@@ -48,11 +49,11 @@ struct ClusterLayout {
     usel = o; o = align16(o + sizeof(double) * Np);
     row = o;  o = align16(o + sizeof(T) * B * B);
     pinv = o; o = align16(o + sizeof(T) * B);
-    wb = o;   o = align16(o + sizeof(T) * (size_t)Np * B);
-    vnew = o; o = align16(o + sizeof(T) * (size_t)Np * B);
+    wb = o;   o = align16(o + sizeof(T) * (size_t)kKC * B);  // chunk of Wb rows / new-row columns
+    vnew = o; o = align16(o + sizeof(T) * (size_t)kKC * B);
     red = o;  o = align16(o + sizeof(double) * 64 + sizeof(int) * 96);
     xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + sizeof(T) * B + 64);  // cluster exchange
-    ring = o; o = align16(o + (size_t)kRingDepth * threads * R * sizeof(T));  // [stage][chunk][thread]
+    ring = o; o = align16(o + (kUseRing ? (size_t)kRingDepth * threads * R * sizeof(T) : 0));
     total = o;
   }
 };
@@ -153,13 +154,8 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 
     for (int k0 = 0; k0 < Np; k0 += B) {
       const int nb = min(B, Np - k0);
-      // W (global) is final for rows < k0 after the previous block's update + cluster barrier
-      for (int idx = t; idx < k0 * B; idx += blockDim.x) {
-        const int ii = idx / B, c = idx % B;
-        Wb[idx] = c < nb ? Wf[(size_t)ii * Np + k0 + c] : S::zero();
-      }
-      __syncthreads();
-      // ---- a3 panel for this CTA's rows
+      // ---- a3 panel for this CTA's rows (W in global memory is final for rows < k0 after the
+      // previous block's update + cluster barrier; its rows are staged kKC at a time)
       T P[R][B];
 #pragma unroll
       for (int c = 0; c < B; ++c) {
@@ -168,19 +164,28 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
       }
       if constexpr (!kUseRing) {
+        for (int c0 = 0; c0 < k0; c0 += kKC) {
+          const int kc = min(kKC, k0 - c0);
+          __syncthreads();
+          for (int idx = t; idx < kc * B; idx += blockDim.x) {
+            const int ii = idx / B, c = idx % B;
+            Wb[idx] = c < nb ? Wf[(size_t)(c0 + ii) * Np + k0 + c] : S::zero();
+          }
+          __syncthreads();
 #pragma unroll 4
-        for (int ii = 0; ii < k0; ++ii) {
-          const T* base = Utg + (size_t)perm[ii] * p.Lpt + row0;
-          T v[R];
+          for (int ii = 0; ii < kc; ++ii) {
+            const T* base = Utg + (size_t)perm[c0 + ii] * p.Lpt + row0;
+            T v[R];
 #pragma unroll
-          for (int r = 0; r < R; ++r) v[r] = base[r];
-          T wb[B];
+            for (int r = 0; r < R; ++r) v[r] = base[r];
+            T wb[B];
 #pragma unroll
-          for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];
+            for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];
 #pragma unroll
-          for (int c = 0; c < B; ++c)
+            for (int c = 0; c < B; ++c)
 #pragma unroll
-            for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
+              for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
+          }
         }
       } else {
       // contraction over the k0 earlier columns; this thread's R rows of column perm[ii] are
@@ -388,33 +393,44 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       });
 
       // ---- Gauss-Jordan update of W with the nb new rows, columns split over the cluster
+      // (thread <-> one later column j; the new rows' entries in columns < k0 and W's rows < k0
+      // are staged kKC at a time through shared memory)
       if (k0 + nb < Np) {
-        for (int idx = t; idx < nb * Np; idx += blockDim.x) {
-          const int tt = idx / Np, j = idx % Np;
-          Vnew[idx] = Ug[(size_t)pos[k0 + tt] * N + perm[j]];
+       for (int jt = k0 + nb; jt < Np; jt += (int)CS * blockDim.x) {  // column tiles (uniform trip count)
+        const int j = jt + (int)rank * blockDim.x + t;
+        const bool has = j < Np;
+        T z[B];
+#pragma unroll
+        for (int tt = 0; tt < B; ++tt)
+          z[tt] = (has && tt < nb) ? Ug[(size_t)pos[k0 + tt] * N + perm[j]] : S::zero();
+        // R_new[:, j] = V[X_new, j] - V[X_new, 0:k0] W[0:k0, j]
+        for (int c0 = 0; c0 < k0; c0 += kKC) {
+          const int kc = min(kKC, k0 - c0);
+          __syncthreads();
+          for (int idx = t; idx < kc * B; idx += blockDim.x) {
+            const int ii = idx / B, tt = idx % B;
+            Vnew[idx] = tt < nb ? Ug[(size_t)pos[k0 + tt] * N + perm[c0 + ii]] : S::zero();
+          }
+          __syncthreads();
+          if (has) {
+            int ii = 0;
+            for (; ii + 8 <= kc; ii += 8) {
+              T w8[8];
+#pragma unroll
+              for (int uu = 0; uu < 8; ++uu) w8[uu] = Wf[(size_t)(c0 + ii + uu) * Np + j];
+#pragma unroll
+              for (int uu = 0; uu < 8; ++uu)
+#pragma unroll
+                for (int tt = 0; tt < B; ++tt) z[tt] = S::fms(Vnew[(ii + uu) * B + tt], w8[uu], z[tt]);
+            }
+            for (; ii < kc; ++ii) {
+              const T wij = Wf[(size_t)(c0 + ii) * Np + j];
+#pragma unroll
+              for (int tt = 0; tt < B; ++tt) z[tt] = S::fms(Vnew[ii * B + tt], wij, z[tt]);
+            }
+          }
         }
-        __syncthreads();
-        for (int j = k0 + nb + (int)rank * blockDim.x + t; j < Np; j += (int)CS * blockDim.x) {
-          T z[B];
-#pragma unroll
-          for (int tt = 0; tt < B; ++tt) z[tt] = tt < nb ? Vnew[tt * Np + j] : S::zero();
-          int ii = 0;
-          for (; ii + 8 <= k0; ii += 8) {
-            T w8[8];
-#pragma unroll
-            for (int uu = 0; uu < 8; ++uu) w8[uu] = Wf[(size_t)(ii + uu) * Np + j];
-#pragma unroll
-            for (int uu = 0; uu < 8; ++uu)
-#pragma unroll
-              for (int tt = 0; tt < B; ++tt)
-                if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii + uu], w8[uu], z[tt]);
-          }
-          for (; ii < k0; ++ii) {
-            const T wij = Wf[(size_t)ii * Np + j];
-#pragma unroll
-            for (int tt = 0; tt < B; ++tt)
-              if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii], wij, z[tt]);
-          }
+        if (has) {
 #pragma unroll
           for (int tt = 1; tt < B; ++tt)
             if (tt < nb) {
@@ -432,27 +448,38 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 #pragma unroll
           for (int tt = 0; tt < B; ++tt)
             if (tt < nb) Wf[(size_t)(k0 + tt) * Np + j] = z[tt];
-          ii = 0;
-          for (; ii + 8 <= k0; ii += 8) {
-            T a8[8];
+        }
+        // W[0:k0, j] -= Wb Z[:, j]
+        for (int c0 = 0; c0 < k0; c0 += kKC) {
+          const int kc = min(kKC, k0 - c0);
+          __syncthreads();
+          for (int idx = t; idx < kc * B; idx += blockDim.x) {
+            const int ii = idx / B, c = idx % B;
+            Wb[idx] = c < nb ? Wf[(size_t)(c0 + ii) * Np + k0 + c] : S::zero();
+          }
+          __syncthreads();
+          if (has) {
+            int ii = 0;
+            for (; ii + 8 <= kc; ii += 8) {
+              T a8[8];
 #pragma unroll
-            for (int uu = 0; uu < 8; ++uu) a8[uu] = Wf[(size_t)(ii + uu) * Np + j];
+              for (int uu = 0; uu < 8; ++uu) a8[uu] = Wf[(size_t)(c0 + ii + uu) * Np + j];
 #pragma unroll
-            for (int uu = 0; uu < 8; ++uu) {
+              for (int uu = 0; uu < 8; ++uu) {
 #pragma unroll
-              for (int tt = 0; tt < B; ++tt)
-                if (tt < nb) a8[uu] = S::fms(Wb[(ii + uu) * B + tt], z[tt], a8[uu]);
-              Wf[(size_t)(ii + uu) * Np + j] = a8[uu];
+                for (int tt = 0; tt < B; ++tt) a8[uu] = S::fms(Wb[(ii + uu) * B + tt], z[tt], a8[uu]);
+                Wf[(size_t)(c0 + ii + uu) * Np + j] = a8[uu];
+              }
+            }
+            for (; ii < kc; ++ii) {
+              T a = Wf[(size_t)(c0 + ii) * Np + j];
+#pragma unroll
+              for (int tt = 0; tt < B; ++tt) a = S::fms(Wb[ii * B + tt], z[tt], a);
+              Wf[(size_t)(c0 + ii) * Np + j] = a;
             }
           }
-          for (; ii < k0; ++ii) {
-            T a = Wf[(size_t)ii * Np + j];
-#pragma unroll
-            for (int tt = 0; tt < B; ++tt)
-              if (tt < nb) a = S::fms(Wb[ii * B + tt], z[tt], a);
-            Wf[(size_t)ii * Np + j] = a;
-          }
         }
+       }
         __threadfence();
         cluster_sync_all();  // W visible to every CTA before the next block's Wb load
       }
