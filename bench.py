@@ -37,6 +37,9 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # FP64 FMA pipe: 148 SMs x 64 FMA/clk x 2 flop x 1.965 GHz (measured: DMMA 36.9,
 # DFMA 34.1, cuBLAS DGEMM 35.5 TFLOP/s — profiles/fp64_peaks_r01.json)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel per launch, from one
+# `ncu --set full` capture of this bench command (profiles/r01_ncu_summary.md)
+TRAFFIC_BYTES = {"dw": 25294336}
 
 
 def paper_flops(cfg_L, Np, cplx):
@@ -271,6 +274,8 @@ def run_gpu(args):
         }
         if args.traffic is not None:
             line["roofline"]["traffic"] = args.traffic
+        elif not args.marginal and cfg.name in TRAFFIC_BYTES:
+            line["roofline"]["traffic"] = TRAFFIC_BYTES[cfg.name]
         if not args.no_cpu and world == 1:
             rate, n, t, cores = cpu_oracle_rate(U, uni, Np, budget_s=args.cpu_budget)
             line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": cores, "kind": "oracle",
