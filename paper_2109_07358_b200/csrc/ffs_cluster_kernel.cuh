@@ -35,9 +35,9 @@ struct ClusterParams {
   double* trace;           // [S][Np][L] or null
 };
 
-constexpr int kRingDepth = 4;  // per-thread cp.async pipeline depth of the contraction
+constexpr int kRingDepth = 8;  // per-thread cp.async pipeline depth of the contraction
 constexpr int kKC = 64;        // rows of W (or columns of the new rows) staged per chunk
-constexpr bool kUseRing = false;  // measured slower on C4/C5 (profiles/r01_ncu_summary.md)
+constexpr bool kUseRing = false;  // cp.async ring measured slower on C4/C5 (profiles/r01_ncu_summary.md)
 
 template <typename T, int B>
 struct ClusterLayout {
@@ -163,7 +163,25 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 #pragma unroll
         for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
       }
-      if constexpr (!kUseRing) {
+      // contraction over the k0 earlier columns. W rows are staged kKC at a time in shared
+      // memory; this thread's R rows of each gathered column perm[ii] are copied global->shared
+      // by cp.async kRingDepth columns ahead into a private ring (no barrier needed for it).
+      {
+        auto issue = [&](int ii) {
+          const double2* src = reinterpret_cast<const double2*>(Utg + (size_t)perm[ii] * p.Lpt + row0);
+#pragma unroll
+          for (int q = 0; q < kChunks; ++q) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ring_at(ii % kRingDepth, q)));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + q) : "memory");
+          }
+        };
+        if constexpr (kUseRing) {
+#pragma unroll
+          for (int d = 0; d < kRingDepth; ++d) {
+            if (d < k0) issue(d);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+          }
+        }
         for (int c0 = 0; c0 < k0; c0 += kKC) {
           const int kc = min(kKC, k0 - c0);
           __syncthreads();
@@ -172,61 +190,39 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             Wb[idx] = c < nb ? Wf[(size_t)(c0 + ii) * Np + k0 + c] : S::zero();
           }
           __syncthreads();
-#pragma unroll 4
-          for (int ii = 0; ii < kc; ++ii) {
-            const T* base = Utg + (size_t)perm[c0 + ii] * p.Lpt + row0;
+#pragma unroll 2
+          for (int i2 = 0; i2 < kc; ++i2) {
+            const int ii = c0 + i2;
             T v[R];
+            if constexpr (kUseRing) {
+              asm volatile("cp.async.wait_group %0;" ::"n"(kRingDepth - 1) : "memory");
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[r] = base[r];
+              for (int q = 0; q < kChunks; ++q) {
+                const double2 d2 = *ring_at(ii % kRingDepth, q);
+                if constexpr (kD == 1) {
+                  reinterpret_cast<double*>(v)[2 * q] = d2.x;
+                  reinterpret_cast<double*>(v)[2 * q + 1] = d2.y;
+                } else {
+                  v[q].re = d2.x;
+                  v[q].im = d2.y;
+                }
+              }
+              if (ii + kRingDepth < k0) issue(ii + kRingDepth);
+              asm volatile("cp.async.commit_group;" ::: "memory");
+            } else {
+              const T* base = Utg + (size_t)perm[ii] * p.Lpt + row0;
+#pragma unroll
+              for (int r = 0; r < R; ++r) v[r] = base[r];
+            }
             T wb[B];
 #pragma unroll
-            for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];
+            for (int c = 0; c < B; ++c) wb[c] = Wb[i2 * B + c];
 #pragma unroll
             for (int c = 0; c < B; ++c)
 #pragma unroll
               for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
           }
         }
-      } else {
-      // contraction over the k0 earlier columns; this thread's R rows of column perm[ii] are
-      // copied global->shared with cp.async kRingDepth columns ahead (private ring: no barrier)
-      auto issue = [&](int ii) {
-        const double2* src = reinterpret_cast<const double2*>(Utg + (size_t)perm[ii] * p.Lpt + row0);
-#pragma unroll
-        for (int q = 0; q < kChunks; ++q) {
-          const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ring_at(ii % kRingDepth, q)));
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + q) : "memory");
-        }
-      };
-#pragma unroll
-      for (int d = 0; d < kRingDepth; ++d) {
-        if (d < k0) issue(d);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      }
-      for (int ii = 0; ii < k0; ++ii) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kRingDepth - 1) : "memory");
-        T v[R];
-#pragma unroll
-        for (int q = 0; q < kChunks; ++q) {
-          const double2 d2 = *ring_at(ii % kRingDepth, q);
-          if constexpr (kD == 1) {
-            reinterpret_cast<double*>(v)[2 * q] = d2.x;
-            reinterpret_cast<double*>(v)[2 * q + 1] = d2.y;
-          } else {
-            v[q].re = d2.x;
-            v[q].im = d2.y;
-          }
-        }
-        if (ii + kRingDepth < k0) issue(ii + kRingDepth);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        T wb[B];
-#pragma unroll
-        for (int c = 0; c < B; ++c) wb[c] = Wb[ii * B + c];
-#pragma unroll
-        for (int c = 0; c < B; ++c)
-#pragma unroll
-          for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
-      }
       }  // kUseRing
       // rows drawn earlier: exactly zero weight in the first column of this block
 #pragma unroll
