@@ -12,6 +12,7 @@
 #include "ffs_warp_kernel.cuh"
 #include "ffs_pc_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
+#include "ffs_kptr.h"
 
 namespace {
 
@@ -67,7 +68,7 @@ constexpr int kWarpMaxThreads = 320;
 template <typename T, bool WARP, int R, int B, bool USMEM, int MAXT = kWarpMaxThreads>
 Variant make_variant() {
   return Variant{WARP, R, B, USMEM, MAXT,
-                 reinterpret_cast<const void*>(&ffsk::ffs_sample_kernel<T, WARP, R, B, USMEM, MAXT>)};
+                 ffsk::sample_kernel_ptr<T, WARP, R, B, USMEM, MAXT>()};
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
@@ -200,9 +201,9 @@ struct WarpPlan {
   size_t perm_smem;
 };
 
-template <int R, int B, int G, int MAXT, bool TIMING = false>
+template <int R, int B, int G, int MAXT, bool TIMING = false, int OPT = 0>
 void warp_fn_seg(WarpPlan& w) {
-  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_seg_kernel<R, B, G, MAXT, TIMING>);
+  w.fn = ffsk::seg_kernel_ptr<R, B, G, MAXT, TIMING, OPT>();
   w.R = R;
   w.B = B;
   w.S = 32 / G;  // samples per warp (one per G-lane segment)
@@ -212,7 +213,7 @@ void warp_fn_seg(WarpPlan& w) {
 
 template <int R, int B, int MAXT, bool WSMEM, bool TIMING = false>
 void warp_fn_pc(WarpPlan& w) {
-  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_pc_kernel<R, B, MAXT, WSMEM, TIMING>);
+  w.fn = ffsk::pc_kernel_ptr<R, B, MAXT, WSMEM, TIMING>();
   w.wsmem = WSMEM;
   w.R = R;
   w.B = B;
@@ -224,7 +225,7 @@ void warp_fn_pc(WarpPlan& w) {
 
 template <int R, int B, int S, int MAXREG>
 void warp_fn_r(WarpPlan& w) {
-  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_warp_kernel_r<R, B, S, MAXREG>);
+  w.fn = ffsk::warp_kernel_r_ptr<R, B, S, MAXREG>();
   w.R = R;
   w.B = B;
   w.S = S;
@@ -233,7 +234,7 @@ void warp_fn_r(WarpPlan& w) {
 
 template <int R, int B, int S, int MAXT>
 void warp_fn(WarpPlan& w) {
-  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_warp_kernel<R, B, S, MAXT>);
+  w.fn = ffsk::warp_kernel_ptr<R, B, S, MAXT>();
   w.R = R;
   w.B = B;
   w.S = S;
@@ -265,6 +266,14 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
     else if (var && strcmp(var, "seg32b8") == 0) warp_fn_seg<8, 8, 32, 256>(w);
     else if (var && strcmp(var, "seg32b4t") == 0) warp_fn_seg<8, 4, 32, 512, true>(w);
     else if (var && strcmp(var, "seg16b4t") == 0) warp_fn_seg<16, 4, 16, 256, true>(w);
+    else if (var && strcmp(var, "o1") == 0) warp_fn_seg<8, 4, 32, 384, false, 1>(w);
+    else if (var && strcmp(var, "o2") == 0) warp_fn_seg<8, 4, 32, 384, false, 2>(w);
+    else if (var && strcmp(var, "o4") == 0) warp_fn_seg<8, 4, 32, 384, false, 4>(w);
+    else if (var && strcmp(var, "o7") == 0) warp_fn_seg<8, 4, 32, 384, false, 7>(w);
+    else if (var && strcmp(var, "d384t") == 0) warp_fn_seg<8, 4, 32, 384, true, 0>(w);
+    else if (var && strcmp(var, "o4t") == 0) warp_fn_seg<8, 4, 32, 384, true, 4>(w);
+    else if (var && strcmp(var, "o7t") == 0) warp_fn_seg<8, 4, 32, 384, true, 7>(w);
+    else if (var && strcmp(var, "o7r128") == 0) warp_fn_seg<8, 4, 32, 512, false, 7>(w);
     else warp_fn_seg<8, 4, 32, 384>(w);  // 12 sample-owning warps/SM, 164 regs (profiles/)
   } else if (L <= 64) warp_fn<2, 8, 1, 384>(w);
   else if (L <= 128) warp_fn<4, 8, 1, 384>(w);
@@ -370,7 +379,7 @@ struct ClusterPlan {
 
 template <typename T, int R, int B, int MAXT>
 void cluster_fn(ClusterPlan& c) {
-  c.fn = reinterpret_cast<const void*>(&ffsk::ffs_cluster_kernel<T, R, B, MAXT>);
+  c.fn = ffsk::cluster_kernel_ptr<T, R, B, MAXT>();
   c.R = R;
   c.B = B;
   c.threads = MAXT;

@@ -129,7 +129,7 @@ __device__ __noinline__ int draw_fallback(const double* col, double T, uint32_t 
 }
 
 // U [L][N] -> per-sample permutation prefix [M][Np] (a1 rule, reading Q6); one thread per sample.
-__global__ void ffs_permute_kernel(const double* __restrict__ uniforms, int32_t* __restrict__ perm, int64_t M,
+static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, int32_t* __restrict__ perm, int64_t M,
                                    int N, int Np) {
   extern __shared__ int pscratch[];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -560,10 +560,34 @@ __device__ __forceinline__ Draw warp_draw_fast(const double (&col)[R], double u,
   return d;
 }
 
-template <int R, int G>
+template <int R, int G, bool KEEP = false>
 __device__ __forceinline__ Draw seg_draw(const double (&col)[R], double u, int seg) {
   if constexpr (false && G == 32 && R <= 8) {  // measured slower (646 vs 544 cycles/draw)
     return warp_draw_fast<R>(col, u, threadIdx.x & 31);
+  }
+  if constexpr (KEEP && R <= 8) {
+    // same partial sums as the two-pass form below (bit-identical), kept in registers so the
+    // row search after the ballot is R-1 independent compares instead of a dependent FMA chain
+    double cs[R];
+    cs[0] = col[0] * col[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) cs[r] = fma(col[r], col[r], cs[r - 1]);
+    const double tot = cs[R - 1];
+    double incl = tot;
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) incl = SegOps<G>::scan_level(incl, d);
+    const double excl = SegOps<G>::prev(incl);
+    Draw d;
+    d.T = SegOps<G>::last(incl);
+    const bool ok = (d.T > 0.0) && (d.T < INFINITY);
+    const double tp = fmax(fma(u, d.T, -excl), 0.0);
+    const unsigned b = __ballot_sync(0xffffffffu, ok && (tot > tp));
+    d.ball = (G == 32) ? b : ((b >> (seg * G)) & ((1u << G) - 1u));
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < R - 1; ++r) cnt += (cs[r] <= tp) ? 1 : 0;
+    d.rsel = cnt;
+    return d;
   }
   // Pass 1: lane total of w_r = col_r^2 (index order; for R > 8 two parallel half chains).
   constexpr int H = R > 8 ? R / 2 : R;
@@ -635,7 +659,87 @@ __device__ __noinline__ int seg_fallback(const double* col, double T, uint32_t c
   return (ln - seg * G) * R + rr;
 }
 
-template <int R, int B, int G, bool TIMING>
+// Gauss-Jordan update of one owner's W with the B new rows X_new = pos[k0 .. k0+B) (nb == B
+// whenever later columns remain), mapped over (column, row) pairs so that all G lanes work:
+//   (1) z_j = V[X_new, j] - V[X_new, 0:k0] W[0:k0, j]           (one lane per (j, t) entry)
+//   (2) z_j <- S^{-1} z_j with S = L U from the in-block draws   (one lane per column j)
+//   (3) W[0:k0, j] -= W[0:k0, k0:k0+B] z_j,  W[k0+t, j] = z_j[t]  (one lane per (i, j) entry)
+// VnT[i][t] = V[x_{k0+t}, perm[i]]; rows j >= k0+B of VnT are overwritten by z_j.
+template <int R, int B, int G>
+__device__ __forceinline__ void seg_gj_flat(const double* __restrict__ Uts, int stride, const int* perm,
+                                            const int* pos, const double* Row, const double* Pinv,
+                                            double* Wf, double* VnT, int ldw, int k0, int Np, int sl) {
+  using Sw = Swz<double, R>;
+  static_assert(G % B == 0, "lane -> t mapping needs B | G");
+  const int j0 = k0 + B, nc = Np - j0;
+  __syncwarp();
+  {
+    const int t = sl % B;  // fixed per lane because B | G
+    const int xp = Sw::phys(pos[k0 + t]);
+    for (int idx = sl; idx < Np * B; idx += G) VnT[idx] = Uts[perm[idx / B] * stride + xp];
+  }
+  __syncwarp();
+  for (int idx = sl; idx < nc * B; idx += G) {
+    const int t = idx % B, j = j0 + idx / B;
+    double a = VnT[j * B + t], a2 = 0.0;
+    int ii = 0;
+#pragma unroll 2
+    for (; ii + 1 < k0; ii += 2) {
+      a = fma(-VnT[ii * B + t], Wf[ii * ldw + j], a);
+      a2 = fma(-VnT[(ii + 1) * B + t], Wf[(ii + 1) * ldw + j], a2);
+    }
+    if (ii < k0) a = fma(-VnT[ii * B + t], Wf[ii * ldw + j], a);
+    VnT[j * B + t] = a + a2;
+  }
+  __syncwarp();
+  for (int jj = sl; jj < nc; jj += G) {
+    const int j = j0 + jj;
+    double z[B];
+#pragma unroll
+    for (int t = 0; t < B; t += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(VnT + j * B + t);
+      z[t] = v.x;
+      z[t + 1] = v.y;
+    }
+#pragma unroll
+    for (int t = 1; t < B; ++t)
+#pragma unroll
+      for (int t2 = 0; t2 < t; ++t2) z[t] = fma(-(Row[t * B + t2] * Pinv[t2]), z[t2], z[t]);
+#pragma unroll
+    for (int t = B - 1; t >= 0; --t) {
+#pragma unroll
+      for (int t2 = t + 1; t2 < B; ++t2) z[t] = fma(-Row[t * B + t2], z[t2], z[t]);
+      z[t] *= Pinv[t];
+    }
+#pragma unroll
+    for (int t = 0; t < B; t += 2) *reinterpret_cast<double2*>(VnT + j * B + t) = make_double2(z[t], z[t + 1]);
+#pragma unroll
+    for (int t = 0; t < B; ++t) Wf[(k0 + t) * ldw + j] = z[t];
+  }
+  __syncwarp();
+  if (k0 > 0) {
+    const float rnc = 1.0f / (float)nc;
+    for (int idx = sl; idx < k0 * nc; idx += G) {
+      int ii = __float2int_rz(((float)idx + 0.5f) * rnc);  // idx / nc (idx < 2^12: exact)
+      const int j = j0 + idx - ii * nc;
+      double a = Wf[ii * ldw + j];
+#pragma unroll
+      for (int t = 0; t < B; t += 2) {
+        const double2 wb = *reinterpret_cast<const double2*>(Wf + ii * ldw + k0 + t);
+        const double2 zz = *reinterpret_cast<const double2*>(VnT + j * B + t);
+        a = fma(-wb.x, zz.x, a);
+        a = fma(-wb.y, zz.y, a);
+      }
+      Wf[ii * ldw + j] = a;
+    }
+  }
+  __syncwarp();
+}
+
+// OPT bits (development variants, FFS_WARP_VARIANT): 1 = draw keeps its partial sums,
+// 2 = pivot row through shared memory (owner lane stores it, no select tree / shuffles),
+// 4 = Gauss-Jordan update mapped over (column, row) pairs instead of one lane per column.
+template <int R, int B, int G, bool TIMING, int OPT = 0>
 __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
   extern __shared__ __align__(16) unsigned char smem[];
   using Sw = Swz<double, R>;
@@ -747,7 +851,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
 #pragma unroll
         for (int r = 0; r < R; ++r) col0[r] = P[r][0];
         if (p.dbg & 2) { dr.ball = 1u; dr.rsel = (k0 / B) % R; dr.T = 1.0; }
-        else dr = seg_draw<R, G>(col0, usel[k0], seg);
+        else dr = seg_draw<R, G, (OPT & 1) != 0>(col0, usel[k0], seg);
       }
       static_for<0, B>([&](auto rrc) {
         constexpr int rr = decltype(rrc)::value;
@@ -755,10 +859,10 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           const int k = k0 + rr;
           long long ts0 = 0;
           if constexpr (tm) ts0 = clock64();
-          int own, orow;  // owner lane within the segment, row within the owner
+          int own, orow = 0;  // owner lane within the segment, row within the owner
           if (__all_sync(0xffffffffu, dr.ball != 0u)) {
             own = __ffs(dr.ball) - 1;
-            orow = __shfl_sync(0xffffffffu, dr.rsel, seg * G + own);
+            if constexpr (!(OPT & 2)) orow = __shfl_sync(0xffffffffu, dr.rsel, seg * G + own);
           } else {
             // rare: some segment has u*T at/after its last partial sum, or T not finite/positive
             int o = 0, rw = 0;
@@ -791,32 +895,50 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           // lane's selection is then broadcast to its segment with shuffles (no smem, no branch)
           const double Tk = dr.T;
           const int rs = dr.ball != 0u ? dr.rsel : orow;
-          double prow[B];
+          double pv;  // pivot P[x_k][rr]
+          if constexpr ((OPT & 2) != 0) {
+            // the owner lane stores row rs of its block (the row it selected itself) into Row
+            const bool mine = (sl == own);
 #pragma unroll
-          for (int c = 0; c < B; ++c) {
-            double t[R];
+            for (int r = 0; r < R; ++r)
+              if (mine && r == rs) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) t[r] = P[r][c];
+                for (int c = 0; c < B; c += 2)
+                  *reinterpret_cast<double2*>(Row + rr * B + c) = make_double2(P[r][c], P[r][c + 1]);
+              }
+            if (mine) pos[k] = own * R + rs;
+            chosen |= mine ? (1u << rs) : 0u;
+            __syncwarp();
+            pv = Row[rr * B + rr];
+          } else {
+            double prow[B];
 #pragma unroll
-            for (int w = 1; w < R; w <<= 1)
+            for (int c = 0; c < B; ++c) {
+              double t[R];
 #pragma unroll
-              for (int i = 0; i < R; i += 2 * w) t[i] = (rs & w) ? t[i + w] : t[i];
-            prow[c] = __shfl_sync(0xffffffffu, t[0], seg * G + own);
+              for (int r = 0; r < R; ++r) t[r] = P[r][c];
+#pragma unroll
+              for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+                for (int i = 0; i < R; i += 2 * w) t[i] = (rs & w) ? t[i + w] : t[i];
+              prow[c] = __shfl_sync(0xffffffffu, t[0], seg * G + own);
+            }
+            chosen |= (sl == own) ? (1u << orow) : 0u;
+            if (sl == 0) {
+              pos[k] = own * R + orow;
+#pragma unroll
+              for (int c = 0; c < B; c += 2)
+                *reinterpret_cast<double2*>(Row + rr * B + c) = make_double2(prow[c], prow[c + 1]);
+            }
+            pv = prow[rr];
           }
-          chosen |= (sl == own) ? (1u << orow) : 0u;
-          if (prow[rr] * prow[rr] < 1e-12 * Tk) flag |= 2;
-          if (sl == 0) {
-            pos[k] = own * R + orow;
-#pragma unroll
-            for (int c = 0; c < B; c += 2)
-              *reinterpret_cast<double2*>(Row + rr * B + c) = make_double2(prow[c], prow[c + 1]);
-          }
+          if (pv * pv < 1e-12 * Tk) flag |= 2;
           if constexpr (tm) {
-            const long long t = clock64() + (long long)(prow[0] * 0.0);
+            const long long t = clock64() + (long long)(pv * 0.0);
             tacc[4] += (t - ts0);
             ts0 = t;
           }
-          const double ip = fast_rcp(prow[rr]);
+          const double ip = fast_rcp(pv);
           if constexpr (tm) {
             const long long t = clock64() + (long long)(ip * 0.0);
             tacc[5] += (t - ts0);
@@ -840,7 +962,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
 #pragma unroll
               for (int r = 0; r < R; ++r) cn[r] = P[r][rr + 1];
               if (p.dbg & 2) { dr.ball = 1u << ((k + 1) % G); dr.rsel = (k + 1) / G % R; dr.T = 1.0 + cn[0] * 1e-300; }
-              else dr = seg_draw<R, G>(cn, usel[k + 1], seg);
+              else dr = seg_draw<R, G, (OPT & 1) != 0>(cn, usel[k + 1], seg);
               if constexpr (tm) {
                 const long long t = clock64() + (long long)(dr.T * 0.0) + dr.rsel * 0;
                 tacc[6] += (t - ts0);
@@ -861,7 +983,9 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
         tA = t;
       }
       // ---- Gauss-Jordan update of W with the nb new rows (only if later columns remain)
-      if (k0 + nb < Np && !(p.dbg & 4)) {
+      if constexpr ((OPT & 4) != 0) {
+        if (k0 + nb < Np && !(p.dbg & 4)) seg_gj_flat<R, B, G>(Uts, stride, perm, pos, Row, Pinv, Wf, VnT, ldw, k0, Np, sl);
+      } else if (k0 + nb < Np && !(p.dbg & 4)) {
         __syncwarp();
         for (int idx = sl; idx < Np * B; idx += G) {
           const int ii = idx / B, tt = idx % B;
@@ -932,9 +1056,9 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
   }
 }
 
-template <int R, int B, int G, int MAXT, bool TIMING = false>
+template <int R, int B, int G, int MAXT, bool TIMING = false, int OPT = 0>
 __global__ void __launch_bounds__(MAXT, 1) ffs_seg_kernel(const WarpParams p) {
-  ffs_seg_body<R, B, G, TIMING>(p);
+  ffs_seg_body<R, B, G, TIMING, OPT>(p);
 }
 
 }  // namespace ffsk

@@ -19,7 +19,7 @@ L.ffs_dev_timing(buf, 1)
 ms = e0.elapsed_time(e1)
 tot = sum(buf[:3])
 sps = cfg.M * cfg.N
-names = ["gemm+init", "steps", "gj", "finish", "switch+sync", "rcp", "col+nextdraw"]
+names = ["gemm+init", "steps", "gj", "owner", "extract", "rcp", "col+nextdraw"]
 if os.environ.get("FFS_WARP_VARIANT", "").startswith("pc"):
     names = ["prod_wait", "prod_gj", "prod_gemm", "cons_wait", "cons_steps"]
 print(f"{os.environ.get('FFS_WARP_VARIANT','default')}: {ms:.3f} ms; cycles per sample-step (sum over warps / sample-steps):",
