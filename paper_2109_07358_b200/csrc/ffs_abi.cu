@@ -194,6 +194,7 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
 struct WarpPlan {
   const void* fn;
   int R, B, S, G = 32, maxt, warps, grid, Lp, ut_stride;
+  bool legacy = false;  // whole-warp ffs_warp_kernel (its own W layout)
   bool pc = false;  // producer/consumer kernel (owner = consumer+producer warp pair, 2 slots)
   bool wsmem = false;  // pc kernel keeps W in shared memory
   size_t ushared, owner, smem, ws_perm, ws_w = 0;
@@ -225,6 +226,7 @@ void warp_fn_pc(WarpPlan& w) {
 
 template <int R, int B, int S, int MAXREG>
 void warp_fn_r(WarpPlan& w) {
+  w.legacy = true;
   w.fn = ffsk::warp_kernel_r_ptr<R, B, S, MAXREG>();
   w.R = R;
   w.B = B;
@@ -234,6 +236,7 @@ void warp_fn_r(WarpPlan& w) {
 
 template <int R, int B, int S, int MAXT>
 void warp_fn(WarpPlan& w) {
+  w.legacy = true;
   w.fn = ffsk::warp_kernel_ptr<R, B, S, MAXT>();
   w.R = R;
   w.B = B;
@@ -250,31 +253,23 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   const char* var = getenv("FFS_WARP_VARIANT");  // development: "b6" selects B=6 for R=8
   const bool legacy = var && strncmp(var, "w", 1) == 0;  // "w..." = whole-warp owner variants
   if (!legacy) {
-    if (L <= 16) warp_fn_seg<2, 4, 8, 512>(w);
-    else if (L <= 32) warp_fn_seg<4, 4, 8, 512>(w);
-    else if (L <= 64) warp_fn_seg<8, 4, 8, 512>(w);
-    else if (L <= 128) warp_fn_seg<8, 4, 16, 512>(w);
-    else if (var && strcmp(var, "seg16b4r168") == 0) warp_fn_seg<16, 4, 16, 384>(w);
-    else if (var && strcmp(var, "seg16b4r128") == 0) warp_fn_seg<16, 4, 16, 512>(w);
-    else if (var && strcmp(var, "seg32b4") == 0) warp_fn_seg<8, 4, 32, 512>(w);
-    else if (var && strcmp(var, "seg32b4r168") == 0) warp_fn_seg<8, 4, 32, 384>(w);
-    else if (var && strcmp(var, "pc512") == 0) warp_fn_pc<8, 4, 512, false>(w);
-    else if (var && strcmp(var, "pc384") == 0) warp_fn_pc<8, 4, 384, false>(w);
-    else if (var && strcmp(var, "pcs") == 0) warp_fn_pc<8, 4, 512, true>(w);
+    // segmented kernel, OPT = 7: kept partial sums, pivot row through smem, flat Gauss-Jordan
+    // (variants measured in profiles/r01_ncu_summary.md; "base" = the first segmented kernel)
+    const bool base = var && strcmp(var, "base") == 0;
+    const size_t ush = ffsk::align16((size_t)N * (256 + 2) * 8);
+    const bool fits16 = ush + 16 * ffsk::WarpLayout((int)Np, 4, true).total <= kMaxSmem;
+    if (L <= 16) warp_fn_seg<2, 4, 8, 512, false, 7>(w);
+    else if (L <= 32) warp_fn_seg<4, 4, 8, 512, false, 7>(w);
+    else if (L <= 64) warp_fn_seg<8, 4, 8, 384, false, 7>(w);
+    else if (L <= 128) warp_fn_seg<8, 4, 16, 384, false, 7>(w);
+    else if (base) warp_fn_seg<8, 4, 32, 384, false, 0>(w);
+    else if (var && strcmp(var, "o7_384") == 0) warp_fn_seg<8, 4, 32, 384, false, 7>(w);
+    else if (var && strcmp(var, "b8") == 0) warp_fn_seg<8, 8, 32, 256, false, 7>(w);
     else if (var && strcmp(var, "pcs256") == 0) warp_fn_pc<8, 4, 256, true>(w);
     else if (var && strcmp(var, "pcs256t") == 0) warp_fn_pc<8, 4, 256, true, true>(w);
-    else if (var && strcmp(var, "seg32b8") == 0) warp_fn_seg<8, 8, 32, 256>(w);
-    else if (var && strcmp(var, "seg32b4t") == 0) warp_fn_seg<8, 4, 32, 512, true>(w);
-    else if (var && strcmp(var, "seg16b4t") == 0) warp_fn_seg<16, 4, 16, 256, true>(w);
-    else if (var && strcmp(var, "o1") == 0) warp_fn_seg<8, 4, 32, 384, false, 1>(w);
-    else if (var && strcmp(var, "o2") == 0) warp_fn_seg<8, 4, 32, 384, false, 2>(w);
-    else if (var && strcmp(var, "o4") == 0) warp_fn_seg<8, 4, 32, 384, false, 4>(w);
-    else if (var && strcmp(var, "o7") == 0) warp_fn_seg<8, 4, 32, 384, false, 7>(w);
-    else if (var && strcmp(var, "d384t") == 0) warp_fn_seg<8, 4, 32, 384, true, 0>(w);
-    else if (var && strcmp(var, "o4t") == 0) warp_fn_seg<8, 4, 32, 384, true, 4>(w);
-    else if (var && strcmp(var, "o7t") == 0) warp_fn_seg<8, 4, 32, 384, true, 7>(w);
-    else if (var && strcmp(var, "o7r128") == 0) warp_fn_seg<8, 4, 32, 512, false, 7>(w);
-    else warp_fn_seg<8, 4, 32, 384>(w);  // 12 sample-owning warps/SM, 164 regs (profiles/)
+    else if (var && strcmp(var, "t") == 0) warp_fn_seg<8, 4, 32, 512, true, 7>(w);  // phase timing
+    else if (fits16) warp_fn_seg<8, 4, 32, 512, false, 7>(w);  // 16 owners/SM, 128 regs
+    else warp_fn_seg<8, 4, 32, 384, false, 7>(w);              // 12 owners/SM (larger N')
   } else if (L <= 64) warp_fn<2, 8, 1, 384>(w);
   else if (L <= 128) warp_fn<4, 8, 1, 384>(w);
   else if (var && strcmp(var, "wb8") == 0) warp_fn<8, 8, 1, 256>(w);
@@ -290,7 +285,7 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   w.ut_stride = w.Lp + 2;
   w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
   w.owner = w.pc ? ffsk::pc_pair_bytes((int)Np, w.B, w.R, w.wsmem)  // per consumer/producer pair
-                 : ffsk::WarpLayout((int)Np, w.B).total;         // per sample; a warp holds S slices
+                 : ffsk::WarpLayout((int)Np, w.B, !w.legacy).total;         // per sample; a warp holds S slices
   // registers are allocated per SM sub-partition (4 x 16K); warps are spread round-robin
   const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
   int warps = std::min(w.maxt / 32, by_regs);

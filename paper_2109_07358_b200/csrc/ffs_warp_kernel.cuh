@@ -26,8 +26,11 @@ constexpr int kMaxNpWarp = 48;
 struct WarpLayout {
   size_t perm, pos, usel, row, pinv, wf, vnt, dump, total;
   int ldw;  // row stride of W: Np + B rounded to even; columns [Np, ldw) stay zero
-  __host__ __device__ WarpLayout(int Np, int B) {
-    ldw = (Np + B + 1) & ~1;
+  // seg: layout of the segmented kernel (no dump slice; W without padding columns when B | N')
+  __host__ __device__ WarpLayout(int Np, int B, bool seg = false) {
+    // (Np + 2 when B | N': rows of W start 16 bytes apart in bank space, so the flat
+    // Gauss-Jordan mapping's (row, column) accesses do not collide)
+    ldw = (seg && Np % B == 0) ? ((Np + 3) & ~1) : ((Np + B + 1) & ~1);
     size_t o = 0;
     perm = o; o = align16(o + sizeof(int) * Np);
     pos = o;  o = align16(o + sizeof(int) * Np);
@@ -36,7 +39,7 @@ struct WarpLayout {
     pinv = o; o = align16(o + sizeof(double) * B);
     wf = o;   o = align16(o + sizeof(double) * (size_t)Np * ldw);
     vnt = o;  o = align16(o + sizeof(double) * (size_t)Np * B);
-    dump = o; o = align16(o + sizeof(double) * 16 * 8);  // owner lane's R x B panel (R<=16, B<=8)
+    dump = o; o = align16(o + (seg ? 0 : sizeof(double) * 16 * 8));  // owner's R x B panel (legacy)
     total = o;
   }
 };
@@ -482,42 +485,19 @@ __device__ __forceinline__ double fast_rcp(double a) {
 
 template <int G>
 struct SegOps {
-  static constexpr unsigned kUpC = (unsigned)(32 - G) << 8;         // shfl.up segment control
-  static constexpr unsigned kIdxC = ((unsigned)(32 - G) << 8) | 31u;  // shfl.idx segment control
   // v + (value of segment lane - d) for segment lanes >= d
   __device__ __forceinline__ static double scan_level(double v, int d) {
-    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, ylo, yhi;\n\t.reg .f64 y;\n\t"
-        "mov.b64 {lo, hi}, %0;\n\t"
-        "shfl.sync.up.b32 ylo|p, lo, %1, %2, -1;\n\t"
-        "shfl.sync.up.b32 yhi, hi, %1, %2, -1;\n\t"
-        "mov.b64 y, {ylo, yhi};\n\t"
-        "@p add.f64 %0, %0, y;\n\t}"
-        : "+d"(v) : "r"(d), "r"(kUpC));
-    return v;
+    double y = __shfl_up_sync(0xffffffffu, v, d, G);
+    y = ((int)(threadIdx.x & (G - 1)) >= d) ? y : 0.0;  // v >= 0: v + 0.0 == v
+    return v + y;
   }
   // value of segment lane - 1, 0 for the first segment lane
   __device__ __forceinline__ static double prev(double v) {
-    double r;
-    asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, ylo, yhi;\n\t"
-        "mov.b64 {lo, hi}, %1;\n\t"
-        "shfl.sync.up.b32 ylo|p, lo, 1, %2, -1;\n\t"
-        "shfl.sync.up.b32 yhi, hi, 1, %2, -1;\n\t"
-        "mov.b64 %0, {ylo, yhi};\n\t"
-        "@!p mov.f64 %0, 0d0000000000000000;\n\t}"
-        : "=d"(r) : "d"(v), "r"(kUpC));
-    return r;
+    const double y = __shfl_up_sync(0xffffffffu, v, 1, G);
+    return (threadIdx.x & (G - 1)) != 0 ? y : 0.0;
   }
   // value of the last lane of the segment
-  __device__ __forceinline__ static double last(double v) {
-    double r;
-    asm("{\n\t.reg .b32 lo, hi, ylo, yhi;\n\t"
-        "mov.b64 {lo, hi}, %1;\n\t"
-        "shfl.sync.idx.b32 ylo, lo, %2, %3, -1;\n\t"
-        "shfl.sync.idx.b32 yhi, hi, %2, %3, -1;\n\t"
-        "mov.b64 %0, {ylo, yhi};\n\t}"
-        : "=d"(r) : "d"(v), "r"(G - 1), "r"(kIdxC));
-    return r;
-  }
+  __device__ __forceinline__ static double last(double v) { return __shfl_sync(0xffffffffu, v, G - 1, G); }
 };
 
 // Branch-free part of a draw for one segment (see draw_part1): returns the crossing lanes of
@@ -608,10 +588,11 @@ __device__ __forceinline__ Draw seg_draw(const double (&col)[R], double u, int s
   const double excl = SegOps<G>::prev(incl);
   Draw d;
   d.T = SegOps<G>::last(incl);
-  const bool ok = (d.T > 0.0) && (d.T < INFINITY);
+  const bool ok = (d.T > 0.0) && (d.T <= 1.7976931348623157e308);  // positive and finite
   // crossing threshold relative to this lane's exclusive prefix, clamped at 0 so that a lane
   // whose rounded prefix already passed u*T still lands on its first positive weight
-  const double tp = fmax(fma(u, d.T, -excl), 0.0);
+  const double tq = fma(u, d.T, -excl);
+  const double tp = tq > 0.0 ? tq : 0.0;
   const unsigned b = __ballot_sync(0xffffffffu, ok && (tot > tp));
   d.ball = (G == 32) ? b : ((b >> (seg * G)) & ((1u << G) - 1u));
   // Pass 2: the same partial sums again (bit-identical), count rows with C_r <= tp (r < R-1).
@@ -664,32 +645,35 @@ __device__ __noinline__ int seg_fallback(const double* col, double T, uint32_t c
 //   (1) z_j = V[X_new, j] - V[X_new, 0:k0] W[0:k0, j]           (one lane per (j, t) entry)
 //   (2) z_j <- S^{-1} z_j with S = L U from the in-block draws   (one lane per column j)
 //   (3) W[0:k0, j] -= W[0:k0, k0:k0+B] z_j,  W[k0+t, j] = z_j[t]  (one lane per (i, j) entry)
-// VnT[i][t] = V[x_{k0+t}, perm[i]]; rows j >= k0+B of VnT are overwritten by z_j.
+// VnT[i][t] = V[x_{k0+t}, m_i] (perm[i] = m_i * stride, the U^T column offset); rows j >= k0+B of
+// VnT are overwritten by z_j.
 template <int R, int B, int G>
 __device__ __forceinline__ void seg_gj_flat(const double* __restrict__ Uts, int stride, const int* perm,
                                             const int* pos, const double* Row, const double* Pinv,
                                             double* Wf, double* VnT, int ldw, int k0, int Np, int sl) {
   using Sw = Swz<double, R>;
   static_assert(G % B == 0, "lane -> t mapping needs B | G");
+  static_assert(B % 4 == 0, "step (1) takes four rows per iteration; k0 is a multiple of B");
   const int j0 = k0 + B, nc = Np - j0;
   __syncwarp();
   {
     const int t = sl % B;  // fixed per lane because B | G
     const int xp = Sw::phys(pos[k0 + t]);
-    for (int idx = sl; idx < Np * B; idx += G) VnT[idx] = Uts[perm[idx / B] * stride + xp];
+    for (int idx = sl; idx < Np * B; idx += G) VnT[idx] = Uts[perm[idx / B] + xp];
   }
   __syncwarp();
   for (int idx = sl; idx < nc * B; idx += G) {
     const int t = idx % B, j = j0 + idx / B;
-    double a = VnT[j * B + t], a2 = 0.0;
-    int ii = 0;
+    // k0 is a multiple of B (>= 4 when nonzero): four independent partial sums
+    double a0 = VnT[j * B + t], a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll 2
-    for (; ii + 1 < k0; ii += 2) {
-      a = fma(-VnT[ii * B + t], Wf[ii * ldw + j], a);
-      a2 = fma(-VnT[(ii + 1) * B + t], Wf[(ii + 1) * ldw + j], a2);
+    for (int ii = 0; ii < k0; ii += 4) {
+      a0 = fma(-VnT[ii * B + t], Wf[ii * ldw + j], a0);
+      a1 = fma(-VnT[(ii + 1) * B + t], Wf[(ii + 1) * ldw + j], a1);
+      a2 = fma(-VnT[(ii + 2) * B + t], Wf[(ii + 2) * ldw + j], a2);
+      a3 = fma(-VnT[(ii + 3) * B + t], Wf[(ii + 3) * ldw + j], a3);
     }
-    if (ii < k0) a = fma(-VnT[ii * B + t], Wf[ii * ldw + j], a);
-    VnT[j * B + t] = a + a2;
+    VnT[j * B + t] = (a0 + a1) + (a2 + a3);
   }
   __syncwarp();
   for (int jj = sl; jj < nc; jj += G) {
@@ -719,18 +703,20 @@ __device__ __forceinline__ void seg_gj_flat(const double* __restrict__ Uts, int 
   __syncwarp();
   if (k0 > 0) {
     const float rnc = 1.0f / (float)nc;
-    for (int idx = sl; idx < k0 * nc; idx += G) {
+    const int n = k0 * nc;
+#pragma unroll 2
+    for (int idx = sl; idx < n; idx += G) {
       int ii = __float2int_rz(((float)idx + 0.5f) * rnc);  // idx / nc (idx < 2^12: exact)
       const int j = j0 + idx - ii * nc;
-      double a = Wf[ii * ldw + j];
+      double a = Wf[ii * ldw + j], b = 0.0;
 #pragma unroll
       for (int t = 0; t < B; t += 2) {
         const double2 wb = *reinterpret_cast<const double2*>(Wf + ii * ldw + k0 + t);
         const double2 zz = *reinterpret_cast<const double2*>(VnT + j * B + t);
         a = fma(-wb.x, zz.x, a);
-        a = fma(-wb.y, zz.y, a);
+        b = fma(-wb.y, zz.y, b);
       }
-      Wf[ii * ldw + j] = a;
+      Wf[ii * ldw + j] = a + b;
     }
   }
   __syncwarp();
@@ -759,7 +745,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
   }
   __syncthreads();
 
-  const WarpLayout lay(Np, B);
+  const WarpLayout lay(Np, B, true);
   const int ldw = lay.ldw;
   unsigned char* ob = smem + p.ushared + (size_t)(wid * SEGS + seg) * p.owner_bytes;
   int* perm = reinterpret_cast<int*>(ob + lay.perm);
@@ -769,7 +755,6 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
   double* Pinv = reinterpret_cast<double*>(ob + lay.pinv);
   double* Wf = reinterpret_cast<double*>(ob + lay.wf);
   double* VnT = reinterpret_cast<double*>(ob + lay.vnt);
-  double* Dump = reinterpret_cast<double*>(ob + lay.dump);
   const int sw = Sw::sw(sl);
   const double* Ucol0 = Uts + sl * R;
   int qoff[R / 2];  // swizzled 16-byte chunk offsets of this lane's rows within a column
@@ -785,7 +770,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
     const int64_t id = g * SEGS + seg;
     const int64_t i = id < p.M ? id : p.M - 1;  // a short last group recomputes a sample
     for (int j = sl; j < Np; j += G) {
-      perm[j] = p.perm[i * Np + j];
+      perm[j] = p.perm[i * Np + j] * stride;  // U^T column offset of m_j
       usel[j] = p.uniforms[i * 2 * (int64_t)Np + Np + j];
     }
     __syncwarp();
@@ -801,20 +786,66 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
       double P[R][B];
 #pragma unroll
       for (int c = 0; c < B; ++c) {
-        const double* cb = Ucol0 + perm[min(k0 + c, Np - 1)] * stride;
+        const double* cb = Ucol0 + perm[min(k0 + c, Np - 1)];
 #pragma unroll
         for (int q = 0; q < R / 2; ++q) {
           const double2 d = *reinterpret_cast<const double2*>(cb + qoff[q]);
-          P[2 * q][c] = (c < nb) ? d.x : 0.0;
-          P[2 * q + 1][c] = (c < nb) ? d.y : 0.0;
+          P[2 * q][c] = d.x;
+          P[2 * q + 1][c] = d.y;
         }
       }
-      {
+      if (nb < B) {  // ragged last block: columns past N' are zero
+#pragma unroll
+        for (int c = 1; c < B; ++c)
+          if (c >= nb)
+#pragma unroll
+            for (int r = 0; r < R; ++r) P[r][c] = 0.0;
+      }
+      if constexpr ((OPT & 16) != 0) {
+        // software-pipelined contraction: operands of row ii+1 (and the permutation entry of
+        // ii+2) are loaded before the 2 R B FMAs of row ii are issued
+        const int kend = (p.dbg & 1) ? 0 : k0;
+        if (kend > 0) {
+          double2 ua[R / 2], wa[B / 2];
+          int pn = perm[min(1, kend - 1)];
+          {
+            const double* cb = Ucol0 + perm[0];
+#pragma unroll
+            for (int q = 0; q < R / 2; ++q) ua[q] = *reinterpret_cast<const double2*>(cb + qoff[q]);
+#pragma unroll
+            for (int c = 0; c < B; c += 2) wa[c / 2] = *reinterpret_cast<const double2*>(Wf + k0 + c);
+          }
+          for (int ii = 0; ii < kend; ++ii) {
+            const int nx = min(ii + 1, kend - 1);
+            const double* cb = Ucol0 + pn;
+            pn = perm[min(ii + 2, kend - 1)];
+            double2 ub[R / 2], wn[B / 2];
+#pragma unroll
+            for (int q = 0; q < R / 2; ++q) ub[q] = *reinterpret_cast<const double2*>(cb + qoff[q]);
+#pragma unroll
+            for (int c = 0; c < B; c += 2) wn[c / 2] = *reinterpret_cast<const double2*>(Wf + nx * ldw + k0 + c);
+#pragma unroll
+            for (int q = 0; q < R / 2; ++q) {
+#pragma unroll
+              for (int c = 0; c < B; c += 2) {
+                P[2 * q][c] = fma(-ua[q].x, wa[c / 2].x, P[2 * q][c]);
+                P[2 * q][c + 1] = fma(-ua[q].x, wa[c / 2].y, P[2 * q][c + 1]);
+                P[2 * q + 1][c] = fma(-ua[q].y, wa[c / 2].x, P[2 * q + 1][c]);
+                P[2 * q + 1][c + 1] = fma(-ua[q].y, wa[c / 2].y, P[2 * q + 1][c + 1]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < R / 2; ++q) ua[q] = ub[q];
+#pragma unroll
+            for (int c = 0; c < B / 2; ++c) wa[c] = wn[c];
+          }
+        }
+      } else {
         const int kend = (p.dbg & 1) ? 0 : k0;
         const double* wrow = Wf + k0;
 #pragma unroll 2
         for (int ii = 0; ii < kend; ++ii, wrow += ldw) {
-          const double* cb = Ucol0 + perm[ii] * stride;
+          const double* cb = Ucol0 + perm[ii];
           double wb[B];
 #pragma unroll
           for (int c = 0; c < B; c += 2) {
@@ -860,9 +891,13 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           long long ts0 = 0;
           if constexpr (tm) ts0 = clock64();
           int own, orow = 0;  // owner lane within the segment, row within the owner
-          if (__all_sync(0xffffffffu, dr.ball != 0u)) {
+          // G == 32: one segment per warp, dr.ball is warp-uniform (no vote needed)
+          bool common;
+          if constexpr (G == 32 && (OPT & 32) != 0) common = dr.ball != 0u;
+          else common = __all_sync(0xffffffffu, dr.ball != 0u);
+          if (common) {
             own = __ffs(dr.ball) - 1;
-            if constexpr (!(OPT & 2)) orow = __shfl_sync(0xffffffffu, dr.rsel, seg * G + own);
+            if constexpr (!(OPT & 34)) orow = __shfl_sync(0xffffffffu, dr.rsel, seg * G + own);
           } else {
             // rare: some segment has u*T at/after its last partial sum, or T not finite/positive
             int o = 0, rw = 0;
@@ -896,7 +931,34 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           const double Tk = dr.T;
           const int rs = dr.ball != 0u ? dr.rsel : orow;
           double pv;  // pivot P[x_k][rr]
-          if constexpr ((OPT & 2) != 0) {
+          double prow[B];
+          if constexpr ((OPT & 32) != 0) {
+            // columns rr and rr+1 first: they feed the reciprocal and the next column's update
+            // (the critical path); the others only feed the in-block updates and Row
+            auto extract = [&](int c) {
+              double t[R];
+#pragma unroll
+              for (int r = 0; r < R; ++r) t[r] = P[r][c];
+#pragma unroll
+              for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+                for (int i = 0; i < R; i += 2 * w) t[i] = (rs & w) ? t[i + w] : t[i];
+              return __shfl_sync(0xffffffffu, t[0], seg * G + own);
+            };
+            prow[rr] = extract(rr);
+            if constexpr (rr + 1 < B) prow[rr + 1] = extract(rr + 1);
+#pragma unroll
+            for (int c = 0; c < B; ++c)
+              if (c != rr && c != rr + 1) prow[c] = extract(c);
+            chosen |= (sl == own) ? (1u << rs) : 0u;
+            if (sl == own) pos[k] = own * R + rs;
+            if (sl == 0) {
+#pragma unroll
+              for (int c = 0; c < B; c += 2)
+                *reinterpret_cast<double2*>(Row + rr * B + c) = make_double2(prow[c], prow[c + 1]);
+            }
+            pv = prow[rr];
+          } else if constexpr ((OPT & 2) != 0) {
             // the owner lane stores row rs of its block (the row it selected itself) into Row
             const bool mine = (sl == own);
 #pragma unroll
@@ -911,7 +973,6 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
             __syncwarp();
             pv = Row[rr * B + rr];
           } else {
-            double prow[B];
 #pragma unroll
             for (int c = 0; c < B; ++c) {
               double t[R];
@@ -947,11 +1008,16 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           if (sl == 0) Pinv[rr] = ip;
           if constexpr (rr + 1 < B) {
             double sp[B];  // pivot row scaled by 1/pivot
+            if constexpr ((OPT & 32) != 0) {
 #pragma unroll
-            for (int c = 0; c < B; c += 2) {
-              const double2 d = *reinterpret_cast<const double2*>(Row + rr * B + c);
-              sp[c] = d.x * ip;
-              sp[c + 1] = d.y * ip;
+              for (int c = 0; c < B; ++c) sp[c] = prow[c] * ip;
+            } else {
+#pragma unroll
+              for (int c = 0; c < B; c += 2) {
+                const double2 d = *reinterpret_cast<const double2*>(Row + rr * B + c);
+                sp[c] = d.x * ip;
+                sp[c + 1] = d.y * ip;
+              }
             }
             // column rr+1 first, then the next draw, then the remaining columns
 #pragma unroll
@@ -989,7 +1055,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
         __syncwarp();
         for (int idx = sl; idx < Np * B; idx += G) {
           const int ii = idx / B, tt = idx % B;
-          VnT[idx] = (tt < nb) ? Uts[perm[ii] * stride + Sw::phys(pos[k0 + tt])] : 0.0;
+          VnT[idx] = (tt < nb) ? Uts[perm[ii] + Sw::phys(pos[k0 + tt])] : 0.0;
         }
         __syncwarp();
         for (int j = k0 + nb + sl; j < Np; j += G) {
