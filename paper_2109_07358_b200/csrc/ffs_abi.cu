@@ -532,6 +532,7 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   char* w = static_cast<char*>(ws);
   ffsk::Params p{};
+  if (const char* dbg = getenv("FFS_DEBUG_SKIP")) p.dbg = atoi(dbg);  // development only
   p.U = static_cast<const double*>(U);
   p.Ut = pl.v.usmem ? nullptr : reinterpret_cast<const double*>(w);
   p.L = (int)L;

@@ -42,6 +42,7 @@ struct Params {
   double* trace;           // [S][Np][L] or null
   size_t owner_smem;       // bytes of per-owner shared memory
   size_t ushared_smem;     // bytes of the shared U^T copy (shared-U path)
+  int dbg;                 // development switches (FFS_DEBUG_SKIP)
 };
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }

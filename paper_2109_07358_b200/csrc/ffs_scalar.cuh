@@ -8,6 +8,17 @@ struct cplx {
   double re, im;
 };
 
+// 1/a to ~1 ulp: hardware approximation + two Newton steps (no slow path; pivots are normal
+// numbers — a zero or subnormal pivot only occurs on the flagged degenerate path)
+__device__ __forceinline__ double fast_rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <typename T> struct Sc;
 
 template <> struct Sc<double> {
@@ -17,7 +28,7 @@ template <> struct Sc<double> {
   __device__ __forceinline__ static double fms(double a, double b, double c) { return fma(-a, b, c); }
   __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
   __device__ __forceinline__ static double abs2(double a) { return a * a; }
-  __device__ __forceinline__ static double recip(double a) { return 1.0 / a; }
+  __device__ __forceinline__ static double recip(double a) { return fast_rcp(a); }
   __device__ __forceinline__ static bool finite(double a) { return isfinite(a); }
 };
 
@@ -38,7 +49,7 @@ template <> struct Sc<cplx> {
   }
   __device__ __forceinline__ static double abs2(cplx a) { return fma(a.re, a.re, a.im * a.im); }
   __device__ __forceinline__ static cplx recip(cplx a) {
-    double d = 1.0 / fma(a.re, a.re, a.im * a.im);
+    double d = fast_rcp(fma(a.re, a.re, a.im * a.im));
     return {a.re * d, -a.im * d};
   }
   __device__ __forceinline__ static bool finite(cplx a) { return isfinite(a.re) && isfinite(a.im); }

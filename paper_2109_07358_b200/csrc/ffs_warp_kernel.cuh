@@ -473,16 +473,6 @@ __global__ void __maxnreg__(MAXREG) ffs_warp_kernel_r(const WarpParams p) {
 // pivot) then serve 32/G samples at once, and the register file holds 32/G panels per warp.
 // Lane s of a segment owns rows s*R .. s*R+R-1 of its sample (index order = scan order).
 // =====================================================================================
-// 1/a to ~1 ulp: hardware approximation + two Newton steps (no slow path; pivots are normal)
-__device__ __forceinline__ double fast_rcp(double a) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
-  double e = fma(-a, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-a, r, 1.0);
-  return fma(r, e, r);
-}
-
 template <int G>
 struct SegOps {
   // v + (value of segment lane - d) for segment lanes >= d
