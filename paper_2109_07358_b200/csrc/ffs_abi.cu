@@ -390,12 +390,15 @@ int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Cl
   const bool cx = dtype == FFS_C128;
   const char* cv = getenv("FFS_CLUSTER_VARIANT");  // development: "b16" selects B=16 (slower)
   const bool b8 = !(cv && strcmp(cv, "b16") == 0);
+  const bool t256 = cv && strcmp(cv, "t256") == 0;  // 256 threads x 2R rows (no spills; slower)
   if (cx) {
-    if (b8) cluster_fn<cplx, 2, 8, 512>(c);
-    else cluster_fn<cplx, 1, 16, 512>(c);
+    if (!b8) cluster_fn<cplx, 1, 16, 512>(c);
+    else if (t256) cluster_fn<cplx, 4, 8, 256>(c);
+    else cluster_fn<cplx, 2, 8, 512>(c);
   } else {
-    if (b8) cluster_fn<double, 4, 8, 512>(c);
-    else cluster_fn<double, 2, 16, 512>(c);
+    if (!b8) cluster_fn<double, 2, 16, 512>(c);
+    else if (t256) cluster_fn<double, 8, 8, 256>(c);
+    else cluster_fn<double, 4, 8, 512>(c);
   }
   c.es = cx ? 16 : 8;
   const int rows_per_cta = c.threads * c.R;
@@ -461,6 +464,7 @@ int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
   p.wfull = reinterpret_cast<double*>(w + c.ws_ut);
   p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
   p.trace = S > 0 ? trace : nullptr;
+  p.timing = g_timing;  // development (ffs_dev_timing); null unless enabled
   dim3 tb(32, 8), tg((unsigned)((c.Lpt + 31) / 32), (unsigned)((N + 31) / 32));
   if (dtype == FFS_C128)
     ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, c.Lpt);

@@ -33,6 +33,7 @@ struct ClusterParams {
   double* wfull;           // per cluster [Np][Np] scalars
   int64_t S;
   double* trace;           // [S][Np][L] or null
+  unsigned long long* timing;  // development (ffs_dev_timing): cycles in contraction/draws/GJ, or null
 };
 
 constexpr int kRingDepth = 8;  // per-thread cp.async pipeline depth of the contraction
@@ -52,7 +53,7 @@ struct ClusterLayout {
     wb = o;   o = align16(o + sizeof(T) * (size_t)kKC * B);  // chunk of Wb rows / new-row columns
     vnew = o; o = align16(o + sizeof(T) * (size_t)kKC * B);
     red = o;  o = align16(o + sizeof(double) * 64 + sizeof(int) * 96);
-    xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + sizeof(T) * B + 64);  // cluster exchange
+    xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + 2 * sizeof(T) * B + 64);  // cluster exchange
     ring = o; o = align16(o + (kUseRing ? (size_t)kRingDepth * threads * R * sizeof(T) : 0));
     total = o;
   }
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   int* xfree = xlast + kMaxCS;                                 // [CS] first unchosen row or INT_MAX
   int* xsel = xfree + kMaxCS;                                  // selected row (global)
   T* xrow = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(xsel) + 16);  // [B] pivot row
+  T* xstage = xrow + B;                                        // [B] claimer's row (local)
 
   const int64_t cid = cluster_id_x();
   const int64_t ncl = nclusters_x();
@@ -131,7 +133,25 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   const T* Ug = reinterpret_cast<const T*>(p.U);
   const T* Utg = reinterpret_cast<const T*>(p.Ut);
   constexpr int kNone = 0x7fffffff;
+  constexpr int kUnset = -0x7fffffff;  // xsel before the crossing CTA's push
 
+  long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // development timing (thread 0): contraction, draws, GJ, draw sub-phases
+  long long tmark = clock64();
+  long long tsub = 0;
+  auto sub = [&](int ph) {  // draw sub-phases (do not move tmark)
+    if (p.timing != nullptr && t == 0) {
+      const long long now = clock64();
+      if (ph >= 0) tph[ph] += now - tsub;
+      tsub = now;
+    }
+  };
+  auto tick = [&](int ph) {
+    if (p.timing != nullptr && t == 0) {
+      const long long now = clock64();
+      tph[ph] += now - tmark;
+      tmark = now;
+    }
+  };
   for (int64_t i = cid; i < p.M; i += ncl) {
     const double* urow = p.uniforms + i * 2 * (int64_t)Np;
     // ---- a1 permutation (every CTA computes the same one)
@@ -224,16 +244,23 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
           }
         }
       }  // kUseRing
+      tick(0);
       // rows drawn earlier: exactly zero weight in the first column of this block
 #pragma unroll
       for (int r = 0; r < R; ++r)
         if ((chosen >> r) & 1u) P[r][0] = S::zero();
 
-      // ---- a4/a5: nb sequential draws
+      // ---- a4/a5: nb sequential draws. Per draw: CTA scan (one CTA barrier), each CTA's total
+      // to every CTA (thread q -> CTA q), cluster barrier #1, every warp derives T, its CTA's
+      // offset and the crossing CTA with CS lanes, the one warp of the crossing CTA whose range
+      // holds u*T pushes x_k and the pivot row to every CTA, cluster barrier #2, rank-1 update.
+      // The fallbacks of reading Q5 (T not finite/positive, no crossing because of rounding)
+      // take an extra, cluster-uniform round (rare).
       static_for<0, B>([&](auto rrc) {
         constexpr int rr = decltype(rrc)::value;
         if (rr < nb) {
           const int k = k0 + rr;
+          sub(-1);
           double w[R], c[R];
           double acc = 0.0;
 #pragma unroll
@@ -242,119 +269,81 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             acc += w[r];
             c[r] = acc;
           }
-          // CTA-level inclusive scan of thread totals
-          double incl = warp_incl_scan(acc, lane);
+          const double incl = warp_incl_scan(acc, lane);
           if (lane == 31) red[warp] = incl;
-          // local fallback candidates
-          int rl = -1, rf = kNone;
-#pragma unroll
-          for (int r = R - 1; r >= 0; --r) {
-            if (row0 + r < L && !((chosen >> r) & 1u)) rf = row0 + r;
-          }
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (w[r] > 0.0) rl = row0 + r;
-          const int wl = __reduce_max_sync(0xffffffffu, rl);
-          const int wf = __reduce_min_sync(0xffffffffu, rf);
-          if (lane == 0) {
-            redi[warp] = wl;
-            redi[32 + warp] = wf;
-          }
           __syncthreads();
-          double woff = 0.0, Tc;
+          double woff, Tc;
           {
             const double wt = lane < nw ? red[lane] : 0.0;
             const double ws = warp_incl_scan(wt, lane);
-            woff = warp > 0 ? __shfl_sync(0xffffffffu, ws, warp - 1) : 0.0;
+            woff = __shfl_sync(0xffffffffu, ws, warp > 0 ? warp - 1 : 0);
+            woff = warp > 0 ? woff : 0.0;
             Tc = __shfl_sync(0xffffffffu, ws, 31);
           }
           double excl = __shfl_up_sync(0xffffffffu, incl, 1);
-          if (lane == 0) excl = 0.0;
-          excl += woff;
-          // publish this CTA's total and fallback candidates to every CTA of the cluster
-          if (t == 0) {
-            int cl = -1, cf = kNone;
-            for (int q = 0; q < nw; ++q) {
-              cl = max(cl, redi[q]);
-              cf = min(cf, redi[32 + q]);
-            }
-            for (unsigned q = 0; q < CS; ++q) {
-              st_remote_f64(&xtot[rank], q, Tc);
-              st_remote_s32(&xlast[rank], q, cl);
-              st_remote_s32(&xfree[rank], q, cf);
-            }
-          }
-          cluster_sync_all();
-          // cluster-uniform: total, this CTA's offset, crossing CTA, fallback row
-          double Ttot = 0.0, off = 0.0;
-          int owner_cta = -1, fb_last = -1, fb_free = kNone;
+          excl = (lane == 0 ? 0.0 : excl) + woff;
+          if (t < (int)CS) st_remote_f64(&xtot[rank], (unsigned)t, Tc);
+          if (t == 0) *xsel = kUnset;  // remote pushes of this step arrive after barrier #1
+          sub(3);
+          cluster_sync_all();  // #1: CTA totals visible
+          sub(4);
+          // cluster-uniform T, this CTA's offset and the crossing CTA (lanes q < CS)
           const double u = usel[k];
+          double Ttot, off;
+          int owner_cta;
           {
-            double run = 0.0;
-            for (unsigned q = 0; q < CS; ++q) {
-              if (q == rank) off = run;
-              run += xtot[q];
-              fb_last = max(fb_last, xlast[q]);
-              fb_free = min(fb_free, xfree[q]);
+            const double tq = lane < (int)CS ? xtot[lane] : 0.0;
+            double ci = tq;
+#pragma unroll
+            for (int d = 1; d < kMaxCS; d <<= 1) {
+              const double y = __shfl_up_sync(0xffffffffu, ci, d);
+              ci = lane >= d ? ci + y : ci;
             }
-            Ttot = run;
+            Ttot = __shfl_sync(0xffffffffu, ci, kMaxCS - 1);
+            double ce = __shfl_up_sync(0xffffffffu, ci, 1);  // exclusive prefix
+            ce = lane == 0 ? 0.0 : ce;
+            off = __shfl_sync(0xffffffffu, ce, (int)rank);
+            const double thr0 = u * Ttot;
+            const unsigned ob = __ballot_sync(0xffffffffu, lane < (int)CS && tq > 0.0 && ci > thr0);
+            owner_cta = ob ? __ffs(ob) - 1 : -1;
           }
-          const bool ok = (Ttot > 0.0) && isfinite(Ttot);
+          const bool ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
           const double thr = u * Ttot;
-          {
-            double run = 0.0;
-            for (unsigned q = 0; q < CS; ++q) {
-              const double tq = xtot[q];
-              if (owner_cta < 0 && tq > 0.0 && run + tq > thr) owner_cta = (int)q;
-              run += tq;
-            }
-          }
-          // the selected row: fallbacks are cluster-uniform; a regular crossing is resolved by the
-          // crossing CTA (first local row with C(x) > u*T, w > 0; clamped threshold as elsewhere)
-          int xs = -1;
-          if (!ok) {
-            xs = fb_free;
-            flag |= 1;
-          } else if (owner_cta < 0) {
-            xs = fb_last;
-          } else if (owner_cta == (int)rank) {
-            const double tp = fmax(thr - off - excl, 0.0);
+          if (ok && owner_cta == (int)rank) {
+            const double thl = thr - off;
+            const double wt = red[warp];
+            const bool mine = (warp == 0 || thl >= woff) && (thl - woff < wt);
+            const double tp = fmax(thl - excl, 0.0);
             int rs = R;
 #pragma unroll
             for (int r = R - 1; r >= 0; --r)
               if (w[r] > 0.0 && c[r] > tp) rs = r;
-            const unsigned bal = __ballot_sync(0xffffffffu, rs < R);
-            int cand = kNone;
-            if (bal) {
+            const unsigned bal = __ballot_sync(0xffffffffu, mine && rs < R);
+            if (bal != 0u) {
               const int ln = __ffs(bal) - 1;
-              cand = (int)rank * Lc + (warp * 32 + ln) * R + __shfl_sync(0xffffffffu, rs, ln);
-            }
-            if (lane == 0) redi[64 + warp] = cand;
-            __syncthreads();
-            int best = kNone;
-            for (int q = 0; q < nw; ++q) best = min(best, redi[64 + q]);
-            xs = best != kNone ? best : xlast[rank];  // rounding corner: last positive row here
-          }
-          // the CTA that holds the selected row publishes it (index + pivot row) to all CTAs
-          if (xs >= 0 && (unsigned)(xs / Lc) == rank) {
-            const int own = (xs - (int)rank * Lc) / R, orow = (xs - (int)rank * Lc) % R;
-            if (t == own) {
+              const int rsel = __shfl_sync(0xffffffffu, rs, ln);
+              const int xs = (int)rank * Lc + (warp * 32 + ln) * R + rsel;
+              // the claiming lane's row by a select tree (constant register indices)
 #pragma unroll
-              for (int r = 0; r < R; ++r)
-                if (r == orow) {
-                  for (unsigned q = 0; q < CS; ++q) {
+              for (int cc = 0; cc < B; ++cc) {
+                T tr[R];
 #pragma unroll
-                    for (int cc = 0; cc < B; ++cc) {
-                      const double* src = reinterpret_cast<const double*>(&P[r][cc]);
-                      double* dst = reinterpret_cast<double*>(&xrow[cc]);
+                for (int r = 0; r < R; ++r) tr[r] = P[r][cc];
 #pragma unroll
-                      for (int h = 0; h < kD; ++h) st_remote_f64(dst + h, q, src[h]);
-                    }
-                    st_remote_s32(xsel, q, xs);
-                  }
-                  if (ok && w[r] < 1e-12 * Ttot) flag |= 2;
-                  chosen |= 1u << r;
-                }
+                for (int wd = 1; wd < R; wd <<= 1)
+#pragma unroll
+                  for (int q = 0; q < R; q += 2 * wd) tr[q] = (rsel & wd) ? tr[q + wd] : tr[q];
+                if (lane == ln) xstage[cc] = tr[0];
+              }
+              __syncwarp();
+              const double* xs_src = reinterpret_cast<const double*>(xstage);
+              double* xr_dst = reinterpret_cast<double*>(xrow);
+              for (int idx = lane; idx < (int)CS * B * kD; idx += 32) {
+                const int q = idx / (B * kD), e = idx % (B * kD);
+                st_remote_f64(xr_dst + e, (unsigned)q, xs_src[e]);
+              }
+              if (lane < (int)CS) st_remote_s32(xsel, (unsigned)lane, xs);
+              if (lane == ln) chosen |= 1u << rsel;
             }
           }
           if (p.trace != nullptr && i < p.S) {
@@ -364,16 +353,79 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             for (int r = 0; r < R; ++r)
               if (row0 + r < L) tr[row0 + r] = w[r] * inv;
           }
-          cluster_sync_all();
-          const int xsel_k = *xsel;
-          if (t == 0) pos[k] = xsel_k;
+          sub(5);
+          cluster_sync_all();  // #2: x_k and the pivot row visible in every CTA
+          sub(6);
+          int xsel_k = *xsel;
+          if (xsel_k == kUnset) {
+            // rare (cluster-uniform): T not finite/positive -> smallest unchosen row (flag bit0);
+            // no crossing -> the crossing CTA's (or, without one, the cluster's) last positive row
+            if (!ok) flag |= 1;
+            int rl = -1, rf = kNone;
 #pragma unroll
-          for (int cc = 0; cc < B; ++cc)
-            if (t == 0) Row[rr * B + cc] = xrow[cc];
+            for (int r = R - 1; r >= 0; --r)
+              if (row0 + r < L && !((chosen >> r) & 1u)) rf = row0 + r;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (w[r] > 0.0) rl = row0 + r;
+            const int wl = __reduce_max_sync(0xffffffffu, rl);
+            const int wf = __reduce_min_sync(0xffffffffu, rf);
+            if (lane == 0) {
+              redi[warp] = wl;
+              redi[32 + warp] = wf;
+            }
+            __syncthreads();
+            if (t < (int)CS) {
+              int cl = -1, cf = kNone;
+              for (int q = 0; q < nw; ++q) {
+                cl = max(cl, redi[q]);
+                cf = min(cf, redi[32 + q]);
+              }
+              st_remote_s32(&xlast[rank], (unsigned)t, cl);
+              st_remote_s32(&xfree[rank], (unsigned)t, cf);
+            }
+            cluster_sync_all();
+            int fb_last = -1, fb_free = kNone;
+            for (unsigned q = 0; q < CS; ++q) {
+              fb_last = max(fb_last, xlast[q]);
+              fb_free = min(fb_free, xfree[q]);
+            }
+            const int xs = !ok ? fb_free : (owner_cta >= 0 ? xlast[owner_cta] : fb_last);
+            if ((unsigned)(xs / Lc) == rank) {  // the holder thread pushes (serially; rare)
+              const int own = (xs - (int)rank * Lc) / R, orow = (xs - (int)rank * Lc) % R;
+#pragma unroll
+              for (int cc = 0; cc < B; ++cc) {
+                T tr[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) tr[r] = P[r][cc];
+#pragma unroll
+                for (int wd = 1; wd < R; wd <<= 1)
+#pragma unroll
+                  for (int q = 0; q < R; q += 2 * wd) tr[q] = (orow & wd) ? tr[q + wd] : tr[q];
+                if (t == own) {
+                  const double* src = reinterpret_cast<const double*>(&tr[0]);
+                  double* dst = reinterpret_cast<double*>(&xrow[cc]);
+                  for (unsigned q = 0; q < CS; ++q)
+#pragma unroll
+                    for (int h = 0; h < kD; ++h) st_remote_f64(dst + h, q, src[h]);
+                }
+              }
+              if (t == own) {
+                for (unsigned q = 0; q < CS; ++q) st_remote_s32(xsel, q, xs);
+                chosen |= 1u << orow;
+              }
+            }
+            cluster_sync_all();
+            xsel_k = *xsel;
+          }
+          if (t == 0) pos[k] = xsel_k;
+          if (t < B) Row[rr * B + t] = xrow[t];
           const T piv = xrow[rr];
+          if (S::abs2(piv) < 1e-12 * Ttot) flag |= 2;
           const T ip = S::recip(piv);
           if (t == 0) Pinv[rr] = ip;
-          // rank-1 update of the remaining panel columns; the drawn row becomes exactly zero
+          // rank-1 update of the remaining panel columns; drawn rows get exactly zero in the
+          // next draw's column (the only column whose weights are formed)
           T lmul[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) lmul[r] = S::mul(P[r][rr], ip);
@@ -382,12 +434,13 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             const T pc = xrow[cc];
 #pragma unroll
             for (int r = 0; r < R; ++r)
-              P[r][cc] = ((chosen >> r) & 1u) ? S::zero() : S::fms(lmul[r], pc, P[r][cc]);
+              P[r][cc] = (cc == rr + 1 && ((chosen >> r) & 1u)) ? S::zero() : S::fms(lmul[r], pc, P[r][cc]);
           }
-          __syncthreads();
+          sub(7);
         }
       });
 
+      tick(1);
       // ---- Gauss-Jordan update of W with the nb new rows, columns split over the cluster
       // (thread <-> one later column j; the new rows' entries in columns < k0 and W's rows < k0
       // are staged kKC at a time through shared memory)
@@ -479,8 +532,10 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         __threadfence();
         cluster_sync_all();  // W visible to every CTA before the next block's Wb load
       }
+      tick(2);
     }
     // ---- a6: positions (rank 0) and flags (OR over the cluster, collected in rank 0)
+    tick(2);
     const int fcta = (__syncthreads_or(flag & 1) ? 1 : 0) | (__syncthreads_or(flag & 2) ? 2 : 0);
     if (rank == 0)
       for (int j = t; j < Np; j += blockDim.x) p.positions[i * Np + j] = pos[j];
@@ -493,6 +548,8 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
     }
     cluster_sync_all();
   }
+  if (p.timing != nullptr && t == 0)
+    for (int q = 0; q < 8; ++q) atomicAdd(p.timing + q, (unsigned long long)tph[q]);
 }
 
 }  // namespace ffsk
