@@ -183,3 +183,24 @@ def test_library_is_the_native_one():
     U = inputs.random_orthonormal(256, 32, 3)
     run_gpu(U, inputs.uniforms(16, 32, 3), 32)
     assert L.ffs_last_launch_count() >= 1
+
+
+EXTREME = [(16, 4, 4, False), (256, 32, 32, False), (300, 33, 33, False), (1500, 19, 19, False),
+           (5000, 11, 11, False), (2000, 9, 9, True), (64, 21, 9, True)]
+
+
+@pytest.mark.parametrize("L,N,Np,cplx", EXTREME)
+@pytest.mark.parametrize("useL", [0.0, 1.0 - 2.0 ** -53])
+def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
+    """Selection uniforms at the ends of [0, 1): u = 0 selects the first site with w > 0 and
+    u = 1 - 2^-53 the last one (reading Q5: strict C(x) > u*T, else the last positive-weight
+    site). Both rules are deterministic, so positions must agree exactly (no tie exclusion);
+    u -> 1 drives the kernels' no-crossing fallback paths."""
+    U = inputs.random_orthonormal(L, N, 4242 + L + N, complex_=cplx)
+    M = 40
+    uni = inputs.uniforms(M, Np, 99 + L)
+    uni[:, Np:] = useL
+    gpos, gfl, _ = run_gpu(U, uni, Np)
+    rpos = ref.sample(U, uni, Np=Np)
+    assert (gpos == rpos).all(), np.argwhere(gpos != rpos)[:5]
+    assert not (gfl & 1).any()
