@@ -549,8 +549,9 @@ __device__ __forceinline__ Draw seg_draw(const double (&col)[R], double u, int s
     const double excl = SegOps<G>::prev(incl);
     Draw d;
     d.T = SegOps<G>::last(incl);
-    const bool ok = (d.T > 0.0) && (d.T < INFINITY);
-    const double tp = fmax(fma(u, d.T, -excl), 0.0);
+    const bool ok = (d.T > 0.0) && (d.T <= 1.7976931348623157e308);  // positive and finite
+    const double tq = fma(u, d.T, -excl);
+    const double tp = tq > 0.0 ? tq : 0.0;
     const unsigned b = __ballot_sync(0xffffffffu, ok && (tot > tp));
     d.ball = (G == 32) ? b : ((b >> (seg * G)) & ((1u << G) - 1u));
     int cnt = 0;
@@ -907,7 +908,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
             tacc[3] += (t - ts0);
             ts0 = t;
           }
-          if (!((dr.T > 0.0) && isfinite(dr.T))) flag |= 1;
+          if (!((dr.T > 0.0) && (dr.T <= 1.7976931348623157e308))) flag |= 1;
           if (p.trace != nullptr && id < p.S) {
             const double inv = dr.T > 0.0 ? 1.0 / dr.T : 0.0;
             double* tr = p.trace + (id * Np + k) * (int64_t)L;
