@@ -253,7 +253,8 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   const char* var = getenv("FFS_WARP_VARIANT");  // development: "b6" selects B=6 for R=8
   const bool legacy = var && strncmp(var, "w", 1) == 0;  // "w..." = whole-warp owner variants
   if (!legacy) {
-    // segmented kernel, OPT = 7: kept partial sums, pivot row through smem, flat Gauss-Jordan
+    // segmented kernel, OPT = 7 (+128 for G = 32): kept partial sums, pivot row through smem,
+    // flat Gauss-Jordan, no warp vote when the segment is the whole warp
     // (variants measured in profiles/r01_ncu_summary.md; "base" = the first segmented kernel)
     const bool base = var && strcmp(var, "base") == 0;
     const size_t ush = ffsk::align16((size_t)N * (256 + 2) * 8);
@@ -268,8 +269,8 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
     else if (var && strcmp(var, "pcs256") == 0) warp_fn_pc<8, 4, 256, true>(w);
     else if (var && strcmp(var, "pcs256t") == 0) warp_fn_pc<8, 4, 256, true, true>(w);
     else if (var && strcmp(var, "t") == 0) warp_fn_seg<8, 4, 32, 512, true, 7>(w);  // phase timing
-    else if (fits16) warp_fn_seg<8, 4, 32, 512, false, 7>(w);  // 16 owners/SM, 128 regs
-    else warp_fn_seg<8, 4, 32, 384, false, 7>(w);              // 12 owners/SM (larger N')
+    else if (fits16) warp_fn_seg<8, 4, 32, 512, false, 135>(w);  // 16 owners/SM, 128 regs
+    else warp_fn_seg<8, 4, 32, 384, false, 135>(w);              // 12 owners/SM (larger N')
   } else if (L <= 64) warp_fn<2, 8, 1, 384>(w);
   else if (L <= 128) warp_fn<4, 8, 1, 384>(w);
   else if (var && strcmp(var, "wb8") == 0) warp_fn<8, 8, 1, 256>(w);

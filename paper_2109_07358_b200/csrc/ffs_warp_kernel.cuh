@@ -715,7 +715,8 @@ __device__ __forceinline__ void seg_gj_flat(const double* __restrict__ Uts, int 
 
 // OPT bits (development variants, FFS_WARP_VARIANT): 1 = draw keeps its partial sums,
 // 2 = pivot row through shared memory (owner lane stores it, no select tree / shuffles),
-// 4 = Gauss-Jordan update mapped over (column, row) pairs instead of one lane per column.
+// 4 = Gauss-Jordan update mapped over (column, row) pairs instead of one lane per column,
+// 32 = pivot row by select tree + shuffles (critical columns first), 128 = no vote when G = 32.
 template <int R, int B, int G, bool TIMING, int OPT = 0>
 __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -884,7 +885,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           int own, orow = 0;  // owner lane within the segment, row within the owner
           // G == 32: one segment per warp, dr.ball is warp-uniform (no vote needed)
           bool common;
-          if constexpr (G == 32 && (OPT & 32) != 0) common = dr.ball != 0u;
+          if constexpr (G == 32 && (OPT & 160) != 0) common = dr.ball != 0u;
           else common = __all_sync(0xffffffffu, dr.ball != 0u);
           if (common) {
             own = __ffs(dr.ball) - 1;
