@@ -12,6 +12,8 @@
 #include "ffs_warp_kernel.cuh"
 #include "ffs_pc_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
+#include "ffs_mma_kernel.cuh"
+#include "ffs_dense.cuh"
 #include "ffs_kptr.h"
 
 namespace {
@@ -197,6 +199,7 @@ struct WarpPlan {
   bool legacy = false;  // whole-warp ffs_warp_kernel (its own W layout)
   bool pc = false;  // producer/consumer kernel (owner = consumer+producer warp pair, 2 slots)
   bool wsmem = false;  // pc kernel keeps W in shared memory
+  bool mma = false;  // ffs_mma_kernel (DMMA contraction, B = 8, its own U^T swizzle and slice)
   size_t ushared, owner, smem, ws_perm, ws_w = 0;
   int perm_tpb;
   size_t perm_smem;
@@ -268,7 +271,18 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
     else if (var && strcmp(var, "b8") == 0) warp_fn_seg<8, 8, 32, 256, false, 7>(w);
     else if (var && strcmp(var, "pcs256") == 0) warp_fn_pc<8, 4, 256, true>(w);
     else if (var && strcmp(var, "pcs256t") == 0) warp_fn_pc<8, 4, 256, true, true>(w);
+    else if (var && strcmp(var, "o647") == 0) warp_fn_seg<8, 4, 32, 512, false, 647>(w);
     else if (var && strcmp(var, "t") == 0) warp_fn_seg<8, 4, 32, 512, true, 7>(w);  // phase timing
+    else if (var && strncmp(var, "mma", 3) == 0) {
+      const bool t256 = strcmp(var, "mma256") == 0;
+      w.fn = t256 ? ffsk::mma_kernel_ptr<256>() : ffsk::mma_kernel_ptr<384>();
+      w.R = 8;
+      w.B = 8;
+      w.S = 1;
+      w.G = 32;
+      w.maxt = t256 ? 256 : 384;
+      w.mma = true;
+    }
     else if (fits16) warp_fn_seg<8, 4, 32, 512, false, 135>(w);  // 16 owners/SM, 128 regs
     else warp_fn_seg<8, 4, 32, 384, false, 135>(w);              // 12 owners/SM (larger N')
   } else if (L <= 64) warp_fn<2, 8, 1, 384>(w);
@@ -283,9 +297,9 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, w.fn) != cudaSuccess) return fail(FFS_ECUDA, "cudaFuncGetAttributes failed");
   w.Lp = w.G * w.R;
-  w.ut_stride = w.Lp + 2;
+  w.ut_stride = w.mma ? ffsk::kMmaRows : w.Lp + 2;
   w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
-  w.owner = w.pc ? ffsk::pc_pair_bytes((int)Np, w.B, w.R, w.wsmem)  // per consumer/producer pair
+  w.owner = w.mma ? ffsk::MmaLayout((int)Np).total : w.pc ? ffsk::pc_pair_bytes((int)Np, w.B, w.R, w.wsmem)  // per consumer/producer pair
                  : ffsk::WarpLayout((int)Np, w.B, !w.legacy).total;         // per sample; a warp holds S slices
   // registers are allocated per SM sub-partition (4 x 16K); warps are spread round-robin
   const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
@@ -505,6 +519,174 @@ int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
   return FFS_OK;
 }
 
+// ------------------------------------------------------------------ lockstep-dense path
+// Full sampling (N' = N) of real U at large L: per block step, one DMMA GEMM P = U Y for a batch
+// of S samples, then one cluster per sample draws on its panel and updates W and Y
+// (ffs_dense.cuh, ffs_cluster_kernel<..., STEP = true>).
+bool dense_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
+  const char* g = getenv("FFS_NO_DENSE");
+  if (g && g[0] == '1') return false;
+  return dtype == FFS_F64 && Np == N && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
+}
+
+struct DensePlan {
+  ClusterPlan c;
+  int64_t S, ldY;
+  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, total;
+};
+
+int make_dense_plan(int64_t L, int64_t N, int64_t Np, int64_t M, DensePlan& d) {
+  int rc = make_cluster_plan(L, N, Np, FFS_F64, M, d.c);
+  if (rc != FFS_OK) return rc;
+  d.c.fn = ffsk::cluster_step_kernel_ptr<double, 4, 8, 512>();
+  d.c.R = 4;
+  d.c.B = 8;
+  if (cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.c.smem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(step smem) failed");
+  if (d.c.CS > 8 && cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return fail(FFS_ECUDA, "non-portable cluster size not allowed");
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffsk::kGemmSmem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(gemm smem) failed");
+  int64_t cap = 1024;  // samples per lockstep batch
+  if (const char* e = getenv("FFS_DENSE_S")) cap = std::max<int64_t>(1, atoll(e));  // development
+  d.S = std::max<int64_t>(1, std::min<int64_t>(M, cap));
+  d.ldY = (d.S * d.c.B + ffsk::kGN - 1) / ffsk::kGN * ffsk::kGN;
+  d.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
+  d.ws_y = align_up((size_t)N * d.ldY * 8);
+  d.ws_p = align_up((size_t)L * d.ldY * 8);
+  d.ws_w = align_up((size_t)d.S * Np * Np * 8);
+  d.ws_ch = align_up((size_t)d.S * (d.c.Lpt / 32) * 4);
+  d.ws_row = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * 8);
+  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row;
+  const size_t gjs = ffsk::dense_gj_smem<8>((int)Np);
+  if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<8>),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(gj smem) failed");
+  return FFS_OK;
+}
+
+int launch_dense(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, const double* uniforms,
+                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
+                 double* trace) {
+  DensePlan d;
+  int rc = make_dense_plan(L, N, Np, M, d);
+  if (rc != FFS_OK) return rc;
+  if (!ws || ws_bytes < d.total) return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, d.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  char* w = static_cast<char*>(ws);
+  int32_t* perm = reinterpret_cast<int32_t*>(w);
+  double* Y = reinterpret_cast<double*>(w + d.ws_perm);
+  double* Pd = reinterpret_cast<double*>(w + d.ws_perm + d.ws_y);
+  double* Wd = reinterpret_cast<double*>(w + d.ws_perm + d.ws_y + d.ws_p);
+  uint32_t* ch = reinterpret_cast<uint32_t*>(w + d.ws_perm + d.ws_y + d.ws_p + d.ws_w);
+  double* rowg = reinterpret_cast<double*>(w + d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch);
+  if (g_prof) {
+    if (!g_ev0) {
+      cudaEventCreate(&g_ev0);
+      cudaEventCreate(&g_ev1);
+    }
+    cudaEventRecord(g_ev0, stream);
+  }
+  {
+    const int tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
+    const int64_t pgrid = (M + tpb - 1) / tpb;
+    ffsk::ffs_permute_kernel<<<(unsigned)pgrid, tpb, (size_t)tpb * N * 4, stream>>>(uniforms, perm, M, (int)N,
+                                                                                       (int)Np);
+    ++g_launches;
+  }
+  ffsk::ClusterParams p{};
+  p.U = static_cast<const double*>(U);
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  p.Lc = d.c.Lc;
+  p.Lpt = d.c.Lpt;
+  p.M = M;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.wfull = Wd;
+  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.trace = S > 0 ? trace : nullptr;
+  p.timing = nullptr;
+  p.Pd = Pd;
+  p.ldY = d.ldY;
+  p.rowg = rowg;
+  ffsk::DenseGjParams q{};
+  q.U = static_cast<const double*>(U);
+  q.perm = perm;
+  q.positions = positions;
+  q.rowg = rowg;
+  q.W = Wd;
+  q.Y = Y;
+  q.ldY = d.ldY;
+  q.N = (int)N;
+  q.Np = (int)Np;
+  p.permg = perm;
+  p.chosen_g = ch;
+  ffsk::DgemmParams gp{};
+  gp.A = static_cast<const double*>(U);
+  gp.B = Y;
+  gp.C = Pd;
+  gp.lda = N;
+  gp.ldb = d.ldY;
+  gp.ldc = d.ldY;
+  gp.M = (int)L;
+  gp.N = (int)d.ldY;
+  gp.K = (int)N;
+  const dim3 ggrid((unsigned)(d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
+  for (int64_t base = 0; base < M; base += d.S) {
+    const int64_t Sb = std::min<int64_t>(d.S, M - base);
+    cudaMemsetAsync(Y, 0, d.ws_y, stream);
+    cudaMemsetAsync(ch, 0, d.ws_ch, stream);
+    if (flags) cudaMemsetAsync(flags + base, 0, (size_t)Sb * 4, stream);
+    ffsk::ffs_dense_y0_kernel<8><<<(unsigned)((Sb * 8 + 255) / 256), 256, 0, stream>>>(perm, Y, d.ldY, base,
+                                                                                       (int)Sb, (int)Np);
+    ++g_launches;
+    p.base = base;
+    p.Sb = (int)Sb;
+    for (int k0 = 0; k0 < Np; k0 += d.c.B) {
+      ffsk::ffs_dgemm_kernel<<<ggrid, ffsk::kGThreads, ffsk::kGemmSmem, stream>>>(gp);
+      ++g_launches;
+      p.k0 = k0;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = d.c.CS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.blockDim = dim3(d.c.threads);
+      cfg.gridDim = dim3((unsigned)(Sb * d.c.CS));
+      cfg.dynamicSmemBytes = d.c.smem;
+      cfg.stream = stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      void* args[] = {&p};
+      cudaError_t e = cudaLaunchKernelExC(&cfg, d.c.fn, args);
+      if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
+      ++g_launches;
+      if (k0 + d.c.B < Np) {
+        q.k0 = k0;
+        q.base = base;
+        const int nc = (int)Np - k0 - d.c.B;
+        const dim3 jg((unsigned)((nc + ffsk::kGjTJ - 1) / ffsk::kGjTJ), (unsigned)Sb);
+        ffsk::ffs_dense_gj_kernel<8><<<jg, 256, ffsk::dense_gj_smem<8>(k0), stream>>>(q);
+        ++g_launches;
+      }
+    }
+  }
+  if (g_prof) {
+    cudaEventRecord(g_ev1, stream);
+    g_ev_pending = true;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  g_err[0] = 0;
+  return FFS_OK;
+}
+
 bool use_warp_path(int64_t L, int64_t N, int64_t Np, int dtype) {
   const char* g = getenv("FFS_FORCE_GENERIC");
   if (g && g[0] == '1') return false;
@@ -524,6 +706,8 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
   if (use_warp_path(L, N, Np, dtype))
     return launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
+  if (dense_eligible(L, N, Np, dtype))
+    return launch_dense(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   if (cluster_eligible(L, dtype))
     return launch_cluster(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   Plan pl;
@@ -581,6 +765,11 @@ size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int6
     WarpPlan w;
     if (make_warp_plan(L, N, Nprime, std::max<int64_t>(M, 1), w) != FFS_OK) return 0;
     return w.ws_perm + w.ws_w;
+  }
+  if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && dense_eligible(L, N, Nprime, dtype)) {
+    DensePlan d;
+    if (make_dense_plan(L, N, Nprime, std::max<int64_t>(M, 1), d) != FFS_OK) return 0;
+    return d.total;
   }
   if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && cluster_eligible(L, dtype)) {
     ClusterPlan c;

@@ -34,6 +34,15 @@ struct ClusterParams {
   int64_t S;
   double* trace;           // [S][Np][L] or null
   unsigned long long* timing;  // development (ffs_dev_timing): cycles in contraction/draws/GJ, or null
+  // STEP mode (lockstep-dense path, ffs_dense.cuh): one block step k0 for the Sb samples
+  // base .. base+Sb-1 (cluster c <-> sample base+c); the panel comes from P = U Y
+  const double* Pd;        // [L][ldY] panels, sample s in columns s*B .. s*B+B-1
+  int64_t ldY;
+  double* rowg;            // [Sb][B*B + B] pivot rows and inverse pivots of this block (out)
+  const int32_t* permg;    // [M][Np] permutation prefixes (ffs_permute_kernel)
+  uint32_t* chosen_g;      // [Sb][Lpt/32] rows drawn so far (bit per row)
+  int k0, Sb;
+  int64_t base;
 };
 
 constexpr int kRingDepth = 8;  // per-thread cp.async pipeline depth of the contraction
@@ -94,7 +103,7 @@ __device__ __forceinline__ void st_remote_s32(void* local_ptr, unsigned rank, in
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
-template <typename T, int R, int B, int MAXT>
+template <typename T, int R, int B, int MAXT, bool STEP = false>
 __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   using S = Sc<T>;
@@ -129,7 +138,6 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 
   const int64_t cid = cluster_id_x();
   const int64_t ncl = nclusters_x();
-  T* Wf = reinterpret_cast<T*>(p.wfull) + cid * (int64_t)Np * Np;
   const T* Ug = reinterpret_cast<const T*>(p.U);
   const T* Utg = reinterpret_cast<const T*>(p.Ut);
   constexpr int kNone = 0x7fffffff;
@@ -152,13 +160,22 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       tmark = now;
     }
   };
-  for (int64_t i = cid; i < p.M; i += ncl) {
+  const int64_t nloc = STEP ? (int64_t)p.Sb : p.M;
+  for (int64_t sl = cid; sl < nloc; sl += ncl) {
+    const int64_t i = STEP ? p.base + sl : sl;
+    // W = A^{-1} V[X, later columns]: per cluster, or per batch sample in STEP mode (it persists
+    // across the block-step launches)
+    T* Wf = reinterpret_cast<T*>(p.wfull) + (STEP ? sl : cid) * (int64_t)Np * Np;
     const double* urow = p.uniforms + i * 2 * (int64_t)Np;
-    // ---- a1 permutation (every CTA computes the same one)
-    for (int j = t; j < N; j += blockDim.x) perm[j] = j;
+    // ---- a1 permutation (every CTA computes the same one; STEP: precomputed prefix)
+    if constexpr (STEP) {
+      for (int j = t; j < Np; j += blockDim.x) perm[j] = p.permg[i * Np + j];
+    } else {
+      for (int j = t; j < N; j += blockDim.x) perm[j] = j;
+    }
     for (int j = t; j < Np; j += blockDim.x) usel[j] = urow[Np + j];
     __syncthreads();
-    if (t == 0) {
+    if (!STEP && t == 0) {
       for (int j = 0; j < Np; ++j) {
         const int n = N - j;
         int r = (int)floor(urow[j] * (double)n);
@@ -171,17 +188,34 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
     __syncthreads();
     uint32_t chosen = 0;
     int flag = 0;
+    uint32_t* chw = nullptr;  // STEP: this thread's word of the drawn-row bitmap
+    if constexpr (STEP) {
+      static_assert(32 % R == 0, "a thread's rows share one bitmap word");
+      chw = p.chosen_g + sl * (int64_t)(p.Lpt / 32) + row0 / 32;
+      chosen = (*chw >> (row0 & 31)) & ((1u << R) - 1u);
+    }
 
-    for (int k0 = 0; k0 < Np; k0 += B) {
+    for (int k0 = STEP ? p.k0 : 0; k0 < Np; k0 += B) {
       const int nb = min(B, Np - k0);
       // ---- a3 panel for this CTA's rows (W in global memory is final for rows < k0 after the
       // previous block's update + cluster barrier; its rows are staged kKC at a time)
       T P[R][B];
+      if constexpr (STEP) {
+        // the panel from the dense GEMM P = U Y (rows >= L are zero)
+        const T* pb = reinterpret_cast<const T*>(p.Pd) + (size_t)sl * B;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool in = row0 + r < L;
+#pragma unroll
+          for (int c = 0; c < B; ++c) P[r][c] = (in && c < nb) ? pb[(size_t)(row0 + r) * p.ldY + c] : S::zero();
+        }
+      } else {
 #pragma unroll
       for (int c = 0; c < B; ++c) {
         const T* base = Utg + (size_t)perm[min(k0 + c, Np - 1)] * p.Lpt + row0;
 #pragma unroll
         for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
+      }
       }
       // contraction over the k0 earlier columns. W rows are staged kKC at a time in shared
       // memory; this thread's R rows of each gathered column perm[ii] are copied global->shared
@@ -202,7 +236,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             asm volatile("cp.async.commit_group;" ::: "memory");
           }
         }
-        for (int c0 = 0; c0 < k0; c0 += kKC) {
+        for (int c0 = 0; c0 < (STEP ? 0 : k0); c0 += kKC) {
           const int kc = min(kKC, k0 - c0);
           __syncthreads();
           for (int idx = t; idx < kc * B; idx += blockDim.x) {
@@ -444,7 +478,14 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       // ---- Gauss-Jordan update of W with the nb new rows, columns split over the cluster
       // (thread <-> one later column j; the new rows' entries in columns < k0 and W's rows < k0
       // are staged kKC at a time through shared memory)
-      if (k0 + nb < Np) {
+      if constexpr (STEP) {
+        // the Gauss-Jordan update runs batched in ffs_dense_gj_kernel: hand it S = L U of this block
+        if (rank == 0 && t < B * B + B) {
+          T* rg = reinterpret_cast<T*>(p.rowg) + sl * (B * B + B);
+          rg[t] = t < B * B ? Row[t] : Pinv[t - B * B];
+        }
+      }
+      if (!STEP && k0 + nb < Np) {
        for (int jt = k0 + nb; jt < Np; jt += (int)CS * blockDim.x) {  // column tiles (uniform trip count)
         const int j = jt + (int)rank * blockDim.x + t;
         const bool has = j < Np;
@@ -533,10 +574,21 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         cluster_sync_all();  // W visible to every CTA before the next block's Wb load
       }
       tick(2);
+      if constexpr (STEP) break;
     }
     // ---- a6: positions (rank 0) and flags (OR over the cluster, collected in rank 0)
     tick(2);
     const int fcta = (__syncthreads_or(flag & 1) ? 1 : 0) | (__syncthreads_or(flag & 2) ? 2 : 0);
+    if constexpr (STEP) {
+      const int nbs = min(B, Np - p.k0);
+      if (rank == 0)
+        for (int j = p.k0 + t; j < p.k0 + nbs; j += blockDim.x) p.positions[i * Np + j] = pos[j];
+      const uint32_t mine = chosen << (row0 & 31);
+      if (mine) atomicOr(chw, mine);
+      if (t == 0 && fcta != 0 && p.flags != nullptr) atomicOr(reinterpret_cast<unsigned*>(p.flags + i), (unsigned)fcta);
+      cluster_sync_all();  // no CTA starts the next sample while DSMEM traffic of this one is pending
+      continue;
+    }
     if (rank == 0)
       for (int j = t; j < Np; j += blockDim.x) p.positions[i * Np + j] = pos[j];
     if (t == 0) st_remote_s32(&xfree[rank], 0, fcta);

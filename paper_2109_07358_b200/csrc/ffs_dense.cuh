@@ -1,0 +1,268 @@
+// Lockstep-dense path for full sampling at large L (the C5 DPP-shaped workload): the candidate-
+// weight contraction (a3) of S samples at the same block step runs as ONE dense FP64 GEMM on the
+// tensor pipe (DMMA), instead of S per-sample gathered contractions that are bound by the
+// bandwidth of the gathered U reads.
+//
+// For sample s at block start k0 (panel width B), the left-looking panel is
+//   P_s = V_s[:, k0:k0+B] - V_s[:, 0:k0] W_s[0:k0, k0:k0+B],   V_s = U[:, m_s]
+// = U Y_s with Y_s (N x B) the scatter of the coefficients into U's column space:
+//   Y_s[m_j, c] = -W_s[j, k0+c] (j < k0),   Y_s[m_{k0+c}, c] = 1,   0 elsewhere.
+// Stacking Y = [Y_0 .. Y_{S-1}] (N x S*B, row-major, row stride ldY), all S panels are
+//   P = U Y   (L x N) (N x S*B)
+// a plain dense GEMM whose A operand U is shared by every sample. It executes L*N*B FMAs per
+// sample-block where the gathered form needs L*k0*B (2x over a full sample) but runs at the
+// FP64 tensor-pipe rate instead of the ~2 flop/B of the gathered reads.
+// The draws (a4), the rank-1 panel updates and the Gauss-Jordan update of W_s (a2/a5) run in
+// ffs_cluster_kernel<..., STEP = true> (one cluster per sample, one block step per launch), which
+// also scatters the next block's Y_s columns, so Y never needs re-zeroing: the nonzero rows of
+// Y_s only grow ({m_j : j < k0+B}).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ffs_kernel.cuh"
+
+namespace ffsk {
+
+// ---------------------------------------------------------------- DMMA DGEMM C = A B
+// Row-major A [M][K] (lda), B [K][N] (ldb), C [M][N] (ldc); N % 128 == 0 and K % 2 == 0 (the
+// host pads); rows >= M and k >= K are zero-filled. CTA tile 128 x 128 x 16, 8 warps as 4 (M) x 2
+// (N), warp tile 32 x 64 = 4 x 8 DMMA m8n8k4 tiles, 4-stage cp.async pipeline (128 KB smem).
+constexpr int kGM = 128, kGN = 128, kGK = 16, kGStages = 4, kGThreads = 256;
+constexpr size_t kGemmSmem = (size_t)kGStages * (kGM * kGK + kGK * kGN) * sizeof(double);
+
+struct DgemmParams {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int M, N, K;
+};
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+
+// Shared-memory swizzles (8-byte element units): the A tile is [128][16] with element (r, c) at
+// r*16 + (c ^ 4(r&3)); the B tile is [16][128] with (k, n) at k*128 + (n ^ 4(k&3)). The XOR only
+// touches bits 2-3, so the 16-byte cp.async chunks stay contiguous, and each half-warp phase of
+// the fragment loads (g = 0..3 or 4..7, t4 = 0..3) hits 16 distinct 8-byte bank slots.
+static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const DgemmParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* As = reinterpret_cast<double*>(smem);
+  double* Bs = As + kGStages * kGM * kGK;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int m0 = blockIdx.y * kGM, n0 = blockIdx.x * kGN;
+  const int KT = (p.K + kGK - 1) / kGK;
+
+  auto load_stage = [&](int st, int kt) {
+    const int kk = kt * kGK;
+    double* as = As + st * kGM * kGK;
+    double* bs = Bs + st * kGK * kGN;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // A: 128 rows x 8 chunks
+      const int c = t + i * kGThreads, r = c >> 3, ch = c & 7;
+      const int gr = m0 + r, gk = kk + 2 * ch;
+      const bool in = gr < p.M && gk < p.K;
+      const double* src = p.A + (in ? (size_t)gr * p.lda + gk : 0);
+      cp_async16(as + r * kGK + ((2 * ch) ^ ((r & 3) << 2)), src, in ? 16 : 0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // B: 16 rows x 64 chunks
+      const int c = t + i * kGThreads, r = c >> 6, ch = c & 63;
+      const int gk = kk + r;
+      const bool in = gk < p.K;
+      const double* src = p.B + (in ? (size_t)gk * p.ldb + n0 + 2 * ch : 0);
+      cp_async16(bs + r * kGN + ((2 * ch) ^ ((r & 3) << 2)), src, in ? 16 : 0);
+    }
+  };
+
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kGStages - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 2) : "memory");
+    __syncthreads();
+    {
+      const int nk = kt + kGStages - 1;
+      if (nk < KT) load_stage(nk % kGStages, nk);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const double* as = As + (kt % kGStages) * kGM * kGK + (wm * 32 + g) * kGK;
+    const double* bs = Bs + (kt % kGStages) * kGK * kGN + t4 * kGN;
+#pragma unroll
+    for (int ks = 0; ks < kGK; ks += 4) {
+      double a[4], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[i * 8 * kGK + ((ks + t4) ^ ((g & 3) << 2))];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = bs[ks * kGN + ((wn * 64 + j * 8 + g) ^ (t4 << 2))];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row < p.M) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = n0 + wn * 64 + j * 8 + 2 * t4;
+        *reinterpret_cast<double2*>(p.C + (size_t)row * p.ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+  }
+}
+
+// Y for the first block: Y[m_c][s*B + c] = 1 (c < min(B, N')); Y is zero otherwise (memset).
+template <int B>
+static __global__ void ffs_dense_y0_kernel(const int32_t* __restrict__ perm, double* __restrict__ Y, int64_t ldY,
+                                    int64_t base, int Sb, int Np) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Sb * B) return;
+  const int s = idx / B, c = idx % B;
+  if (c < Np) Y[(size_t)perm[(base + s) * Np + c] * ldY + (size_t)s * B + c] = 1.0;
+}
+
+
+// ---------------------------------------------------------------- batched Gauss-Jordan update
+// After the draws of block [k0, k0+B) of every batch sample (all samples share k0): with
+// X_new = x_{k0..k0+B-1}, S = L U the B x B Schur block of the draws (pivot rows `Row`, inverse
+// pivots `Pinv`), and j >= k1 = k0+B the later columns,
+//   (1) Z[:, j] = V[X_new, j] - V[X_new, 0:k0] W[0:k0, j]
+//   (2) Z[:, j] <- S^{-1} Z[:, j]
+//   (3) W[0:k0, j] -= W[0:k0, k0:k1] Z[:, j],   W[k0:k1, j] = Z[:, j]
+// then the next block's Y_s columns are scattered from W[0:k1, k1:k1+B] (tile 0 only).
+// Grid (column tiles of kGjTJ, batch samples); 256 threads = kGjTJ columns x 4 slices of i.
+constexpr int kGjTJ = 64;
+
+struct DenseGjParams {
+  const double* U;          // [L][N]
+  const int32_t* perm;      // [M][Np]
+  const int32_t* positions; // [M][Np]
+  const double* rowg;       // [Sb][B*B + B]
+  double* W;                // [Sb][Np][Np]
+  double* Y;                // [N][ldY]
+  int64_t ldY, base;
+  int N, Np, k0;
+};
+
+template <int B>
+__host__ __device__ inline size_t dense_gj_smem(int k0) {
+  return sizeof(double) * ((size_t)2 * B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
+}
+
+template <int B>
+static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjParams q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int k0 = q.k0, k1 = k0 + B, Np = q.Np, N = q.N;
+  const int sl = blockIdx.y;
+  const int64_t i_s = q.base + sl;
+  const int t = threadIdx.x, jl = t % kGjTJ, part = t / kGjTJ;
+  const int j = k1 + blockIdx.x * kGjTJ + jl;
+  const bool has = j < Np;
+  double* Vn = reinterpret_cast<double*>(smem);   // [B][k0]   V[X_new, 0:k0]
+  double* Wb = Vn + (size_t)B * k0;               // [k0][B]   W[0:k0, k0:k1]
+  double* Zp = Wb + (size_t)B * k0;               // [4][B][TJ] partial sums, then Z [B][TJ]
+  double* Zs = Zp + 4 * B * kGjTJ;                // [B][TJ]
+  double* RP = Zs + B * kGjTJ;                    // Row [B][B], Pinv [B]
+  int* xn = reinterpret_cast<int*>(RP + B * B + B);
+  const int32_t* pm = q.perm + i_s * Np;
+  double* W = q.W + (size_t)sl * Np * Np;
+  if (t < B) xn[t] = q.positions[i_s * Np + k0 + t];
+  if (t < B * B + B) RP[t] = q.rowg[(size_t)sl * (B * B + B) + t];
+  __syncthreads();
+  for (int idx = t; idx < B * k0; idx += blockDim.x) {
+    const int tt = idx / k0, ii = idx % k0;
+    Vn[idx] = q.U[(size_t)xn[tt] * N + pm[ii]];
+  }
+  for (int idx = t; idx < B * k0; idx += blockDim.x) Wb[idx] = W[(size_t)(idx / B) * Np + k0 + idx % B];
+  __syncthreads();
+  // (1) partial sums over this thread's slice of i
+  double acc[B];
+#pragma unroll
+  for (int tt = 0; tt < B; ++tt) acc[tt] = 0.0;
+  if (has) {
+#pragma unroll 4
+    for (int ii = part; ii < k0; ii += 4) {
+      const double w = W[(size_t)ii * Np + j];
+#pragma unroll
+      for (int tt = 0; tt < B; ++tt) acc[tt] = fma(Vn[tt * k0 + ii], w, acc[tt]);
+    }
+  }
+#pragma unroll
+  for (int tt = 0; tt < B; ++tt) Zp[(part * B + tt) * kGjTJ + jl] = acc[tt];
+  __syncthreads();
+  // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
+  if (part == 0 && has) {
+    double z[B];
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt)
+      z[tt] = q.U[(size_t)xn[tt] * N + pm[j]] - ((Zp[(0 * B + tt) * kGjTJ + jl] + Zp[(1 * B + tt) * kGjTJ + jl]) +
+                                               (Zp[(2 * B + tt) * kGjTJ + jl] + Zp[(3 * B + tt) * kGjTJ + jl]));
+    const double* Row = RP;
+    const double* Pinv = RP + B * B;
+#pragma unroll
+    for (int tt = 1; tt < B; ++tt)
+#pragma unroll
+      for (int s2 = 0; s2 < tt; ++s2) z[tt] = fma(-(Row[tt * B + s2] * Pinv[s2]), z[s2], z[tt]);
+#pragma unroll
+    for (int tt = B - 1; tt >= 0; --tt) {
+#pragma unroll
+      for (int s2 = tt + 1; s2 < B; ++s2) z[tt] = fma(-Row[tt * B + s2], z[s2], z[tt]);
+      z[tt] *= Pinv[tt];
+    }
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt) {
+      Zs[tt * kGjTJ + jl] = z[tt];
+      W[(size_t)(k0 + tt) * Np + j] = z[tt];
+    }
+  }
+  __syncthreads();
+  // (3) rank-B update of the earlier rows
+  if (has) {
+    double z[B];
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt) z[tt] = Zs[tt * kGjTJ + jl];
+#pragma unroll 4
+    for (int ii = part; ii < k0; ii += 4) {
+      double a = W[(size_t)ii * Np + j];
+#pragma unroll
+      for (int tt = 0; tt < B; ++tt) a = fma(-Wb[ii * B + tt], z[tt], a);
+      W[(size_t)ii * Np + j] = a;
+    }
+  }
+  // next block's Y_s columns (the tile holding columns k1 .. k1+B-1)
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    const int nb1 = min(B, Np - k1);
+    double* Yg = q.Y + (size_t)sl * B;
+    for (int idx = t; idx < k1 * B; idx += blockDim.x) {
+      const int ii = idx / B, c = idx % B;
+      Yg[(size_t)pm[ii] * q.ldY + c] = c < nb1 ? -W[(size_t)ii * Np + k1 + c] : 0.0;
+    }
+    if (t < nb1) Yg[(size_t)pm[k1 + t] * q.ldY + t] = 1.0;
+  }
+}
+
+}  // namespace ffsk

@@ -6,6 +6,7 @@
 #include "ffs_warp_kernel.cuh"
 #include "ffs_pc_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
+#include "ffs_mma_kernel.cuh"
 
 namespace ffsk {
 template <typename T, bool WARP, int R, int B, bool USMEM, int MAXT> const void* sample_kernel_ptr() {
@@ -25,5 +26,11 @@ template <int R, int B, int S, int MAXT> const void* warp_kernel_ptr() {
 }
 template <typename T, int R, int B, int MAXT> const void* cluster_kernel_ptr() {
   return reinterpret_cast<const void*>(&ffs_cluster_kernel<T, R, B, MAXT>);
+}
+template <typename T, int R, int B, int MAXT> const void* cluster_step_kernel_ptr() {
+  return reinterpret_cast<const void*>(&ffs_cluster_kernel<T, R, B, MAXT, true>);
+}
+template <int MAXT> const void* mma_kernel_ptr() {
+  return reinterpret_cast<const void*>(&ffs_mma_kernel<MAXT>);
 }
 }  // namespace ffsk

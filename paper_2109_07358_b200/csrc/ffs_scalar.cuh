@@ -24,6 +24,8 @@ template <typename T> struct Sc;
 template <> struct Sc<double> {
   static constexpr int kDoubles = 1;
   __device__ __forceinline__ static double zero() { return 0.0; }
+  __device__ __forceinline__ static double one() { return 1.0; }
+  __device__ __forceinline__ static double neg(double a) { return -a; }
   // c - a*b
   __device__ __forceinline__ static double fms(double a, double b, double c) { return fma(-a, b, c); }
   __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
@@ -35,6 +37,8 @@ template <> struct Sc<double> {
 template <> struct Sc<cplx> {
   static constexpr int kDoubles = 2;
   __device__ __forceinline__ static cplx zero() { return {0.0, 0.0}; }
+  __device__ __forceinline__ static cplx one() { return {1.0, 0.0}; }
+  __device__ __forceinline__ static cplx neg(cplx a) { return {-a.re, -a.im}; }
   __device__ __forceinline__ static cplx fms(cplx a, cplx b, cplx c) {
     cplx r;
     r.re = fma(-a.re, b.re, fma(a.im, b.im, c.re));

@@ -859,8 +859,10 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
       // rows drawn in earlier blocks: exactly zero (the contraction leaves O(eps) residues)
       // rows drawn earlier get weight exactly 0: mask the column of the next draw (only that
       // column is ever squared; the contraction leaves O(eps) residues in drawn rows)
+      if constexpr ((OPT & 512) == 0) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) P[r][0] = ((chosen >> r) & 1u) ? 0.0 : P[r][0];
+        for (int r = 0; r < R; ++r) P[r][0] = ((chosen >> r) & 1u) ? 0.0 : P[r][0];
+      }
       if constexpr (tm) {
         const long long t = clock64();
         tacc[0] += (t - tA);
@@ -887,7 +889,27 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           bool common;
           if constexpr (G == 32 && (OPT & 160) != 0) common = dr.ball != 0u;
           else common = __all_sync(0xffffffffu, dr.ball != 0u);
-          if (common) {
+          if constexpr ((OPT & 512) != 0) {
+            // rows drawn earlier are not masked (they hold O(eps) residues of weight ~eps^2 T):
+            // a crossing on such a row, or no crossing at all, takes the exact masked redraw
+            static_assert(G == 32, "OPT 512 is written for one segment per warp");
+            own = __ffs(dr.ball) - 1;
+            common = common && !__any_sync(0xffffffffu, (lane == own) && ((chosen >> dr.rsel) & 1u));
+            if (!common) {
+              double colr[R];
+#pragma unroll
+              for (int r = 0; r < R; ++r) colr[r] = ((chosen >> r) & 1u) ? 0.0 : P[r][rr];
+              dr = seg_draw<R, G, (OPT & 1) != 0>(colr, usel[k], seg);
+              if (dr.ball != 0u) {
+                own = __ffs(dr.ball) - 1;
+                orow = __shfl_sync(0xffffffffu, dr.rsel, own);
+              } else {
+                const int xf = seg_fallback<R, G>(colr, dr.T, chosen, L, sl, seg);
+                own = xf / R;
+                orow = xf % R;
+              }
+            }
+          } else if (common) {
             own = __ffs(dr.ball) - 1;
             if constexpr (!(OPT & 34)) orow = __shfl_sync(0xffffffffu, dr.rsel, seg * G + own);
           } else {
@@ -921,10 +943,26 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
           // select tree (rs = its crossing row, or orow on the rare fallback path); the owner
           // lane's selection is then broadcast to its segment with shuffles (no smem, no branch)
           const double Tk = dr.T;
-          const int rs = dr.ball != 0u ? dr.rsel : orow;
+          const int rs = (OPT & 512) ? (common ? dr.rsel : orow) : (dr.ball != 0u ? dr.rsel : orow);
           double pv;  // pivot P[x_k][rr]
           double prow[B];
-          if constexpr ((OPT & 32) != 0) {
+          if constexpr ((OPT & 512) != 0) {
+            // only the owner lane branches into the store of its row rs (8-way switch, 64-bit
+            // stores: no register shuffling into 128-bit groups, no predicated stores elsewhere)
+            if (sl == own) {
+              double* dst = Row + rr * B;
+              switch (rs) {
+#define FFS_ROWST(RR) case RR: _Pragma("unroll") for (int c = 0; c < B; ++c) if (RR < R) dst[c] = P[RR < R ? RR : 0][c]; break;
+                FFS_ROWST(0) FFS_ROWST(1) FFS_ROWST(2) FFS_ROWST(3) FFS_ROWST(4) FFS_ROWST(5) FFS_ROWST(6) FFS_ROWST(7)
+#undef FFS_ROWST
+                default: break;
+              }
+              pos[k] = own * R + rs;
+            }
+            chosen |= (sl == own) ? (1u << rs) : 0u;
+            __syncwarp();
+            pv = Row[rr * B + rr];
+          } else if constexpr ((OPT & 32) != 0) {
             // columns rr and rr+1 first: they feed the reciprocal and the next column's update
             // (the critical path); the others only feed the in-block updates and Row
             auto extract = [&](int c) {
@@ -1013,8 +1051,10 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
             }
             // column rr+1 first, then the next draw, then the remaining columns
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-              P[r][rr + 1] = ((chosen >> r) & 1u) ? 0.0 : fma(-P[r][rr], sp[rr + 1], P[r][rr + 1]);
+            for (int r = 0; r < R; ++r) {
+              if constexpr ((OPT & 512) != 0) P[r][rr + 1] = fma(-P[r][rr], sp[rr + 1], P[r][rr + 1]);
+              else P[r][rr + 1] = ((chosen >> r) & 1u) ? 0.0 : fma(-P[r][rr], sp[rr + 1], P[r][rr + 1]);
+            }
             if (rr + 1 < nb) {
               double cn[R];
 #pragma unroll

@@ -47,7 +47,9 @@ SMALL = [
     # (L, N, N', complex) — spans every variant of pick_variant() and ragged tails
     (16, 4, 4, False), (7, 3, 3, False), (32, 9, 9, False), (50, 17, 17, False),
     (100, 23, 23, False), (128, 40, 13, False), (256, 32, 32, False), (200, 60, 60, False),
-    (256, 90, 90, False), (300, 33, 33, False), (1024, 40, 21, False), (1500, 19, 19, False),
+    (256, 90, 90, False), (300, 33, 33, False),
+    (129, 9, 9, False), (160, 45, 45, False), (250, 48, 17, False), (256, 5, 5, False),
+    (2048, 256, 256, False), (3000, 260, 260, False), (1024, 40, 21, False), (1500, 19, 19, False),
     (5000, 11, 11, False), (9000, 7, 7, False),
     (16, 4, 4, True), (30, 11, 11, True), (64, 21, 9, True), (128, 30, 30, True),
     (500, 26, 26, True), (2000, 9, 9, True), (6000, 5, 5, True),
