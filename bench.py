@@ -263,7 +263,7 @@ def run_gpu(args):
             "weight_gflops": value * weight_flops(cfg.L, Np, cplx) / 1e9,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                         "kernel": "ffs_seg_kernel" if ffs_uses_warp(cfg, Np, cplx) else "ffs_sample_kernel",
+                         "kernel": ffs_path_kernel(cfg, Np, cplx),
                          "kernel_ms": kms, "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"},
             "gpu_launches": launches,
             "sample_flags_nonzero": flags_bad,
@@ -289,6 +289,17 @@ def run_gpu(args):
 
 def ffs_uses_warp(cfg, Np, cplx):
     return (not cplx) and cfg.L <= 256 and Np <= 48
+
+
+def ffs_path_kernel(cfg, Np, cplx):
+    """Name of the timed kernel (sequence) of the path libffs dispatches to (ffs_abi.cu launch())."""
+    if ffs_uses_warp(cfg, Np, cplx):
+        return "ffs_seg_kernel"
+    if cfg.L >= 2048:
+        if (not cplx) and Np == cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
+            return "dense path: ffs_dgemm_kernel + ffs_cluster_kernel<STEP> + ffs_dense_gj_kernel per block"
+        return "ffs_cluster_kernel"
+    return "ffs_sample_kernel"
 
 
 def main():
