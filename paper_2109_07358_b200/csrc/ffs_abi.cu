@@ -526,7 +526,7 @@ int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
 bool dense_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   const char* g = getenv("FFS_NO_DENSE");
   if (g && g[0] == '1') return false;
-  return dtype == FFS_F64 && Np == N && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
+  return Np == N && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
 }
 
 struct DensePlan {
@@ -535,12 +535,17 @@ struct DensePlan {
   size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, total;
 };
 
-int make_dense_plan(int64_t L, int64_t N, int64_t Np, int64_t M, DensePlan& d) {
-  int rc = make_cluster_plan(L, N, Np, FFS_F64, M, d.c);
+int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
+  const bool cx = dtype == FFS_C128;
+  int rc = make_cluster_plan(L, N, Np, dtype, M, d.c);
   if (rc != FFS_OK) return rc;
-  d.c.fn = ffsk::cluster_step_kernel_ptr<double, 4, 8, 512>();
-  d.c.R = 4;
+  d.c.fn = cx ? ffsk::cluster_step_kernel_ptr<cplx, 2, 8, 512>() : ffsk::cluster_step_kernel_ptr<double, 4, 8, 512>();
+  d.c.R = cx ? 2 : 4;
   d.c.B = 8;
+  d.c.Lc = 512 * d.c.R;
+  d.c.CS = std::max<int>(2, (int)((L + d.c.Lc - 1) / d.c.Lc));
+  if (d.c.CS > 8) d.c.CS = 16;
+  d.c.Lpt = d.c.CS * d.c.Lc;
   if (cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.c.smem) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(step smem) failed");
   if (d.c.CS > 8 && cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -551,27 +556,32 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int64_t M, DensePlan& d) {
   int64_t cap = 1024;  // samples per lockstep batch
   if (const char* e = getenv("FFS_DENSE_S")) cap = std::max<int64_t>(1, atoll(e));  // development
   d.S = std::max<int64_t>(1, std::min<int64_t>(M, cap));
-  d.ldY = (d.S * d.c.B + ffsk::kGN - 1) / ffsk::kGN * ffsk::kGN;
+  // ldY in scalars of T; the GEMM's N (2 ldY real columns for complex) is a multiple of 128
+  const int64_t q = cx ? ffsk::kGN / 2 : ffsk::kGN;
+  d.ldY = (d.S * d.c.B + q - 1) / q * q;
+  const size_t es = cx ? 16 : 8;
   d.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-  d.ws_y = align_up((size_t)N * d.ldY * 8);
-  d.ws_p = align_up((size_t)L * d.ldY * 8);
-  d.ws_w = align_up((size_t)d.S * Np * Np * 8);
+  d.ws_y = align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: real 2N x 2ldY expansion
+  d.ws_p = align_up((size_t)L * d.ldY * es);
+  d.ws_w = align_up((size_t)d.S * Np * Np * es);
   d.ws_ch = align_up((size_t)d.S * (d.c.Lpt / 32) * 4);
-  d.ws_row = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * 8);
+  d.ws_row = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * es);
   d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row;
-  const size_t gjs = ffsk::dense_gj_smem<8>((int)Np);
+  const size_t gjs = cx ? ffsk::dense_gj_smem<cplx, 8>((int)Np) : ffsk::dense_gj_smem<double, 8>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
-  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<8>),
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
+  const void* gjf = cx ? reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<cplx, 8>)
+                       : reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<double, 8>);
+  if (cudaFuncSetAttribute(gjf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(gj smem) failed");
   return FFS_OK;
 }
 
-int launch_dense(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, const double* uniforms,
+int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
                  int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
                  double* trace) {
+  const bool cx = dtype == FFS_C128;
   DensePlan d;
-  int rc = make_dense_plan(L, N, Np, M, d);
+  int rc = make_dense_plan(L, N, Np, dtype, M, d);
   if (rc != FFS_OK) return rc;
   if (!ws || ws_bytes < d.total) return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, d.total);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
@@ -630,20 +640,26 @@ int launch_dense(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, con
   gp.A = static_cast<const double*>(U);
   gp.B = Y;
   gp.C = Pd;
-  gp.lda = N;
-  gp.ldb = d.ldY;
-  gp.ldc = d.ldY;
+  // complex: the real GEMM of U viewed as L x 2N with the real 2N x 2ldY expansion of Y
+  const int64_t f = cx ? 2 : 1;
+  gp.lda = f * N;
+  gp.ldb = f * d.ldY;
+  gp.ldc = f * d.ldY;
   gp.M = (int)L;
-  gp.N = (int)d.ldY;
-  gp.K = (int)N;
-  const dim3 ggrid((unsigned)(d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
+  gp.N = (int)(f * d.ldY);
+  gp.K = (int)(f * N);
+  const dim3 ggrid((unsigned)(f * d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
   for (int64_t base = 0; base < M; base += d.S) {
     const int64_t Sb = std::min<int64_t>(d.S, M - base);
     cudaMemsetAsync(Y, 0, d.ws_y, stream);
     cudaMemsetAsync(ch, 0, d.ws_ch, stream);
     if (flags) cudaMemsetAsync(flags + base, 0, (size_t)Sb * 4, stream);
-    ffsk::ffs_dense_y0_kernel<8><<<(unsigned)((Sb * 8 + 255) / 256), 256, 0, stream>>>(perm, Y, d.ldY, base,
-                                                                                       (int)Sb, (int)Np);
+    if (cx)
+      ffsk::ffs_dense_y0_kernel<cplx, 8><<<(unsigned)((Sb * 8 + 255) / 256), 256, 0, stream>>>(perm, Y, d.ldY, base,
+                                                                                              (int)Sb, (int)Np);
+    else
+      ffsk::ffs_dense_y0_kernel<double, 8><<<(unsigned)((Sb * 8 + 255) / 256), 256, 0, stream>>>(perm, Y, d.ldY, base,
+                                                                                                (int)Sb, (int)Np);
     ++g_launches;
     p.base = base;
     p.Sb = (int)Sb;
@@ -672,7 +688,10 @@ int launch_dense(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, con
         q.base = base;
         const int nc = (int)Np - k0 - d.c.B;
         const dim3 jg((unsigned)((nc + ffsk::kGjTJ - 1) / ffsk::kGjTJ), (unsigned)Sb);
-        ffsk::ffs_dense_gj_kernel<8><<<jg, 256, ffsk::dense_gj_smem<8>(k0), stream>>>(q);
+        if (cx)
+          ffsk::ffs_dense_gj_kernel<cplx, 8><<<jg, 256, ffsk::dense_gj_smem<cplx, 8>(k0), stream>>>(q);
+        else
+          ffsk::ffs_dense_gj_kernel<double, 8><<<jg, 256, ffsk::dense_gj_smem<double, 8>(k0), stream>>>(q);
         ++g_launches;
       }
     }
@@ -707,7 +726,7 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   if (use_warp_path(L, N, Np, dtype))
     return launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   if (dense_eligible(L, N, Np, dtype))
-    return launch_dense(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
+    return launch_dense(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   if (cluster_eligible(L, dtype))
     return launch_cluster(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
   Plan pl;
@@ -768,7 +787,7 @@ size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int6
   }
   if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && dense_eligible(L, N, Nprime, dtype)) {
     DensePlan d;
-    if (make_dense_plan(L, N, Nprime, std::max<int64_t>(M, 1), d) != FFS_OK) return 0;
+    if (make_dense_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), d) != FFS_OK) return 0;
     return d.total;
   }
   if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && cluster_eligible(L, dtype)) {

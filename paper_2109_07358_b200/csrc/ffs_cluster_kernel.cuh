@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       // are staged kKC at a time through shared memory)
       if constexpr (STEP) {
         // the Gauss-Jordan update runs batched in ffs_dense_gj_kernel: hand it S = L U of this block
+        __syncthreads();  // the last draw's Row / Pinv entries come from other warps
         if (rank == 0 && t < B * B + B) {
           T* rg = reinterpret_cast<T*>(p.rowg) + sl * (B * B + B);
           rg[t] = t < B * B ? Row[t] : Pinv[t - B * B];

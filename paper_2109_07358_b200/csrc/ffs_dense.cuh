@@ -135,15 +135,32 @@ static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const Dg
 }
 
 // Y for the first block: Y[m_c][s*B + c] = 1 (c < min(B, N')); Y is zero otherwise (memset).
-template <int B>
+// Complex T: Y is stored as its real 2N x 2ldY expansion (see dense_y_store).
+template <typename T>
+__device__ __forceinline__ void dense_y_store(double* Y, int64_t ldY, int n, int64_t col, T v);
+template <>
+__device__ __forceinline__ void dense_y_store<double>(double* Y, int64_t ldY, int n, int64_t col, double v) {
+  Y[(size_t)n * ldY + col] = v;
+}
+// complex y at (n, col) -> real 2x2 block [[re, im], [-im, re]] at rows 2n, 2n+1, columns 2col, 2col+1
+// of the real (2N x 2ldY) matrix, so that the real GEMM of U viewed as L x 2N (interleaved re, im)
+// with it yields P interleaved: P'[x][2c] = sum Ur yr - Ui yi, P'[x][2c+1] = sum Ur yi + Ui yr.
+template <>
+__device__ __forceinline__ void dense_y_store<cplx>(double* Y, int64_t ldY, int n, int64_t col, cplx v) {
+  double* r0 = Y + (size_t)(2 * n) * (2 * ldY) + 2 * col;
+  double* r1 = r0 + 2 * ldY;
+  *reinterpret_cast<double2*>(r0) = make_double2(v.re, v.im);
+  *reinterpret_cast<double2*>(r1) = make_double2(-v.im, v.re);
+}
+
+template <typename T, int B>
 static __global__ void ffs_dense_y0_kernel(const int32_t* __restrict__ perm, double* __restrict__ Y, int64_t ldY,
-                                    int64_t base, int Sb, int Np) {
+                                           int64_t base, int Sb, int Np) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= Sb * B) return;
   const int s = idx / B, c = idx % B;
-  if (c < Np) Y[(size_t)perm[(base + s) * Np + c] * ldY + (size_t)s * B + c] = 1.0;
+  if (c < Np) dense_y_store<T>(Y, ldY, perm[(base + s) * Np + c], (int64_t)s * B + c, Sc<T>::one());
 }
-
 
 // ---------------------------------------------------------------- batched Gauss-Jordan update
 // After the draws of block [k0, k0+B) of every batch sample (all samples share k0): with
@@ -162,18 +179,19 @@ struct DenseGjParams {
   const int32_t* positions; // [M][Np]
   const double* rowg;       // [Sb][B*B + B]
   double* W;                // [Sb][Np][Np]
-  double* Y;                // [N][ldY]
-  int64_t ldY, base;
+  double* Y;                // [N][ldY] (complex: the real 2N x 2ldY expansion)
+  int64_t ldY, base;        // ldY in scalars of T
   int N, Np, k0;
 };
 
-template <int B>
+template <typename T, int B>
 __host__ __device__ inline size_t dense_gj_smem(int k0) {
-  return sizeof(double) * ((size_t)2 * B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
+  return sizeof(T) * ((size_t)2 * B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
 }
 
-template <int B>
+template <typename T, int B>
 static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjParams q) {
+  using S = Sc<T>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int k0 = q.k0, k1 = k0 + B, Np = q.Np, N = q.N;
   const int sl = blockIdx.y;
@@ -181,33 +199,34 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   const int t = threadIdx.x, jl = t % kGjTJ, part = t / kGjTJ;
   const int j = k1 + blockIdx.x * kGjTJ + jl;
   const bool has = j < Np;
-  double* Vn = reinterpret_cast<double*>(smem);   // [B][k0]   V[X_new, 0:k0]
-  double* Wb = Vn + (size_t)B * k0;               // [k0][B]   W[0:k0, k0:k1]
-  double* Zp = Wb + (size_t)B * k0;               // [4][B][TJ] partial sums, then Z [B][TJ]
-  double* Zs = Zp + 4 * B * kGjTJ;                // [B][TJ]
-  double* RP = Zs + B * kGjTJ;                    // Row [B][B], Pinv [B]
+  T* Vn = reinterpret_cast<T*>(smem);   // [B][k0]   V[X_new, 0:k0]
+  T* Wb = Vn + (size_t)B * k0;          // [k0][B]   W[0:k0, k0:k1]
+  T* Zp = Wb + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
+  T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
+  T* RP = Zs + B * kGjTJ;               // Row [B][B], Pinv [B]
   int* xn = reinterpret_cast<int*>(RP + B * B + B);
   const int32_t* pm = q.perm + i_s * Np;
-  double* W = q.W + (size_t)sl * Np * Np;
+  const T* Ug = reinterpret_cast<const T*>(q.U);
+  T* W = reinterpret_cast<T*>(q.W) + (size_t)sl * Np * Np;
   if (t < B) xn[t] = q.positions[i_s * Np + k0 + t];
-  if (t < B * B + B) RP[t] = q.rowg[(size_t)sl * (B * B + B) + t];
+  if (t < B * B + B) RP[t] = reinterpret_cast<const T*>(q.rowg)[(size_t)sl * (B * B + B) + t];
   __syncthreads();
   for (int idx = t; idx < B * k0; idx += blockDim.x) {
     const int tt = idx / k0, ii = idx % k0;
-    Vn[idx] = q.U[(size_t)xn[tt] * N + pm[ii]];
+    Vn[idx] = Ug[(size_t)xn[tt] * N + pm[ii]];
   }
   for (int idx = t; idx < B * k0; idx += blockDim.x) Wb[idx] = W[(size_t)(idx / B) * Np + k0 + idx % B];
   __syncthreads();
   // (1) partial sums over this thread's slice of i
-  double acc[B];
+  T acc[B];  // minus the partial sums
 #pragma unroll
-  for (int tt = 0; tt < B; ++tt) acc[tt] = 0.0;
+  for (int tt = 0; tt < B; ++tt) acc[tt] = S::zero();
   if (has) {
 #pragma unroll 4
     for (int ii = part; ii < k0; ii += 4) {
-      const double w = W[(size_t)ii * Np + j];
+      const T w = W[(size_t)ii * Np + j];
 #pragma unroll
-      for (int tt = 0; tt < B; ++tt) acc[tt] = fma(Vn[tt * k0 + ii], w, acc[tt]);
+      for (int tt = 0; tt < B; ++tt) acc[tt] = S::fms(Vn[tt * k0 + ii], w, acc[tt]);
     }
   }
 #pragma unroll
@@ -215,22 +234,24 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   __syncthreads();
   // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
   if (part == 0 && has) {
-    double z[B];
+    T z[B];
 #pragma unroll
-    for (int tt = 0; tt < B; ++tt)
-      z[tt] = q.U[(size_t)xn[tt] * N + pm[j]] - ((Zp[(0 * B + tt) * kGjTJ + jl] + Zp[(1 * B + tt) * kGjTJ + jl]) +
-                                               (Zp[(2 * B + tt) * kGjTJ + jl] + Zp[(3 * B + tt) * kGjTJ + jl]));
-    const double* Row = RP;
-    const double* Pinv = RP + B * B;
+    for (int tt = 0; tt < B; ++tt) {
+      const T a01 = S::add(Zp[(0 * B + tt) * kGjTJ + jl], Zp[(1 * B + tt) * kGjTJ + jl]);
+      const T a23 = S::add(Zp[(2 * B + tt) * kGjTJ + jl], Zp[(3 * B + tt) * kGjTJ + jl]);
+      z[tt] = S::add(Ug[(size_t)xn[tt] * N + pm[j]], S::add(a01, a23));
+    }
+    const T* Row = RP;
+    const T* Pinv = RP + B * B;
 #pragma unroll
     for (int tt = 1; tt < B; ++tt)
 #pragma unroll
-      for (int s2 = 0; s2 < tt; ++s2) z[tt] = fma(-(Row[tt * B + s2] * Pinv[s2]), z[s2], z[tt]);
+      for (int s2 = 0; s2 < tt; ++s2) z[tt] = S::fms(S::mul(Row[tt * B + s2], Pinv[s2]), z[s2], z[tt]);
 #pragma unroll
     for (int tt = B - 1; tt >= 0; --tt) {
 #pragma unroll
-      for (int s2 = tt + 1; s2 < B; ++s2) z[tt] = fma(-Row[tt * B + s2], z[s2], z[tt]);
-      z[tt] *= Pinv[tt];
+      for (int s2 = tt + 1; s2 < B; ++s2) z[tt] = S::fms(Row[tt * B + s2], z[s2], z[tt]);
+      z[tt] = S::mul(z[tt], Pinv[tt]);
     }
 #pragma unroll
     for (int tt = 0; tt < B; ++tt) {
@@ -241,14 +262,14 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   __syncthreads();
   // (3) rank-B update of the earlier rows
   if (has) {
-    double z[B];
+    T z[B];
 #pragma unroll
     for (int tt = 0; tt < B; ++tt) z[tt] = Zs[tt * kGjTJ + jl];
 #pragma unroll 4
     for (int ii = part; ii < k0; ii += 4) {
-      double a = W[(size_t)ii * Np + j];
+      T a = W[(size_t)ii * Np + j];
 #pragma unroll
-      for (int tt = 0; tt < B; ++tt) a = fma(-Wb[ii * B + tt], z[tt], a);
+      for (int tt = 0; tt < B; ++tt) a = S::fms(Wb[ii * B + tt], z[tt], a);
       W[(size_t)ii * Np + j] = a;
     }
   }
@@ -256,12 +277,12 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   if (blockIdx.x == 0) {
     __syncthreads();
     const int nb1 = min(B, Np - k1);
-    double* Yg = q.Y + (size_t)sl * B;
+    const int64_t col0 = (int64_t)sl * B;
     for (int idx = t; idx < k1 * B; idx += blockDim.x) {
       const int ii = idx / B, c = idx % B;
-      Yg[(size_t)pm[ii] * q.ldY + c] = c < nb1 ? -W[(size_t)ii * Np + k1 + c] : 0.0;
+      dense_y_store<T>(q.Y, q.ldY, pm[ii], col0 + c, c < nb1 ? S::neg(W[(size_t)ii * Np + k1 + c]) : S::zero());
     }
-    if (t < nb1) Yg[(size_t)pm[k1 + t] * q.ldY + t] = 1.0;
+    if (t < nb1) dense_y_store<T>(q.Y, q.ldY, pm[k1 + t], col0 + t, S::one());
   }
 }
 

@@ -26,6 +26,7 @@ template <> struct Sc<double> {
   __device__ __forceinline__ static double zero() { return 0.0; }
   __device__ __forceinline__ static double one() { return 1.0; }
   __device__ __forceinline__ static double neg(double a) { return -a; }
+  __device__ __forceinline__ static double add(double a, double b) { return a + b; }
   // c - a*b
   __device__ __forceinline__ static double fms(double a, double b, double c) { return fma(-a, b, c); }
   __device__ __forceinline__ static double mul(double a, double b) { return a * b; }
@@ -39,6 +40,7 @@ template <> struct Sc<cplx> {
   __device__ __forceinline__ static cplx zero() { return {0.0, 0.0}; }
   __device__ __forceinline__ static cplx one() { return {1.0, 0.0}; }
   __device__ __forceinline__ static cplx neg(cplx a) { return {-a.re, -a.im}; }
+  __device__ __forceinline__ static cplx add(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
   __device__ __forceinline__ static cplx fms(cplx a, cplx b, cplx c) {
     cplx r;
     r.re = fma(-a.re, b.re, fma(a.im, b.im, c.re));

@@ -52,7 +52,7 @@ SMALL = [
     (2048, 256, 256, False), (3000, 260, 260, False), (1024, 40, 21, False), (1500, 19, 19, False),
     (5000, 11, 11, False), (9000, 7, 7, False),
     (16, 4, 4, True), (30, 11, 11, True), (64, 21, 9, True), (128, 30, 30, True),
-    (500, 26, 26, True), (2000, 9, 9, True), (6000, 5, 5, True),
+    (500, 26, 26, True), (2000, 9, 9, True), (6000, 5, 5, True), (2048, 256, 256, True), (2500, 258, 258, True),
 ]
 
 
