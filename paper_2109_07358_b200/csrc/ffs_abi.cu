@@ -648,6 +648,7 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
   gp.M = (int)L;
   gp.N = (int)(f * d.ldY);
   gp.K = (int)(f * N);
+  gp.panel = (int)(f * d.c.B);  // P in per-sample [L][B] panels (contiguous reads in the step kernel)
   const dim3 ggrid((unsigned)(f * d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
   for (int64_t base = 0; base < M; base += d.S) {
     const int64_t Sb = std::min<int64_t>(d.S, M - base);

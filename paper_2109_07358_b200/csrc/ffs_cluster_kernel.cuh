@@ -201,13 +201,30 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       // previous block's update + cluster barrier; its rows are staged kKC at a time)
       T P[R][B];
       if constexpr (STEP) {
-        // the panel from the dense GEMM P = U Y (rows >= L are zero)
-        const T* pb = reinterpret_cast<const T*>(p.Pd) + (size_t)sl * B;
+        // the panel from the dense GEMM P = U Y, per-sample layout [L][B] (rows >= L are zero):
+        // this thread's R rows are R*B contiguous scalars, read as 16-byte vectors
+        const double2* pb = reinterpret_cast<const double2*>(reinterpret_cast<const T*>(p.Pd) +
+                                                             ((size_t)sl * L + row0) * B);
+        constexpr int kV = B * S::kDoubles / 2;  // 16-byte vectors per row
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool in = row0 + r < L;
 #pragma unroll
-          for (int c = 0; c < B; ++c) P[r][c] = (in && c < nb) ? pb[(size_t)(row0 + r) * p.ldY + c] : S::zero();
+          for (int v = 0; v < kV; ++v) {
+            const double2 d2 = in ? pb[r * kV + v] : make_double2(0.0, 0.0);
+            if constexpr (S::kDoubles == 1) {
+              P[r][2 * v] = d2.x;
+              P[r][2 * v + 1] = d2.y;
+            } else {
+              reinterpret_cast<double*>(&P[r][v])[0] = d2.x;
+              reinterpret_cast<double*>(&P[r][v])[1] = d2.y;
+            }
+          }
+          if (nb < B) {
+#pragma unroll
+            for (int c = 0; c < B; ++c)
+              if (c >= nb) P[r][c] = S::zero();
+          }
         }
       } else {
 #pragma unroll

@@ -26,9 +26,9 @@ namespace ffsk {
 
 // ---------------------------------------------------------------- DMMA DGEMM C = A B
 // Row-major A [M][K] (lda), B [K][N] (ldb), C [M][N] (ldc); N % 128 == 0 and K % 2 == 0 (the
-// host pads); rows >= M and k >= K are zero-filled. CTA tile 128 x 128 x 16, 8 warps as 4 (M) x 2
-// (N), warp tile 32 x 64 = 4 x 8 DMMA m8n8k4 tiles, 4-stage cp.async pipeline (128 KB smem).
-constexpr int kGM = 128, kGN = 128, kGK = 16, kGStages = 4, kGThreads = 256;
+// host pads); rows >= M and k >= K are zero-filled. CTA tile 128 x 128 x 32, 8 warps as 4 (M) x 2
+// (N), warp tile 32 x 64 = 4 x 8 DMMA m8n8k4 tiles, 3-stage cp.async pipeline of 32-deep K slices (192 KB smem).
+constexpr int kGM = 128, kGN = 128, kGK = 32, kGStages = 3, kGThreads = 256;
 constexpr size_t kGemmSmem = (size_t)kGStages * (kGM * kGK + kGK * kGN) * sizeof(double);
 
 struct DgemmParams {
@@ -37,6 +37,7 @@ struct DgemmParams {
   double* C;
   int64_t lda, ldb, ldc;
   int M, N, K;
+  int panel;  // > 0: C in per-sample panel layout, column n -> C[(n / panel) * M * panel + row * panel + n % panel]
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -50,8 +51,8 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
 }
 
-// Shared-memory swizzles (8-byte element units): the A tile is [128][16] with element (r, c) at
-// r*16 + (c ^ 4(r&3)); the B tile is [16][128] with (k, n) at k*128 + (n ^ 4(k&3)). The XOR only
+// Shared-memory swizzles (8-byte element units): the A tile is [128][32] with element (r, c) at
+// r*32 + (c ^ 4(r&3)); the B tile is [32][128] with (k, n) at k*128 + (n ^ 4(k&3)). The XOR only
 // touches bits 2-3, so the 16-byte cp.async chunks stay contiguous, and each half-warp phase of
 // the fragment loads (g = 0..3 or 4..7, t4 = 0..3) hits 16 distinct 8-byte bank slots.
 static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const DgemmParams p) {
@@ -69,15 +70,15 @@ static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const Dg
     double* as = As + st * kGM * kGK;
     double* bs = Bs + st * kGK * kGN;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {  // A: 128 rows x 8 chunks
-      const int c = t + i * kGThreads, r = c >> 3, ch = c & 7;
+    for (int i = 0; i < kGM * kGK / 2 / kGThreads; ++i) {  // A: 128 rows x kGK/2 chunks
+      const int c = t + i * kGThreads, r = c / (kGK / 2), ch = c % (kGK / 2);
       const int gr = m0 + r, gk = kk + 2 * ch;
       const bool in = gr < p.M && gk < p.K;
       const double* src = p.A + (in ? (size_t)gr * p.lda + gk : 0);
       cp_async16(as + r * kGK + ((2 * ch) ^ ((r & 3) << 2)), src, in ? 16 : 0);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {  // B: 16 rows x 64 chunks
+    for (int i = 0; i < kGK * kGN / 2 / kGThreads; ++i) {  // B: kGK rows x 64 chunks
       const int c = t + i * kGThreads, r = c >> 6, ch = c & 63;
       const int gk = kk + r;
       const bool in = gk < p.K;
@@ -128,7 +129,9 @@ static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const Dg
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int col = n0 + wn * 64 + j * 8 + 2 * t4;
-        *reinterpret_cast<double2*>(p.C + (size_t)row * p.ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        const size_t off = p.panel > 0 ? (size_t)(col / p.panel) * p.M * p.panel + (size_t)row * p.panel + col % p.panel
+                                       : (size_t)row * p.ldc + col;
+        *reinterpret_cast<double2*>(p.C + off) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
     }
   }
