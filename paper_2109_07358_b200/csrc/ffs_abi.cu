@@ -531,9 +531,17 @@ bool dense_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
 
 struct DensePlan {
   ClusterPlan c;
-  int64_t S, ldY;
-  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, total;
+  int64_t S, Sh, ldY;  // batch, half-batch (per stream), Y row stride in scalars of T
+  int nstr;            // streams (half-batches) in flight
+  bool small_gemm;     // GEMM <16, 4> (co-resident with the GJ kernel) instead of <32, 3>
+  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, total, y_half, p_half;
 };
+
+template <typename T>
+const void* dense_gj_fn(bool lean) {
+  return lean ? reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, 32>)
+              : reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, 64>);
+}
 
 int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
   const bool cx = dtype == FFS_C128;
@@ -550,31 +558,48 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(step smem) failed");
   if (d.c.CS > 8 && cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
     return fail(FFS_ECUDA, "non-portable cluster size not allowed");
-  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel),
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffsk::kGemmSmem) != cudaSuccess)
+  // one stream and the <32, 3> GEMM: two half-batches on two streams with the co-residable
+  // <16, 4> GEMM + 128-thread GJ measured no overlap gain (C4 1.570 vs 1.526 s, C5 1.663 vs 1.549 s)
+  d.nstr = 1;
+  if (const char* e = getenv("FFS_DENSE_STREAMS")) d.nstr = std::max(1, std::min(2, atoi(e)));  // development
+  d.small_gemm = false;
+  if (const char* e = getenv("FFS_DENSE_GEMM")) d.small_gemm = atoi(e) == 16;  // development
+  const void* gf = d.small_gemm ? reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel<16, 4>)
+                                : reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel<32, 3>);
+  const size_t gsm = d.small_gemm ? ffsk::gemm_smem<16, 4>() : ffsk::gemm_smem<32, 3>();
+  if (cudaFuncSetAttribute(gf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(gemm smem) failed");
   int64_t cap = 1024;  // samples per lockstep batch
   if (const char* e = getenv("FFS_DENSE_S")) cap = std::max<int64_t>(1, atoll(e));  // development
   d.S = std::max<int64_t>(1, std::min<int64_t>(M, cap));
+  if (d.S < 2) d.nstr = 1;
+  d.Sh = (d.S + d.nstr - 1) / d.nstr;
   // ldY in scalars of T; the GEMM's N (2 ldY real columns for complex) is a multiple of 128
   const int64_t q = cx ? ffsk::kGN / 2 : ffsk::kGN;
-  d.ldY = (d.S * d.c.B + q - 1) / q * q;
+  d.ldY = (d.Sh * d.c.B + q - 1) / q * q;
   const size_t es = cx ? 16 : 8;
+  d.y_half = align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: real 2N x 2ldY expansion
+  d.p_half = align_up((size_t)L * d.ldY * es);
   d.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-  d.ws_y = align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: real 2N x 2ldY expansion
-  d.ws_p = align_up((size_t)L * d.ldY * es);
-  d.ws_w = align_up((size_t)d.S * Np * Np * es);
-  d.ws_ch = align_up((size_t)d.S * (d.c.Lpt / 32) * 4);
-  d.ws_row = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * es);
+  d.ws_y = d.nstr * d.y_half;
+  d.ws_p = d.nstr * d.p_half;
+  d.ws_w = align_up((size_t)d.nstr * d.Sh * Np * Np * es);
+  d.ws_ch = align_up((size_t)d.nstr * d.Sh * (d.c.Lpt / 32) * 4);
+  d.ws_row = align_up((size_t)d.nstr * d.Sh * (d.c.B * d.c.B + d.c.B) * es);
   d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row;
-  const size_t gjs = cx ? ffsk::dense_gj_smem<cplx, 8>((int)Np) : ffsk::dense_gj_smem<double, 8>((int)Np);
+  const bool lean = d.small_gemm;
+  const size_t gjs = lean ? (cx ? ffsk::dense_gj_smem<cplx, 8, 32>((int)Np) : ffsk::dense_gj_smem<double, 8, 32>((int)Np))
+                          : (cx ? ffsk::dense_gj_smem<cplx, 8, 64>((int)Np) : ffsk::dense_gj_smem<double, 8, 64>((int)Np));
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
-  const void* gjf = cx ? reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<cplx, 8>)
-                       : reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<double, 8>);
+  const void* gjf = cx ? dense_gj_fn<cplx>(lean) : dense_gj_fn<double>(lean);
   if (cudaFuncSetAttribute(gjf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(gj smem) failed");
   return FFS_OK;
 }
+
+// a second stream (and fork/join events) per host thread for the 2-stream dense schedule
+thread_local cudaStream_t g_dense_s1 = nullptr;
+thread_local cudaEvent_t g_dense_fork = nullptr, g_dense_join = nullptr;
 
 int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
                  int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
@@ -585,13 +610,25 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
   if (rc != FFS_OK) return rc;
   if (!ws || ws_bytes < d.total) return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, d.total);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  const size_t es = cx ? 16 : 8;
+  const int B = d.c.B;
   char* w = static_cast<char*>(ws);
   int32_t* perm = reinterpret_cast<int32_t*>(w);
-  double* Y = reinterpret_cast<double*>(w + d.ws_perm);
-  double* Pd = reinterpret_cast<double*>(w + d.ws_perm + d.ws_y);
-  double* Wd = reinterpret_cast<double*>(w + d.ws_perm + d.ws_y + d.ws_p);
-  uint32_t* ch = reinterpret_cast<uint32_t*>(w + d.ws_perm + d.ws_y + d.ws_p + d.ws_w);
-  double* rowg = reinterpret_cast<double*>(w + d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch);
+  char* Yb = w + d.ws_perm;
+  char* Pb = Yb + d.ws_y;
+  char* Wb = Pb + d.ws_p;
+  uint32_t* ch = reinterpret_cast<uint32_t*>(Wb + d.ws_w);
+  char* rowb = Wb + d.ws_w + d.ws_ch;
+  cudaStream_t st[2] = {stream, stream};
+  if (d.nstr > 1) {
+    if (!g_dense_s1) {
+      if (cudaStreamCreateWithFlags(&g_dense_s1, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_dense_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g_dense_join, cudaEventDisableTiming) != cudaSuccess)
+        return fail(FFS_ECUDA, "dense path: stream/event creation failed");
+    }
+    st[1] = g_dense_s1;
+  }
   if (g_prof) {
     if (!g_ev0) {
       cudaEventCreate(&g_ev0);
@@ -606,96 +643,123 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
                                                                                        (int)Np);
     ++g_launches;
   }
-  ffsk::ClusterParams p{};
-  p.U = static_cast<const double*>(U);
-  p.L = (int)L;
-  p.N = (int)N;
-  p.Np = (int)Np;
-  p.Lc = d.c.Lc;
-  p.Lpt = d.c.Lpt;
-  p.M = M;
-  p.uniforms = uniforms;
-  p.positions = positions;
-  p.flags = flags;
-  p.wfull = Wd;
-  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
-  p.trace = S > 0 ? trace : nullptr;
-  p.timing = nullptr;
-  p.Pd = Pd;
-  p.ldY = d.ldY;
-  p.rowg = rowg;
-  ffsk::DenseGjParams q{};
-  q.U = static_cast<const double*>(U);
-  q.perm = perm;
-  q.positions = positions;
-  q.rowg = rowg;
-  q.W = Wd;
-  q.Y = Y;
-  q.ldY = d.ldY;
-  q.N = (int)N;
-  q.Np = (int)Np;
-  p.permg = perm;
-  p.chosen_g = ch;
-  ffsk::DgemmParams gp{};
-  gp.A = static_cast<const double*>(U);
-  gp.B = Y;
-  gp.C = Pd;
-  // complex: the real GEMM of U viewed as L x 2N with the real 2N x 2ldY expansion of Y
+  if (d.nstr > 1) {
+    cudaEventRecord(g_dense_fork, stream);
+    cudaStreamWaitEvent(st[1], g_dense_fork, 0);
+  }
   const int64_t f = cx ? 2 : 1;
-  gp.lda = f * N;
-  gp.ldb = f * d.ldY;
-  gp.ldc = f * d.ldY;
-  gp.M = (int)L;
-  gp.N = (int)(f * d.ldY);
-  gp.K = (int)(f * N);
-  gp.panel = (int)(f * d.c.B);  // P in per-sample [L][B] panels (contiguous reads in the step kernel)
-  const dim3 ggrid((unsigned)(f * d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
+  const void* gjf = cx ? dense_gj_fn<cplx>(d.small_gemm) : dense_gj_fn<double>(d.small_gemm);
+  const int gj_tj = d.small_gemm ? 32 : 64;
+  const size_t rstride = (size_t)(B * B + B) * es;
   for (int64_t base = 0; base < M; base += d.S) {
     const int64_t Sb = std::min<int64_t>(d.S, M - base);
-    cudaMemsetAsync(Y, 0, d.ws_y, stream);
-    cudaMemsetAsync(ch, 0, d.ws_ch, stream);
-    if (flags) cudaMemsetAsync(flags + base, 0, (size_t)Sb * 4, stream);
-    if (cx)
-      ffsk::ffs_dense_y0_kernel<cplx, 8><<<(unsigned)((Sb * 8 + 255) / 256), 256, 0, stream>>>(perm, Y, d.ldY, base,
-                                                                                              (int)Sb, (int)Np);
-    else
-      ffsk::ffs_dense_y0_kernel<double, 8><<<(unsigned)((Sb * 8 + 255) / 256), 256, 0, stream>>>(perm, Y, d.ldY, base,
-                                                                                                (int)Sb, (int)Np);
-    ++g_launches;
-    p.base = base;
-    p.Sb = (int)Sb;
-    for (int k0 = 0; k0 < Np; k0 += d.c.B) {
-      ffsk::ffs_dgemm_kernel<<<ggrid, ffsk::kGThreads, ffsk::kGemmSmem, stream>>>(gp);
+    ffsk::ClusterParams p[2] = {};
+    ffsk::DgemmParams gp[2] = {};
+    ffsk::DenseGjParams q[2] = {};
+    int64_t nh[2] = {0, 0};
+    for (int h = 0; h < d.nstr; ++h) {
+      const int64_t b0 = std::min<int64_t>(Sb, h * d.Sh);
+      nh[h] = std::min<int64_t>(Sb, b0 + d.Sh) - b0;
+      if (nh[h] <= 0) continue;
+      double* Y = reinterpret_cast<double*>(Yb + h * d.y_half);
+      double* Pd = reinterpret_cast<double*>(Pb + h * d.p_half);
+      double* Wd = reinterpret_cast<double*>(Wb + (size_t)h * d.Sh * Np * Np * es);
+      uint32_t* chh = ch + (size_t)h * d.Sh * (d.c.Lpt / 32);
+      double* rowg = reinterpret_cast<double*>(rowb + (size_t)h * d.Sh * rstride);
+      cudaMemsetAsync(Y, 0, d.y_half, st[h]);
+      cudaMemsetAsync(chh, 0, (size_t)nh[h] * (d.c.Lpt / 32) * 4, st[h]);
+      if (flags) cudaMemsetAsync(flags + base + b0, 0, (size_t)nh[h] * 4, st[h]);
+      const unsigned yg = (unsigned)((nh[h] * B + 255) / 256);
+      if (cx) ffsk::ffs_dense_y0_kernel<cplx, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
+      else ffsk::ffs_dense_y0_kernel<double, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
       ++g_launches;
-      p.k0 = k0;
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = d.c.CS;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.blockDim = dim3(d.c.threads);
-      cfg.gridDim = dim3((unsigned)(Sb * d.c.CS));
-      cfg.dynamicSmemBytes = d.c.smem;
-      cfg.stream = stream;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      void* args[] = {&p};
-      cudaError_t e = cudaLaunchKernelExC(&cfg, d.c.fn, args);
-      if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
-      ++g_launches;
-      if (k0 + d.c.B < Np) {
-        q.k0 = k0;
-        q.base = base;
-        const int nc = (int)Np - k0 - d.c.B;
-        const dim3 jg((unsigned)((nc + ffsk::kGjTJ - 1) / ffsk::kGjTJ), (unsigned)Sb);
-        if (cx)
-          ffsk::ffs_dense_gj_kernel<cplx, 8><<<jg, 256, ffsk::dense_gj_smem<cplx, 8>(k0), stream>>>(q);
+      ffsk::ClusterParams& c = p[h];
+      c.U = static_cast<const double*>(U);
+      c.L = (int)L;
+      c.N = (int)N;
+      c.Np = (int)Np;
+      c.Lc = d.c.Lc;
+      c.Lpt = d.c.Lpt;
+      c.M = M;
+      c.uniforms = uniforms;
+      c.positions = positions;
+      c.flags = flags;
+      c.wfull = Wd;
+      c.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+      c.trace = S > 0 ? trace : nullptr;
+      c.timing = nullptr;
+      c.Pd = Pd;
+      c.ldY = d.ldY;
+      c.rowg = rowg;
+      c.permg = perm;
+      c.chosen_g = chh;
+      c.base = base + b0;
+      c.Sb = (int)nh[h];
+      // complex: the real GEMM of U viewed as L x 2N with the real 2N x 2ldY expansion of Y
+      gp[h].A = static_cast<const double*>(U);
+      gp[h].B = Y;
+      gp[h].C = Pd;
+      gp[h].lda = f * N;
+      gp[h].ldb = f * d.ldY;
+      gp[h].ldc = f * d.ldY;
+      gp[h].M = (int)L;
+      gp[h].N = (int)(f * d.ldY);
+      gp[h].K = (int)(f * N);
+      gp[h].panel = (int)(f * B);  // P in per-sample [L][B] panels (contiguous reads in the step kernel)
+      q[h].U = static_cast<const double*>(U);
+      q[h].perm = perm;
+      q[h].positions = positions;
+      q[h].rowg = rowg;
+      q[h].W = Wd;
+      q[h].Y = Y;
+      q[h].ldY = d.ldY;
+      q[h].N = (int)N;
+      q[h].Np = (int)Np;
+      q[h].base = base + b0;
+    }
+    const dim3 ggrid((unsigned)(f * d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
+    for (int k0 = 0; k0 < Np; k0 += B) {
+      for (int h = 0; h < d.nstr; ++h) {
+        if (nh[h] <= 0) continue;
+        if (d.small_gemm)
+          ffsk::ffs_dgemm_kernel<16, 4><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<16, 4>(), st[h]>>>(gp[h]);
         else
-          ffsk::ffs_dense_gj_kernel<double, 8><<<jg, 256, ffsk::dense_gj_smem<double, 8>(k0), stream>>>(q);
+          ffsk::ffs_dgemm_kernel<32, 3><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<32, 3>(), st[h]>>>(gp[h]);
         ++g_launches;
+        p[h].k0 = k0;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = d.c.CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(d.c.threads);
+        cfg.gridDim = dim3((unsigned)(nh[h] * d.c.CS));
+        cfg.dynamicSmemBytes = d.c.smem;
+        cfg.stream = st[h];
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void* args[] = {&p[h]};
+        cudaError_t e = cudaLaunchKernelExC(&cfg, d.c.fn, args);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
+        ++g_launches;
+        if (k0 + B < Np) {
+          q[h].k0 = k0;
+          const int nc = (int)Np - k0 - B;
+          const dim3 jg((unsigned)((nc + gj_tj - 1) / gj_tj), (unsigned)nh[h]);
+          const size_t gsm = d.small_gemm ? (cx ? ffsk::dense_gj_smem<cplx, 8, 32>(k0) : ffsk::dense_gj_smem<double, 8, 32>(k0))
+                                          : (cx ? ffsk::dense_gj_smem<cplx, 8, 64>(k0) : ffsk::dense_gj_smem<double, 8, 64>(k0));
+          void* qargs[] = {&q[h]};
+          e = cudaLaunchKernel(gjf, jg, dim3(4 * gj_tj), qargs, gsm, st[h]);
+          if (e != cudaSuccess) return fail(FFS_ECUDA, "gj launch failed: %s", cudaGetErrorString(e));
+          ++g_launches;
+        }
       }
     }
+  }
+  if (d.nstr > 1) {
+    cudaEventRecord(g_dense_join, st[1]);
+    cudaStreamWaitEvent(stream, g_dense_join, 0);
   }
   if (g_prof) {
     cudaEventRecord(g_ev1, stream);

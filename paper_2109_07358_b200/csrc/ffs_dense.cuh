@@ -28,8 +28,9 @@ namespace ffsk {
 // Row-major A [M][K] (lda), B [K][N] (ldb), C [M][N] (ldc); N % 128 == 0 and K % 2 == 0 (the
 // host pads); rows >= M and k >= K are zero-filled. CTA tile 128 x 128 x 32, 8 warps as 4 (M) x 2
 // (N), warp tile 32 x 64 = 4 x 8 DMMA m8n8k4 tiles, 3-stage cp.async pipeline of 32-deep K slices (192 KB smem).
-constexpr int kGM = 128, kGN = 128, kGK = 32, kGStages = 3, kGThreads = 256;
-constexpr size_t kGemmSmem = (size_t)kGStages * (kGM * kGK + kGK * kGN) * sizeof(double);
+constexpr int kGM = 128, kGN = 128, kGThreads = 256;
+template <int kGK, int kGStages>
+constexpr size_t gemm_smem() { return (size_t)kGStages * (kGM * kGK + kGK * kGN) * sizeof(double); }
 
 struct DgemmParams {
   const double* A;
@@ -55,6 +56,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int
 // r*32 + (c ^ 4(r&3)); the B tile is [32][128] with (k, n) at k*128 + (n ^ 4(k&3)). The XOR only
 // touches bits 2-3, so the 16-byte cp.async chunks stay contiguous, and each half-warp phase of
 // the fragment loads (g = 0..3 or 4..7, t4 = 0..3) hits 16 distinct 8-byte bank slots.
+// <32, 3>: 192 KB smem, 255 registers (fastest alone); <16, 4>: 128 KB, ~200 registers, which leaves
+// room on each SM for a co-resident ffs_dense_gj_kernel CTA of the other half-batch (2-stream mode)
+template <int kGK, int kGStages>
 static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const DgemmParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* As = reinterpret_cast<double*>(smem);
@@ -173,8 +177,8 @@ static __global__ void ffs_dense_y0_kernel(const int32_t* __restrict__ perm, dou
 //   (2) Z[:, j] <- S^{-1} Z[:, j]
 //   (3) W[0:k0, j] -= W[0:k0, k0:k1] Z[:, j],   W[k0:k1, j] = Z[:, j]
 // then the next block's Y_s columns are scattered from W[0:k1, k1:k1+B] (tile 0 only).
-// Grid (column tiles of kGjTJ, batch samples); 256 threads = kGjTJ columns x 4 slices of i.
-constexpr int kGjTJ = 64;
+// Grid (column tiles of TJ, batch samples); 4*TJ threads = TJ columns x 4 slices of i. W[0:k0, k0:k1]
+// (the same B scalars for every column of a row) is read from global memory (L1 broadcast).
 
 struct DenseGjParams {
   const double* U;          // [L][N]
@@ -187,13 +191,13 @@ struct DenseGjParams {
   int N, Np, k0;
 };
 
-template <typename T, int B>
+template <typename T, int B, int kGjTJ>
 __host__ __device__ inline size_t dense_gj_smem(int k0) {
-  return sizeof(T) * ((size_t)2 * B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
+  return sizeof(T) * ((size_t)B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
 }
 
-template <typename T, int B>
-static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjParams q) {
+template <typename T, int B, int kGjTJ>
+static __global__ void __launch_bounds__(4 * kGjTJ) ffs_dense_gj_kernel(const DenseGjParams q) {
   using S = Sc<T>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int k0 = q.k0, k1 = k0 + B, Np = q.Np, N = q.N;
@@ -203,8 +207,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   const int j = k1 + blockIdx.x * kGjTJ + jl;
   const bool has = j < Np;
   T* Vn = reinterpret_cast<T*>(smem);   // [B][k0]   V[X_new, 0:k0]
-  T* Wb = Vn + (size_t)B * k0;          // [k0][B]   W[0:k0, k0:k1]
-  T* Zp = Wb + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
+  T* Zp = Vn + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
   T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
   T* RP = Zs + B * kGjTJ;               // Row [B][B], Pinv [B]
   int* xn = reinterpret_cast<int*>(RP + B * B + B);
@@ -218,7 +221,6 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     const int tt = idx / k0, ii = idx % k0;
     Vn[idx] = Ug[(size_t)xn[tt] * N + pm[ii]];
   }
-  for (int idx = t; idx < B * k0; idx += blockDim.x) Wb[idx] = W[(size_t)(idx / B) * Np + k0 + idx % B];
   __syncthreads();
   // (1) partial sums over this thread's slice of i
   T acc[B];  // minus the partial sums
@@ -272,7 +274,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     for (int ii = part; ii < k0; ii += 4) {
       T a = W[(size_t)ii * Np + j];
 #pragma unroll
-      for (int tt = 0; tt < B; ++tt) a = S::fms(Wb[ii * B + tt], z[tt], a);
+      for (int tt = 0; tt < B; ++tt) a = S::fms(W[(size_t)ii * Np + k0 + tt], z[tt], a);
       W[(size_t)ii * Np + j] = a;
     }
   }
