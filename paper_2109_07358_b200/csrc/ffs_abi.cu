@@ -537,11 +537,12 @@ struct DensePlan {
   size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, total, y_half, p_half;
 };
 
+// GJ tile: real 128 columns (two per thread, 16-byte W accesses), complex 64
+template <typename T> constexpr int gj_tj() { return sizeof(T) == 8 ? 128 : 64; }
 template <typename T>
-const void* dense_gj_fn(bool lean) {
-  return lean ? reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, 32>)
-              : reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, 64>);
-}
+const void* dense_gj_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, gj_tj<T>()>); }
+template <typename T>
+size_t dense_gj_bytes(int k0) { return ffsk::dense_gj_smem<T, 8, gj_tj<T>()>(k0); }
 
 int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
   const bool cx = dtype == FFS_C128;
@@ -587,11 +588,9 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   d.ws_ch = align_up((size_t)d.nstr * d.Sh * (d.c.Lpt / 32) * 4);
   d.ws_row = align_up((size_t)d.nstr * d.Sh * (d.c.B * d.c.B + d.c.B) * es);
   d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row;
-  const bool lean = d.small_gemm;
-  const size_t gjs = lean ? (cx ? ffsk::dense_gj_smem<cplx, 8, 32>((int)Np) : ffsk::dense_gj_smem<double, 8, 32>((int)Np))
-                          : (cx ? ffsk::dense_gj_smem<cplx, 8, 64>((int)Np) : ffsk::dense_gj_smem<double, 8, 64>((int)Np));
+  const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
-  const void* gjf = cx ? dense_gj_fn<cplx>(lean) : dense_gj_fn<double>(lean);
+  const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
   if (cudaFuncSetAttribute(gjf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(gj smem) failed");
   return FFS_OK;
@@ -648,8 +647,8 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
     cudaStreamWaitEvent(st[1], g_dense_fork, 0);
   }
   const int64_t f = cx ? 2 : 1;
-  const void* gjf = cx ? dense_gj_fn<cplx>(d.small_gemm) : dense_gj_fn<double>(d.small_gemm);
-  const int gj_tj = d.small_gemm ? 32 : 64;
+  const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
+  const int gjt = cx ? gj_tj<cplx>() : gj_tj<double>();
   const size_t rstride = (size_t)(B * B + B) * es;
   for (int64_t base = 0; base < M; base += d.S) {
     const int64_t Sb = std::min<int64_t>(d.S, M - base);
@@ -746,11 +745,10 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
         if (k0 + B < Np) {
           q[h].k0 = k0;
           const int nc = (int)Np - k0 - B;
-          const dim3 jg((unsigned)((nc + gj_tj - 1) / gj_tj), (unsigned)nh[h]);
-          const size_t gsm = d.small_gemm ? (cx ? ffsk::dense_gj_smem<cplx, 8, 32>(k0) : ffsk::dense_gj_smem<double, 8, 32>(k0))
-                                          : (cx ? ffsk::dense_gj_smem<cplx, 8, 64>(k0) : ffsk::dense_gj_smem<double, 8, 64>(k0));
+          const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh[h]);
+          const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
           void* qargs[] = {&q[h]};
-          e = cudaLaunchKernel(gjf, jg, dim3(4 * gj_tj), qargs, gsm, st[h]);
+          e = cudaLaunchKernel(gjf, jg, dim3(256), qargs, gsm, st[h]);
           if (e != cudaSuccess) return fail(FFS_ECUDA, "gj launch failed: %s", cudaGetErrorString(e));
           ++g_launches;
         }

@@ -196,16 +196,23 @@ __host__ __device__ inline size_t dense_gj_smem(int k0) {
   return sizeof(T) * ((size_t)B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
 }
 
+// CPT adjacent columns per thread (2 for real: 16-byte W accesses), kGjTJ = 64 * CPT columns per
+// CTA of 256 threads; the i loops keep UNR independent W loads in flight per thread.
 template <typename T, int B, int kGjTJ>
-static __global__ void __launch_bounds__(4 * kGjTJ) ffs_dense_gj_kernel(const DenseGjParams q) {
+static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjParams q) {
   using S = Sc<T>;
+  constexpr int CPT = kGjTJ / 64;
+  constexpr int UNR = 8;
+  static_assert(CPT == 1 || (CPT == 2 && sizeof(T) == 8), "two columns per thread only for real");
   extern __shared__ __align__(16) unsigned char smem[];
   const int k0 = q.k0, k1 = k0 + B, Np = q.Np, N = q.N;
   const int sl = blockIdx.y;
   const int64_t i_s = q.base + sl;
-  const int t = threadIdx.x, jl = t % kGjTJ, part = t / kGjTJ;
-  const int j = k1 + blockIdx.x * kGjTJ + jl;
+  const int t = threadIdx.x, jg = t % 64, part = t / 64;
+  const int jl = jg * CPT;                        // first column of this thread within the tile
+  const int j = k1 + blockIdx.x * kGjTJ + jl;     // first global column
   const bool has = j < Np;
+  const bool full = j + CPT - 1 < Np;             // every column of the group in range
   T* Vn = reinterpret_cast<T*>(smem);   // [B][k0]   V[X_new, 0:k0]
   T* Zp = Vn + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
   T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
@@ -222,29 +229,65 @@ static __global__ void __launch_bounds__(4 * kGjTJ) ffs_dense_gj_kernel(const De
     Vn[idx] = Ug[(size_t)xn[tt] * N + pm[ii]];
   }
   __syncthreads();
+  auto ldw = [&](int ii, T (&w)[CPT]) {
+    const T* src = W + (size_t)ii * Np + j;
+    if constexpr (CPT == 2) {
+      if (full) {
+        const double2 v = *reinterpret_cast<const double2*>(src);
+        w[0] = v.x;
+        w[1] = v.y;
+      } else {
+        w[0] = src[0];
+        w[1] = S::zero();
+      }
+    } else {
+      w[0] = src[0];
+    }
+  };
   // (1) partial sums over this thread's slice of i
-  T acc[B];  // minus the partial sums
+  T acc[CPT][B];  // minus the partial sums
 #pragma unroll
-  for (int tt = 0; tt < B; ++tt) acc[tt] = S::zero();
+  for (int e = 0; e < CPT; ++e)
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt) acc[e][tt] = S::zero();
   if (has) {
-#pragma unroll 4
-    for (int ii = part; ii < k0; ii += 4) {
-      const T w = W[(size_t)ii * Np + j];
+    int ii = part;
+    for (; ii + 4 * (UNR - 1) < k0; ii += 4 * UNR) {
+      T w[UNR][CPT];
 #pragma unroll
-      for (int tt = 0; tt < B; ++tt) acc[tt] = S::fms(Vn[tt * k0 + ii], w, acc[tt]);
+      for (int u = 0; u < UNR; ++u) ldw(ii + 4 * u, w[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int tt = 0; tt < B; ++tt) {
+          const T vn = Vn[tt * k0 + ii + 4 * u];
+#pragma unroll
+          for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(vn, w[u][e], acc[e][tt]);
+        }
+    }
+    for (; ii < k0; ii += 4) {
+      T w[CPT];
+      ldw(ii, w);
+#pragma unroll
+      for (int tt = 0; tt < B; ++tt)
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(Vn[tt * k0 + ii], w[e], acc[e][tt]);
     }
   }
 #pragma unroll
-  for (int tt = 0; tt < B; ++tt) Zp[(part * B + tt) * kGjTJ + jl] = acc[tt];
+  for (int e = 0; e < CPT; ++e)
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt) Zp[(part * B + tt) * kGjTJ + jl + e] = acc[e][tt];
   __syncthreads();
   // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
-  if (part == 0 && has) {
+  if (t < kGjTJ && k1 + blockIdx.x * kGjTJ + t < Np) {
+    const int c = t, jc = k1 + blockIdx.x * kGjTJ + c;
     T z[B];
 #pragma unroll
     for (int tt = 0; tt < B; ++tt) {
-      const T a01 = S::add(Zp[(0 * B + tt) * kGjTJ + jl], Zp[(1 * B + tt) * kGjTJ + jl]);
-      const T a23 = S::add(Zp[(2 * B + tt) * kGjTJ + jl], Zp[(3 * B + tt) * kGjTJ + jl]);
-      z[tt] = S::add(Ug[(size_t)xn[tt] * N + pm[j]], S::add(a01, a23));
+      const T a01 = S::add(Zp[(0 * B + tt) * kGjTJ + c], Zp[(1 * B + tt) * kGjTJ + c]);
+      const T a23 = S::add(Zp[(2 * B + tt) * kGjTJ + c], Zp[(3 * B + tt) * kGjTJ + c]);
+      z[tt] = S::add(Ug[(size_t)xn[tt] * N + pm[jc]], S::add(a01, a23));
     }
     const T* Row = RP;
     const T* Pinv = RP + B * B;
@@ -260,22 +303,46 @@ static __global__ void __launch_bounds__(4 * kGjTJ) ffs_dense_gj_kernel(const De
     }
 #pragma unroll
     for (int tt = 0; tt < B; ++tt) {
-      Zs[tt * kGjTJ + jl] = z[tt];
-      W[(size_t)(k0 + tt) * Np + j] = z[tt];
+      Zs[tt * kGjTJ + c] = z[tt];
+      W[(size_t)(k0 + tt) * Np + jc] = z[tt];
     }
   }
   __syncthreads();
   // (3) rank-B update of the earlier rows
   if (has) {
-    T z[B];
+    T z[CPT][B];
 #pragma unroll
-    for (int tt = 0; tt < B; ++tt) z[tt] = Zs[tt * kGjTJ + jl];
-#pragma unroll 4
-    for (int ii = part; ii < k0; ii += 4) {
-      T a = W[(size_t)ii * Np + j];
+    for (int e = 0; e < CPT; ++e)
 #pragma unroll
-      for (int tt = 0; tt < B; ++tt) a = S::fms(W[(size_t)ii * Np + k0 + tt], z[tt], a);
-      W[(size_t)ii * Np + j] = a;
+      for (int tt = 0; tt < B; ++tt) z[e][tt] = Zs[tt * kGjTJ + jl + e];
+    auto upd = [&](int ii, T (&a)[CPT]) {
+      const T* wb = W + (size_t)ii * Np + k0;  // the same B scalars for every thread: L1 broadcast
+#pragma unroll
+      for (int tt = 0; tt < B; ++tt) {
+        const T wv = wb[tt];
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) a[e] = S::fms(wv, z[e][tt], a[e]);
+      }
+      T* dst = W + (size_t)ii * Np + j;
+      if constexpr (CPT == 2) {
+        if (full) *reinterpret_cast<double2*>(dst) = make_double2(a[0], a[1]);
+        else dst[0] = a[0];
+      } else {
+        dst[0] = a[0];
+      }
+    };
+    int ii = part;
+    for (; ii + 4 * (UNR - 1) < k0; ii += 4 * UNR) {
+      T a[UNR][CPT];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) ldw(ii + 4 * u, a[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) upd(ii + 4 * u, a[u]);
+    }
+    for (; ii < k0; ii += 4) {
+      T a[CPT];
+      ldw(ii, a);
+      upd(ii, a);
     }
   }
   // next block's Y_s columns (the tile holding columns k1 .. k1+B-1)
