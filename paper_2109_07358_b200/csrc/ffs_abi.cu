@@ -686,7 +686,7 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
       c.wfull = Wd;
       c.S = S > 0 ? std::min<int64_t>(S, M) : 0;
       c.trace = S > 0 ? trace : nullptr;
-      c.timing = nullptr;
+      c.timing = g_timing;  // development (ffs_dev_timing); null unless enabled
       c.Pd = Pd;
       c.ldY = d.ldY;
       c.rowg = rowg;

@@ -48,10 +48,14 @@ struct ClusterParams {
 constexpr int kRingDepth = 8;  // per-thread cp.async pipeline depth of the contraction
 constexpr int kKC = 64;        // rows of W (or columns of the new rows) staged per chunk
 constexpr bool kUseRing = false;  // cp.async ring measured slower on C4/C5 (profiles/r01_ncu_summary.md)
+// draws exchange totals and the pivot row through mbarrier + st.async instead of two cluster
+// barriers: parity-green, but not faster end to end (C4 1.502 vs 1.488 s, C5 1.480 vs 1.487 s,
+// C5 marginal 208 vs 198 ms: the st.async pushes lengthen the crossing CTA's select+push)
+constexpr bool kMbarDraw = false;
 
 template <typename T, int B>
 struct ClusterLayout {
-  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, ring, total;
+  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, mbx, ring, total;
   __host__ __device__ ClusterLayout(int N, int Np, int threads = 0, int R = 0) {
     size_t o = 0;
     perm = o; o = align16(o + sizeof(int) * N);
@@ -63,6 +67,7 @@ struct ClusterLayout {
     vnew = o; o = align16(o + sizeof(T) * (size_t)kKC * B);
     red = o;  o = align16(o + sizeof(double) * 64 + sizeof(int) * 96);
     xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + 2 * sizeof(T) * B + 64);  // cluster exchange
+    mbx = o;  o = align16(o + 4 * 8 + 2 * sizeof(double) * kMaxCS + 2 * (sizeof(T) * B + 8));  // mbarrier exchange
     ring = o; o = align16(o + (kUseRing ? (size_t)kRingDepth * threads * R * sizeof(T) : 0));
     total = o;
   }
@@ -103,6 +108,40 @@ __device__ __forceinline__ void st_remote_s32(void* local_ptr, unsigned rank, in
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
+// ---- point-to-point cluster exchange (mbarrier + st.async), replacing the two cluster barriers
+// per draw: every CTA pushes its total into every CTA's slot and the crossing CTA pushes x_k and
+// the pivot row; each CTA waits only for the bytes it needs (double-buffered by use parity).
+__device__ __forceinline__ unsigned cl_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned map_rank(const void* local_ptr, unsigned rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(cl_smem_u32(local_ptr)), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cl_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cta.b64 _, [%0], %1;" ::"r"(cl_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(cl_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 8 bytes into CTA `rank`'s copy of `local_dst`, completing tx bytes on its copy of `local_bar`
+__device__ __forceinline__ void st_async_f64(void* local_dst, void* local_bar, unsigned rank, double v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(map_rank(local_dst, rank)),
+               "l"(__double_as_longlong(v)), "r"(map_rank(local_bar, rank))
+               : "memory");
+}
+
 template <typename T, int R, int B, int MAXT, bool STEP = false>
 __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -135,6 +174,15 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   int* xsel = xfree + kMaxCS;                                  // selected row (global)
   T* xrow = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(xsel) + 16);  // [B] pivot row
   T* xstage = xrow + B;                                        // [B] claimer's row (local)
+  // mbarrier exchange: bars [tot0, tot1, row0, row1], totals [2][kMaxCS], rows [2][B] + xsel [2]
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + lay.mbx);
+  double* mtot = reinterpret_cast<double*>(mbar + 4);
+  T* mrow = reinterpret_cast<T*>(mtot + 2 * kMaxCS);
+  double* msel = reinterpret_cast<double*>(mrow + 2 * B);  // x_k as a double (exact for ints)
+  if (t < 4) mbar_init(mbar + t, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  cluster_sync_all();
+  unsigned n_tot = 0, n_row = 0;  // uses of the totals / pivot-row barriers (cluster-uniform)
 
   const int64_t cid = cluster_id_x();
   const int64_t ncl = nclusters_x();
@@ -321,11 +369,14 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             c[r] = acc;
           }
           const double incl = warp_incl_scan(acc, lane);
-          if (lane == 31) red[warp] = incl;
+          // warp totals, double-buffered by draw parity: with the mbarrier exchange no CTA-wide
+          // barrier separates this draw's reads of red from the next draw's writes
+          double* redp = red + (kMbarDraw ? 32 * (n_tot & 1u) : 0);
+          if (lane == 31) redp[warp] = incl;
           __syncthreads();
           double woff, Tc;
           {
-            const double wt = lane < nw ? red[lane] : 0.0;
+            const double wt = lane < nw ? redp[lane] : 0.0;
             const double ws = warp_incl_scan(wt, lane);
             woff = __shfl_sync(0xffffffffu, ws, warp > 0 ? warp - 1 : 0);
             woff = warp > 0 ? woff : 0.0;
@@ -333,17 +384,28 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
           }
           double excl = __shfl_up_sync(0xffffffffu, incl, 1);
           excl = (lane == 0 ? 0.0 : excl) + woff;
-          if (t < (int)CS) st_remote_f64(&xtot[rank], (unsigned)t, Tc);
-          if (t == 0) *xsel = kUnset;  // remote pushes of this step arrive after barrier #1
-          sub(3);
-          cluster_sync_all();  // #1: CTA totals visible
+          const double* xt = xtot;
+          if constexpr (kMbarDraw) {
+            const unsigned ts = n_tot & 1u, tpar = (n_tot >> 1) & 1u;
+            ++n_tot;
+            if (t == 0) mbar_expect_tx(mbar + ts, 8u * CS);
+            if (t < (int)CS) st_async_f64(&mtot[ts * kMaxCS + rank], mbar + ts, (unsigned)t, Tc);
+            sub(3);
+            mbar_wait(mbar + ts, tpar);  // every CTA's total has landed here
+            xt = mtot + ts * kMaxCS;
+          } else {
+            if (t < (int)CS) st_remote_f64(&xtot[rank], (unsigned)t, Tc);
+            if (t == 0) *xsel = kUnset;  // remote pushes of this step arrive after barrier #1
+            sub(3);
+            cluster_sync_all();  // #1: CTA totals visible
+          }
           sub(4);
           // cluster-uniform T, this CTA's offset and the crossing CTA (lanes q < CS)
           const double u = usel[k];
           double Ttot, off;
           int owner_cta;
           {
-            const double tq = lane < (int)CS ? xtot[lane] : 0.0;
+            const double tq = lane < (int)CS ? xt[lane] : 0.0;
             double ci = tq;
 #pragma unroll
             for (int d = 1; d < kMaxCS; d <<= 1) {
@@ -360,10 +422,18 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
           }
           const bool ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
           const double thr = u * Ttot;
+          // the crossing CTA always answers through the row barrier (x_k, or kUnset for the rare path)
+          const bool use_row = kMbarDraw && ok && owner_cta >= 0;
+          const unsigned rsl = n_row & 1u, rpar = (n_row >> 1) & 1u;
+          if (use_row) {
+            ++n_row;
+            if (t == 0) mbar_expect_tx(mbar + 2 + rsl, (unsigned)(sizeof(T) * B + 8));
+          }
           if (ok && owner_cta == (int)rank) {
             const double thl = thr - off;
-            const double wt = red[warp];
-            const bool mine = (warp == 0 || thl >= woff) && (thl - woff < wt);
+            const double wt = redp[warp];
+            // exactly one warp is responsible for the threshold (the first / last absorb rounding)
+            const bool mine = (warp == 0 || thl >= woff) && (warp == nw - 1 || thl - woff < wt);
             const double tp = fmax(thl - excl, 0.0);
             int rs = R;
 #pragma unroll
@@ -388,13 +458,31 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
               }
               __syncwarp();
               const double* xs_src = reinterpret_cast<const double*>(xstage);
-              double* xr_dst = reinterpret_cast<double*>(xrow);
-              for (int idx = lane; idx < (int)CS * B * kD; idx += 32) {
-                const int q = idx / (B * kD), e = idx % (B * kD);
-                st_remote_f64(xr_dst + e, (unsigned)q, xs_src[e]);
+              if constexpr (kMbarDraw) {
+                double* xr_dst = reinterpret_cast<double*>(mrow + rsl * B);
+                for (int idx = lane; idx < (int)CS * (B * kD + 1); idx += 32) {
+                  const int q = idx / (B * kD + 1), e = idx % (B * kD + 1);
+                  if (e < B * kD) st_async_f64(xr_dst + e, mbar + 2 + rsl, (unsigned)q, xs_src[e]);
+                  else st_async_f64(msel + rsl, mbar + 2 + rsl, (unsigned)q, (double)xs);
+                }
+              } else {
+                double* xr_dst = reinterpret_cast<double*>(xrow);
+                for (int idx = lane; idx < (int)CS * B * kD; idx += 32) {
+                  const int q = idx / (B * kD), e = idx % (B * kD);
+                  st_remote_f64(xr_dst + e, (unsigned)q, xs_src[e]);
+                }
+                if (lane < (int)CS) st_remote_s32(xsel, (unsigned)lane, xs);
               }
-              if (lane < (int)CS) st_remote_s32(xsel, (unsigned)lane, xs);
               if (lane == ln) chosen |= 1u << rsel;
+            } else if (kMbarDraw && mine) {
+              // no row crosses in the responsible warp (rounding): tell every CTA to take the
+              // rare, cluster-uniform round
+              double* xr_dst = reinterpret_cast<double*>(mrow + rsl * B);
+              for (int idx = lane; idx < (int)CS * (B * kD + 1); idx += 32) {
+                const int q = idx / (B * kD + 1), e = idx % (B * kD + 1);
+                if (e < B * kD) st_async_f64(xr_dst + e, mbar + 2 + rsl, (unsigned)q, 0.0);
+                else st_async_f64(msel + rsl, mbar + 2 + rsl, (unsigned)q, (double)kUnset);
+              }
             }
           }
           if (p.trace != nullptr && i < p.S) {
@@ -405,9 +493,23 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
               if (row0 + r < L) tr[row0 + r] = w[r] * inv;
           }
           sub(5);
-          cluster_sync_all();  // #2: x_k and the pivot row visible in every CTA
+          int xsel_k;
+          const T* xr = xrow;
+          if constexpr (kMbarDraw) {
+            if (use_row) {
+              mbar_wait(mbar + 2 + rsl, rpar);  // x_k and the pivot row have landed here
+              xsel_k = (int)msel[rsl];
+              xr = mrow + rsl * B;
+            } else {
+              xsel_k = kUnset;
+            }
+            if (xsel_k == kUnset && t == 0) *xsel = kUnset;
+            if (xsel_k == kUnset) __syncthreads();
+          } else {
+            cluster_sync_all();  // #2: x_k and the pivot row visible in every CTA
+            xsel_k = *xsel;
+          }
           sub(6);
-          int xsel_k = *xsel;
           if (xsel_k == kUnset) {
             // rare (cluster-uniform): T not finite/positive -> smallest unchosen row (flag bit0);
             // no crossing -> the crossing CTA's (or, without one, the cluster's) last positive row
@@ -468,10 +570,11 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             }
             cluster_sync_all();
             xsel_k = *xsel;
+            xr = xrow;
           }
           if (t == 0) pos[k] = xsel_k;
-          if (t < B) Row[rr * B + t] = xrow[t];
-          const T piv = xrow[rr];
+          if (t < B) Row[rr * B + t] = xr[t];
+          const T piv = xr[rr];
           if (S::abs2(piv) < 1e-12 * Ttot) flag |= 2;
           const T ip = S::recip(piv);
           if (t == 0) Pinv[rr] = ip;
@@ -482,7 +585,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
           for (int r = 0; r < R; ++r) lmul[r] = S::mul(P[r][rr], ip);
 #pragma unroll
           for (int cc = rr + 1; cc < B; ++cc) {
-            const T pc = xrow[cc];
+            const T pc = xr[cc];
 #pragma unroll
             for (int r = 0; r < R; ++r)
               P[r][cc] = (cc == rr + 1 && ((chosen >> r) & 1u)) ? S::zero() : S::fms(lmul[r], pc, P[r][cc]);
@@ -504,6 +607,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         }
       }
       if (!STEP && k0 + nb < Np) {
+       __syncthreads();  // Row / Pinv / pos of the block's last draw come from other warps
        for (int jt = k0 + nb; jt < Np; jt += (int)CS * blockDim.x) {  // column tiles (uniform trip count)
         const int j = jt + (int)rank * blockDim.x + t;
         const bool has = j < Np;
