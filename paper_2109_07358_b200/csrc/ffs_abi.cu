@@ -534,7 +534,8 @@ struct DensePlan {
   int64_t S, Sh, ldY;  // batch, half-batch (per stream), Y row stride in scalars of T
   int nstr;            // streams (half-batches) in flight
   bool small_gemm;     // GEMM <16, 4> (co-resident with the GJ kernel) instead of <32, 3>
-  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, total, y_half, p_half;
+  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, total, y_half, p_half;
+  int k_gather;        // blocks with k0 < k_gather contract the gathered columns in the step kernel
 };
 
 // GJ tile: real 128 columns (two per thread, 16-byte W accesses), complex 64
@@ -587,7 +588,15 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   d.ws_w = align_up((size_t)d.nstr * d.Sh * Np * Np * es);
   d.ws_ch = align_up((size_t)d.nstr * d.Sh * (d.c.Lpt / 32) * 4);
   d.ws_row = align_up((size_t)d.nstr * d.Sh * (d.c.B * d.c.B + d.c.B) * es);
-  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row;
+  // hybrid: while k0 is small the gathered contraction (L k0 B per sample, from the transposed U)
+  // costs less than the GEMM's full-N one (L N B); crossover measured on C4/C5
+  // (measured optimum: C5 real 0.3 -> 1.35 s vs 1.51 s dense-only; C4 complex 0.6 -> 1.19 s vs
+  // 1.52 s; complex contractions do 2x the flops per gathered byte, so gathering pays longer)
+  double theta = cx ? 0.6 : 0.3;
+  if (const char* e = getenv("FFS_DENSE_THETA")) theta = atof(e);  // development
+  d.k_gather = (int)(theta * (double)Np);
+  d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
+  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
   const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
@@ -618,6 +627,13 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
   char* Wb = Pb + d.ws_p;
   uint32_t* ch = reinterpret_cast<uint32_t*>(Wb + d.ws_w);
   char* rowb = Wb + d.ws_w + d.ws_ch;
+  double* Ut = reinterpret_cast<double*>(rowb + d.ws_row);
+  if (d.k_gather > 0) {
+    dim3 tb(32, 8), tg((unsigned)((d.c.Lpt + 31) / 32), (unsigned)((N + 31) / 32));
+    if (cx) ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, d.c.Lpt);
+    else ffsk::transpose_pad_kernel<double><<<tg, tb, 0, stream>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, d.c.Lpt);
+    ++g_launches;
+  }
   cudaStream_t st[2] = {stream, stream};
   if (d.nstr > 1) {
     if (!g_dense_s1) {
@@ -674,6 +690,7 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
       ++g_launches;
       ffsk::ClusterParams& c = p[h];
       c.U = static_cast<const double*>(U);
+      c.Ut = Ut;
       c.L = (int)L;
       c.N = (int)N;
       c.Np = (int)Np;
@@ -720,11 +737,14 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
     for (int k0 = 0; k0 < Np; k0 += B) {
       for (int h = 0; h < d.nstr; ++h) {
         if (nh[h] <= 0) continue;
-        if (d.small_gemm)
+        p[h].gather = k0 < d.k_gather ? 1 : 0;
+        if (p[h].gather) {
+          // no GEMM: the step kernel contracts the gathered columns itself
+        } else if (d.small_gemm)
           ffsk::ffs_dgemm_kernel<16, 4><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<16, 4>(), st[h]>>>(gp[h]);
         else
           ffsk::ffs_dgemm_kernel<32, 3><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<32, 3>(), st[h]>>>(gp[h]);
-        ++g_launches;
+        if (!p[h].gather) ++g_launches;
         p[h].k0 = k0;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];

@@ -42,6 +42,7 @@ struct ClusterParams {
   const int32_t* permg;    // [M][Np] permutation prefixes (ffs_permute_kernel)
   uint32_t* chosen_g;      // [Sb][Lpt/32] rows drawn so far (bit per row)
   int k0, Sb;
+  int gather;              // STEP: 1 = contract the gathered columns of Ut (no GEMM for this block)
   int64_t base;
 };
 
@@ -248,7 +249,10 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       // ---- a3 panel for this CTA's rows (W in global memory is final for rows < k0 after the
       // previous block's update + cluster barrier; its rows are staged kKC at a time)
       T P[R][B];
-      if constexpr (STEP) {
+      // STEP with p.gather: early blocks (small k0) contract the gathered columns here, like the
+      // cluster path, instead of paying the dense GEMM's full-N contraction
+      const bool from_gemm = STEP && !p.gather;
+      if (from_gemm) {
         // the panel from the dense GEMM P = U Y, per-sample layout [L][B] (rows >= L are zero):
         // this thread's R rows are R*B contiguous scalars, read as 16-byte vectors
         const double2* pb = reinterpret_cast<const double2*>(reinterpret_cast<const T*>(p.Pd) +
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             asm volatile("cp.async.commit_group;" ::: "memory");
           }
         }
-        for (int c0 = 0; c0 < (STEP ? 0 : k0); c0 += kKC) {
+        for (int c0 = 0; c0 < (from_gemm ? 0 : k0); c0 += kKC) {
           const int kc = min(kKC, k0 - c0);
           __syncthreads();
           for (int idx = t; idx < kc * B; idx += blockDim.x) {
