@@ -206,3 +206,24 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
     rpos = ref.sample(U, uni, Np=Np)
     assert (gpos == rpos).all(), np.argwhere(gpos != rpos)[:5]
     assert not (gfl & 1).any()
+
+
+# Lockstep-dense path schedules (ffs_abi.cu launch_dense): several batches with a ragged last one
+# (FFS_DENSE_S), all-GEMM (theta 0), all-gathered (theta 1) and the default hybrid; real and
+# complex; the environment is read per call, so each case runs the same kernels in another order.
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("env", [{"FFS_DENSE_S": "16"}, {"FFS_DENSE_THETA": "0"}, {"FFS_DENSE_THETA": "1"},
+                                 {"FFS_DENSE_S": "7", "FFS_DENSE_THETA": "0.5"}])
+def test_dense_path_schedules(env, cplx, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    L, N = 2100, 258  # L: 2 clusters' rows with a ragged tail; N' = N: ragged last panel block
+    U = inputs.random_orthonormal(L, N, 77 + int(cplx), complex_=cplx)
+    uni = inputs.uniforms(40, N, 4242)
+    gpos, gflags, gw = run_gpu(U, uni, N, trace_S=2)
+    rpos = ref.sample(U, uni, Np=N)
+    r = compare_positions(U, uni, gpos, rpos, N)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    _, rw = ref.weights(U, uni[:2], Np=N)
+    assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
