@@ -122,7 +122,7 @@ def cpu_oracle_rate(U, uni, Np, budget_s=15.0, max_samples=None):
     """Oracle samples/s on a bounded prefix of the workload (host cores, OpenMP)."""
     from oracle import ref
     ref.lib()
-    n = 64
+    n = max(1, ref.num_threads())  # one sample per host thread first (C5: ~50 s per sample-thread)
     t_used = 0.0
     while True:
         n = min(n, uni.shape[0] if max_samples is None else min(uni.shape[0], max_samples))
