@@ -296,8 +296,9 @@ def ffs_path_kernel(cfg, Np, cplx):
     if ffs_uses_warp(cfg, Np, cplx):
         return "ffs_seg_kernel"
     if cfg.L >= 2048:
-        if (not cplx) and Np == cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
-            return "dense path: ffs_dgemm_kernel + ffs_cluster_kernel<STEP> + ffs_dense_gj_kernel per block"
+        if Np == cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
+            return ("dense path (hybrid): ffs_cluster_kernel<STEP> (+ ffs_dgemm_kernel for k0 >= theta N') "
+                    "+ ffs_dense_gj_kernel per block")
         return "ffs_cluster_kernel"
     return "ffs_sample_kernel"
 
