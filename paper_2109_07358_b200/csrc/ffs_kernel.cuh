@@ -320,7 +320,7 @@ ffs_sample_kernel(const Params p) {
         for (int r = 0; r < R; ++r) P[r][c] = v[r];
       }
 #pragma unroll 4
-      for (int ii = 0; ii < k0; ++ii) {
+      for (int ii = 0; ii < ((p.dbg & 1) ? 0 : k0); ++ii) {  // dbg bit0: development, WRONG results
         T v[R];
         load_col<T, R, USMEM>(p, Uts, perm[ii], t, v);
         T wb[B];
@@ -381,7 +381,7 @@ ffs_sample_kernel(const Params p) {
         }
       });
       // ---- Gauss-Jordan update of W with the nb new rows (only if later columns remain)
-      if (k0 + nb < Np) {
+      if (k0 + nb < Np && !(p.dbg & 4)) {  // dbg bit2: development, WRONG results
         gsync<WARP>();
         for (int idx = t; idx < nb * Np; idx += G) {
           const int tt = idx / Np, j = idx % Np;
