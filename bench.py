@@ -296,6 +296,8 @@ def ffs_path_kernel(cfg, Np, cplx):
     if ffs_uses_warp(cfg, Np, cplx):
         return "ffs_seg_kernel"
     if cfg.L >= 2048:
+        if Np < cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
+            return "step path (marginal): ffs_cluster_kernel<STEP> (gathered contraction) + ffs_dense_gj_kernel per block"
         if Np == cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
             return ("dense path (hybrid): ffs_cluster_kernel<STEP> (+ ffs_dgemm_kernel for k0 >= theta N') "
                     "+ ffs_dense_gj_kernel per block")

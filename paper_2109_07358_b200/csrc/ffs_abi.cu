@@ -526,7 +526,11 @@ int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
 bool dense_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   const char* g = getenv("FFS_NO_DENSE");
   if (g && g[0] == '1') return false;
-  return Np == N && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
+  // marginals (N' < N) take the same step + batched-GJ kernels with every block contracted gathered
+  // (no GEMM): C5 marginal 201 -> 180 ms against the per-sample cluster kernel
+  const char* m = getenv("FFS_STEP_MARGINAL");  // development: "0" keeps marginals on the cluster kernel
+  const bool marg = !(m && m[0] == '0') && Np < N;
+  return (Np == N || marg) && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
 }
 
 struct DensePlan {
@@ -571,7 +575,7 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   const size_t gsm = d.small_gemm ? ffsk::gemm_smem<16, 4>() : ffsk::gemm_smem<32, 3>();
   if (cudaFuncSetAttribute(gf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(gemm smem) failed");
-  int64_t cap = 1024;  // samples per lockstep batch
+  int64_t cap = Np < N ? 8192 : 1024;  // samples per lockstep batch (no GEMM operands for marginals)
   if (const char* e = getenv("FFS_DENSE_S")) cap = std::max<int64_t>(1, atoll(e));  // development
   d.S = std::max<int64_t>(1, std::min<int64_t>(M, cap));
   if (d.S < 2) d.nstr = 1;
@@ -580,8 +584,9 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   const int64_t q = cx ? ffsk::kGN / 2 : ffsk::kGN;
   d.ldY = (d.Sh * d.c.B + q - 1) / q * q;
   const size_t es = cx ? 16 : 8;
-  d.y_half = align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: real 2N x 2ldY expansion
-  d.p_half = align_up((size_t)L * d.ldY * es);
+  const bool no_gemm = Np < N;  // marginals: gathered contraction only (the GEMM would be N/N' x wasteful)
+  d.y_half = no_gemm ? 0 : align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: 2N x 2ldY expansion
+  d.p_half = no_gemm ? 0 : align_up((size_t)L * d.ldY * es);
   d.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
   d.ws_y = d.nstr * d.y_half;
   d.ws_p = d.nstr * d.p_half;
@@ -594,7 +599,7 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   // 1.52 s; complex contractions do 2x the flops per gathered byte, so gathering pays longer)
   double theta = cx ? 0.6 : 0.3;
   if (const char* e = getenv("FFS_DENSE_THETA")) theta = atof(e);  // development
-  d.k_gather = (int)(theta * (double)Np);
+  d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
   d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
   d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
@@ -681,13 +686,14 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
       double* Wd = reinterpret_cast<double*>(Wb + (size_t)h * d.Sh * Np * Np * es);
       uint32_t* chh = ch + (size_t)h * d.Sh * (d.c.Lpt / 32);
       double* rowg = reinterpret_cast<double*>(rowb + (size_t)h * d.Sh * rstride);
-      cudaMemsetAsync(Y, 0, d.y_half, st[h]);
+      if (d.y_half) cudaMemsetAsync(Y, 0, d.y_half, st[h]);
       cudaMemsetAsync(chh, 0, (size_t)nh[h] * (d.c.Lpt / 32) * 4, st[h]);
       if (flags) cudaMemsetAsync(flags + base + b0, 0, (size_t)nh[h] * 4, st[h]);
       const unsigned yg = (unsigned)((nh[h] * B + 255) / 256);
-      if (cx) ffsk::ffs_dense_y0_kernel<cplx, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
+      if (!d.y_half) Y = nullptr;
+      else if (cx) ffsk::ffs_dense_y0_kernel<cplx, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
       else ffsk::ffs_dense_y0_kernel<double, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
-      ++g_launches;
+      if (Y) ++g_launches;
       ffsk::ClusterParams& c = p[h];
       c.U = static_cast<const double*>(U);
       c.Ut = Ut;

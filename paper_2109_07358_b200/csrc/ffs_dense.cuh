@@ -346,7 +346,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     }
   }
   // next block's Y_s columns (the tile holding columns k1 .. k1+B-1)
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0 && q.Y != nullptr) {  // (no Y when every block is contracted gathered)
     __syncthreads();
     const int nb1 = min(B, Np - k1);
     const int64_t col0 = (int64_t)sl * B;

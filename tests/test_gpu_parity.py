@@ -227,3 +227,21 @@ def test_dense_path_schedules(env, cplx, monkeypatch):
     assert (gflags == 0).all()
     _, rw = ref.weights(U, uni[:2], Np=N)
     assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
+
+
+# Marginals at large L run the step + batched-GJ kernels with every block contracted gathered
+# (ffs_abi.cu dense_eligible); FFS_STEP_MARGINAL=0 keeps them on the per-sample cluster kernel.
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("step", ["1", "0"])
+def test_large_L_marginal_paths(step, cplx, monkeypatch):
+    monkeypatch.setenv("FFS_STEP_MARGINAL", step)
+    L, N, Np = 2100, 300, 42  # ragged last block (42 = 5 x 8 + 2)
+    U = inputs.random_orthonormal(L, N, 91 + int(cplx), complex_=cplx)
+    uni = inputs.uniforms(64, Np, 515)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=2)
+    rpos = ref.sample(U, uni, Np=Np)
+    r = compare_positions(U, uni, gpos, rpos, Np)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    _, rw = ref.weights(U, uni[:2], Np=Np)
+    assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
