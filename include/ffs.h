@@ -46,7 +46,11 @@ typedef enum { FFS_F64 = 0, FFS_C128 = 1 } ffs_dtype;
 typedef enum { FFS_OK = 0, FFS_EINVAL = -1, FFS_ECUDA = -2, FFS_ENOWS = -3 } ffs_status;
 
 /* Device workspace bytes needed by ffs_sample / ffs_sample_marginal / ffs_debug_trace on the
- * current CUDA device. Returns 0 for invalid arguments. */
+ * current CUDA device. Returns 0 for invalid arguments. Size depends on the path the call takes:
+ * small for L <= 256 (permutations only); for L >= 2048 with N >= 256 (the lockstep block-step
+ * path) it holds, per batch of up to 1024 samples (8192 for marginals), the factor
+ * W [N'][N'] of every batch sample, the coefficient and panel matrices Y [N][8 S] and P [L][8 S]
+ * of the dense GEMM, U^T and the permutations: e.g. 9.4 GB for the C5 config (L=16384, N=1024). */
 size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M);
 
 /* Full sampling (N' = N): Eq. 1-3. uniforms [M][2N], positions [M][N]. */
