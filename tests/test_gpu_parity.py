@@ -245,3 +245,26 @@ def test_large_L_marginal_paths(step, cplx, monkeypatch):
     assert (gflags == 0).all()
     _, rw = ref.weights(U, uni[:2], Np=Np)
     assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
+
+
+# Degenerate marginals (N' = 1: one draw with w(x) = |U[x, m_1]|^2; N' = 2: one GJ-free block)
+# on every path: warp (L <= 256), CTA owner, cluster (N < 256), block-step (N >= 256).
+@pytest.mark.parametrize("L,N,Np,cplx", [
+    (200, 30, 1, False), (300, 40, 1, False), (300, 40, 2, True), (2100, 9, 1, False), (2100, 9, 2, True),
+    (2100, 300, 1, False), (2100, 300, 2, True), (4096, 256, 9, False),
+])
+def test_degenerate_marginals(L, N, Np, cplx):
+    U = inputs.random_orthonormal(L, N, 7 * L + N, complex_=cplx)
+    uni = inputs.uniforms(48, Np, L + 3 * N)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=2)
+    rpos = ref.sample(U, uni, Np=Np)
+    r = compare_positions(U, uni, gpos, rpos, Np)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    _, rw = ref.weights(U, uni[:2], Np=Np)
+    assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
+    if Np == 1:  # the first conditional is |U[x, m_1]|^2 exactly (Eq. 3 with k = 1)
+        m1 = np.floor(uni[:2, 0] * N).astype(int)
+        for s in range(2):
+            ref_w = np.abs(U[:, m1[s]]) ** 2
+            assert np.max(np.abs(gw[s, 0] - ref_w / ref_w.sum())) <= 1e-13
