@@ -1,0 +1,236 @@
+// Prototype (round-2 groundwork): an INT8 GEMM on the 5th-generation tensor cores
+// (tcgen05.mma.kind::i8, accumulator in TMEM), the building block of an Ozaki-style FP64
+// emulation of the dense path's P = U Y. Not used by libffs.
+//   C[M][N] (int32, row-major) = A[M][K] (int8, row-major) * B[N][K]^T (int8, row-major = K-major)
+// CTA tile 128 x 128, K staged 64 bytes at a time (two tcgen05.mma of K = 32), 4-stage cp.async
+// ring into the canonical no-swizzle K-major layout (8-row x 16-byte core matrices), one thread
+// issues the MMAs, tcgen05.commit -> mbarrier releases a stage, 4 warps read the accumulator
+// back with tcgen05.ld. Checks a 512 x 384 x 1024 product against the host, then times 8192^3.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_i8_gemm tc_i8_gemm.cu
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
+
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4, THREADS = 128;
+constexpr int TILE_BYTES = BM * BK;  // 8 KB per operand per stage
+
+__device__ __forceinline__ unsigned sm_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+// canonical K-major, no swizzle: core matrix (row group g = r/8, 16-byte K chunk c) at
+// (g * (BK/16) + c) * 128 bytes, row r%8 at +16*(r%8). LBO (K-adjacent cores) = 128 B,
+// SBO (8-row-adjacent cores) = (BK/16) * 128 B.
+__device__ __forceinline__ int core_off(int r, int c) { return ((r >> 3) * (BK / 16) + c) * 128 + (r & 7) * 16; }
+
+__device__ __forceinline__ uint64_t smem_desc(const void* base) {
+  const uint64_t addr = sm_u32(base);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFF;                          // start address [0,14)
+  d |= (uint64_t)((128 >> 4) & 0x3FFF) << 16;         // leading byte offset [16,30)
+  d |= (uint64_t)((((BK / 16) * 128) >> 4) & 0x3FFF) << 32;  // stride byte offset [32,46)
+  d |= (uint64_t)1 << 46;                             // version (sm100)
+  // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// kind::i8 instruction descriptor: D s32, A s8, B s8, both K-major, N = 128, M = 128
+__device__ __forceinline__ uint32_t idesc_i8() {
+  uint32_t d = 0;
+  d |= 2u << 4;                // c_format S32
+  d |= 1u << 7;                // a_format s8
+  d |= 1u << 10;               // b_format s8
+  d |= (uint32_t)(BN >> 3) << 17;
+  d |= (uint32_t)(BM >> 4) << 24;
+  return d;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(sm_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1) tc_i8_gemm(const int8_t* __restrict__ A, const int8_t* __restrict__ B,
+                                                         int32_t* __restrict__ C, int M, int N, int K) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sa = smem;                                 // [STAGES][TILE_BYTES]
+  unsigned char* sb = smem + STAGES * TILE_BYTES;           // [STAGES][TILE_BYTES]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * TILE_BYTES);  // [STAGES] + done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES + 1);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int KT = K / BK;
+
+  if (warp == 0) {  // TMEM: 128 columns of 32-bit accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_u32(tmem_slot)), "r"(128)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (t == 0) {
+    for (int s = 0; s <= STAGES; ++s) mbar_init(mbar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  auto load = [&](int st, int kt) {
+    const int k0 = kt * BK;
+    // 128 rows x 4 chunks of 16 B per operand: 512 chunks, 4 per thread
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = t + i * THREADS, r = idx >> 2, c = idx & 3;
+      const int8_t* ga = A + (size_t)(m0 + r) * K + k0 + c * 16;
+      const int8_t* gb = B + (size_t)(n0 + r) * K + k0 + c * 16;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(sa + st * TILE_BYTES + core_off(r, c))), "l"(ga)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(sb + st * TILE_BYTES + core_off(r, c))), "l"(gb)
+                   : "memory");
+    }
+  };
+
+  const uint32_t idesc = idesc_i8();
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % STAGES;
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
+    // make this thread's cp.async writes visible to the tensor core (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int ks = 0; ks < BK / 32; ++ks) {  // K = 32 bytes per instruction = 2 core matrices
+        const uint64_t da = smem_desc(sa + st * TILE_BYTES + ks * 2 * 128);
+        const uint64_t db = smem_desc(sb + st * TILE_BYTES + ks * 2 * 128);
+        const uint32_t acc = (kt > 0 || ks > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc)
+            : "memory");
+      }
+      // stage st is free once these MMAs have read it
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(mbar + st))
+                   : "memory");
+    }
+    // refill the stage consumed STAGES-1 iterations later; wait until its MMAs are done
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) {
+      const int ns = nk % STAGES;
+      if (nk >= STAGES) mbar_wait(mbar + ns, ((nk / STAGES) - 1) & 1);
+      load(ns, nk);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // all MMAs done -> accumulator readable
+  if (t == 0)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(mbar + STAGES))
+                 : "memory");
+  mbar_wait(mbar + STAGES, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // warp w reads TMEM lanes 32w .. 32w+31 (rows of the tile), 32 columns at a time
+  const int row = m0 + warp * 32 + lane;
+#pragma unroll
+  for (int cb = 0; cb < BN; cb += 32) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < M) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<int4*>(C + (size_t)row * N + n0 + cb + j) =
+            make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+}
+
+static size_t smem_bytes() { return 2 * STAGES * TILE_BYTES + (STAGES + 1) * 8 + 16; }
+
+static double run(int M, int N, int K, bool check) {
+  std::vector<int8_t> ha((size_t)M * K), hb((size_t)N * K);
+  unsigned s = 12345;
+  for (auto& x : ha) { s = s * 1103515245u + 12345u; x = (int8_t)((s >> 16) % 255 - 127); }
+  for (auto& x : hb) { s = s * 1103515245u + 12345u; x = (int8_t)((s >> 16) % 255 - 127); }
+  int8_t *da, *db;
+  int32_t* dc;
+  CK(cudaMalloc(&da, ha.size()));
+  CK(cudaMalloc(&db, hb.size()));
+  CK(cudaMalloc(&dc, (size_t)M * N * 4));
+  CK(cudaMemcpy(da, ha.data(), ha.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(db, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+  CK(cudaFuncSetAttribute(tc_i8_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+  dim3 grid(N / BN, M / BM);
+  tc_i8_gemm<<<grid, THREADS, smem_bytes()>>>(da, db, dc, M, N, K);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  double tops = 0;
+  if (check) {
+    std::vector<int32_t> hc((size_t)M * N);
+    CK(cudaMemcpy(hc.data(), dc, hc.size() * 4, cudaMemcpyDeviceToHost));
+    long bad = 0;
+    for (int i = 0; i < M; ++i)
+      for (int j = 0; j < N; ++j) {
+        long ref = 0;
+        for (int k = 0; k < K; ++k) ref += (long)ha[(size_t)i * K + k] * hb[(size_t)j * K + k];
+        if (ref != hc[(size_t)i * N + j]) {
+          if (bad < 5) fprintf(stderr, "mismatch C[%d][%d] = %d, ref %ld\n", i, j, hc[(size_t)i * N + j], ref);
+          ++bad;
+        }
+      }
+    printf("{\"check\": \"%s\", \"M\": %d, \"N\": %d, \"K\": %d, \"mismatches\": %ld}\n", bad ? "FAIL" : "ok", M, N, K, bad);
+  } else {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      tc_i8_gemm<<<grid, THREADS, smem_bytes()>>>(da, db, dc, M, N, K);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms < best ? ms : best;
+    }
+    tops = 2.0 * M * N * (double)K / (best * 1e-3) / 1e12;
+    printf("{\"tc_i8_gemm_tops\": %.1f, \"M\": %d, \"N\": %d, \"K\": %d, \"ms\": %.3f}\n", tops, M, N, K, best);
+  }
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dc);
+  return tops;
+}
+
+int main() {
+  run(512, 384, 1024, true);
+  run(8192, 8192, 8192, false);
+  return 0;
+}
