@@ -2,10 +2,10 @@
 // (tcgen05.mma.kind::i8, accumulator in TMEM), the building block of an Ozaki-style FP64
 // emulation of the dense path's P = U Y. Not used by libffs.
 //   C[M][N] (int32, row-major) = A[M][K] (int8, row-major) * B[N][K]^T (int8, row-major = K-major)
-// CTA tile 128 x 128, K staged 64 bytes at a time (two tcgen05.mma of K = 32), 4-stage cp.async
-// ring into the canonical no-swizzle K-major layout (8-row x 16-byte core matrices), one thread
-// issues the MMAs, tcgen05.commit -> mbarrier releases a stage, 4 warps read the accumulator
-// back with tcgen05.ld. Checks a 512 x 384 x 1024 product against the host, then times 8192^3.
+// CTA tile 128 x 256, K staged 128 bytes at a time (four tcgen05.mma of K = 32), 3-stage cp.async
+// ring into the canonical no-swizzle K-major layout (8-row x 16-byte core matrices); producer warps
+// and one MMA-issuing thread hand stages over through full/empty mbarriers; 4 warps read the
+// accumulator back with tcgen05.ld. Checks 512 x 512 x 1024 against the host, then times 8192^3.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_i8_gemm tc_i8_gemm.cu
 #include <cstdint>
 #include <cstdio>
@@ -16,8 +16,8 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4, THREADS = 128;
-constexpr int TILE_BYTES = BM * BK;  // 8 KB per operand per stage
+constexpr int BM = 128, BN = 256, BK = 128, STAGES = 3, THREADS = 256;
+constexpr int TILE_A = BM * BK, TILE_B = BN * BK;  // bytes per stage
 
 __device__ __forceinline__ unsigned sm_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -61,24 +61,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       : "memory");
 }
 
+// Warp-specialised: warps 4..7 load (cp.async, wait, proxy fence, arrive on full[st]); warp 0
+// lane 0 waits full[st], issues BK/32 MMAs and commits them to empty[st]; the producers wait
+// empty[st] before refilling it. Epilogue: warps 0..3 read TMEM lanes 32w..32w+31.
 __global__ void __launch_bounds__(THREADS, 1) tc_i8_gemm(const int8_t* __restrict__ A, const int8_t* __restrict__ B,
                                                          int32_t* __restrict__ C, int M, int N, int K) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* sa = smem;                                 // [STAGES][TILE_BYTES]
-  unsigned char* sb = smem + STAGES * TILE_BYTES;           // [STAGES][TILE_BYTES]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * TILE_BYTES);  // [STAGES] + done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES + 1);
+  unsigned char* sa = smem;                                 // [STAGES][TILE_A]
+  unsigned char* sb = smem + STAGES * TILE_A;               // [STAGES][TILE_B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (TILE_A + TILE_B));
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int KT = K / BK;
+  constexpr int PRODUCERS = 128;  // warps 4..7
 
-  if (warp == 0) {  // TMEM: 128 columns of 32-bit accumulators
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_u32(tmem_slot)), "r"(128)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_u32(tmem_slot)), "r"(BN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (t == 0) {
-    for (int s = 0; s <= STAGES; ++s) mbar_init(mbar + s, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, PRODUCERS);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -86,38 +96,48 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_gemm(const int8_t* __restric
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  auto load = [&](int st, int kt) {
-    const int k0 = kt * BK;
-    // 128 rows x 4 chunks of 16 B per operand: 512 chunks, 4 per thread
+  if (warp >= 4) {  // producers
+    const int pt = t - 128;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      if (kt >= STAGES) mbar_wait(empty + st, ((kt / STAGES) - 1) & 1);
+      const int k0 = kt * BK;
+      // A: 128 rows x 8 chunks = 1024 chunks (8 per thread); B: 256 rows x 8 chunks = 2048 (16 per thread)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int idx = t + i * THREADS, r = idx >> 2, c = idx & 3;
-      const int8_t* ga = A + (size_t)(m0 + r) * K + k0 + c * 16;
-      const int8_t* gb = B + (size_t)(n0 + r) * K + k0 + c * 16;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(sa + st * TILE_BYTES + core_off(r, c))), "l"(ga)
-                   : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(sb + st * TILE_BYTES + core_off(r, c))), "l"(gb)
-                   : "memory");
+      for (int i = 0; i < TILE_A / 16 / PRODUCERS; ++i) {
+        const int idx = pt + i * PRODUCERS, r = idx / (BK / 16), c = idx % (BK / 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(sa + st * TILE_A + core_off(r, c))),
+                     "l"(A + (size_t)(m0 + r) * K + k0 + c * 16)
+                     : "memory");
+      }
+#pragma unroll
+      for (int i = 0; i < TILE_B / 16 / PRODUCERS; ++i) {
+        const int idx = pt + i * PRODUCERS, r = idx / (BK / 16), c = idx % (BK / 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sm_u32(sb + st * TILE_B + core_off(r, c))),
+                     "l"(B + (size_t)(n0 + r) * K + k0 + c * 16)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      // complete the stage issued one iteration ago (keeps two stages in flight per thread)
+      if (kt >= 1) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(full + (kt - 1) % STAGES)) : "memory");
+      }
     }
-  };
-
-  const uint32_t idesc = idesc_i8();
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load(s, s);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  for (int kt = 0; kt < KT; ++kt) {
-    const int st = kt % STAGES;
-    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
-    // make this thread's cp.async writes visible to the tensor core (async proxy)
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (t == 0) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(full + (KT - 1) % STAGES)) : "memory");
+  } else if (warp == 0 && lane == 0) {  // MMA issuer
+    const uint32_t idesc = idesc_i8();
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      mbar_wait(full + st, (kt / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int ks = 0; ks < BK / 32; ++ks) {  // K = 32 bytes per instruction = 2 core matrices
-        const uint64_t da = smem_desc(sa + st * TILE_BYTES + ks * 2 * 128);
-        const uint64_t db = smem_desc(sb + st * TILE_BYTES + ks * 2 * 128);
+      for (int ks = 0; ks < BK / 32; ++ks) {
+        const uint64_t da = smem_desc(sa + st * TILE_A + ks * 2 * 128);
+        const uint64_t db = smem_desc(sb + st * TILE_B + ks * 2 * 128);
         const uint32_t acc = (kt > 0 || ks > 0) ? 1u : 0u;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -126,53 +146,43 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_gemm(const int8_t* __restric
             "l"(da), "l"(db), "r"(idesc), "r"(acc)
             : "memory");
       }
-      // stage st is free once these MMAs have read it
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(mbar + st))
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(empty + st))
                    : "memory");
     }
-    // refill the stage consumed STAGES-1 iterations later; wait until its MMAs are done
-    const int nk = kt + STAGES - 1;
-    if (nk < KT) {
-      const int ns = nk % STAGES;
-      if (nk >= STAGES) mbar_wait(mbar + ns, ((nk / STAGES) - 1) & 1);
-      load(ns, nk);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  // all MMAs done -> accumulator readable
-  if (t == 0)
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(mbar + STAGES))
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(done))
                  : "memory");
-  mbar_wait(mbar + STAGES, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // warp w reads TMEM lanes 32w .. 32w+31 (rows of the tile), 32 columns at a time
-  const int row = m0 + warp * 32 + lane;
+  }
+  if (warp < 4) {
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+    for (int cb = 0; cb < BN; cb += 32) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
 #pragma unroll
-  for (int cb = 0; cb < BN; cb += 32) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<int4*>(C + (size_t)row * N + n0 + cb + j) =
-            make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<int4*>(C + (size_t)row * N + n0 + cb + j) =
+              make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
 }
 
-static size_t smem_bytes() { return 2 * STAGES * TILE_BYTES + (STAGES + 1) * 8 + 16; }
+static size_t smem_bytes() { return STAGES * (TILE_A + TILE_B) + (2 * STAGES + 1) * 8 + 16; }
 
 static double run(int M, int N, int K, bool check) {
   std::vector<int8_t> ha((size_t)M * K), hb((size_t)N * K);
@@ -230,7 +240,7 @@ static double run(int M, int N, int K, bool check) {
 }
 
 int main() {
-  run(512, 384, 1024, true);
+  run(512, 512, 1024, true);
   run(8192, 8192, 8192, false);
   return 0;
 }
