@@ -16,7 +16,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
 
-constexpr int BM = 128, BN = 256, BK = 128, STAGES = 3, THREADS = 256;
+constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4, THREADS = 256;
 constexpr int TILE_A = BM * BK, TILE_B = BN * BK;  // bytes per stage
 
 __device__ __forceinline__ unsigned sm_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -117,22 +117,18 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_gemm(const int8_t* __restric
                      "l"(B + (size_t)(n0 + r) * K + k0 + c * 16)
                      : "memory");
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      // complete the stage issued one iteration ago (keeps two stages in flight per thread)
-      if (kt >= 1) {
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(full + (kt - 1) % STAGES)) : "memory");
-      }
+      // the stage's full barrier receives this thread's arrival when its copies have landed
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sm_u32(full + st)) : "memory");
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(full + (KT - 1) % STAGES)) : "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 0 && lane == 0) {  // MMA issuer
     const uint32_t idesc = idesc_i8();
     for (int kt = 0; kt < KT; ++kt) {
       const int st = kt % STAGES;
       mbar_wait(full + st, (kt / STAGES) & 1);
+      // the stage was written by other threads' cp.async (generic proxy): order it before the
+      // tensor core's (async proxy) reads
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int ks = 0; ks < BK / 32; ++ks) {
@@ -242,5 +238,7 @@ static double run(int M, int N, int K, bool check) {
 int main() {
   run(512, 512, 1024, true);
   run(8192, 8192, 8192, false);
+  run(16384, 8192, 1024, false);  // the C5 dense block's shape (one slice pair): M = L, N = 8 S, K = N
+  run(4096, 16384, 2048, false);  // C4 (complex as real 2N)
   return 0;
 }
