@@ -48,9 +48,10 @@ typedef enum { FFS_OK = 0, FFS_EINVAL = -1, FFS_ECUDA = -2, FFS_ENOWS = -3 } ffs
 /* Device workspace bytes needed by ffs_sample / ffs_sample_marginal / ffs_debug_trace on the
  * current CUDA device. Returns 0 for invalid arguments. Size depends on the path the call takes:
  * small for L <= 256 (permutations only); for L >= 2048 with N >= 256 (the lockstep block-step
- * path) it holds, per batch of up to 1024 samples (8192 for marginals), the factor
- * W [N'][N'] of every batch sample, the coefficient and panel matrices Y [N][8 S] and P [L][8 S]
- * of the dense GEMM, U^T and the permutations: e.g. 9.4 GB for the C5 config (L=16384, N=1024). */
+ * path) it holds, per batch of S samples (the most whose factors W [N'][N'] fit a
+ * 24 GB budget, at least 1024 and at most 8192, at most M), every batch sample's W, the coefficient
+ * and panel matrices Y [N][8 S] and P [L][8 S] of the dense GEMM, U^T and the permutations: e.g.
+ * 9.4 GB for the C5 config (L=16384, N=1024, M=1024), 20 GB for C4 (L=4096, N=512, c128). */
 size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M);
 
 /* Full sampling (N' = N): Eq. 1-3. uniforms [M][2N], positions [M][N]. */
