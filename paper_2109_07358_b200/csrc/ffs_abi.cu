@@ -10,7 +10,6 @@
 #include "ffs.h"
 #include "ffs_kernel.cuh"
 #include "ffs_warp_kernel.cuh"
-#include "ffs_pc_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
 #include "ffs_mma_kernel.cuh"
 #include "ffs_dense.cuh"
@@ -191,14 +190,11 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
 }
 
 // ------------------------------------------------------------------ fast warp-owner path
-// Real U, L <= 256, N' <= kMaxNpWarp, U^T small enough for shared memory: ffs_warp_kernel
-// (one CTA per SM, warps = sample owners) after ffs_permute_kernel.
+// Real U, L <= 256, N' <= kMaxNpWarp, U^T small enough for shared memory: ffs_seg_kernel
+// (one CTA per SM, G-lane segments of warps = sample owners) after ffs_permute_kernel.
 struct WarpPlan {
   const void* fn;
   int R, B, S, G = 32, maxt, warps, grid, Lp, ut_stride;
-  bool legacy = false;  // whole-warp ffs_warp_kernel (its own W layout)
-  bool pc = false;  // producer/consumer kernel (owner = consumer+producer warp pair, 2 slots)
-  bool wsmem = false;  // pc kernel keeps W in shared memory
   bool mma = false;  // ffs_mma_kernel (DMMA contraction, B = 8, its own U^T swizzle and slice)
   size_t ushared, owner, smem, ws_perm, ws_w = 0;
   int perm_tpb;
@@ -215,47 +211,14 @@ void warp_fn_seg(WarpPlan& w) {
   w.maxt = MAXT;
 }
 
-template <int R, int B, int MAXT, bool WSMEM, bool TIMING = false>
-void warp_fn_pc(WarpPlan& w) {
-  w.fn = ffsk::pc_kernel_ptr<R, B, MAXT, WSMEM, TIMING>();
-  w.wsmem = WSMEM;
-  w.R = R;
-  w.B = B;
-  w.S = 1;
-  w.G = 32;
-  w.maxt = MAXT;
-  w.pc = true;
-}
-
-template <int R, int B, int S, int MAXREG>
-void warp_fn_r(WarpPlan& w) {
-  w.legacy = true;
-  w.fn = ffsk::warp_kernel_r_ptr<R, B, S, MAXREG>();
-  w.R = R;
-  w.B = B;
-  w.S = S;
-  w.maxt = 4 * 32 * (16384 / (32 * MAXREG));  // per-SMSP register file: 16K regs
-}
-
-template <int R, int B, int S, int MAXT>
-void warp_fn(WarpPlan& w) {
-  w.legacy = true;
-  w.fn = ffsk::warp_kernel_ptr<R, B, S, MAXT>();
-  w.R = R;
-  w.B = B;
-  w.S = S;
-  w.maxt = MAXT;
-}
-
 bool warp_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   if (dtype != FFS_F64 || L > 256 || Np > ffsk::kMaxNpWarp || N > 4096) return false;
   return (size_t)N * (256 + 2) * 8 <= 100 * 1024;  // padded U^T fits shared memory
 }
 
 int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
-  const char* var = getenv("FFS_WARP_VARIANT");  // development: "b6" selects B=6 for R=8
-  const bool legacy = var && strncmp(var, "w", 1) == 0;  // "w..." = whole-warp owner variants
-  if (!legacy) {
+  const char* var = getenv("FFS_WARP_VARIANT");  // development: measured variants (profiles/)
+  {
     // segmented kernel, OPT = 7 (+128 for G = 32): kept partial sums, pivot row through smem,
     // flat Gauss-Jordan, no warp vote when the segment is the whole warp
     // (variants measured in profiles/r01_ncu_summary.md; "base" = the first segmented kernel)
@@ -270,8 +233,6 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
     else if (base) warp_fn_seg<8, 4, 32, 384, false, 0>(w);
     else if (var && strcmp(var, "o7_384") == 0) warp_fn_seg<8, 4, 32, 384, false, 7>(w);
     else if (var && strcmp(var, "b8") == 0) warp_fn_seg<8, 8, 32, 256, false, 7>(w);
-    else if (var && strcmp(var, "pcs256") == 0) warp_fn_pc<8, 4, 256, true>(w);
-    else if (var && strcmp(var, "pcs256t") == 0) warp_fn_pc<8, 4, 256, true, true>(w);
     else if (var && strcmp(var, "o647") == 0) warp_fn_seg<8, 4, 32, 512, false, 647>(w);
     else if (var && strcmp(var, "t") == 0) warp_fn_seg<8, 4, 32, 512, true, 7>(w);  // phase timing
     else if (var && strncmp(var, "mma", 3) == 0) {
@@ -286,12 +247,7 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
     }
     else if (fits16) warp_fn_seg<8, 4, 32, 512, false, 135>(w);  // 16 owners/SM, 128 regs
     else warp_fn_seg<8, 4, 32, 384, false, 135>(w);              // 12 owners/SM (larger N')
-  } else if (L <= 64) warp_fn<2, 8, 1, 384>(w);
-  else if (L <= 128) warp_fn<4, 8, 1, 384>(w);
-  else if (var && strcmp(var, "wb8") == 0) warp_fn<8, 8, 1, 256>(w);
-  else if (var && strcmp(var, "wb8r168") == 0) warp_fn_r<8, 8, 1, 168>(w);
-  else if (var && strcmp(var, "ws2") == 0) warp_fn<8, 4, 2, 256>(w);
-  else warp_fn<8, 4, 1, 512>(w);  // fastest measured on B200 (profiles/)
+  }
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(FFS_ECUDA, "cudaGetDevice failed");
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -300,34 +256,19 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   w.Lp = w.G * w.R;
   w.ut_stride = w.mma ? ffsk::kMmaRows : w.Lp + 2;
   w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
-  w.owner = w.mma ? ffsk::MmaLayout((int)Np).total : w.pc ? ffsk::pc_pair_bytes((int)Np, w.B, w.R, w.wsmem)  // per consumer/producer pair
-                 : ffsk::WarpLayout((int)Np, w.B, !w.legacy).total;         // per sample; a warp holds S slices
+  w.owner = w.mma ? ffsk::MmaLayout((int)Np).total
+                 : ffsk::WarpLayout((int)Np, w.B, true).total;  // per sample; a warp holds S slices
   // registers are allocated per SM sub-partition (4 x 16K); warps are spread round-robin
   const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
   int warps = std::min(w.maxt / 32, by_regs);
-  if (w.pc) {
-    // warps come in (consumer, producer) pairs; each pair owns two sample slots
-    int pairs = std::max(1, warps / 2);
-    while (pairs > 1 && w.ushared + (size_t)pairs * w.owner > kMaxSmem) --pairs;
-    if (const char* fw = getenv("FFS_WARPS")) pairs = std::max(1, std::min(pairs, atoi(fw) / 2));
-    w.warps = 2 * pairs;
-    w.smem = w.ushared + (size_t)pairs * w.owner;
-    if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "pc path smem %zu too large", w.smem);
-    const int64_t ctas = (M + 2LL * pairs - 1) / (2LL * pairs);
-    w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
-    const int ldw = (int)((Np + w.B + 1) & ~1);
-    w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-    w.ws_w = w.wsmem ? 0 : align_up((size_t)w.grid * pairs * 2 * Np * ldw * 8);
-  } else {
-    while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
-    if (const char* fw = getenv("FFS_WARPS")) warps = std::max(1, std::min(warps, atoi(fw)));  // development
-    w.warps = warps;
-    w.smem = w.ushared + (size_t)warps * w.S * w.owner;
-    if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
-    const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
-    w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
-    w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-  }
+  while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
+  if (const char* fw = getenv("FFS_WARPS")) warps = std::max(1, std::min(warps, atoi(fw)));  // development
+  w.warps = warps;
+  w.smem = w.ushared + (size_t)warps * w.S * w.owner;
+  if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
+  const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
+  w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
+  w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
   w.perm_tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
   w.perm_smem = (size_t)w.perm_tpb * N * 4;
   return FFS_OK;
@@ -362,7 +303,7 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   p.ut_stride = w.ut_stride;
   p.ushared = w.ushared;
   p.owner_bytes = w.owner;
-  p.wfull = w.pc ? reinterpret_cast<double*>(static_cast<char*>(ws) + w.ws_perm) : nullptr;
+  p.wfull = nullptr;
   p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
   p.trace = S > 0 ? trace : nullptr;
   const char* dbg = getenv("FFS_DEBUG_SKIP");  // development only: bits 0-2 break the results

@@ -4,7 +4,6 @@
 #include "ffs_kptr.h"
 #include "ffs_kernel.cuh"
 #include "ffs_warp_kernel.cuh"
-#include "ffs_pc_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
 #include "ffs_mma_kernel.cuh"
 
@@ -14,15 +13,6 @@ template <typename T, bool WARP, int R, int B, bool USMEM, int MAXT> const void*
 }
 template <int R, int B, int G, int MAXT, bool TIMING, int OPT> const void* seg_kernel_ptr() {
   return reinterpret_cast<const void*>(&ffs_seg_kernel<R, B, G, MAXT, TIMING, OPT>);
-}
-template <int R, int B, int MAXT, bool WSMEM, bool TIMING> const void* pc_kernel_ptr() {
-  return reinterpret_cast<const void*>(&ffs_pc_kernel<R, B, MAXT, WSMEM, TIMING>);
-}
-template <int R, int B, int S, int MAXREG> const void* warp_kernel_r_ptr() {
-  return reinterpret_cast<const void*>(&ffs_warp_kernel_r<R, B, S, MAXREG>);
-}
-template <int R, int B, int S, int MAXT> const void* warp_kernel_ptr() {
-  return reinterpret_cast<const void*>(&ffs_warp_kernel<R, B, S, MAXT>);
 }
 template <typename T, int R, int B, int MAXT> const void* cluster_kernel_ptr() {
   return reinterpret_cast<const void*>(&ffs_cluster_kernel<T, R, B, MAXT>);

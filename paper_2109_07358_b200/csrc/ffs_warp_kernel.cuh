@@ -1,14 +1,15 @@
-// Warp-owner FFS kernel for small real problems (L <= 32*R, N' <= kMaxNpWarp): the headline
+// Warp-owner FFS kernels for small real problems (L <= 32*R, N' <= kMaxNpWarp): the headline
 // double-well workload (L=256, N=32) and the tiny exact-check config.
 //
 // Same mathematics as ffs_kernel.cuh (blocked left-looking randomized-pivot LU: panel
 // contraction, B sequential draws on the register panel, Gauss-Jordan update of
-// W = A^{-1} V[X, later cols]); organised for throughput on one SM:
+// W = A^{-1} V[X, later cols]); organised for throughput on one SM (ffs_seg_kernel):
 //   * one CTA per SM holds U^T once in shared memory (bank-conflict-free swizzle) and runs
-//     `warps` independent sample owners; everything a sample needs (W, pivot rows, new rows,
-//     permutation, selection uniforms) lives in that warp's shared-memory slice;
-//   * lane l owns rows l*R .. l*R+R-1 (index order == scan order); the L x B panel is in
-//     registers; rows already drawn are ZEROED in the panel, so the weights need no mask;
+//     independent sample owners: G-lane segments of its warps (G = 32 for C2: one sample per
+//     warp; G = 4 for C1); everything a sample needs (W, pivot rows, new rows, permutation,
+//     selection uniforms) lives in that owner's shared-memory slice;
+//   * segment lane l owns rows l*R .. l*R+R-1 (index order == scan order); the L x B panel is in
+//     registers;
 //   * the draw of step r+1 (scan, crossing search) is issued before the rank-1 update of the
 //     panel columns r+2.. so the shuffle latency overlaps FP64 work (one-column lookahead);
 //   * the permutation rows come precomputed from ffs_permute_kernel.
@@ -68,69 +69,6 @@ struct Draw {
   double T;       // total weight
 };
 
-// Weights w_r = col_r^2 (drawn rows are zero), local inclusive prefix in index order, warp
-// inclusive scan, total T, crossing search (reading Q5). The crossing lane is the first lane
-// whose inclusive prefix exceeds thr = u*T; its exclusive prefix (the previous lane's inclusive
-// value) is <= thr, so the first row with excl + C_r > thr exists in it and has w > 0.
-// Branch-free: the scheduler interleaves it with independent FP64 work.
-// v + (value of lane - d) for lanes >= d, v otherwise (one inclusive-scan level, fp64)
-__device__ __forceinline__ double scan_level(double v, int d) {
-  double r;
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, ylo, yhi;\n\t.reg .f64 y;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.up.b32 ylo|p, lo, %2, 0, -1;\n\t"
-      "shfl.sync.up.b32 yhi, hi, %2, 0, -1;\n\t"
-      "mov.b64 y, {ylo, yhi};\n\t"
-      "mov.f64 %0, %1;\n\t"
-      "@p add.f64 %0, %1, y;\n\t}"
-      : "=d"(r) : "d"(v), "r"(d));
-  return r;
-}
-
-template <int R>
-__device__ __forceinline__ Draw draw_part1(const double (&col)[R], double u, int lane) {
-  double c[R];
-  c[0] = col[0] * col[0];
-#pragma unroll
-  for (int r = 1; r < R; ++r) c[r] = fma(col[r], col[r], c[r - 1]);
-  double incl = c[R - 1];
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) incl = scan_level(incl, d);
-  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
-  if (lane == 0) excl = 0.0;
-  Draw d;
-  d.T = __shfl_sync(0xffffffffu, incl, 31);
-  const bool ok = (d.T > 0.0) && (d.T < INFINITY);
-  // crossing threshold relative to this lane's exclusive prefix, clamped at 0 so that a lane
-  // whose rounded prefix already passed u*T still lands on its first positive weight
-  const double tp = fmax(fma(u, d.T, -excl), 0.0);
-  d.ball = __ballot_sync(0xffffffffu, ok && (c[R - 1] > tp));
-  unsigned m = 0;
-#pragma unroll
-  for (int r = 0; r < R - 1; ++r) m |= (c[r] <= tp) ? (1u << r) : 0u;
-  d.rsel = __popc(m);
-  return d;
-}
-
-// Rare paths (T not finite/positive, or u*T beyond the last partial sum): reading Q5/Q8.
-template <int R>
-__device__ __noinline__ int draw_fallback(const double* col, double T, uint32_t chosen, int L, int lane) {
-  const bool ok = (T > 0.0) && isfinite(T);
-  int rl = -1, rf = R;
-  for (int r = 0; r < R; ++r) {
-    if (col[r] * col[r] > 0.0) rl = r;
-    if (rf == R && lane * R + r < L && !((chosen >> r) & 1u)) rf = r;
-  }
-  if (ok) {  // largest x with w(x) > 0
-    const unsigned b = __ballot_sync(0xffffffffu, rl >= 0);
-    const int ln = 31 - __clz(b);
-    return ln * R + __shfl_sync(0xffffffffu, rl, ln);
-  }
-  const unsigned b = __ballot_sync(0xffffffffu, rf < R);  // smallest unchosen site
-  const int ln = __ffs(b) - 1;
-  return ln * R + __shfl_sync(0xffffffffu, rf, ln);
-}
-
 // U [L][N] -> per-sample permutation prefix [M][Np] (a1 rule, reading Q6); one thread per sample.
 static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, int32_t* __restrict__ perm, int64_t M,
                                    int N, int Np) {
@@ -150,322 +88,6 @@ static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, i
     perm[i * Np + j] = m[j];
   }
 }
-
-// S samples per warp advance in lockstep: their draws are independent dependency chains that
-// the scheduler interleaves (S=2 doubles the latency hiding per warp at the same register cost
-// as one sample with a 2x wider panel).
-template <int R, int B, int S>
-__device__ __forceinline__ void ffs_warp_body(const WarpParams& p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  using Sw = Swz<double, R>;
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int L = p.L, N = p.N, Np = p.Np;
-  const int stride = p.ut_stride;
-
-  // ---- U^T into shared memory (swizzled 16-byte chunks; rows >= L zero)
-  double* Uts = reinterpret_cast<double*>(smem);
-  for (int idx = threadIdx.x; idx < N * p.Lp; idx += blockDim.x) {
-    const int x = idx / N, c = idx % N;
-    Uts[(size_t)c * stride + Sw::phys(x)] = (x < L) ? p.U[(size_t)x * N + c] : 0.0;
-  }
-  __syncthreads();
-
-  const WarpLayout lay(Np, B);
-  const int ldw = lay.ldw;
-  unsigned char* wbase = smem + p.ushared + (size_t)wid * S * p.owner_bytes;
-  auto slice = [&](int s) { return wbase + (size_t)s * p.owner_bytes; };
-#define FFS_PERM(s) reinterpret_cast<int*>(slice(s) + lay.perm)
-#define FFS_POS(s) reinterpret_cast<int*>(slice(s) + lay.pos)
-#define FFS_USEL(s) reinterpret_cast<double*>(slice(s) + lay.usel)
-#define FFS_ROW(s) reinterpret_cast<double*>(slice(s) + lay.row)
-#define FFS_PINV(s) reinterpret_cast<double*>(slice(s) + lay.pinv)
-#define FFS_WF(s) reinterpret_cast<double*>(slice(s) + lay.wf)
-#define FFS_VNT(s) reinterpret_cast<double*>(slice(s) + lay.vnt)
-  const int sw = Sw::sw(lane);
-  const double* Ucol0 = Uts + lane * R;
-  for (int s = 0; s < S; ++s) {
-    for (int idx = lane; idx < Np * ldw; idx += 32) FFS_WF(s)[idx] = 0.0;  // padding cols stay 0
-    for (int idx = lane; idx < B * B; idx += 32) FFS_ROW(s)[idx] = 0.0;
-  }
-  __syncwarp();
-
-  const int64_t ngroups = (p.M + S - 1) / S;
-  for (int64_t g = (int64_t)blockIdx.x * nwarps + wid; g < ngroups; g += (int64_t)gridDim.x * nwarps) {
-    int64_t ids[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      ids[s] = g * S + s;
-      const int64_t i = ids[s] < p.M ? ids[s] : p.M - 1;  // a short last group recomputes a sample
-      for (int j = lane; j < Np; j += 32) {
-        FFS_PERM(s)[j] = p.perm[i * Np + j];
-        FFS_USEL(s)[j] = p.uniforms[i * 2 * (int64_t)Np + Np + j];
-      }
-    }
-    __syncwarp();
-    uint32_t chosen[S];
-    int flag[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      chosen[s] = 0;
-      flag[s] = 0;
-    }
-
-    for (int k0 = 0; k0 < Np; k0 += B) {
-      const int nb = min(B, Np - k0);
-      // ---- a3 panel: P = V[:, k0:k0+B] - V[:, 0:k0] Wb  (Wb = Wf[0:k0][k0:k0+B], smem)
-      double P[S][R][B];
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int c = 0; c < B; ++c) {
-          const double* cb = Ucol0 + FFS_PERM(s)[min(k0 + c, Np - 1)] * stride;
-#pragma unroll
-          for (int q = 0; q < R / 2; ++q) {
-            const double2 d = *reinterpret_cast<const double2*>(cb + ((q ^ sw) << 1));
-            P[s][2 * q][c] = (c < nb) ? d.x : 0.0;
-            P[s][2 * q + 1][c] = (c < nb) ? d.y : 0.0;
-          }
-        }
-#pragma unroll 1
-      for (int ii = 0; ii < k0; ++ii) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const double* cb = Ucol0 + FFS_PERM(s)[ii] * stride;
-          const double* wrow = FFS_WF(s) + ii * ldw + k0;
-          double wb[B];
-#pragma unroll
-          for (int c = 0; c < B; c += 2) {
-            const double2 d = *reinterpret_cast<const double2*>(wrow + c);
-            wb[c] = d.x;
-            wb[c + 1] = d.y;
-          }
-#pragma unroll
-          for (int q = 0; q < R / 2; ++q) {
-            const double2 d = *reinterpret_cast<const double2*>(cb + ((q ^ sw) << 1));
-#pragma unroll
-            for (int c = 0; c < B; ++c) {
-              P[s][2 * q][c] = fma(-d.x, wb[c], P[s][2 * q][c]);
-              P[s][2 * q + 1][c] = fma(-d.y, wb[c], P[s][2 * q + 1][c]);
-            }
-          }
-        }
-      }
-      // rows drawn in earlier blocks: exactly zero (the contraction leaves O(eps) residues)
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const bool drawn = (chosen[s] >> r) & 1u;
-#pragma unroll
-          for (int c = 0; c < B; ++c) P[s][r][c] = drawn ? 0.0 : P[s][r][c];
-        }
-
-      // ---- a4/a5: nb sequential draws on the panels, one-column lookahead
-      Draw dr[S];
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        double col0[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) col0[r] = P[s][r][0];
-        dr[s] = draw_part1<R>(col0, FFS_USEL(s)[k0], lane);
-      }
-      static_for<0, B>([&](auto rrc) {
-        constexpr int rr = decltype(rrc)::value;
-        if (rr < nb) {
-          const int k = k0 + rr;
-          int own[S], orow[S];
-#pragma unroll
-          for (int s = 0; s < S; ++s) {
-            if (dr[s].ball != 0u) {
-              own[s] = __ffs(dr[s].ball) - 1;
-              orow[s] = __shfl_sync(0xffffffffu, dr[s].rsel, own[s]);
-            } else {  // rare: u*T at/after the last partial sum, or T not finite and positive
-              double colr[R];
-#pragma unroll
-              for (int r = 0; r < R; ++r) colr[r] = P[s][r][rr];
-              const int xf = draw_fallback<R>(colr, dr[s].T, chosen[s], L, lane);
-              own[s] = xf / R;
-              orow[s] = xf % R;
-            }
-            if (!((dr[s].T > 0.0) && isfinite(dr[s].T))) flag[s] |= 1;
-            if (p.trace != nullptr && ids[s] < p.S) {
-              const double inv = dr[s].T > 0.0 ? 1.0 / dr[s].T : 0.0;
-              double* tr = p.trace + (ids[s] * Np + k) * (int64_t)L;
-#pragma unroll
-              for (int r = 0; r < R; ++r)
-                if (lane * R + r < L) tr[lane * R + r] = P[s][r][rr] * P[s][r][rr] * inv;
-            }
-          }
-          // pivot row -> smem, zeroed in the panel: uniform switch on the row, one lane acts
-          static_for<0, S>([&](auto sc) {
-            constexpr int s = decltype(sc)::value;
-            double* Row = FFS_ROW(s);
-            const double Tk = dr[s].T;
-            auto extract = [&](auto rc) {
-              constexpr int r = decltype(rc)::value;
-              if constexpr (r < R) {
-                if (lane == own[s]) {
-#pragma unroll
-                  for (int c = 0; c < B; c += 2)
-                    *reinterpret_cast<double2*>(Row + rr * B + c) = make_double2(P[s][r][c], P[s][r][c + 1]);
-                  if (P[s][r][rr] * P[s][r][rr] < 1e-12 * Tk) flag[s] |= 2;
-                  chosen[s] |= 1u << r;
-#pragma unroll
-                  for (int c = rr; c < B; ++c) P[s][r][c] = 0.0;
-                }
-              }
-            };
-            switch (orow[s]) {
-              case 0: extract(std::integral_constant<int, 0>{}); break;
-              case 1: extract(std::integral_constant<int, 1>{}); break;
-              case 2: extract(std::integral_constant<int, 2>{}); break;
-              case 3: extract(std::integral_constant<int, 3>{}); break;
-              case 4: extract(std::integral_constant<int, 4>{}); break;
-              case 5: extract(std::integral_constant<int, 5>{}); break;
-              case 6: extract(std::integral_constant<int, 6>{}); break;
-              default: extract(std::integral_constant<int, 7>{}); break;
-            }
-            if (lane == 0) FFS_POS(s)[k] = own[s] * R + orow[s];
-          });
-          __syncwarp();
-          double sp[S][B];
-#pragma unroll
-          for (int s = 0; s < S; ++s) {
-            const double* Row = FFS_ROW(s);
-            const double ip = 1.0 / Row[rr * B + rr];
-            if (lane == 0) FFS_PINV(s)[rr] = ip;
-#pragma unroll
-            for (int c = 0; c < B; c += 2) {
-              const double2 d = *reinterpret_cast<const double2*>(Row + rr * B + c);
-              sp[s][c] = d.x * ip;
-              sp[s][c + 1] = d.y * ip;
-            }
-          }
-          if constexpr (rr + 1 < B) {
-            // column rr+1 first, then the next draws, then the remaining columns
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-              for (int r = 0; r < R; ++r) P[s][r][rr + 1] = fma(-P[s][r][rr], sp[s][rr + 1], P[s][r][rr + 1]);
-            if (rr + 1 < nb) {
-#pragma unroll
-              for (int s = 0; s < S; ++s) {
-                double cn[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) cn[r] = P[s][r][rr + 1];
-                dr[s] = draw_part1<R>(cn, FFS_USEL(s)[k + 1], lane);
-              }
-            }
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-              for (int c = rr + 2; c < B; ++c)
-#pragma unroll
-                for (int r = 0; r < R; ++r) P[s][r][c] = fma(-P[s][r][rr], sp[s][c], P[s][r][c]);
-          }
-        }
-      });
-
-      // ---- Gauss-Jordan update of W with the nb new rows (only if later columns remain)
-      if (k0 + nb < Np) {
-        __syncwarp();
-        for (int s = 0; s < S; ++s) {
-          // VnT[ii][tt] = V[x_{k0+tt}, ii] = U[x][perm[ii]]  (ii < Np)
-          const int* perm = FFS_PERM(s);
-          const int* pos = FFS_POS(s);
-          double* VnT = FFS_VNT(s);
-          for (int idx = lane; idx < Np * B; idx += 32) {
-            const int ii = idx / B, tt = idx % B;
-            VnT[idx] = (tt < nb) ? p.U[(size_t)pos[k0 + tt] * N + perm[ii]] : 0.0;
-          }
-        }
-        __syncwarp();
-        for (int s = 0; s < S; ++s) {
-          const double* VnT = FFS_VNT(s);
-          const double* Row = FFS_ROW(s);
-          const double* Pinv = FFS_PINV(s);
-          double* Wf = FFS_WF(s);
-          for (int j = k0 + nb + lane; j < Np; j += 32) {
-            double z[B];
-#pragma unroll
-            for (int tt = 0; tt < B; ++tt) z[tt] = VnT[j * B + tt];
-#pragma unroll 2
-            for (int ii = 0; ii < k0; ++ii) {
-              const double wij = Wf[ii * ldw + j];
-#pragma unroll
-              for (int tt = 0; tt < B; tt += 2) {
-                const double2 v = *reinterpret_cast<const double2*>(VnT + ii * B + tt);
-                z[tt] = fma(-v.x, wij, z[tt]);
-                z[tt + 1] = fma(-v.y, wij, z[tt + 1]);
-              }
-            }
-            // solve S z = rhs, S = LU from the draws: L[tt][t2] = Row[tt][t2]/Row[t2][t2] (t2<tt),
-            // U[tt][t2] = Row[tt][t2] (t2>=tt)
-            double ipv[B];
-#pragma unroll
-            for (int t2 = 0; t2 < B; ++t2) ipv[t2] = (t2 < nb) ? Pinv[t2] : 0.0;
-#pragma unroll
-            for (int tt = 1; tt < B; ++tt)
-#pragma unroll
-              for (int t2 = 0; t2 < tt; ++t2) z[tt] = fma(-(Row[tt * B + t2] * ipv[t2]), z[t2], z[tt]);
-#pragma unroll
-            for (int tt = B - 1; tt >= 0; --tt) {
-#pragma unroll
-              for (int t2 = tt + 1; t2 < B; ++t2) z[tt] = fma(-Row[tt * B + t2], z[t2], z[tt]);
-              z[tt] *= ipv[tt];
-            }
-#pragma unroll 2
-            for (int ii = 0; ii < k0; ++ii) {
-              double a = Wf[ii * ldw + j];
-#pragma unroll
-              for (int tt = 0; tt < B; tt += 2) {
-                const double2 wbv = *reinterpret_cast<const double2*>(Wf + ii * ldw + k0 + tt);
-                a = fma(-wbv.x, z[tt], a);
-                a = fma(-wbv.y, z[tt + 1], a);
-              }
-              Wf[ii * ldw + j] = a;
-            }
-#pragma unroll
-            for (int tt = 0; tt < B; ++tt)
-              if (tt < nb) Wf[(k0 + tt) * ldw + j] = z[tt];
-          }
-        }
-        __syncwarp();
-      }
-    }
-    // ---- a6: positions and flags
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int f = __reduce_or_sync(0xffffffffu, flag[s]);
-      if (ids[s] < p.M) {
-        for (int j = lane; j < Np; j += 32) p.positions[ids[s] * Np + j] = FFS_POS(s)[j];
-        if (lane == 0 && p.flags != nullptr) p.flags[ids[s]] = f;
-      }
-    }
-    __syncwarp();
-  }
-#undef FFS_PERM
-#undef FFS_POS
-#undef FFS_USEL
-#undef FFS_ROW
-#undef FFS_PINV
-#undef FFS_WF
-#undef FFS_VNT
-}
-
-template <int R, int B, int S, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) ffs_warp_kernel(const WarpParams p) {
-  ffs_warp_body<R, B, S>(p);
-}
-
-// register-capped variant: MAXREG x (owners*32) fills the register file exactly
-template <int R, int B, int S, int MAXREG>
-__global__ void __maxnreg__(MAXREG) ffs_warp_kernel_r(const WarpParams p) {
-  ffs_warp_body<R, B, S>(p);
-}
-
 
 // =====================================================================================
 // Segmented warp kernel: a warp is split into 32/G segments of G lanes, one sample per segment.
@@ -490,7 +112,7 @@ struct SegOps {
   __device__ __forceinline__ static double last(double v) { return __shfl_sync(0xffffffffu, v, G - 1, G); }
 };
 
-// Branch-free part of a draw for one segment (see draw_part1): returns the crossing lanes of
+// Branch-free part of a draw for one segment: returns the crossing lanes of
 // this lane's segment (bit i = segment lane i), the crossing row in this lane, and T.
 // Whole-warp draw (G = 32, R <= 8) with a shorter dependency chain: the local inclusive prefix is
 // kept (no second pass), and the 32-lane scan runs as a 3-level scan inside 8-lane groups plus
