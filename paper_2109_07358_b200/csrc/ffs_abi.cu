@@ -480,6 +480,9 @@ struct DensePlan {
   int64_t S, Sh, ldY;  // batch, half-batch (per stream), Y row stride in scalars of T
   int nstr;            // streams (half-batches) in flight
   bool small_gemm;     // GEMM <16, 4> (co-resident with the GJ kernel) instead of <32, 3>
+  bool ozaki;          // Ozaki-emulated GEMM on the INT8 tensor cores instead of the DMMA GEMM
+  int Kp;              // GEMM K (f N) padded to the Ozaki K chunk
+  size_t ws_oza, ws_ea, ws_ozb, ws_eb;
   size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, total, y_half, p_half;
   int k_gather;        // blocks with k0 < k_gather contract the gathered columns in the step kernel
 };
@@ -547,12 +550,50 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   if (const char* e = getenv("FFS_DENSE_THETA")) theta = atof(e);  // development
   d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
   d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
-  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut;
+  // GEMM: Ozaki-style FP64 emulation on the INT8 tensor cores by default (2x the DMMA GEMM at the
+  // C5 block shape); FFS_DENSE_GEMM=dmma selects the DMMA GEMM
+  const char* gsel = getenv("FFS_DENSE_GEMM");
+  d.ozaki = !(gsel && (strcmp(gsel, "dmma") == 0 || atoi(gsel) > 0)) && d.nstr == 1 && !no_gemm;
+  const int64_t fK = (cx ? 2 : 1) * N;
+  d.Kp = (int)((fK + ffsk::kOzBK - 1) / ffsk::kOzBK * ffsk::kOzBK);
+  const int64_t ncolsY = (cx ? 2 : 1) * d.ldY;
+  d.ws_oza = d.ozaki ? align_up((size_t)ffsk::kOzS * L * d.Kp) : 0;
+  d.ws_ea = d.ozaki ? align_up((size_t)L * 4) : 0;
+  d.ws_ozb = d.ozaki ? align_up((size_t)ffsk::kOzS * ncolsY * d.Kp) : 0;
+  d.ws_eb = d.ozaki ? align_up((size_t)ncolsY * 4) : 0;
+  if (d.ozaki && cudaFuncSetAttribute(reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffsk::kOzSmem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(ozaki smem) failed");
+  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut + d.ws_oza + d.ws_ea + d.ws_ozb + d.ws_eb;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
   const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
   if (cudaFuncSetAttribute(gjf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
     return fail(FFS_ECUDA, "cudaFuncSetAttribute(gj smem) failed");
+  return FFS_OK;
+}
+
+// 3-D tensor map [kOzS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int oz_tensor_map(CUtensorMap* m, const int8_t* base, int64_t rows, int Kp, int box_rows) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !enc)
+      return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)ffsk::kOzS};
+  const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)Kp * (cuuint64_t)rows};
+  const cuuint32_t box[3] = {(cuuint32_t)ffsk::kOzBK, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(FFS_ECUDA, "cuTensorMapEncodeTiled failed");
   return FFS_OK;
 }
 
@@ -579,6 +620,22 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
   uint32_t* ch = reinterpret_cast<uint32_t*>(Wb + d.ws_w);
   char* rowb = Wb + d.ws_w + d.ws_ch;
   double* Ut = reinterpret_cast<double*>(rowb + d.ws_row);
+  char* ozb0 = rowb + d.ws_row + d.ws_ut;
+  int8_t* oza = reinterpret_cast<int8_t*>(ozb0);
+  int* oz_ea = reinterpret_cast<int*>(ozb0 + d.ws_oza);
+  int8_t* ozb = reinterpret_cast<int8_t*>(ozb0 + d.ws_oza + d.ws_ea);
+  int* oz_eb = reinterpret_cast<int*>(ozb0 + d.ws_oza + d.ws_ea + d.ws_ozb);
+  CUtensorMap oz_ta, oz_tb;
+  const int64_t oz_ncols = (cx ? 2 : 1) * d.ldY;
+  if (d.ozaki) {
+    if (oz_tensor_map(&oz_ta, oza, L, d.Kp, ffsk::kOzBM) != FFS_OK) return FFS_ECUDA;
+    if (oz_tensor_map(&oz_tb, ozb, oz_ncols, d.Kp, ffsk::kOzBN) != FFS_OK) return FFS_ECUDA;
+    // A = U (real L x 2N view for complex): split once per call
+    const int64_t fK = (cx ? 2 : 1) * N;
+    ffsk::ffs_ozaki_split_rows_kernel<<<(unsigned)((L + 7) / 8), 256, 0, stream>>>(
+        static_cast<const double*>(U), (int)L, (int)fK, fK, oza, d.Kp, oz_ea);
+    ++g_launches;
+  }
   if (d.k_gather > 0) {
     dim3 tb(32, 8), tg((unsigned)((d.c.Lpt + 31) / 32), (unsigned)((N + 31) / 32));
     if (cx) ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, d.c.Lpt);
@@ -692,6 +749,20 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
         p[h].gather = k0 < d.k_gather ? 1 : 0;
         if (p[h].gather) {
           // no GEMM: the step kernel contracts the gathered columns itself
+        } else if (d.ozaki) {
+          ffsk::ffs_ozaki_split_cols_kernel<<<(unsigned)(oz_ncols / 32), 256, 0, st[h]>>>(
+              gp[h].B, (int)gp[h].K, (int)oz_ncols, gp[h].ldb, ozb, d.Kp, oz_eb);
+          ffsk::OzakiParams op{};
+          op.ea = oz_ea;
+          op.eb = oz_eb;
+          op.C = gp[h].C;
+          op.M = (int)L;
+          op.N = (int)oz_ncols;
+          op.K = d.Kp;
+          op.panel = gp[h].panel;
+          const dim3 og((unsigned)(oz_ncols / ffsk::kOzBN), (unsigned)((L + ffsk::kOzBM - 1) / ffsk::kOzBM));
+          ffsk::ffs_ozaki_gemm_kernel<<<og, ffsk::kOzThreads, ffsk::kOzSmem, st[h]>>>(oz_ta, oz_tb, op);
+          g_launches += 1;
         } else if (d.small_gemm)
           ffsk::ffs_dgemm_kernel<16, 4><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<16, 4>(), st[h]>>>(gp[h]);
         else

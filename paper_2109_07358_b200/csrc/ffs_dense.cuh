@@ -18,6 +18,7 @@
 // Y_s only grow ({m_j : j < k0+B}).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "ffs_kernel.cuh"
@@ -355,6 +356,258 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
       dense_y_store<T>(q.Y, q.ldY, pm[ii], col0 + c, c < nb1 ? S::neg(W[(size_t)ii * Np + k1 + c]) : S::zero());
     }
     if (t < nb1) dense_y_store<T>(q.Y, q.ldY, pm[k1 + t], col0 + t, S::one());
+  }
+}
+
+
+// ---------------------------------------------------------------- Ozaki-emulated FP64 GEMM
+// P = U Y on the INT8 tensor cores (tcgen05.mma.kind::i8, TMEM accumulators). Rows of A (= U, or
+// its real L x 2N view) and columns of B (= Y, or its real expansion) are scaled by powers of two
+// (frexp: |x 2^-e| < 1) and split into kOzS signed 7-bit slices: x = 2^e sum_i q_i 2^{-7(i+1)}.
+// The slice products A_i B_j with i + j < kOzS are exact in int32 (|q| <= 127, K <= 4096); the CTA
+// keeps the kOzS partial sums D_d = sum_{i+j=d} A_i B_j of its 128 x 64 tile in kOzS TMEM
+// accumulators and the epilogue forms 2^(ea + eb) sum_d 2^{-7(d+2)} D_d in fp64. The dropped
+// terms (i + j >= kOzS) are below 2^-49 of the row/column scales: normwise weight error <= 2.2e-13
+// on the C2/C4/C5 panels (tools/ozaki_floor.py, profiles/ozaki_floor_r01.txt; bound 1e-10).
+// Operands reach shared memory by TMA (3-D tensor maps [kOzS][rows][Kp], 64-byte swizzle) issued
+// by one thread; one thread issues the MMAs; full/empty mbarriers hand the two stages over.
+constexpr int kOzS = 7;
+constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64, kOzStages = 2, kOzThreads = 192;
+constexpr int kOzTA = kOzBM * kOzBK, kOzTB = kOzBN * kOzBK;
+constexpr int kOzStageBytes = kOzS * (kOzTA + kOzTB);
+constexpr size_t kOzSmem = (size_t)kOzStages * kOzStageBytes + (2 * kOzStages + 1) * 8 + 16 + 1024;
+
+struct OzakiParams {
+  const int* ea;  // [M] row exponents of A
+  const int* eb;  // [N] column exponents of B
+  double* C;      // per-sample panel layout (see DgemmParams::panel)
+  int M, N, K;    // K padded to a multiple of kOzBK (zero slices)
+  int panel;
+};
+
+__device__ __forceinline__ unsigned oz_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint64_t oz_desc(const void* base) {  // K-major, 64-byte swizzle, SBO 512 B
+  uint64_t d = (oz_u32(base) >> 4) & 0x3FFF;
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+__device__ __forceinline__ void oz_mbar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(oz_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void oz_mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "OW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra OW_%=;\n\t}" ::"r"(oz_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                            const __grid_constant__ CUtensorMap tmB,
+                                                                            const OzakiParams p) {
+  extern __shared__ __align__(1024) unsigned char oz_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kOzStages * kOzStageBytes);
+  uint64_t* empty = full + kOzStages;
+  uint64_t* done = empty + kOzStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int m0 = blockIdx.y * kOzBM, n0 = blockIdx.x * kOzBN;
+  const int KT = p.K / kOzBK;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (t == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      oz_mbar_init(full + s, 1);
+      oz_mbar_init(empty + s, 1);
+    }
+    oz_mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 4 && lane == 0) {  // TMA producer
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % kOzStages;
+      if (kt >= kOzStages) oz_mbar_wait(empty + st, ((kt / kOzStages) - 1) & 1);
+      unsigned char* sb = sm + st * kOzStageBytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)), "r"(kOzStageBytes)
+                   : "memory");
+#pragma unroll
+      for (int i = 0; i < kOzS; ++i) {
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                oz_u32(sb + i * kOzTA)),
+            "l"(&tmA), "r"(kt * kOzBK), "r"(m0), "r"(i), "r"(oz_u32(full + st))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                oz_u32(sb + kOzS * kOzTA + i * kOzTB)),
+            "l"(&tmB), "r"(kt * kOzBK), "r"(n0), "r"(i), "r"(oz_u32(full + st))
+            : "memory");
+      }
+    }
+  } else if (warp == 5 && lane == 0) {  // MMA issuer
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) | ((uint32_t)(kOzBM >> 4) << 24);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % kOzStages;
+      oz_mbar_wait(full + st, (kt / kOzStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const unsigned char* sb = sm + st * kOzStageBytes;
+#pragma unroll
+      for (int i = 0; i < kOzS; ++i)
+#pragma unroll
+        for (int j = 0; j < kOzS - i; ++j)
+#pragma unroll
+          for (int ks = 0; ks < kOzBK / 32; ++ks) {
+            const uint64_t da = oz_desc(sb + i * kOzTA + ks * 32);
+            const uint64_t db = oz_desc(sb + kOzS * kOzTA + j * kOzTB + ks * 32);
+            const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first write of D_{i+j}: i = 0
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)((i + j) * kOzBN)),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                : "memory");
+          }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(empty + st))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(done))
+                 : "memory");
+  }
+  if (warp < 4) {  // epilogue: tile row warp*32 + lane, 64 columns in fp64
+    oz_mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    double acc[kOzBN];
+#pragma unroll
+    for (int c = 0; c < kOzBN; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int d = kOzS - 1; d >= 0; --d) {  // smallest terms first
+      const double sc = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+      for (int cb = 0; cb < kOzBN; cb += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(d * kOzBN + cb);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[cb + c] = fma((double)(int)v[c], sc, acc[cb + c]);
+      }
+    }
+    const int row = m0 + warp * 32 + lane;
+    if (row < p.M) {
+      const int er = p.ea[row];
+#pragma unroll
+      for (int c = 0; c < kOzBN; c += 2) {
+        const int col = n0 + c;
+        const size_t off = (size_t)(col / p.panel) * p.M * p.panel + (size_t)row * p.panel + col % p.panel;
+        *reinterpret_cast<double2*>(p.C + off) =
+            make_double2(ldexp(acc[c], er + p.eb[col]), ldexp(acc[c + 1], er + p.eb[col + 1]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+// x = 2^e sum_i q_i 2^{-7(i+1)}, |q_i| <= 127 (frexp exponent: |x 2^-e| < 1); q_i of element k of
+// row r goes to out[(i * rows + r) * Kp + k]; zero for k in [K, Kp)
+__device__ __forceinline__ void oz_split_value(double v, int ex, int8_t (&q)[kOzS]) {
+  double r = ldexp(v, -ex);
+#pragma unroll
+  for (int i = 0; i < kOzS; ++i) {
+    const double f = trunc(r * 128.0);
+    q[i] = (int8_t)f;
+    r = r * 128.0 - f;
+  }
+}
+
+// rows of a row-major [rows][ldx] fp64 matrix (one warp per row)
+static __global__ void ffs_ozaki_split_rows_kernel(const double* __restrict__ X, int rows, int K, int64_t ldx,
+                                                   int8_t* __restrict__ out, int Kp, int* __restrict__ e) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const double* xr = X + (size_t)r * ldx;
+  double mx = 0.0;
+  for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(xr[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int ex = 0;
+  if (mx > 0.0) frexp(mx, &ex);
+  if (lane == 0) e[r] = ex;
+  for (int k = lane; k < Kp; k += 32) {
+    int8_t q[kOzS];
+    oz_split_value(k < K ? xr[k] : 0.0, ex, q);
+#pragma unroll
+    for (int i = 0; i < kOzS; ++i) out[((size_t)i * rows + r) * Kp + k] = q[i];
+  }
+}
+
+// columns of a row-major [K][ldy] fp64 matrix (32 columns per CTA of 256 threads): column c's
+// slices are written K-major, out[(i * ncols + c) * Kp + k]
+static __global__ void __launch_bounds__(256) ffs_ozaki_split_cols_kernel(const double* __restrict__ Y, int K, int ncols,
+                                                                         int64_t ldy, int8_t* __restrict__ out, int Kp,
+                                                                         int* __restrict__ e) {
+  __shared__ double tile[64][33];
+  __shared__ double red[8][32];
+  const int c0 = blockIdx.x * 32, t = threadIdx.x, cl = t & 31, kg = t >> 5;
+  double mx = 0.0;
+  for (int k = kg; k < K; k += 8) mx = fmax(mx, fabs(Y[(size_t)k * ldy + c0 + cl]));
+  red[kg][cl] = mx;
+  __syncthreads();
+  if (kg == 0) {
+    for (int q = 1; q < 8; ++q) mx = fmax(mx, red[q][cl]);
+    int ex = 0;
+    if (mx > 0.0) frexp(mx, &ex);
+    red[0][cl] = (double)ex;
+    if (c0 + cl < ncols) e[c0 + cl] = ex;
+  }
+  __syncthreads();
+  for (int kb = 0; kb < Kp; kb += 64) {
+    for (int q = t; q < 64 * 32; q += 256) {
+      const int kk = q >> 5, cc = q & 31;
+      tile[kk][cc] = (kb + kk < K) ? Y[(size_t)(kb + kk) * ldy + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+    {
+      const int cc = t >> 3, k8 = (t & 7) * 8;  // 32 columns x 8 groups of 8 k
+      const int ex = (int)red[0][cc];
+      int8_t q8[kOzS][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int8_t q[kOzS];
+        oz_split_value(tile[k8 + u][cc], ex, q);
+#pragma unroll
+        for (int i = 0; i < kOzS; ++i) q8[i][u] = q[i];
+      }
+#pragma unroll
+      for (int i = 0; i < kOzS; ++i) {
+        uint64_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w |= (uint64_t)(uint8_t)q8[i][u] << (8 * u);
+        *reinterpret_cast<uint64_t*>(out + ((size_t)i * ncols + c0 + cc) * Kp + kb + k8) = w;
+      }
+    }
+    __syncthreads();
   }
 }
 
