@@ -542,18 +542,19 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
   d.ws_w = align_up((size_t)d.nstr * d.Sh * Np * Np * es);
   d.ws_ch = align_up((size_t)d.nstr * d.Sh * (d.c.Lpt / 32) * 4);
   d.ws_row = align_up((size_t)d.nstr * d.Sh * (d.c.B * d.c.B + d.c.B) * es);
-  // hybrid: while k0 is small the gathered contraction (L k0 B per sample, from the transposed U)
-  // costs less than the GEMM's full-N one (L N B); crossover measured on C4/C5
-  // (measured optimum: C5 real 0.3 -> 1.35 s vs 1.51 s dense-only; C4 complex 0.6 -> 1.19 s vs
-  // 1.52 s; complex contractions do 2x the flops per gathered byte, so gathering pays longer)
-  double theta = cx ? 0.6 : 0.3;
-  if (const char* e = getenv("FFS_DENSE_THETA")) theta = atof(e);  // development
-  d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
-  d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
   // GEMM: Ozaki-style FP64 emulation on the INT8 tensor cores by default (2x the DMMA GEMM at the
   // C5 block shape); FFS_DENSE_GEMM=dmma selects the DMMA GEMM
   const char* gsel = getenv("FFS_DENSE_GEMM");
   d.ozaki = !(gsel && (strcmp(gsel, "dmma") == 0 || atoi(gsel) > 0)) && d.nstr == 1 && !no_gemm;
+  // hybrid: while k0 is small the gathered contraction (L k0 B per sample, from the transposed U)
+  // costs less than the GEMM's full-N one (L N B); crossover measured on C4/C5:
+  // Ozaki GEMM: C5 0.15-0.2 -> 0.97 s (1.01 s at 0), C4 0.35-0.4 -> 0.94 s (0.99 s at 0.6);
+  // DMMA GEMM: C5 0.3 -> 1.35 s, C4 0.6 -> 1.19 s. Complex contractions do 2x the flops per
+  // gathered byte, so gathering pays longer.
+  double theta = d.ozaki ? (cx ? 0.35 : 0.15) : (cx ? 0.6 : 0.3);
+  if (const char* e = getenv("FFS_DENSE_THETA")) theta = atof(e);  // development
+  d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
+  d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
   const int64_t fK = (cx ? 2 : 1) * N;
   d.Kp = (int)((fK + ffsk::kOzBK - 1) / ffsk::kOzBK * ffsk::kOzBK);
   const int64_t ncolsY = (cx ? 2 : 1) * d.ldY;

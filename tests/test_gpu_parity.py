@@ -209,11 +209,13 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
 
 
 # Lockstep-dense path schedules (ffs_abi.cu launch_dense): several batches with a ragged last one
-# (FFS_DENSE_S), all-GEMM (theta 0), all-gathered (theta 1) and the default hybrid; real and
-# complex; the environment is read per call, so each case runs the same kernels in another order.
+# (FFS_DENSE_S), all-GEMM (theta 0; Ozaki-emulated GEMM by default, the DMMA GEMM with
+# FFS_DENSE_GEMM=dmma), all-gathered (theta 1) and the default hybrid; real and complex; the
+# environment is read per call, so each case runs the same kernels in another order.
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("env", [{"FFS_DENSE_S": "16"}, {"FFS_DENSE_THETA": "0"}, {"FFS_DENSE_THETA": "1"},
-                                 {"FFS_DENSE_S": "7", "FFS_DENSE_THETA": "0.5"}])
+                                 {"FFS_DENSE_S": "7", "FFS_DENSE_THETA": "0.5"},
+                                 {"FFS_DENSE_THETA": "0", "FFS_DENSE_GEMM": "dmma"}])
 def test_dense_path_schedules(env, cplx, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
