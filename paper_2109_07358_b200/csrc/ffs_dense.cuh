@@ -514,13 +514,21 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
     }
     const int row = m0 + warp * 32 + lane;
     if (row < p.M) {
+      // 2^(ea + eb) as one multiply by an exact power of two built from its biased exponent
+      // (ldexp outside the normal range); panel (8 or 16) is a power of two
       const int er = p.ea[row];
+      const int lp = __ffs(p.panel) - 1;
+      double* crow = p.C + (size_t)row * p.panel;
+      const size_t sstride = (size_t)p.M * p.panel;
 #pragma unroll
       for (int c = 0; c < kOzBN; c += 2) {
         const int col = n0 + c;
-        const size_t off = (size_t)(col / p.panel) * p.M * p.panel + (size_t)row * p.panel + col % p.panel;
-        *reinterpret_cast<double2*>(p.C + off) =
-            make_double2(ldexp(acc[c], er + p.eb[col]), ldexp(acc[c + 1], er + p.eb[col + 1]));
+        const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
+        const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;  // biased exponents
+        const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
+        const double s1 = (b1 > 0 && b1 < 2047) ? __longlong_as_double((long long)b1 << 52) : ldexp(1.0, er + e2.y);
+        *reinterpret_cast<double2*>(crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1))) =
+            make_double2(acc[c] * s0, acc[c + 1] * s1);
       }
     }
   }
