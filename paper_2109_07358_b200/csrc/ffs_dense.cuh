@@ -372,7 +372,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
 // Operands reach shared memory by TMA (3-D tensor maps [kOzS][rows][Kp], 64-byte swizzle) issued
 // by one thread; one thread issues the MMAs; full/empty mbarriers hand the two stages over.
 constexpr int kOzS = 7;
-constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64, kOzStages = 2, kOzThreads = 192;
+constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64, kOzStages = 2, kOzThreads = 320;  // 8 epilogue warps + TMA + MMA
 constexpr int kOzTA = kOzBM * kOzBK, kOzTB = kOzBN * kOzBK;
 constexpr int kOzStageBytes = kOzS * (kOzTA + kOzTB);
 constexpr size_t kOzSmem = (size_t)kOzStages * kOzStageBytes + (2 * kOzStages + 1) * 8 + 16 + 1024;
@@ -436,7 +436,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (warp == 4 && lane == 0) {  // TMA producer
+  if (warp == 8 && lane == 0) {  // TMA producer
     for (int kt = 0; kt < KT; ++kt) {
       const int st = kt % kOzStages;
       if (kt >= kOzStages) oz_mbar_wait(empty + st, ((kt / kOzStages) - 1) & 1);
@@ -457,7 +457,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
             : "memory");
       }
     }
-  } else if (warp == 5 && lane == 0) {  // MMA issuer
+  } else if (warp == 9 && lane == 0) {  // MMA issuer
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) | ((uint32_t)(kOzBM >> 4) << 24);
     for (int kt = 0; kt < KT; ++kt) {
       const int st = kt % kOzStages;
@@ -486,19 +486,21 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(done))
                  : "memory");
   }
-  if (warp < 4) {  // epilogue: tile row warp*32 + lane, 64 columns in fp64
+  if (warp < 8) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. (tile rows), columns 32 (w / 4) ..
     oz_mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    double acc[kOzBN];
+    constexpr int kEC = kOzBN / 2;  // columns per epilogue warp
+    const int q = warp & 3, ch = (warp >> 2) * kEC;
+    double acc[kEC];
 #pragma unroll
-    for (int c = 0; c < kOzBN; ++c) acc[c] = 0.0;
+    for (int c = 0; c < kEC; ++c) acc[c] = 0.0;
 #pragma unroll
     for (int d = kOzS - 1; d >= 0; --d) {  // smallest terms first
       const double sc = ldexp(1.0, -7 * (d + 2));
-#pragma unroll
-      for (int cb = 0; cb < kOzBN; cb += 32) {
+      {
+        constexpr int cb = 0;
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(d * kOzBN + cb);
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * kOzBN + ch);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
             "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -512,7 +514,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
         for (int c = 0; c < 32; ++c) acc[cb + c] = fma((double)(int)v[c], sc, acc[cb + c]);
       }
     }
-    const int row = m0 + warp * 32 + lane;
+    const int row = m0 + q * 32 + lane;
     if (row < p.M) {
       // 2^(ea + eb) as one multiply by an exact power of two built from its biased exponent
       // (ldexp outside the normal range); panel (8 or 16) is a power of two
@@ -521,8 +523,8 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
       double* crow = p.C + (size_t)row * p.panel;
       const size_t sstride = (size_t)p.M * p.panel;
 #pragma unroll
-      for (int c = 0; c < kOzBN; c += 2) {
-        const int col = n0 + c;
+      for (int c = 0; c < kEC; c += 2) {
+        const int col = n0 + ch + c;
         const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
         const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;  // biased exponents
         const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
