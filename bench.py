@@ -299,7 +299,7 @@ def ffs_path_kernel(cfg, Np, cplx):
         if Np < cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
             return "step path (marginal): ffs_cluster_kernel<STEP> (gathered contraction) + ffs_dense_gj_kernel per block"
         if Np == cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
-            return ("dense path (hybrid): ffs_cluster_kernel<STEP> (+ ffs_dgemm_kernel for k0 >= theta N') "
+            return ("dense path (hybrid): ffs_cluster_kernel<STEP> (+ ffs_ozaki_gemm_kernel for k0 >= theta N') "
                     "+ ffs_dense_gj_kernel per block")
         return "ffs_cluster_kernel"
     return "ffs_sample_kernel"
