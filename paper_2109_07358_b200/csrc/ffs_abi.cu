@@ -579,14 +579,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 int oz_tensor_map(CUtensorMap* m, const int8_t* base, int64_t rows, int Kp, int box_rows) {
-  static EncodeTiledFn enc = nullptr;
-  if (!enc) {
+  // resolved once (thread-safe function-local static)
+  static const EncodeTiledFn enc = [] {
+    void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        !enc)
-      return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) fn = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  if (!enc) return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)ffsk::kOzS};
   const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)Kp * (cuuint64_t)rows};
   const cuuint32_t box[3] = {(cuuint32_t)ffsk::kOzBK, (cuuint32_t)box_rows, 1};
