@@ -270,3 +270,18 @@ def test_degenerate_marginals(L, N, Np, cplx):
         for s in range(2):
             ref_w = np.abs(U[:, m1[s]]) ** 2
             assert np.max(np.abs(gw[s, 0] - ref_w / ref_w.sum())) <= 1e-13
+
+
+# Large-L full sampling with very few samples (a batch far below the GEMM's 128-column tile) and
+# with an odd N (not dense-eligible: the per-sample cluster kernel).
+@pytest.mark.parametrize("L,N,M,cplx", [(2100, 256, 1, False), (2100, 256, 3, True), (2100, 257, 5, False)])
+def test_large_L_small_batches(L, N, M, cplx):
+    U = inputs.random_orthonormal(L, N, 3 * L + N + M, complex_=cplx)
+    uni = inputs.uniforms(M, N, 99 + M)
+    gpos, gflags, gw = run_gpu(U, uni, N, trace_S=1)
+    rpos = ref.sample(U, uni, Np=N)
+    r = compare_positions(U, uni, gpos, rpos, N)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    _, rw = ref.weights(U, uni[:1], Np=N)
+    assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
