@@ -74,18 +74,21 @@ static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, i
                                    int N, int Np) {
   extern __shared__ int pscratch[];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int* m = pscratch + (size_t)threadIdx.x * N;  // [blockDim][N] scratch (N <= 64); else global
+  // per-thread working permutation, interleaved across the block ([N][blockDim]): the threads of
+  // a warp touch 32 consecutive words (no bank conflicts)
+  int* m = pscratch + threadIdx.x;
+  const int bs = blockDim.x;
   if (i >= M) return;
-  for (int j = 0; j < N; ++j) m[j] = j;
+  for (int j = 0; j < N; ++j) m[j * bs] = j;
   const double* u = uniforms + i * 2 * (int64_t)Np;
   for (int j = 0; j < Np; ++j) {
     const int n = N - j;
     int r = (int)floor(u[j] * (double)n);
     r = (r > n - 1 ? n - 1 : r) + j;
-    const int a = m[j];
-    m[j] = m[r];
-    m[r] = a;
-    perm[i * Np + j] = m[j];
+    const int a = m[j * bs];
+    const int b = m[r * bs];
+    m[r * bs] = a;
+    perm[i * Np + j] = b;
   }
 }
 
