@@ -332,18 +332,21 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
         dst[0] = a[0];
       }
     };
-    int ii = part;
-    for (; ii + 4 * (UNR - 1) < k0; ii += 4 * UNR) {
+    // rows part, part + 4, ... < k0 in REVERSE order: step (1) streamed them upwards, so the rows
+    // it read last are the ones most likely still in L2 (forward order re-reads a working set larger
+    // than L2 in LRU's worst order)
+    int m = ((k0 - part + 3) >> 2) - 1;
+    for (; m >= UNR - 1; m -= UNR) {
       T a[UNR][CPT];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) ldw(ii + 4 * u, a[u]);
+      for (int u = 0; u < UNR; ++u) ldw(part + 4 * (m - u), a[u]);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) upd(ii + 4 * u, a[u]);
+      for (int u = 0; u < UNR; ++u) upd(part + 4 * (m - u), a[u]);
     }
-    for (; ii < k0; ii += 4) {
+    for (; m >= 0; --m) {
       T a[CPT];
-      ldw(ii, a);
-      upd(ii, a);
+      ldw(part + 4 * m, a);
+      upd(part + 4 * m, a);
     }
   }
   // next block's Y_s columns (the tile holding columns k1 .. k1+B-1)
