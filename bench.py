@@ -122,7 +122,11 @@ def cpu_oracle_rate(U, uni, Np, budget_s=15.0, max_samples=None):
     """Oracle samples/s on a bounded prefix of the workload (host cores, OpenMP)."""
     from oracle import ref
     ref.lib()
-    n = max(1, ref.num_threads())  # one sample per host thread first (C5: ~50 s per sample-thread)
+    L = U.shape[0]
+    work = (4 if np.iscomplexobj(U) else 1) * (L * Np * Np + Np ** 3)
+    # one sample per host thread first, except where one sample is already ~10+ s of CPU work
+    # (C5 full: 1.8e10 flop per sample; 16 concurrent samples took 217 s, memory-bound)
+    n = 1 if work > 8e9 else max(1, ref.num_threads())
     t_used = 0.0
     while True:
         n = min(n, uni.shape[0] if max_samples is None else min(uni.shape[0], max_samples))
@@ -133,7 +137,7 @@ def cpu_oracle_rate(U, uni, Np, budget_s=15.0, max_samples=None):
             t_used = t
             break
         n = int(n * max(2.0, min(16.0, (budget_s / 4) / max(t, 1e-3))))
-    return n / t_used, n, t_used, ref.num_threads()
+    return n / t_used, n, t_used, min(n, ref.num_threads())  # threads actually used (OpenMP over samples)
 
 
 def run_reference(args):
