@@ -280,6 +280,10 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
 #pragma unroll
     for (int tt = 0; tt < B; ++tt) Zp[(part * B + tt) * kGjTJ + jl + e] = acc[e][tt];
   __syncthreads();
+  // Vn is dead: stage Wb = W[0:k0, k0:k1] ([k0][B], the same size) in its place for step (3), whose
+  // per-row reads of it would otherwise be one dependent L2 round trip per row
+  T* Wb = Vn;
+  for (int idx = t; idx < k0 * B; idx += blockDim.x) Wb[idx] = W[(size_t)(idx / B) * Np + k0 + idx % B];
   // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
   if (t < kGjTJ && k1 + blockIdx.x * kGjTJ + t < Np) {
     const int c = t, jc = k1 + blockIdx.x * kGjTJ + c;
@@ -317,7 +321,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
 #pragma unroll
       for (int tt = 0; tt < B; ++tt) z[e][tt] = Zs[tt * kGjTJ + jl + e];
     auto upd = [&](int ii, T (&a)[CPT]) {
-      const T* wb = W + (size_t)ii * Np + k0;  // the same B scalars for every thread: L1 broadcast
+      const T* wb = Wb + (size_t)ii * B;  // the same B scalars for every thread of the warp: broadcast
 #pragma unroll
       for (int tt = 0; tt < B; ++tt) {
         const T wv = wb[tt];
