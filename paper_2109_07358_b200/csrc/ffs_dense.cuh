@@ -225,10 +225,23 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   if (t < B) xn[t] = q.positions[i_s * Np + k0 + t];
   if (t < B * B + B) RP[t] = reinterpret_cast<const T*>(q.rowg)[(size_t)sl * (B * B + B) + t];
   __syncthreads();
-  for (int idx = t; idx < B * k0; idx += blockDim.x) {
-    const int tt = idx / k0, ii = idx % k0;
-    Vn[idx] = Ug[(size_t)xn[tt] * N + pm[ii]];
-  }
+  // gathers in batches of 8 independent loads per thread (one latency per batch, not per element)
+  auto stage = [&](T* dst, int n, auto&& src) {
+    for (int b0 = t; b0 < n; b0 += 8 * (int)blockDim.x) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = b0 + u * (int)blockDim.x;
+        if (idx < n) v[u] = src(idx);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = b0 + u * (int)blockDim.x;
+        if (idx < n) dst[idx] = v[u];
+      }
+    }
+  };
+  stage(Vn, B * k0, [&](int idx) { return Ug[(size_t)xn[idx / k0] * N + pm[idx % k0]]; });
   __syncthreads();
   auto ldw = [&](int ii, T (&w)[CPT]) {
     const T* src = W + (size_t)ii * Np + j;
@@ -283,7 +296,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   // Vn is dead: stage Wb = W[0:k0, k0:k1] ([k0][B], the same size) in its place for step (3), whose
   // per-row reads of it would otherwise be one dependent L2 round trip per row
   T* Wb = Vn;
-  for (int idx = t; idx < k0 * B; idx += blockDim.x) Wb[idx] = W[(size_t)(idx / B) * Np + k0 + idx % B];
+  stage(Wb, k0 * B, [&](int idx) { return W[(size_t)(idx / B) * Np + k0 + idx % B]; });
   // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
   if (t < kGjTJ && k1 + blockIdx.x * kGjTJ + t < Np) {
     const int c = t, jc = k1 + blockIdx.x * kGjTJ + c;
