@@ -214,7 +214,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   const int j = k1 + blockIdx.x * kGjTJ + jl;     // first global column
   const bool has = j < Np;
   const bool full = j + CPT - 1 < Np;             // every column of the group in range
-  T* Vn = reinterpret_cast<T*>(smem);   // [B][k0]   V[X_new, 0:k0]
+  T* Vn = reinterpret_cast<T*>(smem);   // [k0][B]   V[X_new, 0:k0] transposed (a row's B values contiguous)
   T* Zp = Vn + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
   T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
   T* RP = Zs + B * kGjTJ;               // Row [B][B], Pinv [B]
@@ -241,7 +241,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
       }
     }
   };
-  stage(Vn, B * k0, [&](int idx) { return Ug[(size_t)xn[idx / k0] * N + pm[idx % k0]]; });
+  stage(Vn, B * k0, [&](int idx) { return Ug[(size_t)xn[idx % B] * N + pm[idx / B]]; });
   __syncthreads();
   auto ldw = [&](int ii, T (&w)[CPT]) {
     const T* src = W + (size_t)ii * Np + j;
@@ -274,7 +274,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
       for (int u = 0; u < UNR; ++u)
 #pragma unroll
         for (int tt = 0; tt < B; ++tt) {
-          const T vn = Vn[tt * k0 + ii + 4 * u];
+          const T vn = Vn[(ii + 4 * u) * B + tt];
 #pragma unroll
           for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(vn, w[u][e], acc[e][tt]);
         }
@@ -285,7 +285,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
 #pragma unroll
       for (int tt = 0; tt < B; ++tt)
 #pragma unroll
-        for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(Vn[tt * k0 + ii], w[e], acc[e][tt]);
+        for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(Vn[ii * B + tt], w[e], acc[e][tt]);
     }
   }
 #pragma unroll
