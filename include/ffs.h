@@ -28,9 +28,12 @@
  * re-entrant across streams with distinct workspaces. U orthonormality is the caller's
  * precondition and is not checked.
  *
- * Errors: FFS_EINVAL (synchronous) for null pointers when M > 0, N < 1, N > L, N' not in [1, N],
- * L > 2^31-1, unknown dtype, workspace too small, or a shape the kernels do not support
- * (see ffs_last_error()); FFS_ECUDA for CUDA launch/runtime errors. M == 0 is an OK no-op.
+ * Errors (all synchronous, message in ffs_last_error()): FFS_EINVAL for null pointers when M > 0,
+ * N < 1, N > L, N' not in [1, N], unknown dtype, or L beyond the supported range (L <= 16384 real,
+ * L <= 8192 complex: one sample's L x 8 panel must fit the register files of one thread-block
+ * cluster / one SM; larger L returns FFS_EINVAL, it is never truncated); FFS_ENOWS if the workspace
+ * is NULL or smaller than ffs_workspace_bytes(...); FFS_ECUDA for CUDA launch/runtime errors.
+ * M == 0 is an OK no-op.
  */
 #ifndef FFS_H
 #define FFS_H
@@ -52,32 +55,35 @@ typedef enum { FFS_OK = 0, FFS_EINVAL = -1, FFS_ECUDA = -2, FFS_ENOWS = -3 } ffs
  * 24 GB budget, at least 1024 and at most 8192, at most M), every batch sample's W, the coefficient
  * and panel matrices Y [N][8 S] and P [L][8 S] of the dense GEMM, U^T and the permutations: e.g.
  * 9.4 GB for the C5 config (L=16384, N=1024, M=1024), 20 GB for C4 (L=4096, N=512, c128). */
-size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M);
+size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M);
 
 /* Full sampling (N' = N): Eq. 1-3. uniforms [M][2N], positions [M][N]. */
-int ffs_sample(const void* U, int64_t L, int64_t N, int dtype, int64_t M,
+int ffs_sample(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M,
                const double* uniforms, int32_t* positions, int32_t* sample_flags,
                void* workspace, size_t ws_bytes, void* stream);
 
 /* Marginal sampling of N' <= N particles: the same chain stopped after N' steps.
  * uniforms [M][2N'], positions [M][N']. */
-int ffs_sample_marginal(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+int ffs_sample_marginal(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
                         const double* uniforms, int32_t* positions, int32_t* sample_flags,
                         void* workspace, size_t ws_bytes, void* stream);
 
-/* As ffs_sample_marginal, and also writes the normalised conditional weight vectors of the first
- * S samples along their own path: weights double[S][N'][L] (DEVICE), w(x)/T per step. */
-int ffs_debug_trace(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+/* As ffs_sample_marginal, and also writes the normalised conditional weight vectors (Eq. 3,
+ * w(x)/T per step) of samples S0 .. S0+S-1 along their own path: weights double[S][N'][L]
+ * (DEVICE). The traced samples run in the same launch configuration as every other sample, so a
+ * trace of the last samples checks the last tiles/clusters/batches. FFS_EINVAL if S0 < 0, S < 0 or
+ * S0 + S > M. */
+int ffs_debug_trace(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
                     const double* uniforms, int32_t* positions, int32_t* sample_flags,
-                    void* workspace, size_t ws_bytes, void* stream, int64_t S, double* weights);
+                    void* workspace, size_t ws_bytes, void* stream, int64_t S0, int64_t S, double* weights);
 
 /* Host-buffer entry point (end-to-end path): U, uniforms, positions, sample_flags are HOST
  * pointers (pinned memory recommended); the call copies inputs host->device, samples, copies the
  * results device->host and returns after the results are in host memory. `workspace` is a DEVICE
  * buffer of at least ffs_host_workspace_bytes(...) bytes. Samples are processed in chunks so that
  * the copies of one chunk overlap the sampling of another. */
-size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M);
-int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M);
+int ffs_sample_host(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
                     const double* uniforms, int32_t* positions, int32_t* sample_flags,
                     void* workspace, size_t ws_bytes, void* stream);
 
@@ -90,6 +96,32 @@ int ffs_last_launch_count(void);
  * (-1 if none). Per calling thread. */
 int ffs_profile_enable(int on);
 float ffs_last_kernel_ms(void);
+
+/* Tuning options (process-wide; read when a call plans its launch, so they apply to later calls).
+ * Defaults are the measured best; tests use them to drive every schedule of a path.
+ * ffs_set_option returns FFS_OK, or FFS_EINVAL for an unknown option; a NaN value restores the
+ * default. ffs_get_option returns the current value (NaN for an unknown option). */
+typedef enum {
+  FFS_OPT_DENSE_GEMM = 1,       /* full sampling at large L, blocks with k0 >= theta N': the GEMM P = U Y
+                                   8 = Ozaki FP64 emulation on the INT8 tensor cores, 8 slices (default;
+                                       normwise panel error <= 1.3e-15, fp64 level)
+                                   7 = the same with 7 slices (<= 2.2e-13)
+                                   0 = FP64 DMMA (mma.sync m8n8k4) */
+  FFS_OPT_DENSE_THETA = 2,      /* gathered/GEMM crossover fraction theta; < 0 = default */
+  FFS_OPT_DENSE_BATCH = 3,      /* samples per lockstep batch of the block-step paths; 0 = default */
+  FFS_OPT_BLOCK_STEP = 4,       /* 1 (default): L >= 2048, even N >= 256 on the block-step paths;
+                                   0: the per-sample cluster kernel */
+  FFS_OPT_LARGE_L_MARGINAL = 5, /* 1 (default): large-L marginals on the block-step kernels;
+                                   0: the per-sample cluster kernel */
+  FFS_OPT_CLUSTER = 6,          /* 1 (default): L >= 2048 on cluster kernels; 0: one CTA per sample */
+  FFS_OPT_GRAPH = 7,            /* 1 (default): the block-step paths' launches are captured once and
+                                   replayed as a CUDA graph (not while the caller's stream is being
+                                   captured); 0: direct launches */
+  FFS_OPT_FORCE_GENERIC = 8,    /* 1: every shape on the per-sample warp/CTA-owner kernel (testing) */
+  FFS_OPT_LAST = 8
+} ffs_option;
+int ffs_set_option(int option, double value);
+double ffs_get_option(int option);
 
 /* Thread-local message for the last non-OK return on this thread ("" if none). */
 const char* ffs_last_error(void);

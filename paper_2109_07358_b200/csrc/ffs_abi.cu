@@ -1,46 +1,66 @@
 // C ABI of libffs.so (declarations and contracts: include/ffs.h).
-// Argument validation, kernel-variant dispatch, workspace carving and the host-buffer path.
-// No torch types, no hidden allocations; everything runs in the kernels of ffs_kernel.cuh.
+// Argument validation, plan selection (cached per shape), workspace carving, the CUDA-graph
+// driver of the block-step paths, and the host-buffer path. No torch types and no hidden device
+// allocations; every step of the method runs in the kernels of ffs_*.cuh.
+#include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
-#include <cstring>
 #include <cstdlib>
+#include <cstring>
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
+#include <utility>
 
 #include "ffs.h"
+#include "ffs_host.h"
 #include "ffs_kernel.cuh"
 #include "ffs_warp_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
-#include "ffs_mma_kernel.cuh"
 #include "ffs_dense.cuh"
 #include "ffs_kptr.h"
 
+// ====================================================================== shared host helpers
+namespace ffsh {
 namespace {
-
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
-
-// Optional CUDA-event timing of the dominant (sampling) kernel of each call, on the launch stream.
 thread_local bool g_prof = false;
 thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
 thread_local bool g_ev_pending = false;
-unsigned long long* g_timing = nullptr;  // development: device counters for FFS_DEBUG_SKIP bit3
 
-cudaError_t launch_timed(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
-  if (g_prof) {
-    if (!g_ev0) {
-      cudaEventCreate(&g_ev0);
-      cudaEventCreate(&g_ev1);
-    }
-    cudaEventRecord(g_ev0, s);
+constexpr int kNumOpts = 16;
+// defaults of include/ffs.h ffs_option
+double default_option(int o) {
+  switch (o) {
+    case FFS_OPT_DENSE_GEMM: return 8.0;
+    case FFS_OPT_DENSE_THETA: return -1.0;
+    case FFS_OPT_DENSE_BATCH: return 0.0;
+    case FFS_OPT_BLOCK_STEP: return 1.0;
+    case FFS_OPT_LARGE_L_MARGINAL: return 1.0;
+    case FFS_OPT_CLUSTER: return 1.0;
+    case FFS_OPT_GRAPH: return 1.0;
+    case FFS_OPT_FORCE_GENERIC: return 0.0;
+    default: return 0.0;
   }
-  cudaError_t e = cudaLaunchKernel(fn, grid, block, args, smem, s);
-  if (g_prof && e == cudaSuccess) {
-    cudaEventRecord(g_ev1, s);
-    g_ev_pending = true;
-  }
-  return e;
 }
+struct Options {
+  std::atomic<double> v[kNumOpts];
+  std::atomic<uint64_t> version{1};
+  Options() {
+    for (int o = 0; o < kNumOpts; ++o) v[o].store(default_option(o));
+  }
+};
+Options& opts() {
+  static Options o;
+  return o;
+}
+std::mutex g_attr_mu;
+std::set<std::pair<int, const void*>> g_attr_done;
+}  // namespace
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -49,30 +69,106 @@ int fail(int code, const char* fmt, ...) {
   va_end(ap);
   return code;
 }
+void clear_error() { g_err[0] = 0; }
+int& launches() { return g_launches; }
+double option(int o) { return (o > 0 && o < kNumOpts) ? opts().v[o].load() : 0.0; }
+uint64_t options_version() { return opts().version.load(); }
 
-constexpr size_t kAlign = 256;
-size_t align_up(size_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
+int device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+int sm_count(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = sms;
+  return sms;
+}
+int ensure_max_smem(const void* fn) {
+  const int dev = device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done.count({dev, fn})) return FFS_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+  g_attr_done.insert({dev, fn});
+  return FFS_OK;
+}
 
-// ------------------------------------------------------------------ variant table
-// A variant is a kernel instantiation ffs_sample_kernel<T, WARP, R, B, USMEM>.
+bool profiling() { return g_prof; }
+void prof_begin(cudaStream_t s) {
+  if (!g_prof) return;
+  if (!g_ev0) {
+    cudaEventCreate(&g_ev0);
+    cudaEventCreate(&g_ev1);
+  }
+  cudaEventRecord(g_ev0, s);
+}
+void prof_end(cudaStream_t s) {
+  if (!g_prof) return;
+  cudaEventRecord(g_ev1, s);
+  g_ev_pending = true;
+}
+}  // namespace ffsh
+
+using ffsh::align_up;
+using ffsh::fail;
+using ffsh::kAlign;
+using ffsh::kMaxSmem;
+
+namespace {
+
+// ====================================================================== plan cache
+// Plans depend on the shape, M, the device and the tuning options; they are made once (with the
+// CUDA attribute / occupancy queries) and reused by every later call of the same shape.
+using PlanKey = std::tuple<int, int, int64_t, int64_t, int64_t, int64_t, int, uint64_t>;
+template <typename P>
+struct PlanCache {
+  std::mutex mu;
+  std::map<PlanKey, P> m;
+  template <typename F>
+  int get(const PlanKey& k, P& out, F&& make) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = m.find(k);
+      if (it != m.end()) {
+        out = it->second;
+        return FFS_OK;
+      }
+    }
+    int rc = make(out);
+    if (rc != FFS_OK) return rc;
+    std::lock_guard<std::mutex> lk(mu);
+    if (m.size() > 256) m.clear();
+    m[k] = out;
+    return FFS_OK;
+  }
+};
+PlanKey plan_key(int kind, int64_t L, int64_t N, int64_t Np, int64_t M, int dtype) {
+  return PlanKey{ffsh::device(), kind, L, N, Np, M, dtype, ffsh::options_version()};
+}
+
+// ------------------------------------------------------------------ generic per-sample kernel
+// ffs_sample_kernel<T, WARP, R, B, USMEM>: one warp (small L) or one CTA per sample.
 struct Variant {
-  bool warp;      // owner = one warp (true) or one CTA of G threads (false)
+  bool warp;      // owner = one warp (true) or one CTA (false)
   int R, B;       // rows per thread, panel width
   bool usmem;     // U^T held in shared memory (shared by all owners of a CTA)
   int maxt;       // __launch_bounds__ of the instantiation
   const void* fn; // kernel
 };
 
-// warp-owner kernels: up to kWarpMaxThreads threads (= owners x 32) per CTA
 constexpr int kWarpMaxThreads = 320;
 
 template <typename T, bool WARP, int R, int B, bool USMEM, int MAXT = kWarpMaxThreads>
 Variant make_variant() {
-  return Variant{WARP, R, B, USMEM, MAXT,
-                 ffsk::sample_kernel_ptr<T, WARP, R, B, USMEM, MAXT>()};
+  return Variant{WARP, R, B, USMEM, MAXT, ffsk::sample_kernel_ptr<T, WARP, R, B, USMEM, MAXT>()};
 }
-
-constexpr size_t kMaxSmem = 227 * 1024;
 
 struct Plan {
   Variant v;
@@ -87,7 +183,11 @@ struct Plan {
   size_t ws_ut, ws_wfull;  // workspace bytes
 };
 
-bool pick_variant(int L, int N, int Np, int dtype, Variant& v) {
+// The largest L each dtype supports on the per-sample kernels: the L x B panel of one sample
+// lives in one SM's register file (B = 1 at the limit).
+constexpr int64_t kMaxLReal = 16384, kMaxLComplex = 8192;
+
+bool pick_variant(int L, int N, int dtype, Variant& v) {
   const bool c = dtype == FFS_C128;
   const size_t es = c ? 16 : 8;
   // U^T in shared memory if the whole (padded) matrix takes <= 96 KB: one copy per CTA,
@@ -95,7 +195,7 @@ bool pick_variant(int L, int N, int Np, int dtype, Variant& v) {
   auto fits = [&](int R) { return (size_t)N * (size_t)(32 * R + 2) * es <= 96 * 1024; };
   // Warp owners (L <= 256 real / 128 complex): panel R x B per lane in registers.
   // CTA owners: one sample per CTA; the L x B panel must fit the SM's register file, so B
-  // shrinks as L grows (the large-L configs are register-capacity bound).
+  // shrinks as L grows.
   if (!c) {
     if (L <= 32)  { v = fits(1) ? make_variant<double, true, 1, 8, true>() : make_variant<double, true, 1, 8, false>(); return true; }
     if (L <= 64)  { v = fits(2) ? make_variant<double, true, 2, 8, true>() : make_variant<double, true, 2, 8, false>(); return true; }
@@ -104,16 +204,15 @@ bool pick_variant(int L, int N, int Np, int dtype, Variant& v) {
     if (L <= 1024)  { v = make_variant<double, false, 4, 8, false, 256>(); return true; }
     if (L <= 4096)  { v = make_variant<double, false, 4, 4, false, 1024>(); return true; }
     if (L <= 8192)  { v = make_variant<double, false, 8, 2, false, 1024>(); return true; }
-    if (L <= 16384) { v = make_variant<double, false, 16, 1, false, 1024>(); return true; }
+    if (L <= kMaxLReal) { v = make_variant<double, false, 16, 1, false, 1024>(); return true; }
   } else {
     if (L <= 32)  { v = fits(1) ? make_variant<cplx, true, 1, 4, true>() : make_variant<cplx, true, 1, 4, false>(); return true; }
     if (L <= 64)  { v = fits(2) ? make_variant<cplx, true, 2, 4, true>() : make_variant<cplx, true, 2, 4, false>(); return true; }
     if (L <= 128) { v = fits(4) ? make_variant<cplx, true, 4, 4, true>() : make_variant<cplx, true, 4, 4, false>(); return true; }
     if (L <= 1024)  { v = make_variant<cplx, false, 4, 4, false, 256>(); return true; }
     if (L <= 4096)  { v = make_variant<cplx, false, 4, 2, false, 1024>(); return true; }
-    if (L <= 8192)  { v = make_variant<cplx, false, 8, 1, false, 1024>(); return true; }
+    if (L <= kMaxLComplex) { v = make_variant<cplx, false, 8, 1, false, 1024>(); return true; }
   }
-  (void)Np;
   return false;
 }
 
@@ -134,19 +233,13 @@ size_t owner_bytes(bool c, int B, int N, int Np) {
   }
 }
 
-int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) {
-  if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0)
-    return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M=%lld", (long long)L, (long long)N,
-                (long long)Np, (long long)M);
-  if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
-  if (!pick_variant((int)L, (int)N, (int)Np, dtype, pl.v))
-    return fail(FFS_EINVAL, "unsupported L=%lld for dtype %d (max 16384)", (long long)L, dtype);
+int make_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) {
+  if (!pick_variant((int)L, (int)N, dtype, pl.v))
+    return fail(FFS_EINVAL, "unsupported L=%lld for dtype %d (max %lld real, %lld complex)", (long long)L, dtype,
+                (long long)kMaxLReal, (long long)kMaxLComplex);
   const bool c = dtype == FFS_C128;
   pl.es = c ? 16 : 8;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return fail(FFS_ECUDA, "cudaGetDevice failed");
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = ffsh::sm_count(ffsh::device());
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, pl.v.fn) != cudaSuccess) return fail(FFS_ECUDA, "cudaFuncGetAttributes failed");
   const int regs = std::max(fa.numRegs, 1);
@@ -156,7 +249,7 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
     pl.Lp = 32 * pl.v.R;
     pl.ut_stride = pl.Lp + (c ? 1 : 2);  // +16 B per column: spreads column bases over banks
     pl.ushared_smem = pl.v.usmem ? ffsk::align16((size_t)N * pl.ut_stride * pl.es) : 0;
-    // warps per CTA: bounded by registers (one CTA per SM when U^T is shared), smem, and 16
+    // warps per CTA: bounded by registers (one CTA per SM when U^T is shared), smem, and 10
     const int by_regs = std::max(1, 65536 / (((regs * 32 + 255) / 256) * 256));
     int w = std::min(pl.v.maxt / 32, by_regs);
     while (w > 1 && pl.ushared_smem + (size_t)w * pl.owner_smem > kMaxSmem) --w;
@@ -172,13 +265,11 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
     pl.ushared_smem = 0;
     pl.owners_per_cta = 1;
     pl.threads = pl.G;
-    if (pl.G > pl.v.maxt)
-      return fail(FFS_EINVAL, "variant needs %d threads > %d", pl.G, pl.v.maxt);
+    if (pl.G > pl.v.maxt) return fail(FFS_EINVAL, "variant needs %d threads > %d", pl.G, pl.v.maxt);
   }
   pl.smem = pl.ushared_smem + (size_t)pl.owners_per_cta * pl.owner_smem;
   if (pl.smem > kMaxSmem) return fail(FFS_EINVAL, "shared memory %zu > %zu (N=%lld)", pl.smem, kMaxSmem, (long long)N);
-  if (cudaFuncSetAttribute(pl.v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem=%zu) failed", pl.smem);
+  if (int rc = ffsh::ensure_max_smem(pl.v.fn)) return rc;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.v.fn, pl.threads, pl.smem) != cudaSuccess || per_sm < 1)
     return fail(FFS_EINVAL, "kernel does not fit on an SM (threads=%d smem=%zu regs=%d)", pl.threads, pl.smem, regs);
@@ -189,21 +280,26 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
   return FFS_OK;
 }
 
+PlanCache<Plan> g_plans;
+int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) {
+  return g_plans.get(plan_key(0, L, N, Np, M, dtype), pl,
+                     [&](Plan& p) { return make_plan_uncached(L, N, Np, dtype, M, p); });
+}
+
 // ------------------------------------------------------------------ fast warp-owner path
 // Real U, L <= 256, N' <= kMaxNpWarp, U^T small enough for shared memory: ffs_seg_kernel
 // (one CTA per SM, G-lane segments of warps = sample owners) after ffs_permute_kernel.
 struct WarpPlan {
   const void* fn;
   int R, B, S, G = 32, maxt, warps, grid, Lp, ut_stride;
-  bool mma = false;  // ffs_mma_kernel (DMMA contraction, B = 8, its own U^T swizzle and slice)
-  size_t ushared, owner, smem, ws_perm, ws_w = 0;
+  size_t ushared, owner, smem, ws_perm;
   int perm_tpb;
   size_t perm_smem;
 };
 
-template <int R, int B, int G, int MAXT, bool TIMING = false, int OPT = 0>
+template <int R, int B, int G, int MAXT>
 void warp_fn_seg(WarpPlan& w) {
-  w.fn = ffsk::seg_kernel_ptr<R, B, G, MAXT, TIMING, OPT>();
+  w.fn = ffsk::seg_kernel_ptr<R, B, G, MAXT>();
   w.R = R;
   w.B = B;
   w.S = 32 / G;  // samples per warp (one per G-lane segment)
@@ -212,60 +308,38 @@ void warp_fn_seg(WarpPlan& w) {
 }
 
 bool warp_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
+  if (ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0) return false;
   if (dtype != FFS_F64 || L > 256 || Np > ffsk::kMaxNpWarp || N > 4096) return false;
   return (size_t)N * (256 + 2) * 8 <= 100 * 1024;  // padded U^T fits shared memory
 }
 
-int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
-  const char* var = getenv("FFS_WARP_VARIANT");  // development: measured variants (profiles/)
-  {
-    // segmented kernel, OPT = 7 (+128 for G = 32): kept partial sums, pivot row through smem,
-    // flat Gauss-Jordan, no warp vote when the segment is the whole warp
-    // (variants measured in profiles/r01_ncu_summary.md; "base" = the first segmented kernel)
-    const bool base = var && strcmp(var, "base") == 0;
-    const size_t ush = ffsk::align16((size_t)N * (256 + 2) * 8);
-    const bool fits16 = ush + 16 * ffsk::WarpLayout((int)Np, 4, true).total <= kMaxSmem;
-    // L <= 16 (C1): 4-lane segments, 8 samples per warp (0.086 ms vs 0.092 ms with 8-lane segments)
-    if (L <= 16) warp_fn_seg<4, 4, 4, 512, false, 7>(w);
-    else if (L <= 32) warp_fn_seg<4, 4, 8, 512, false, 7>(w);
-    else if (L <= 64) warp_fn_seg<8, 4, 8, 384, false, 7>(w);
-    else if (L <= 128) warp_fn_seg<8, 4, 16, 384, false, 7>(w);
-    else if (base) warp_fn_seg<8, 4, 32, 384, false, 0>(w);
-    else if (var && strcmp(var, "o7_384") == 0) warp_fn_seg<8, 4, 32, 384, false, 7>(w);
-    else if (var && strcmp(var, "b8") == 0) warp_fn_seg<8, 8, 32, 256, false, 7>(w);
-    else if (var && strcmp(var, "o647") == 0) warp_fn_seg<8, 4, 32, 512, false, 647>(w);
-    else if (var && strcmp(var, "t") == 0) warp_fn_seg<8, 4, 32, 512, true, 7>(w);  // phase timing
-    else if (var && strncmp(var, "mma", 3) == 0) {
-      const bool t256 = strcmp(var, "mma256") == 0;
-      w.fn = t256 ? ffsk::mma_kernel_ptr<256>() : ffsk::mma_kernel_ptr<384>();
-      w.R = 8;
-      w.B = 8;
-      w.S = 1;
-      w.G = 32;
-      w.maxt = t256 ? 256 : 384;
-      w.mma = true;
-    }
-    else if (fits16) warp_fn_seg<8, 4, 32, 512, false, 135>(w);  // 16 owners/SM, 128 regs
-    else warp_fn_seg<8, 4, 32, 384, false, 135>(w);              // 12 owners/SM (larger N')
-  }
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return fail(FFS_ECUDA, "cudaGetDevice failed");
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+int make_warp_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
+  // segment width by L (measured: profiles/r01_ncu_summary.md); L <= 16 (C1): 4-lane segments,
+  // 8 samples per warp (0.086 ms vs 0.092 ms with 8-lane segments); 256 (C2): one sample per warp,
+  // 16 owners/SM at 128 registers (12 when 16 W slices do not fit shared memory)
+  const size_t ush = ffsk::align16((size_t)N * (256 + 2) * 8);
+  const bool fits16 = ush + 16 * ffsk::WarpLayout((int)Np, 4).total <= kMaxSmem;
+  if (L <= 16) warp_fn_seg<4, 4, 4, 512>(w);
+  else if (L <= 32) warp_fn_seg<4, 4, 8, 512>(w);
+  else if (L <= 64) warp_fn_seg<8, 4, 8, 384>(w);
+  else if (L <= 128) warp_fn_seg<8, 4, 16, 384>(w);
+  else if (fits16) warp_fn_seg<8, 4, 32, 512>(w);
+  else warp_fn_seg<8, 4, 32, 384>(w);
+  const int sms = ffsh::sm_count(ffsh::device());
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, w.fn) != cudaSuccess) return fail(FFS_ECUDA, "cudaFuncGetAttributes failed");
   w.Lp = w.G * w.R;
-  w.ut_stride = w.mma ? ffsk::kMmaRows : w.Lp + 2;
+  w.ut_stride = w.Lp + 2;
   w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
-  w.owner = w.mma ? ffsk::MmaLayout((int)Np).total
-                 : ffsk::WarpLayout((int)Np, w.B, true).total;  // per sample; a warp holds S slices
+  w.owner = ffsk::WarpLayout((int)Np, w.B).total;  // per sample; a warp holds S slices
   // registers are allocated per SM sub-partition (4 x 16K); warps are spread round-robin
   const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
   int warps = std::min(w.maxt / 32, by_regs);
   while (warps > 1 && w.ushared + (size_t)warps * w.S * w.owner > kMaxSmem) --warps;
-  if (const char* fw = getenv("FFS_WARPS")) warps = std::max(1, std::min(warps, atoi(fw)));  // development
   w.warps = warps;
   w.smem = w.ushared + (size_t)warps * w.S * w.owner;
   if (w.smem > kMaxSmem) return fail(FFS_EINVAL, "warp path smem %zu too large", w.smem);
+  if (int rc = ffsh::ensure_max_smem(w.fn)) return rc;
   const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
   w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
   w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
@@ -274,21 +348,25 @@ int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
   return FFS_OK;
 }
 
+PlanCache<WarpPlan> g_warp_plans;
+int make_warp_plan(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPlan& w) {
+  return g_warp_plans.get(plan_key(1, L, N, Np, M, FFS_F64), w,
+                          [&](WarpPlan& p) { return make_warp_plan_uncached(L, N, Np, M, p); });
+}
+
 int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, const double* uniforms,
-                int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
+                int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
                 double* trace) {
   WarpPlan w;
   int rc = make_warp_plan(L, N, Np, M, w);
   if (rc != FFS_OK) return rc;
-  if (!ws || ws_bytes < w.ws_perm + w.ws_w)
-    return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, w.ws_perm + w.ws_w);
+  if (!ws || ws_bytes < w.ws_perm)
+    return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, w.ws_perm);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   int32_t* perm = static_cast<int32_t*>(ws);
   const int64_t pgrid = (M + w.perm_tpb - 1) / w.perm_tpb;
   ffsk::ffs_permute_kernel<<<(unsigned)pgrid, w.perm_tpb, w.perm_smem, stream>>>(uniforms, perm, M, (int)N, (int)Np);
-  ++g_launches;
-  if (cudaFuncSetAttribute(w.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.smem) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem=%zu) failed", w.smem);
+  ++ffsh::launches();
   ffsk::WarpParams p{};
   p.U = static_cast<const double*>(U);
   p.perm = perm;
@@ -303,22 +381,17 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   p.ut_stride = w.ut_stride;
   p.ushared = w.ushared;
   p.owner_bytes = w.owner;
-  p.wfull = nullptr;
-  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.S0 = S0;
+  p.S = S > 0 ? S : 0;
   p.trace = S > 0 ? trace : nullptr;
-  const char* dbg = getenv("FFS_DEBUG_SKIP");  // development only: bits 0-2 break the results
-  p.dbg = dbg ? atoi(dbg) : 0;
-  p.timing = g_timing;
   void* args[] = {&p};
-  cudaError_t e = launch_timed(w.fn, dim3(w.grid), dim3(32 * w.warps), args, w.smem, stream);
+  ffsh::prof_begin(stream);
+  cudaError_t e = cudaLaunchKernel(w.fn, dim3(w.grid), dim3(32 * w.warps), args, w.smem, stream);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
-  ++g_launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
-  g_err[0] = 0;
+  ffsh::prof_end(stream);
+  ++ffsh::launches();
   return FFS_OK;
 }
-
 
 // ------------------------------------------------------------------ cluster-owner path
 // Large L (>= 2048): one thread-block cluster of CS CTAs per sample (ffs_cluster_kernel), the
@@ -329,66 +402,78 @@ struct ClusterPlan {
   size_t smem, ws_ut, ws_w;
 };
 
-template <typename T, int R, int B, int MAXT>
-void cluster_fn(ClusterPlan& c) {
-  c.fn = ffsk::cluster_kernel_ptr<T, R, B, MAXT>();
-  c.R = R;
-  c.B = B;
-  c.threads = MAXT;
-}
+constexpr int64_t kMaxLClusterReal = 16 * 512 * 4, kMaxLClusterComplex = 16 * 512 * 2;
 
 bool cluster_eligible(int64_t L, int dtype) {
-  const char* g = getenv("FFS_NO_CLUSTER");
-  if (g && g[0] == '1') return false;
-  return L >= 2048 && L <= (dtype == FFS_C128 ? 16 * 512 * 1 : 16 * 512 * 2);
+  if (ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0 || ffsh::option(FFS_OPT_CLUSTER) == 0.0) return false;
+  return L >= 2048 && L <= (dtype == FFS_C128 ? kMaxLClusterComplex : kMaxLClusterReal);
 }
 
-int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, ClusterPlan& c) {
-  const bool cx = dtype == FFS_C128;
-  const char* cv = getenv("FFS_CLUSTER_VARIANT");  // development: "b16" selects B=16 (slower)
-  const bool b8 = !(cv && strcmp(cv, "b16") == 0);
-  const bool t256 = cv && strcmp(cv, "t256") == 0;  // 256 threads x 2R rows (no spills; slower)
-  if (cx) {
-    if (!b8) cluster_fn<cplx, 1, 16, 512>(c);
-    else if (t256) cluster_fn<cplx, 4, 8, 256>(c);
-    else cluster_fn<cplx, 2, 8, 512>(c);
-  } else {
-    if (!b8) cluster_fn<double, 2, 16, 512>(c);
-    else if (t256) cluster_fn<double, 8, 8, 256>(c);
-    else cluster_fn<double, 4, 8, 512>(c);
-  }
-  c.es = cx ? 16 : 8;
-  const int rows_per_cta = c.threads * c.R;
-  c.CS = (int)((L + rows_per_cta - 1) / rows_per_cta);
-  if (c.CS < 2) c.CS = 2;
-  if (c.CS > 8) c.CS = 16;
-  c.Lc = rows_per_cta;
-  c.Lpt = c.CS * c.Lc;
-  if (cx)
-    c.smem = c.B == 8 ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np, c.threads, c.R).total
-                      : ffsk::ClusterLayout<cplx, 16>((int)N, (int)Np, c.threads, c.R).total;
-  else
-    c.smem = c.B == 8 ? ffsk::ClusterLayout<double, 8>((int)N, (int)Np, c.threads, c.R).total
-                      : ffsk::ClusterLayout<double, 16>((int)N, (int)Np, c.threads, c.R).total;
-  if (c.smem > kMaxSmem) return fail(FFS_EINVAL, "cluster path smem %zu > %zu (N'=%lld)", c.smem, kMaxSmem, (long long)Np);
-  if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(smem) failed");
-  if (c.CS > 8 && cudaFuncSetAttribute(c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+// cluster of CS CTAs of `threads` x R rows (CS = 2..8, or 16 with the non-portable size)
+int cluster_dims(int64_t L, int rows_per_cta, int& CS) {
+  CS = (int)((L + rows_per_cta - 1) / rows_per_cta);
+  if (CS < 2) CS = 2;
+  if (CS > 8) CS = 16;
+  return CS * rows_per_cta >= L ? FFS_OK : fail(FFS_EINVAL, "L=%lld exceeds a 16-CTA cluster", (long long)L);
+}
+
+int cluster_occupancy(const void* fn, int CS, int threads, size_t smem, int& maxcl) {
+  if (int rc = ffsh::ensure_max_smem(fn)) return rc;
+  if (CS > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
     return fail(FFS_ECUDA, "non-portable cluster size not allowed");
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = c.CS;
+  attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(c.threads);
-  cfg.gridDim = dim3(c.CS);
-  cfg.dynamicSmemBytes = c.smem;
+  cfg.blockDim = dim3(threads);
+  cfg.gridDim = dim3(CS);
+  cfg.dynamicSmemBytes = smem;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  maxcl = 0;
+  if (cudaOccupancyMaxActiveClusters(&maxcl, fn, &cfg) != cudaSuccess || maxcl < 1)
+    return fail(FFS_EINVAL, "cluster of %d CTAs does not fit", CS);
+  return FFS_OK;
+}
+
+cudaError_t launch_cluster_kernel(const void* fn, int CS, int grid, int threads, size_t smem, cudaStream_t s,
+                                  void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(threads);
+  cfg.gridDim = dim3(grid);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+int make_cluster_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, ClusterPlan& c) {
+  const bool cx = dtype == FFS_C128;
+  if (cx) {
+    c.fn = ffsk::cluster_kernel_ptr<cplx, 2, 8, 512>();
+    c.R = 2;
+  } else {
+    c.fn = ffsk::cluster_kernel_ptr<double, 4, 8, 512>();
+    c.R = 4;
+  }
+  c.B = 8;
+  c.threads = 512;
+  c.es = cx ? 16 : 8;
+  c.Lc = c.threads * c.R;
+  if (int rc = cluster_dims(L, c.Lc, c.CS)) return rc;
+  c.Lpt = c.CS * c.Lc;
+  c.smem = cx ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np).total : ffsk::ClusterLayout<double, 8>((int)N, (int)Np).total;
+  if (c.smem > kMaxSmem) return fail(FFS_EINVAL, "cluster path smem %zu > %zu (N'=%lld)", c.smem, kMaxSmem, (long long)Np);
   int maxcl = 0;
-  if (cudaOccupancyMaxActiveClusters(&maxcl, c.fn, &cfg) != cudaSuccess || maxcl < 1)
-    return fail(FFS_EINVAL, "cluster of %d CTAs does not fit", c.CS);
+  if (int rc = cluster_occupancy(c.fn, c.CS, c.threads, c.smem, maxcl)) return rc;
   const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(M, maxcl));
   c.grid = (int)(ncl * c.CS);
   c.ws_ut = align_up((size_t)N * c.Lpt * c.es);
@@ -396,14 +481,29 @@ int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Cl
   return FFS_OK;
 }
 
+PlanCache<ClusterPlan> g_cluster_plans;
+int make_cluster_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, ClusterPlan& c) {
+  return g_cluster_plans.get(plan_key(2, L, N, Np, M, dtype), c,
+                             [&](ClusterPlan& p) { return make_cluster_plan_uncached(L, N, Np, dtype, M, p); });
+}
+
+void launch_transpose(const void* U, double* Ut, int64_t L, int64_t N, int Lpt, int dtype, cudaStream_t s) {
+  dim3 tb(32, 8), tg((unsigned)((Lpt + 31) / 32), (unsigned)((N + 31) / 32));
+  if (dtype == FFS_C128)
+    ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, s>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, Lpt);
+  else
+    ffsk::transpose_pad_kernel<double><<<tg, tb, 0, s>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, Lpt);
+  ++ffsh::launches();
+}
+
 int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
-                   int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
+                   int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
                    double* trace) {
   ClusterPlan c;
   int rc = make_cluster_plan(L, N, Np, dtype, M, c);
   if (rc != FFS_OK) return rc;
   if (!ws || ws_bytes < c.ws_ut + c.ws_w)
-    return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, c.ws_ut + c.ws_w);
+    return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, c.ws_ut + c.ws_w);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   char* w = static_cast<char*>(ws);
   ffsk::ClusterParams p{};
@@ -419,71 +519,40 @@ int launch_cluster(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
   p.positions = positions;
   p.flags = flags;
   p.wfull = reinterpret_cast<double*>(w + c.ws_ut);
-  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.S0 = S0;
+  p.S = S > 0 ? S : 0;
   p.trace = S > 0 ? trace : nullptr;
-  p.timing = g_timing;  // development (ffs_dev_timing); null unless enabled
-  dim3 tb(32, 8), tg((unsigned)((c.Lpt + 31) / 32), (unsigned)((N + 31) / 32));
-  if (dtype == FFS_C128)
-    ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, c.Lpt);
-  else
-    ffsk::transpose_pad_kernel<double><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, c.Lpt);
-  ++g_launches;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = c.CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(c.threads);
-  cfg.gridDim = dim3(c.grid);
-  cfg.dynamicSmemBytes = c.smem;
-  cfg.stream = stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  launch_transpose(U, const_cast<double*>(p.Ut), L, N, c.Lpt, dtype, stream);
   void* args[] = {&p};
-  if (g_prof) {
-    if (!g_ev0) {
-      cudaEventCreate(&g_ev0);
-      cudaEventCreate(&g_ev1);
-    }
-    cudaEventRecord(g_ev0, stream);
-  }
-  cudaError_t e = cudaLaunchKernelExC(&cfg, c.fn, args);
+  ffsh::prof_begin(stream);
+  cudaError_t e = launch_cluster_kernel(c.fn, c.CS, c.grid, c.threads, c.smem, stream, args);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "cluster launch failed: %s", cudaGetErrorString(e));
-  if (g_prof) {
-    cudaEventRecord(g_ev1, stream);
-    g_ev_pending = true;
-  }
-  ++g_launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
-  g_err[0] = 0;
+  ffsh::prof_end(stream);
+  ++ffsh::launches();
   return FFS_OK;
 }
 
-// ------------------------------------------------------------------ lockstep-dense path
-// Full sampling (N' = N) of real U at large L: per block step, one DMMA GEMM P = U Y for a batch
-// of S samples, then one cluster per sample draws on its panel and updates W and Y
-// (ffs_dense.cuh, ffs_cluster_kernel<..., STEP = true>).
+// ------------------------------------------------------------------ block-step paths
+// Large L, N >= 256: per block step of B = 8 draws, one launch of the step kernel (cluster per
+// sample) for a batch of S samples, then one batched Gauss-Jordan launch. Full sampling
+// contracts blocks with k0 >= theta N' as ONE dense GEMM P = U Y over the batch (Ozaki-emulated
+// FP64 on the INT8 tensor cores, or DMMA); marginals contract every block gathered
+// (DESIGN.md §3). The ~4 launches per block are replayed as one CUDA graph.
 bool dense_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
-  const char* g = getenv("FFS_NO_DENSE");
-  if (g && g[0] == '1') return false;
+  if (ffsh::option(FFS_OPT_BLOCK_STEP) == 0.0) return false;
   // marginals (N' < N) take the same step + batched-GJ kernels with every block contracted gathered
   // (no GEMM): C5 marginal 201 -> 180 ms against the per-sample cluster kernel
-  const char* m = getenv("FFS_STEP_MARGINAL");  // development: "0" keeps marginals on the cluster kernel
-  const bool marg = !(m && m[0] == '0') && Np < N;
+  const bool marg = ffsh::option(FFS_OPT_LARGE_L_MARGINAL) != 0.0 && Np < N;
   return (Np == N || marg) && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
 }
 
 struct DensePlan {
   ClusterPlan c;
-  int64_t S, Sh, ldY;  // batch, half-batch (per stream), Y row stride in scalars of T
-  int nstr;            // streams (half-batches) in flight
-  bool small_gemm;     // GEMM <16, 4> (co-resident with the GJ kernel) instead of <32, 3>
-  bool ozaki;          // Ozaki-emulated GEMM on the INT8 tensor cores instead of the DMMA GEMM
+  int64_t S, ldY;      // batch, Y row stride in scalars of T
+  int gemm;            // 8 / 7: Ozaki-emulated GEMM with that many slices; 0: DMMA GEMM; -1: no GEMM
   int Kp;              // GEMM K (f N) padded to the Ozaki K chunk
   size_t ws_oza, ws_ea, ws_ozb, ws_eb;
-  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, total, y_half, p_half;
+  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, total;
   int k_gather;        // blocks with k0 < k_gather contract the gathered columns in the step kernel
 };
 
@@ -493,92 +562,88 @@ template <typename T>
 const void* dense_gj_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, gj_tj<T>()>); }
 template <typename T>
 size_t dense_gj_bytes(int k0) { return ffsk::dense_gj_smem<T, 8, gj_tj<T>()>(k0); }
+template <int NS>
+const void* ozaki_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel<NS>); }
 
-int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
+int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
   const bool cx = dtype == FFS_C128;
-  int rc = make_cluster_plan(L, N, Np, dtype, M, d.c);
-  if (rc != FFS_OK) return rc;
   d.c.fn = cx ? ffsk::cluster_step_kernel_ptr<cplx, 2, 8, 512>() : ffsk::cluster_step_kernel_ptr<double, 4, 8, 512>();
   d.c.R = cx ? 2 : 4;
   d.c.B = 8;
+  d.c.threads = 512;
+  d.c.es = cx ? 16 : 8;
   d.c.Lc = 512 * d.c.R;
-  d.c.CS = std::max<int>(2, (int)((L + d.c.Lc - 1) / d.c.Lc));
-  if (d.c.CS > 8) d.c.CS = 16;
+  if (int rc = cluster_dims(L, d.c.Lc, d.c.CS)) return rc;
   d.c.Lpt = d.c.CS * d.c.Lc;
-  if (cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.c.smem) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(step smem) failed");
-  if (d.c.CS > 8 && cudaFuncSetAttribute(d.c.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-    return fail(FFS_ECUDA, "non-portable cluster size not allowed");
-  // one stream and the <32, 3> GEMM: two half-batches on two streams with the co-residable
-  // <16, 4> GEMM + 128-thread GJ measured no overlap gain (C4 1.570 vs 1.526 s, C5 1.663 vs 1.549 s)
-  d.nstr = 1;
-  if (const char* e = getenv("FFS_DENSE_STREAMS")) d.nstr = std::max(1, std::min(2, atoi(e)));  // development
-  d.small_gemm = false;
-  if (const char* e = getenv("FFS_DENSE_GEMM")) d.small_gemm = atoi(e) == 16;  // development
-  const void* gf = d.small_gemm ? reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel<16, 4>)
-                                : reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel<32, 3>);
-  const size_t gsm = d.small_gemm ? ffsk::gemm_smem<16, 4>() : ffsk::gemm_smem<32, 3>();
-  if (cudaFuncSetAttribute(gf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(gemm smem) failed");
+  d.c.smem = cx ? ffsk::ClusterLayout<cplx, 8>((int)N, (int)Np).total : ffsk::ClusterLayout<double, 8>((int)N, (int)Np).total;
+  int maxcl = 0;
+  if (int rc = cluster_occupancy(d.c.fn, d.c.CS, d.c.threads, d.c.smem, maxcl)) return rc;
+  if (int rc = ffsh::ensure_max_smem(reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel<32, 3>))) return rc;
   // samples per lockstep batch: as many as ~24 GB of per-sample factors W allow (larger batches =
   // larger GEMMs and fewer launches: C4 1.188 s at 1024, 1.161 s at 4096), at least 1024, at most
   // 8192 (marginals have no GEMM operands)
-  const double wbytes = (double)Np * (double)Np * (dtype == FFS_C128 ? 16.0 : 8.0);
+  const double wbytes = (double)Np * (double)Np * (cx ? 16.0 : 8.0);
   int64_t cap = std::max<int64_t>(1024, std::min<int64_t>(8192, (int64_t)(24e9 / wbytes)));
-  if (const char* e = getenv("FFS_DENSE_S")) cap = std::max<int64_t>(1, atoll(e));  // development
+  const double ob = ffsh::option(FFS_OPT_DENSE_BATCH);
+  if (ob >= 1.0) cap = (int64_t)ob;
   d.S = std::max<int64_t>(1, std::min<int64_t>(M, cap));
-  if (d.S < 2) d.nstr = 1;
-  d.Sh = (d.S + d.nstr - 1) / d.nstr;
   // ldY in scalars of T; the GEMM's N (2 ldY real columns for complex) is a multiple of 128
   const int64_t q = cx ? ffsk::kGN / 2 : ffsk::kGN;
-  d.ldY = (d.Sh * d.c.B + q - 1) / q * q;
+  d.ldY = (d.S * d.c.B + q - 1) / q * q;
   const size_t es = cx ? 16 : 8;
   const bool no_gemm = Np < N;  // marginals: gathered contraction only (the GEMM would be N/N' x wasteful)
-  d.y_half = no_gemm ? 0 : align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: 2N x 2ldY expansion
-  d.p_half = no_gemm ? 0 : align_up((size_t)L * d.ldY * es);
+  const int gsel = (int)ffsh::option(FFS_OPT_DENSE_GEMM);
+  if (gsel != 0 && gsel != 7 && gsel != 8) return fail(FFS_EINVAL, "FFS_OPT_DENSE_GEMM must be 0, 7 or 8");
+  d.gemm = no_gemm ? -1 : gsel;
+  const size_t y_bytes = no_gemm ? 0 : align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: 2N x 2ldY expansion
+  const size_t p_bytes = no_gemm ? 0 : align_up((size_t)L * d.ldY * es);
   d.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-  d.ws_y = d.nstr * d.y_half;
-  d.ws_p = d.nstr * d.p_half;
-  d.ws_w = align_up((size_t)d.nstr * d.Sh * Np * Np * es);
-  d.ws_ch = align_up((size_t)d.nstr * d.Sh * (d.c.Lpt / 32) * 4);
-  d.ws_row = align_up((size_t)d.nstr * d.Sh * (d.c.B * d.c.B + d.c.B) * es);
-  // GEMM: Ozaki-style FP64 emulation on the INT8 tensor cores by default (2x the DMMA GEMM at the
-  // C5 block shape); FFS_DENSE_GEMM=dmma selects the DMMA GEMM
-  const char* gsel = getenv("FFS_DENSE_GEMM");
-  d.ozaki = !(gsel && (strcmp(gsel, "dmma") == 0 || atoi(gsel) > 0)) && d.nstr == 1 && !no_gemm;
+  d.ws_y = y_bytes;
+  d.ws_p = p_bytes;
+  d.ws_w = align_up((size_t)d.S * Np * Np * es);
+  d.ws_ch = align_up((size_t)d.S * (d.c.Lpt / 32) * 4);
+  d.ws_row = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * es);
   // hybrid: while k0 is small the gathered contraction (L k0 B per sample, from the transposed U)
-  // costs less than the GEMM's full-N one (L N B); crossover measured on C4/C5:
-  // Ozaki GEMM: C5 0.15-0.2 -> 0.97 s (1.01 s at 0), C4 0.35-0.4 -> 0.94 s (0.99 s at 0.6);
-  // DMMA GEMM: C5 0.3 -> 1.35 s, C4 0.6 -> 1.19 s. Complex contractions do 2x the flops per
-  // gathered byte, so gathering pays longer.
-  double theta = d.ozaki ? (cx ? 0.35 : 0.15) : (cx ? 0.6 : 0.3);
-  if (const char* e = getenv("FFS_DENSE_THETA")) theta = atof(e);  // development
+  // costs less than the GEMM's full-N one (L N B); crossover measured on C4/C5.
+  // Complex contractions do 2x the flops per gathered byte, so gathering pays longer.
+  double theta;
+  if (d.gemm == 0) theta = cx ? 0.6 : 0.3;
+  else if (d.gemm == 7) theta = cx ? 0.35 : 0.15;
+  else theta = cx ? 0.4 : 0.2;
+  const double ot = ffsh::option(FFS_OPT_DENSE_THETA);
+  if (ot >= 0.0) theta = ot;
   d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
   d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
   const int64_t fK = (cx ? 2 : 1) * N;
   d.Kp = (int)((fK + ffsk::kOzBK - 1) / ffsk::kOzBK * ffsk::kOzBK);
   const int64_t ncolsY = (cx ? 2 : 1) * d.ldY;
-  d.ws_oza = d.ozaki ? align_up((size_t)ffsk::kOzS * L * d.Kp) : 0;
-  d.ws_ea = d.ozaki ? align_up((size_t)L * 4) : 0;
-  d.ws_ozb = d.ozaki ? align_up((size_t)ffsk::kOzS * ncolsY * d.Kp) : 0;
-  d.ws_eb = d.ozaki ? align_up((size_t)ncolsY * 4) : 0;
-  if (d.ozaki && cudaFuncSetAttribute(reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ffsk::kOzSmem) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(ozaki smem) failed");
+  const int ns = d.gemm > 0 ? d.gemm : 0;
+  d.ws_oza = ns ? align_up((size_t)ns * L * d.Kp) : 0;
+  d.ws_ea = ns ? align_up((size_t)L * 4) : 0;
+  d.ws_ozb = ns ? align_up((size_t)ns * ncolsY * d.Kp) : 0;
+  d.ws_eb = ns ? align_up((size_t)ncolsY * 4) : 0;
+  if (ns == 8) {
+    if (int rc = ffsh::ensure_max_smem(ozaki_fn<8>())) return rc;
+  } else if (ns == 7) {
+    if (int rc = ffsh::ensure_max_smem(ozaki_fn<7>())) return rc;
+  }
   d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut + d.ws_oza + d.ws_ea + d.ws_ozb + d.ws_eb;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
-  if (gjs > kMaxSmem) return fail(FFS_EINVAL, "dense path: N'=%lld too large for the GJ tile", (long long)Np);
-  const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
-  if (cudaFuncSetAttribute(gjf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gjs) != cudaSuccess)
-    return fail(FFS_ECUDA, "cudaFuncSetAttribute(gj smem) failed");
-  return FFS_OK;
+  if (gjs > kMaxSmem) return fail(FFS_EINVAL, "block-step path: N'=%lld too large for the GJ tile", (long long)Np);
+  return ffsh::ensure_max_smem(cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>());
 }
 
-// 3-D tensor map [kOzS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
+PlanCache<DensePlan> g_dense_plans;
+int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
+  return g_dense_plans.get(plan_key(3, L, N, Np, M, dtype), d,
+                           [&](DensePlan& p) { return make_dense_plan_uncached(L, N, Np, dtype, M, p); });
+}
+
+// 3-D tensor map [NS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-int oz_tensor_map(CUtensorMap* m, const int8_t* base, int64_t rows, int Kp, int box_rows) {
+int oz_tensor_map(CUtensorMap* m, const int8_t* base, int ns, int64_t rows, int Kp, int box_rows) {
   // resolved once (thread-safe function-local static)
   static const EncodeTiledFn enc = [] {
     void* fn = nullptr;
@@ -587,7 +652,7 @@ int oz_tensor_map(CUtensorMap* m, const int8_t* base, int64_t rows, int Kp, int 
     return reinterpret_cast<EncodeTiledFn>(fn);
   }();
   if (!enc) return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)ffsk::kOzS};
+  const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)ns};
   const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)Kp * (cuuint64_t)rows};
   const cuuint32_t box[3] = {(cuuint32_t)ffsk::kOzBK, (cuuint32_t)box_rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
@@ -598,19 +663,11 @@ int oz_tensor_map(CUtensorMap* m, const int8_t* base, int64_t rows, int Kp, int 
   return FFS_OK;
 }
 
-// a second stream (and fork/join events) per host thread for the 2-stream dense schedule
-thread_local cudaStream_t g_dense_s1 = nullptr;
-thread_local cudaEvent_t g_dense_fork = nullptr, g_dense_join = nullptr;
-
-int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
-                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
-                 double* trace) {
+// Issues every launch of one block-step call on `stream` (directly, or into a stream capture).
+int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np,
+                const double* uniforms, int32_t* positions, int32_t* flags, void* ws, cudaStream_t stream, int64_t S0, int64_t S,
+                double* trace) {
   const bool cx = dtype == FFS_C128;
-  DensePlan d;
-  int rc = make_dense_plan(L, N, Np, dtype, M, d);
-  if (rc != FFS_OK) return rc;
-  if (!ws || ws_bytes < d.total) return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, d.total);
-  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   const size_t es = cx ? 16 : 8;
   const int B = d.c.B;
   char* w = static_cast<char*>(ws);
@@ -626,228 +683,231 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
   int* oz_ea = reinterpret_cast<int*>(ozb0 + d.ws_oza);
   int8_t* ozb = reinterpret_cast<int8_t*>(ozb0 + d.ws_oza + d.ws_ea);
   int* oz_eb = reinterpret_cast<int*>(ozb0 + d.ws_oza + d.ws_ea + d.ws_ozb);
+  const int ns = d.gemm > 0 ? d.gemm : 0;
+  const int64_t f = cx ? 2 : 1;
+  const int64_t oz_ncols = f * d.ldY;
   CUtensorMap oz_ta, oz_tb;
-  const int64_t oz_ncols = (cx ? 2 : 1) * d.ldY;
-  if (d.ozaki) {
-    if (oz_tensor_map(&oz_ta, oza, L, d.Kp, ffsk::kOzBM) != FFS_OK) return FFS_ECUDA;
-    if (oz_tensor_map(&oz_tb, ozb, oz_ncols, d.Kp, ffsk::kOzBN) != FFS_OK) return FFS_ECUDA;
+  if (ns) {
+    if (oz_tensor_map(&oz_ta, oza, ns, L, d.Kp, ffsk::kOzBM) != FFS_OK) return FFS_ECUDA;
+    if (oz_tensor_map(&oz_tb, ozb, ns, oz_ncols, d.Kp, ffsk::kOzBN) != FFS_OK) return FFS_ECUDA;
     // A = U (real L x 2N view for complex): split once per call
-    const int64_t fK = (cx ? 2 : 1) * N;
-    ffsk::ffs_ozaki_split_rows_kernel<<<(unsigned)((L + 7) / 8), 256, 0, stream>>>(
-        static_cast<const double*>(U), (int)L, (int)fK, fK, oza, d.Kp, oz_ea);
-    ++g_launches;
+    const int64_t fK = f * N;
+    const unsigned g = (unsigned)((L + 7) / 8);
+    if (ns == 8)
+      ffsk::ffs_ozaki_split_rows_kernel<8><<<g, 256, 0, stream>>>(static_cast<const double*>(U), (int)L, (int)fK, fK, oza, d.Kp, oz_ea);
+    else
+      ffsk::ffs_ozaki_split_rows_kernel<7><<<g, 256, 0, stream>>>(static_cast<const double*>(U), (int)L, (int)fK, fK, oza, d.Kp, oz_ea);
+    ++ffsh::launches();
   }
-  if (d.k_gather > 0) {
-    dim3 tb(32, 8), tg((unsigned)((d.c.Lpt + 31) / 32), (unsigned)((N + 31) / 32));
-    if (cx) ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, d.c.Lpt);
-    else ffsk::transpose_pad_kernel<double><<<tg, tb, 0, stream>>>(static_cast<const double*>(U), Ut, (int)L, (int)N, d.c.Lpt);
-    ++g_launches;
-  }
-  cudaStream_t st[2] = {stream, stream};
-  if (d.nstr > 1) {
-    if (!g_dense_s1) {
-      if (cudaStreamCreateWithFlags(&g_dense_s1, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&g_dense_fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&g_dense_join, cudaEventDisableTiming) != cudaSuccess)
-        return fail(FFS_ECUDA, "dense path: stream/event creation failed");
-    }
-    st[1] = g_dense_s1;
-  }
-  if (g_prof) {
-    if (!g_ev0) {
-      cudaEventCreate(&g_ev0);
-      cudaEventCreate(&g_ev1);
-    }
-    cudaEventRecord(g_ev0, stream);
-  }
+  if (d.k_gather > 0) launch_transpose(U, Ut, L, N, d.c.Lpt, dtype, stream);
   {
     const int tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
     const int64_t pgrid = (M + tpb - 1) / tpb;
-    ffsk::ffs_permute_kernel<<<(unsigned)pgrid, tpb, (size_t)tpb * N * 4, stream>>>(uniforms, perm, M, (int)N,
-                                                                                       (int)Np);
-    ++g_launches;
+    ffsk::ffs_permute_kernel<<<(unsigned)pgrid, tpb, (size_t)tpb * N * 4, stream>>>(uniforms, perm, M, (int)N, (int)Np);
+    ++ffsh::launches();
   }
-  if (d.nstr > 1) {
-    cudaEventRecord(g_dense_fork, stream);
-    cudaStreamWaitEvent(st[1], g_dense_fork, 0);
-  }
-  const int64_t f = cx ? 2 : 1;
   const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
   const int gjt = cx ? gj_tj<cplx>() : gj_tj<double>();
-  const size_t rstride = (size_t)(B * B + B) * es;
+  double* Y = d.ws_y ? reinterpret_cast<double*>(Yb) : nullptr;
+  double* Pd = reinterpret_cast<double*>(Pb);
+  double* Wd = reinterpret_cast<double*>(Wb);
+  double* rowg = reinterpret_cast<double*>(rowb);
   for (int64_t base = 0; base < M; base += d.S) {
-    const int64_t Sb = std::min<int64_t>(d.S, M - base);
-    ffsk::ClusterParams p[2] = {};
-    ffsk::DgemmParams gp[2] = {};
-    ffsk::DenseGjParams q[2] = {};
-    int64_t nh[2] = {0, 0};
-    for (int h = 0; h < d.nstr; ++h) {
-      const int64_t b0 = std::min<int64_t>(Sb, h * d.Sh);
-      nh[h] = std::min<int64_t>(Sb, b0 + d.Sh) - b0;
-      if (nh[h] <= 0) continue;
-      double* Y = reinterpret_cast<double*>(Yb + h * d.y_half);
-      double* Pd = reinterpret_cast<double*>(Pb + h * d.p_half);
-      double* Wd = reinterpret_cast<double*>(Wb + (size_t)h * d.Sh * Np * Np * es);
-      uint32_t* chh = ch + (size_t)h * d.Sh * (d.c.Lpt / 32);
-      double* rowg = reinterpret_cast<double*>(rowb + (size_t)h * d.Sh * rstride);
-      if (d.y_half) cudaMemsetAsync(Y, 0, d.y_half, st[h]);
-      cudaMemsetAsync(chh, 0, (size_t)nh[h] * (d.c.Lpt / 32) * 4, st[h]);
-      if (flags) cudaMemsetAsync(flags + base + b0, 0, (size_t)nh[h] * 4, st[h]);
-      const unsigned yg = (unsigned)((nh[h] * B + 255) / 256);
-      if (!d.y_half) Y = nullptr;
-      else if (cx) ffsk::ffs_dense_y0_kernel<cplx, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
-      else ffsk::ffs_dense_y0_kernel<double, 8><<<yg, 256, 0, st[h]>>>(perm, Y, d.ldY, base + b0, (int)nh[h], (int)Np);
-      if (Y) ++g_launches;
-      ffsk::ClusterParams& c = p[h];
-      c.U = static_cast<const double*>(U);
-      c.Ut = Ut;
-      c.L = (int)L;
-      c.N = (int)N;
-      c.Np = (int)Np;
-      c.Lc = d.c.Lc;
-      c.Lpt = d.c.Lpt;
-      c.M = M;
-      c.uniforms = uniforms;
-      c.positions = positions;
-      c.flags = flags;
-      c.wfull = Wd;
-      c.S = S > 0 ? std::min<int64_t>(S, M) : 0;
-      c.trace = S > 0 ? trace : nullptr;
-      c.timing = g_timing;  // development (ffs_dev_timing); null unless enabled
-      c.Pd = Pd;
-      c.ldY = d.ldY;
-      c.rowg = rowg;
-      c.permg = perm;
-      c.chosen_g = chh;
-      c.base = base + b0;
-      c.Sb = (int)nh[h];
-      // complex: the real GEMM of U viewed as L x 2N with the real 2N x 2ldY expansion of Y
-      gp[h].A = static_cast<const double*>(U);
-      gp[h].B = Y;
-      gp[h].C = Pd;
-      gp[h].lda = f * N;
-      gp[h].ldb = f * d.ldY;
-      gp[h].ldc = f * d.ldY;
-      gp[h].M = (int)L;
-      gp[h].N = (int)(f * d.ldY);
-      gp[h].K = (int)(f * N);
-      gp[h].panel = (int)(f * B);  // P in per-sample [L][B] panels (contiguous reads in the step kernel)
-      q[h].U = static_cast<const double*>(U);
-      q[h].perm = perm;
-      q[h].positions = positions;
-      q[h].rowg = rowg;
-      q[h].W = Wd;
-      q[h].Y = Y;
-      q[h].ldY = d.ldY;
-      q[h].N = (int)N;
-      q[h].Np = (int)Np;
-      q[h].base = base + b0;
+    const int64_t nh = std::min<int64_t>(d.S, M - base);
+    if (Y && cudaMemsetAsync(Y, 0, d.ws_y, stream) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
+    if (cudaMemsetAsync(ch, 0, (size_t)nh * (d.c.Lpt / 32) * 4, stream) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
+    if (flags && cudaMemsetAsync(flags + base, 0, (size_t)nh * 4, stream) != cudaSuccess)
+      return fail(FFS_ECUDA, "memset failed");
+    if (Y) {
+      const unsigned yg = (unsigned)((nh * B + 255) / 256);
+      if (cx) ffsk::ffs_dense_y0_kernel<cplx, 8><<<yg, 256, 0, stream>>>(perm, Y, d.ldY, base, (int)nh, (int)Np);
+      else ffsk::ffs_dense_y0_kernel<double, 8><<<yg, 256, 0, stream>>>(perm, Y, d.ldY, base, (int)nh, (int)Np);
+      ++ffsh::launches();
     }
+    ffsk::ClusterParams c{};
+    c.U = static_cast<const double*>(U);
+    c.Ut = Ut;
+    c.L = (int)L;
+    c.N = (int)N;
+    c.Np = (int)Np;
+    c.Lc = d.c.Lc;
+    c.Lpt = d.c.Lpt;
+    c.M = M;
+    c.uniforms = uniforms;
+    c.positions = positions;
+    c.flags = flags;
+    c.wfull = Wd;
+    c.S0 = S0;
+    c.S = S > 0 ? S : 0;
+    c.trace = S > 0 ? trace : nullptr;
+    c.Pd = Pd;
+    c.ldY = d.ldY;
+    c.rowg = rowg;
+    c.permg = perm;
+    c.chosen_g = ch;
+    c.base = base;
+    c.Sb = (int)nh;
+    // complex: the real GEMM of U viewed as L x 2N with the real 2N x 2ldY expansion of Y
+    ffsk::DgemmParams gp{};
+    gp.A = static_cast<const double*>(U);
+    gp.B = Y;
+    gp.C = Pd;
+    gp.lda = f * N;
+    gp.ldb = f * d.ldY;
+    gp.ldc = f * d.ldY;
+    gp.M = (int)L;
+    gp.N = (int)(f * d.ldY);
+    gp.K = (int)(f * N);
+    gp.panel = (int)(f * B);  // P in per-sample [L][B] panels (contiguous reads in the step kernel)
+    ffsk::DenseGjParams q{};
+    q.U = static_cast<const double*>(U);
+    q.perm = perm;
+    q.positions = positions;
+    q.rowg = rowg;
+    q.W = Wd;
+    q.Y = Y;
+    q.ldY = d.ldY;
+    q.N = (int)N;
+    q.Np = (int)Np;
+    q.base = base;
     const dim3 ggrid((unsigned)(f * d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
     for (int k0 = 0; k0 < Np; k0 += B) {
-      for (int h = 0; h < d.nstr; ++h) {
-        if (nh[h] <= 0) continue;
-        p[h].gather = k0 < d.k_gather ? 1 : 0;
-        if (p[h].gather) {
-          // no GEMM: the step kernel contracts the gathered columns itself
-        } else if (d.ozaki) {
-          ffsk::ffs_ozaki_split_cols_kernel<<<(unsigned)(oz_ncols / 32), 256, 0, st[h]>>>(
-              gp[h].B, (int)gp[h].K, (int)oz_ncols, gp[h].ldb, ozb, d.Kp, oz_eb);
+      c.gather = k0 < d.k_gather ? 1 : 0;
+      if (!c.gather) {
+        if (ns) {
+          const unsigned sg = (unsigned)(oz_ncols / 32);
+          if (ns == 8)
+            ffsk::ffs_ozaki_split_cols_kernel<8><<<sg, 256, 0, stream>>>(gp.B, (int)gp.K, (int)oz_ncols, gp.ldb, ozb, d.Kp, oz_eb);
+          else
+            ffsk::ffs_ozaki_split_cols_kernel<7><<<sg, 256, 0, stream>>>(gp.B, (int)gp.K, (int)oz_ncols, gp.ldb, ozb, d.Kp, oz_eb);
           ffsk::OzakiParams op{};
           op.ea = oz_ea;
           op.eb = oz_eb;
-          op.C = gp[h].C;
+          op.C = gp.C;
           op.M = (int)L;
           op.N = (int)oz_ncols;
           op.K = d.Kp;
-          op.panel = gp[h].panel;
+          op.panel = gp.panel;
           const dim3 og((unsigned)(oz_ncols / ffsk::kOzBN), (unsigned)((L + ffsk::kOzBM - 1) / ffsk::kOzBM));
-          ffsk::ffs_ozaki_gemm_kernel<<<og, ffsk::kOzThreads, ffsk::kOzSmem, st[h]>>>(oz_ta, oz_tb, op);
-          g_launches += 1;
-        } else if (d.small_gemm)
-          ffsk::ffs_dgemm_kernel<16, 4><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<16, 4>(), st[h]>>>(gp[h]);
-        else
-          ffsk::ffs_dgemm_kernel<32, 3><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<32, 3>(), st[h]>>>(gp[h]);
-        if (!p[h].gather) ++g_launches;
-        p[h].k0 = k0;
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = d.c.CS;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.blockDim = dim3(d.c.threads);
-        cfg.gridDim = dim3((unsigned)(nh[h] * d.c.CS));
-        cfg.dynamicSmemBytes = d.c.smem;
-        cfg.stream = st[h];
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        void* args[] = {&p[h]};
-        cudaError_t e = cudaLaunchKernelExC(&cfg, d.c.fn, args);
-        if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
-        ++g_launches;
-        if (k0 + B < Np) {
-          q[h].k0 = k0;
-          const int nc = (int)Np - k0 - B;
-          const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh[h]);
-          const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
-          void* qargs[] = {&q[h]};
-          e = cudaLaunchKernel(gjf, jg, dim3(256), qargs, gsm, st[h]);
-          if (e != cudaSuccess) return fail(FFS_ECUDA, "gj launch failed: %s", cudaGetErrorString(e));
-          ++g_launches;
+          if (ns == 8)
+            ffsk::ffs_ozaki_gemm_kernel<8><<<og, ffsk::kOzThreads, ffsk::oz_smem<8>(), stream>>>(oz_ta, oz_tb, op);
+          else
+            ffsk::ffs_ozaki_gemm_kernel<7><<<og, ffsk::kOzThreads, ffsk::oz_smem<7>(), stream>>>(oz_ta, oz_tb, op);
+          ffsh::launches() += 2;
+        } else {
+          ffsk::ffs_dgemm_kernel<32, 3><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<32, 3>(), stream>>>(gp);
+          ++ffsh::launches();
         }
+      }
+      c.k0 = k0;
+      void* args[] = {&c};
+      cudaError_t e = launch_cluster_kernel(d.c.fn, d.c.CS, (int)(nh * d.c.CS), d.c.threads, d.c.smem, stream, args);
+      if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
+      ++ffsh::launches();
+      if (k0 + B < Np) {
+        q.k0 = k0;
+        const int nc = (int)Np - k0 - B;
+        const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
+        const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
+        void* qargs[] = {&q};
+        e = cudaLaunchKernel(gjf, jg, dim3(256), qargs, gsm, stream);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "gj launch failed: %s", cudaGetErrorString(e));
+        ++ffsh::launches();
       }
     }
   }
-  if (d.nstr > 1) {
-    cudaEventRecord(g_dense_join, st[1]);
-    cudaStreamWaitEvent(stream, g_dense_join, 0);
-  }
-  if (g_prof) {
-    cudaEventRecord(g_ev1, stream);
-    g_ev_pending = true;
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
-  g_err[0] = 0;
   return FFS_OK;
 }
 
-bool use_warp_path(int64_t L, int64_t N, int64_t Np, int dtype) {
-  const char* g = getenv("FFS_FORCE_GENERIC");
-  if (g && g[0] == '1') return false;
-  return warp_eligible(L, N, Np, dtype);
+// CUDA-graph driver (north_star (d)): the block loop is captured once per (arguments, options)
+// and replayed with one cudaGraphLaunch; a change of pointers or sizes re-captures and updates
+// the executable graph in place. Per host thread, the last few argument sets are kept.
+struct GraphEntry {
+  std::tuple<const void*, int64_t, int64_t, int, int64_t, int64_t, const double*, int32_t*, int32_t*, void*, int64_t,
+             int64_t, double*, uint64_t, int>
+      key;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+};
+thread_local GraphEntry g_graphs[4];
+thread_local unsigned g_graph_next = 0;
+
+int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
+                 double* trace) {
+  DensePlan d;
+  int rc = make_dense_plan(L, N, Np, dtype, M, d);
+  if (rc != FFS_OK) return rc;
+  if (!ws || ws_bytes < d.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, d.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return fail(FFS_ECUDA, "cudaStreamIsCapturing failed");
+  const bool graph = ffsh::option(FFS_OPT_GRAPH) != 0.0 && cs == cudaStreamCaptureStatusNone;
+  if (!graph) {
+    ffsh::prof_begin(stream);
+    rc = issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, stream, S0, S, trace);
+    ffsh::prof_end(stream);
+    return rc;
+  }
+  const auto key = std::make_tuple(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, S0, S, trace,
+                                   ffsh::options_version(), ffsh::device());
+  GraphEntry* ge = nullptr;
+  for (auto& g : g_graphs)
+    if (g.exec && g.key == key) ge = &g;
+  if (!ge) {
+    ge = &g_graphs[g_graph_next++ % 4];
+    cudaGraph_t graph_def = nullptr;
+    if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return fail(FFS_ECUDA, "cudaStreamBeginCapture failed");
+    const int l0 = ffsh::launches();
+    rc = issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, stream, S0, S, trace);
+    const cudaError_t ce = cudaStreamEndCapture(stream, &graph_def);
+    if (rc != FFS_OK) {
+      if (graph_def) cudaGraphDestroy(graph_def);
+      return rc;
+    }
+    if (ce != cudaSuccess || !graph_def) return fail(FFS_ECUDA, "stream capture failed: %s", cudaGetErrorString(ce));
+    bool updated = false;
+    if (ge->exec) {
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(ge->exec, graph_def, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(ge->exec);
+        ge->exec = nullptr;
+      }
+    }
+    if (!updated && cudaGraphInstantiate(&ge->exec, graph_def, 0) != cudaSuccess) {
+      cudaGraphDestroy(graph_def);
+      ge->exec = nullptr;
+      return fail(FFS_ECUDA, "cudaGraphInstantiate failed");
+    }
+    cudaGraphDestroy(graph_def);
+    ge->key = key;
+    ge->launches = ffsh::launches() - l0;
+  } else {
+    ffsh::launches() += ge->launches;
+  }
+  ffsh::prof_begin(stream);
+  const cudaError_t e = cudaGraphLaunch(ge->exec, stream);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "cudaGraphLaunch failed: %s", cudaGetErrorString(e));
+  ffsh::prof_end(stream);
+  return FFS_OK;
 }
 
-int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
-           int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S,
-           double* trace) {
-  g_launches = 0;
-  if (M == 0) return FFS_OK;
-  if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0)
-    return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M=%lld", (long long)L, (long long)N,
-                (long long)Np, (long long)M);
-  if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
-  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions with M=%lld", (long long)M);
-  if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
-  if (use_warp_path(L, N, Np, dtype))
-    return launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
-  if (dense_eligible(L, N, Np, dtype))
-    return launch_dense(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
-  if (cluster_eligible(L, dtype))
-    return launch_cluster(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S, trace);
+// ------------------------------------------------------------------ generic CTA/warp-owner path
+int launch_generic(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+                   int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
+                   double* trace) {
   Plan pl;
   int rc = make_plan(L, N, Np, dtype, M, pl);
   if (rc != FFS_OK) return rc;
-  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions with M=%lld", (long long)M);
-  if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
   const size_t need = pl.ws_ut + pl.ws_wfull;
   if (need > 0 && (!ws || ws_bytes < need))
-    return fail(FFS_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, need);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   char* w = static_cast<char*>(ws);
   ffsk::Params p{};
-  if (const char* dbg = getenv("FFS_DEBUG_SKIP")) p.dbg = atoi(dbg);  // development only
   p.U = static_cast<const double*>(U);
   p.Ut = pl.v.usmem ? nullptr : reinterpret_cast<const double*>(w);
   p.L = (int)L;
@@ -860,85 +920,118 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   p.positions = positions;
   p.flags = flags;
   p.wfull = reinterpret_cast<double*>(w + pl.ws_ut);
-  p.S = S > 0 ? std::min<int64_t>(S, M) : 0;
+  p.S0 = S0;
+  p.S = S > 0 ? S : 0;
   p.trace = S > 0 ? trace : nullptr;
   p.owner_smem = pl.owner_smem;
   p.ushared_smem = pl.ushared_smem;
-  if (!pl.v.usmem) {
-    dim3 tb(32, 8), tg((unsigned)((pl.Lp + 31) / 32), (unsigned)((N + 31) / 32));
-    if (dtype == FFS_C128)
-      ffsk::transpose_pad_kernel<cplx><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, pl.Lp);
-    else
-      ffsk::transpose_pad_kernel<double><<<tg, tb, 0, stream>>>(p.U, const_cast<double*>(p.Ut), (int)L, (int)N, pl.Lp);
-    ++g_launches;
-  }
+  if (!pl.v.usmem) launch_transpose(U, const_cast<double*>(p.Ut), L, N, pl.Lp, dtype, stream);
   void* args[] = {&p};
-  cudaError_t e = launch_timed(pl.v.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, stream);
+  ffsh::prof_begin(stream);
+  cudaError_t e = cudaLaunchKernel(pl.v.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, stream);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
-  ++g_launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
-  g_err[0] = 0;
+  ffsh::prof_end(stream);
+  ++ffsh::launches();
   return FFS_OK;
+}
+
+int check_shape(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
+  if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0)
+    return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M=%lld", (long long)L, (long long)N, (long long)Np,
+                (long long)M);
+  if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
+  const int64_t maxL = dtype == FFS_C128 ? kMaxLComplex : kMaxLReal;
+  if (L > maxL)
+    return fail(FFS_EINVAL, "unsupported L=%lld for dtype %d: the per-sample panel must fit one SM's registers "
+                "(max L %lld); see include/ffs.h", (long long)L, dtype, (long long)maxL);
+  return FFS_OK;
+}
+
+int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+           int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
+           double* trace) {
+  ffsh::launches() = 0;
+  if (M == 0) return FFS_OK;
+  if (int rc = check_shape(L, N, Np, dtype, M)) return rc;
+  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions with M=%lld", (long long)M);
+  if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
+  int rc;
+  if (warp_eligible(L, N, Np, dtype))
+    rc = launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
+  else if (dense_eligible(L, N, Np, dtype))
+    rc = launch_dense(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
+  else if (cluster_eligible(L, dtype))
+    rc = launch_cluster(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
+  else
+    rc = launch_generic(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
+  if (rc != FFS_OK) return rc;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  ffsh::clear_error();
+  return FFS_OK;
+}
+
+size_t workspace_bytes(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
+  if (check_shape(L, N, Np, dtype, std::max<int64_t>(M, 1)) != FFS_OK) return 0;
+  M = std::max<int64_t>(M, 1);
+  if (warp_eligible(L, N, Np, dtype)) {
+    WarpPlan w;
+    return make_warp_plan(L, N, Np, M, w) == FFS_OK ? w.ws_perm : 0;
+  }
+  if (dense_eligible(L, N, Np, dtype)) {
+    DensePlan d;
+    return make_dense_plan(L, N, Np, dtype, M, d) == FFS_OK ? d.total : 0;
+  }
+  if (cluster_eligible(L, dtype)) {
+    ClusterPlan c;
+    return make_cluster_plan(L, N, Np, dtype, M, c) == FFS_OK ? c.ws_ut + c.ws_w : 0;
+  }
+  Plan pl;
+  return make_plan(L, N, Np, dtype, M, pl) == FFS_OK ? pl.ws_ut + pl.ws_wfull : 0;
 }
 
 }  // namespace
 
+// ====================================================================== extern "C"
 extern "C" {
 
-size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M) {
-  if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && use_warp_path(L, N, Nprime, dtype)) {
-    WarpPlan w;
-    if (make_warp_plan(L, N, Nprime, std::max<int64_t>(M, 1), w) != FFS_OK) return 0;
-    return w.ws_perm + w.ws_w;
-  }
-  if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && dense_eligible(L, N, Nprime, dtype)) {
-    DensePlan d;
-    if (make_dense_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), d) != FFS_OK) return 0;
-    return d.total;
-  }
-  if (L >= 1 && N >= 1 && N <= L && Nprime >= 1 && Nprime <= N && cluster_eligible(L, dtype)) {
-    ClusterPlan c;
-    if (make_cluster_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), c) != FFS_OK) return 0;
-    return c.ws_ut + c.ws_w;
-  }
-  Plan pl;
-  if (make_plan(L, N, Nprime, dtype, std::max<int64_t>(M, 1), pl) != FFS_OK) return 0;
-  return pl.ws_ut + pl.ws_wfull;
+size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M) {
+  return workspace_bytes(L, N, Nprime, dtype, M);
 }
 
-int ffs_sample(const void* U, int64_t L, int64_t N, int dtype, int64_t M, const double* uniforms,
+int ffs_sample(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, const double* uniforms,
                int32_t* positions, int32_t* sample_flags, void* workspace, size_t ws_bytes, void* stream) {
   return launch(U, L, N, dtype, M, N, uniforms, positions, sample_flags, workspace, ws_bytes,
-                static_cast<cudaStream_t>(stream), 0, nullptr);
+                static_cast<cudaStream_t>(stream), 0, 0, nullptr);
 }
 
-int ffs_sample_marginal(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+int ffs_sample_marginal(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
                         const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
                         size_t ws_bytes, void* stream) {
   return launch(U, L, N, dtype, M, Nprime, uniforms, positions, sample_flags, workspace, ws_bytes,
-                static_cast<cudaStream_t>(stream), 0, nullptr);
+                static_cast<cudaStream_t>(stream), 0, 0, nullptr);
 }
 
-int ffs_debug_trace(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+int ffs_debug_trace(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
                     const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
-                    size_t ws_bytes, void* stream, int64_t S, double* weights) {
+                    size_t ws_bytes, void* stream, int64_t S0, int64_t S, double* weights) {
+  if (S < 0 || S0 < 0 || (M > 0 && S0 + S > M))
+    return fail(FFS_EINVAL, "trace range [%lld, %lld) outside [0, M=%lld)", (long long)S0, (long long)(S0 + S), (long long)M);
   return launch(U, L, N, dtype, M, Nprime, uniforms, positions, sample_flags, workspace, ws_bytes,
-                static_cast<cudaStream_t>(stream), S, weights);
+                static_cast<cudaStream_t>(stream), S0, S, weights);
 }
 
 // ---------------------------------------------------------------- host-buffer path
 // Device layout inside the caller's workspace: [U | uniforms chunk x2 | positions chunk x2 |
 // flags chunk x2 | sampling workspace]. Chunks alternate between two buffers so the copies of
-// chunk c+1 overlap the kernel of chunk c on the caller's stream (copies and kernels of one
-// stream serialise; overlap comes from a second stream created lazily per thread).
+// chunk c+1 overlap the kernel of chunk c.
 namespace {
 struct HostLayout {
   size_t u, uni[2], pos[2], flg[2], ws, total;
   int64_t chunk;
 };
 int64_t host_chunk(int64_t M) { return std::max<int64_t>(1, std::min<int64_t>(M, M > 32768 ? 16384 : M)); }
-bool host_layout(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HostLayout& h) {
+bool host_layout(int64_t L, int64_t N, int64_t Np, ffs_dtype dtype, int64_t M, HostLayout& h) {
   const size_t es = dtype == FFS_C128 ? 16 : 8;
   h.chunk = host_chunk(M);
   size_t o = 0;
@@ -947,25 +1040,16 @@ bool host_layout(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HostLay
   for (int b = 0; b < 2; ++b) { h.pos[b] = o; o = align_up(o + (size_t)h.chunk * Np * 4); }
   for (int b = 0; b < 2; ++b) { h.flg[b] = o; o = align_up(o + (size_t)h.chunk * 4); }
   h.ws = o;
-  const size_t need = ffs_workspace_bytes(L, N, Np, dtype, h.chunk);
+  const size_t need = workspace_bytes(L, N, Np, dtype, h.chunk);
   if (need == 0) return false;
   o += need;
   h.total = o;
   return true;
 }
-}  // namespace
-
-size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int dtype, int64_t M) {
-  HostLayout h;
-  if (!host_layout(L, N, Nprime, dtype, std::max<int64_t>(M, 1), h)) return 0;
-  return h.total;
-}
 
 // Three-stage pipeline over sample chunks, double-buffered in the workspace: copy-in stream
 // (U once, then uniforms of chunk c) -> caller's stream (sampling of chunk c) -> copy-out stream
-// (positions/flags of chunk c). Chunk c+1's upload and chunk c-1's download overlap chunk c's
-// kernels. Streams/events are created once per host thread (no device memory is allocated).
-namespace {
+// (positions/flags of chunk c). Streams/events are created once per host thread.
 struct HostPipe {
   cudaStream_t ci = nullptr, co = nullptr;
   cudaEvent_t entry, in_ready[2], done[2], out_done[2];
@@ -987,10 +1071,17 @@ struct HostPipe {
 thread_local HostPipe g_pipe;
 }  // namespace
 
-int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Nprime,
+size_t ffs_host_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M) {
+  HostLayout h;
+  if (!host_layout(L, N, Nprime, dtype, std::max<int64_t>(M, 1), h)) return 0;
+  return h.total;
+}
+
+int ffs_sample_host(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
                     const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
                     size_t ws_bytes, void* stream) {
   if (M == 0) return FFS_OK;
+  if (int rc = check_shape(L, N, Nprime, dtype, M)) return rc;
   HostLayout h;
   if (!host_layout(L, N, Nprime, dtype, M, h)) return FFS_EINVAL;
   if (!U || !uniforms || !positions || !workspace || ws_bytes < h.total)
@@ -1020,9 +1111,9 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, i
     if (c >= 2) FFS_CK(cudaStreamWaitEvent(s0, hp.out_done[b], 0), "wait");  // positions[b] drained
     int rc = launch(w + h.u, L, N, dtype, mc, Np, reinterpret_cast<const double*>(w + h.uni[b]),
                     reinterpret_cast<int32_t*>(w + h.pos[b]), reinterpret_cast<int32_t*>(w + h.flg[b]), w + h.ws,
-                    h.total - h.ws, s0, 0, nullptr);
+                    h.total - h.ws, s0, 0, 0, nullptr);
     if (rc != FFS_OK) return rc;
-    launches += g_launches;
+    launches += ffsh::launches();
     FFS_CK(cudaEventRecord(hp.done[b], s0), "record");
     FFS_CK(cudaStreamWaitEvent(hp.co, hp.done[b], 0), "wait");
     FFS_CK(cudaMemcpyAsync(positions + c0 * Np, w + h.pos[b], (size_t)mc * Np * 4, cudaMemcpyDeviceToHost, hp.co),
@@ -1035,37 +1126,39 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, int dtype, int64_t M, i
   FFS_CK(cudaStreamSynchronize(hp.co), "host path sync");
   FFS_CK(cudaStreamSynchronize(s0), "host path sync");
 #undef FFS_CK
-  g_launches = launches;
+  ffsh::launches() = launches;
   return FFS_OK;
 }
 
-int ffs_last_launch_count(void) { return g_launches; }
-
-// development only (not in ffs.h): per-phase clock64 sums of the segmented warp kernel
-int ffs_dev_timing(unsigned long long* host8, int reset) {
-  if (!g_timing) {
-    if (cudaMalloc(&g_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return FFS_ECUDA;
-    cudaMemset(g_timing, 0, 8 * sizeof(unsigned long long));
-  }
-  if (host8) cudaMemcpy(host8, g_timing, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  if (reset) cudaMemset(g_timing, 0, 8 * sizeof(unsigned long long));
-  return FFS_OK;
-}
+int ffs_last_launch_count(void) { return ffsh::launches(); }
 
 int ffs_profile_enable(int on) {
-  g_prof = on != 0;
-  g_ev_pending = false;
+  ffsh::g_prof = on != 0;
+  ffsh::g_ev_pending = false;
   return FFS_OK;
 }
 
 float ffs_last_kernel_ms(void) {
-  if (!g_ev_pending) return -1.0f;
+  if (!ffsh::g_ev_pending) return -1.0f;
   float ms = -1.0f;
-  if (cudaEventSynchronize(g_ev1) != cudaSuccess) return -1.0f;
-  if (cudaEventElapsedTime(&ms, g_ev0, g_ev1) != cudaSuccess) return -1.0f;
+  if (cudaEventSynchronize(ffsh::g_ev1) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, ffsh::g_ev0, ffsh::g_ev1) != cudaSuccess) return -1.0f;
   return ms;
 }
 
-const char* ffs_last_error(void) { return g_err; }
+int ffs_set_option(int opt, double value) {
+  if (opt <= 0 || opt >= ffsh::kNumOpts || opt > FFS_OPT_LAST) return fail(FFS_EINVAL, "unknown option %d", opt);
+  auto& o = ffsh::opts();
+  o.v[opt].store(std::isnan(value) || value < -1e300 ? ffsh::default_option(opt) : value);
+  o.version.fetch_add(1);
+  return FFS_OK;
+}
+
+double ffs_get_option(int opt) {
+  if (opt <= 0 || opt >= ffsh::kNumOpts || opt > FFS_OPT_LAST) return NAN;
+  return ffsh::option(opt);
+}
+
+const char* ffs_last_error(void) { return ffsh::g_err; }
 
 }  // extern "C"

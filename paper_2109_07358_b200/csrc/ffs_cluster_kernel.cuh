@@ -31,9 +31,8 @@ struct ClusterParams {
   int32_t* positions;      // [M][Np]
   int32_t* flags;
   double* wfull;           // per cluster [Np][Np] scalars
-  int64_t S;
+  int64_t S0, S;           // debug trace of samples S0 .. S0+S-1
   double* trace;           // [S][Np][L] or null
-  unsigned long long* timing;  // development (ffs_dev_timing): cycles in contraction/draws/GJ, or null
   // STEP mode (lockstep-dense path, ffs_dense.cuh): one block step k0 for the Sb samples
   // base .. base+Sb-1 (cluster c <-> sample base+c); the panel comes from P = U Y
   const double* Pd;        // [L][ldY] panels, sample s in columns s*B .. s*B+B-1
@@ -46,18 +45,12 @@ struct ClusterParams {
   int64_t base;
 };
 
-constexpr int kRingDepth = 8;  // per-thread cp.async pipeline depth of the contraction
 constexpr int kKC = 64;        // rows of W (or columns of the new rows) staged per chunk
-constexpr bool kUseRing = false;  // cp.async ring measured slower on C4/C5 (profiles/r01_ncu_summary.md)
-// draws exchange totals and the pivot row through mbarrier + st.async instead of two cluster
-// barriers: parity-green, but not faster end to end (C4 1.502 vs 1.488 s, C5 1.480 vs 1.487 s,
-// C5 marginal 208 vs 198 ms: the st.async pushes lengthen the crossing CTA's select+push)
-constexpr bool kMbarDraw = false;
 
 template <typename T, int B>
 struct ClusterLayout {
-  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, mbx, ring, total;
-  __host__ __device__ ClusterLayout(int N, int Np, int threads = 0, int R = 0) {
+  size_t perm, pos, usel, row, pinv, wb, vnew, red, xch, total;
+  __host__ __device__ ClusterLayout(int N, int Np) {
     size_t o = 0;
     perm = o; o = align16(o + sizeof(int) * N);
     pos = o;  o = align16(o + sizeof(int) * Np);
@@ -68,8 +61,6 @@ struct ClusterLayout {
     vnew = o; o = align16(o + sizeof(T) * (size_t)kKC * B);
     red = o;  o = align16(o + sizeof(double) * 64 + sizeof(int) * 96);
     xch = o;  o = align16(o + sizeof(double) * 4 * kMaxCS + 2 * sizeof(T) * B + 64);  // cluster exchange
-    mbx = o;  o = align16(o + 4 * 8 + 2 * sizeof(double) * kMaxCS + 2 * (sizeof(T) * B + 8));  // mbarrier exchange
-    ring = o; o = align16(o + (kUseRing ? (size_t)kRingDepth * threads * R * sizeof(T) : 0));
     total = o;
   }
 };
@@ -109,40 +100,6 @@ __device__ __forceinline__ void st_remote_s32(void* local_ptr, unsigned rank, in
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
-// ---- point-to-point cluster exchange (mbarrier + st.async), replacing the two cluster barriers
-// per draw: every CTA pushes its total into every CTA's slot and the crossing CTA pushes x_k and
-// the pivot row; each CTA waits only for the bytes it needs (double-buffered by use parity).
-__device__ __forceinline__ unsigned cl_smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ unsigned map_rank(const void* local_ptr, unsigned rank) {
-  unsigned ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(cl_smem_u32(local_ptr)), "r"(rank));
-  return ra;
-}
-__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cl_smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cta.b64 _, [%0], %1;" ::"r"(cl_smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(cl_smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 8 bytes into CTA `rank`'s copy of `local_dst`, completing tx bytes on its copy of `local_bar`
-__device__ __forceinline__ void st_async_f64(void* local_dst, void* local_bar, unsigned rank, double v) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(map_rank(local_dst, rank)),
-               "l"(__double_as_longlong(v)), "r"(map_rank(local_bar, rank))
-               : "memory");
-}
-
 template <typename T, int R, int B, int MAXT, bool STEP = false>
 __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -156,10 +113,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   const int L = p.L, N = p.N, Np = p.Np, Lc = p.Lc;
   const int row0 = (int)rank * Lc + t * R;  // first global row of this thread
 
-  const ClusterLayout<T, B> lay(N, Np, blockDim.x, R);
-  constexpr int kChunks = R * kD / 2;  // 16-byte chunks per thread per column
-  double2* ring = reinterpret_cast<double2*>(smem + lay.ring);
-  auto ring_at = [&](int d, int q) { return ring + ((size_t)(d * kChunks + q) * blockDim.x + t); };
+  const ClusterLayout<T, B> lay(N, Np);
   int* perm = reinterpret_cast<int*>(smem + lay.perm);
   int* pos = reinterpret_cast<int*>(smem + lay.pos);
   double* usel = reinterpret_cast<double*>(smem + lay.usel);
@@ -175,15 +129,6 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   int* xsel = xfree + kMaxCS;                                  // selected row (global)
   T* xrow = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(xsel) + 16);  // [B] pivot row
   T* xstage = xrow + B;                                        // [B] claimer's row (local)
-  // mbarrier exchange: bars [tot0, tot1, row0, row1], totals [2][kMaxCS], rows [2][B] + xsel [2]
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + lay.mbx);
-  double* mtot = reinterpret_cast<double*>(mbar + 4);
-  T* mrow = reinterpret_cast<T*>(mtot + 2 * kMaxCS);
-  double* msel = reinterpret_cast<double*>(mrow + 2 * B);  // x_k as a double (exact for ints)
-  if (t < 4) mbar_init(mbar + t, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  cluster_sync_all();
-  unsigned n_tot = 0, n_row = 0;  // uses of the totals / pivot-row barriers (cluster-uniform)
 
   const int64_t cid = cluster_id_x();
   const int64_t ncl = nclusters_x();
@@ -192,23 +137,6 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
   constexpr int kNone = 0x7fffffff;
   constexpr int kUnset = -0x7fffffff;  // xsel before the crossing CTA's push
 
-  long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // development timing (thread 0): contraction, draws, GJ, draw sub-phases
-  long long tmark = clock64();
-  long long tsub = 0;
-  auto sub = [&](int ph) {  // draw sub-phases (do not move tmark)
-    if (p.timing != nullptr && t == 0) {
-      const long long now = clock64();
-      if (ph >= 0) tph[ph] += now - tsub;
-      tsub = now;
-    }
-  };
-  auto tick = [&](int ph) {
-    if (p.timing != nullptr && t == 0) {
-      const long long now = clock64();
-      tph[ph] += now - tmark;
-      tmark = now;
-    }
-  };
   const int64_t nloc = STEP ? (int64_t)p.Sb : p.M;
   for (int64_t sl = cid; sl < nloc; sl += ncl) {
     const int64_t i = STEP ? p.base + sl : sl;
@@ -286,68 +214,30 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
       }
       }
-      // contraction over the k0 earlier columns. W rows are staged kKC at a time in shared
-      // memory; this thread's R rows of each gathered column perm[ii] are copied global->shared
-      // by cp.async kRingDepth columns ahead into a private ring (no barrier needed for it).
-      {
-        auto issue = [&](int ii) {
-          const double2* src = reinterpret_cast<const double2*>(Utg + (size_t)perm[ii] * p.Lpt + row0);
-#pragma unroll
-          for (int q = 0; q < kChunks; ++q) {
-            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ring_at(ii % kRingDepth, q)));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + q) : "memory");
-          }
-        };
-        if constexpr (kUseRing) {
-#pragma unroll
-          for (int d = 0; d < kRingDepth; ++d) {
-            if (d < k0) issue(d);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-          }
+      // contraction over the k0 earlier columns; W rows are staged kKC at a time in shared memory
+      for (int c0 = 0; c0 < (from_gemm ? 0 : k0); c0 += kKC) {
+        const int kc = min(kKC, k0 - c0);
+        __syncthreads();
+        for (int idx = t; idx < kc * B; idx += blockDim.x) {
+          const int ii = idx / B, c = idx % B;
+          Wb[idx] = c < nb ? Wf[(size_t)(c0 + ii) * Np + k0 + c] : S::zero();
         }
-        for (int c0 = 0; c0 < (from_gemm ? 0 : k0); c0 += kKC) {
-          const int kc = min(kKC, k0 - c0);
-          __syncthreads();
-          for (int idx = t; idx < kc * B; idx += blockDim.x) {
-            const int ii = idx / B, c = idx % B;
-            Wb[idx] = c < nb ? Wf[(size_t)(c0 + ii) * Np + k0 + c] : S::zero();
-          }
-          __syncthreads();
+        __syncthreads();
 #pragma unroll 2
-          for (int i2 = 0; i2 < kc; ++i2) {
-            const int ii = c0 + i2;
-            T v[R];
-            if constexpr (kUseRing) {
-              asm volatile("cp.async.wait_group %0;" ::"n"(kRingDepth - 1) : "memory");
+        for (int i2 = 0; i2 < kc; ++i2) {
+          const T* base = Utg + (size_t)perm[c0 + i2] * p.Lpt + row0;
+          T v[R];
 #pragma unroll
-              for (int q = 0; q < kChunks; ++q) {
-                const double2 d2 = *ring_at(ii % kRingDepth, q);
-                if constexpr (kD == 1) {
-                  reinterpret_cast<double*>(v)[2 * q] = d2.x;
-                  reinterpret_cast<double*>(v)[2 * q + 1] = d2.y;
-                } else {
-                  v[q].re = d2.x;
-                  v[q].im = d2.y;
-                }
-              }
-              if (ii + kRingDepth < k0) issue(ii + kRingDepth);
-              asm volatile("cp.async.commit_group;" ::: "memory");
-            } else {
-              const T* base = Utg + (size_t)perm[ii] * p.Lpt + row0;
+          for (int r = 0; r < R; ++r) v[r] = base[r];
+          T wb[B];
 #pragma unroll
-              for (int r = 0; r < R; ++r) v[r] = base[r];
-            }
-            T wb[B];
+          for (int c = 0; c < B; ++c) wb[c] = Wb[i2 * B + c];
 #pragma unroll
-            for (int c = 0; c < B; ++c) wb[c] = Wb[i2 * B + c];
+          for (int c = 0; c < B; ++c)
 #pragma unroll
-            for (int c = 0; c < B; ++c)
-#pragma unroll
-              for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
-          }
+            for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
         }
-      }  // kUseRing
-      tick(0);
+      }
       // rows drawn earlier: exactly zero weight in the first column of this block
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -363,7 +253,6 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         constexpr int rr = decltype(rrc)::value;
         if (rr < nb) {
           const int k = k0 + rr;
-          sub(-1);
           double w[R], c[R];
           double acc = 0.0;
 #pragma unroll
@@ -373,9 +262,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             c[r] = acc;
           }
           const double incl = warp_incl_scan(acc, lane);
-          // warp totals, double-buffered by draw parity: with the mbarrier exchange no CTA-wide
-          // barrier separates this draw's reads of red from the next draw's writes
-          double* redp = red + (kMbarDraw ? 32 * (n_tot & 1u) : 0);
+          double* redp = red;  // warp totals
           if (lane == 31) redp[warp] = incl;
           __syncthreads();
           double woff, Tc;
@@ -389,21 +276,9 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
           double excl = __shfl_up_sync(0xffffffffu, incl, 1);
           excl = (lane == 0 ? 0.0 : excl) + woff;
           const double* xt = xtot;
-          if constexpr (kMbarDraw) {
-            const unsigned ts = n_tot & 1u, tpar = (n_tot >> 1) & 1u;
-            ++n_tot;
-            if (t == 0) mbar_expect_tx(mbar + ts, 8u * CS);
-            if (t < (int)CS) st_async_f64(&mtot[ts * kMaxCS + rank], mbar + ts, (unsigned)t, Tc);
-            sub(3);
-            mbar_wait(mbar + ts, tpar);  // every CTA's total has landed here
-            xt = mtot + ts * kMaxCS;
-          } else {
-            if (t < (int)CS) st_remote_f64(&xtot[rank], (unsigned)t, Tc);
-            if (t == 0) *xsel = kUnset;  // remote pushes of this step arrive after barrier #1
-            sub(3);
-            cluster_sync_all();  // #1: CTA totals visible
-          }
-          sub(4);
+          if (t < (int)CS) st_remote_f64(&xtot[rank], (unsigned)t, Tc);
+          if (t == 0) *xsel = kUnset;  // remote pushes of this step arrive after barrier #1
+          cluster_sync_all();  // #1: CTA totals visible
           // cluster-uniform T, this CTA's offset and the crossing CTA (lanes q < CS)
           const double u = usel[k];
           double Ttot, off;
@@ -426,13 +301,6 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
           }
           const bool ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
           const double thr = u * Ttot;
-          // the crossing CTA always answers through the row barrier (x_k, or kUnset for the rare path)
-          const bool use_row = kMbarDraw && ok && owner_cta >= 0;
-          const unsigned rsl = n_row & 1u, rpar = (n_row >> 1) & 1u;
-          if (use_row) {
-            ++n_row;
-            if (t == 0) mbar_expect_tx(mbar + 2 + rsl, (unsigned)(sizeof(T) * B + 8));
-          }
           if (ok && owner_cta == (int)rank) {
             const double thl = thr - off;
             const double wt = redp[warp];
@@ -462,58 +330,25 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
               }
               __syncwarp();
               const double* xs_src = reinterpret_cast<const double*>(xstage);
-              if constexpr (kMbarDraw) {
-                double* xr_dst = reinterpret_cast<double*>(mrow + rsl * B);
-                for (int idx = lane; idx < (int)CS * (B * kD + 1); idx += 32) {
-                  const int q = idx / (B * kD + 1), e = idx % (B * kD + 1);
-                  if (e < B * kD) st_async_f64(xr_dst + e, mbar + 2 + rsl, (unsigned)q, xs_src[e]);
-                  else st_async_f64(msel + rsl, mbar + 2 + rsl, (unsigned)q, (double)xs);
-                }
-              } else {
-                double* xr_dst = reinterpret_cast<double*>(xrow);
-                for (int idx = lane; idx < (int)CS * B * kD; idx += 32) {
-                  const int q = idx / (B * kD), e = idx % (B * kD);
-                  st_remote_f64(xr_dst + e, (unsigned)q, xs_src[e]);
-                }
-                if (lane < (int)CS) st_remote_s32(xsel, (unsigned)lane, xs);
+              double* xr_dst = reinterpret_cast<double*>(xrow);
+              for (int idx = lane; idx < (int)CS * B * kD; idx += 32) {
+                const int q = idx / (B * kD), e = idx % (B * kD);
+                st_remote_f64(xr_dst + e, (unsigned)q, xs_src[e]);
               }
+              if (lane < (int)CS) st_remote_s32(xsel, (unsigned)lane, xs);
               if (lane == ln) chosen |= 1u << rsel;
-            } else if (kMbarDraw && mine) {
-              // no row crosses in the responsible warp (rounding): tell every CTA to take the
-              // rare, cluster-uniform round
-              double* xr_dst = reinterpret_cast<double*>(mrow + rsl * B);
-              for (int idx = lane; idx < (int)CS * (B * kD + 1); idx += 32) {
-                const int q = idx / (B * kD + 1), e = idx % (B * kD + 1);
-                if (e < B * kD) st_async_f64(xr_dst + e, mbar + 2 + rsl, (unsigned)q, 0.0);
-                else st_async_f64(msel + rsl, mbar + 2 + rsl, (unsigned)q, (double)kUnset);
-              }
             }
           }
-          if (p.trace != nullptr && i < p.S) {
+          if (p.trace != nullptr && (uint64_t)(i - p.S0) < (uint64_t)p.S) {
             const double inv = Ttot > 0.0 ? 1.0 / Ttot : 0.0;
-            double* tr = p.trace + (i * Np + k) * (int64_t)L;
+            double* tr = p.trace + ((i - p.S0) * Np + k) * (int64_t)L;
 #pragma unroll
             for (int r = 0; r < R; ++r)
               if (row0 + r < L) tr[row0 + r] = w[r] * inv;
           }
-          sub(5);
-          int xsel_k;
+          cluster_sync_all();  // #2: x_k and the pivot row visible in every CTA
+          int xsel_k = *xsel;
           const T* xr = xrow;
-          if constexpr (kMbarDraw) {
-            if (use_row) {
-              mbar_wait(mbar + 2 + rsl, rpar);  // x_k and the pivot row have landed here
-              xsel_k = (int)msel[rsl];
-              xr = mrow + rsl * B;
-            } else {
-              xsel_k = kUnset;
-            }
-            if (xsel_k == kUnset && t == 0) *xsel = kUnset;
-            if (xsel_k == kUnset) __syncthreads();
-          } else {
-            cluster_sync_all();  // #2: x_k and the pivot row visible in every CTA
-            xsel_k = *xsel;
-          }
-          sub(6);
           if (xsel_k == kUnset) {
             // rare (cluster-uniform): T not finite/positive -> smallest unchosen row (flag bit0);
             // no crossing -> the crossing CTA's (or, without one, the cluster's) last positive row
@@ -594,11 +429,9 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             for (int r = 0; r < R; ++r)
               P[r][cc] = (cc == rr + 1 && ((chosen >> r) & 1u)) ? S::zero() : S::fms(lmul[r], pc, P[r][cc]);
           }
-          sub(7);
         }
       });
 
-      tick(1);
       // ---- Gauss-Jordan update of W with the nb new rows, columns split over the cluster
       // (thread <-> one later column j; the new rows' entries in columns < k0 and W's rows < k0
       // are staged kKC at a time through shared memory)
@@ -699,11 +532,9 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         __threadfence();
         cluster_sync_all();  // W visible to every CTA before the next block's Wb load
       }
-      tick(2);
       if constexpr (STEP) break;
     }
     // ---- a6: positions (rank 0) and flags (OR over the cluster, collected in rank 0)
-    tick(2);
     const int fcta = (__syncthreads_or(flag & 1) ? 1 : 0) | (__syncthreads_or(flag & 2) ? 2 : 0);
     if constexpr (STEP) {
       const int nbs = min(B, Np - p.k0);
@@ -726,8 +557,6 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
     }
     cluster_sync_all();
   }
-  if (p.timing != nullptr && t == 0)
-    for (int q = 0; q < 8; ++q) atomicAdd(p.timing + q, (unsigned long long)tph[q]);
 }
 
 }  // namespace ffsk

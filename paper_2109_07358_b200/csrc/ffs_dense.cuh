@@ -213,7 +213,6 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   const int jl = jg * CPT;                        // first column of this thread within the tile
   const int j = k1 + blockIdx.x * kGjTJ + jl;     // first global column
   const bool has = j < Np;
-  const bool full = j + CPT - 1 < Np;             // every column of the group in range
   T* Vn = reinterpret_cast<T*>(smem);   // [k0][B]   V[X_new, 0:k0] transposed (a row's B values contiguous)
   T* Zp = Vn + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
   T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
@@ -243,16 +242,20 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   };
   stage(Vn, B * k0, [&](int idx) { return Ug[(size_t)xn[idx % B] * N + pm[idx / B]]; });
   __syncthreads();
+  // 16-byte W accesses only when every row start is 16-byte aligned (N' even); the pair of
+  // columns j, j+1 is loaded element-wise otherwise, and a pair past N' keeps its second slot 0
+  const bool two = j + 1 < Np;
+  const bool vec = two && (Np & 1) == 0;
   auto ldw = [&](int ii, T (&w)[CPT]) {
     const T* src = W + (size_t)ii * Np + j;
     if constexpr (CPT == 2) {
-      if (full) {
+      if (vec) {
         const double2 v = *reinterpret_cast<const double2*>(src);
         w[0] = v.x;
         w[1] = v.y;
       } else {
         w[0] = src[0];
-        w[1] = S::zero();
+        w[1] = two ? src[1] : S::zero();
       }
     } else {
       w[0] = src[0];
@@ -343,8 +346,12 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
       }
       T* dst = W + (size_t)ii * Np + j;
       if constexpr (CPT == 2) {
-        if (full) *reinterpret_cast<double2*>(dst) = make_double2(a[0], a[1]);
-        else dst[0] = a[0];
+        if (vec) {
+          *reinterpret_cast<double2*>(dst) = make_double2(a[0], a[1]);
+        } else {
+          dst[0] = a[0];
+          if (two) dst[1] = a[1];
+        }
       } else {
         dst[0] = a[0];
       }
@@ -383,19 +390,23 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
 // ---------------------------------------------------------------- Ozaki-emulated FP64 GEMM
 // P = U Y on the INT8 tensor cores (tcgen05.mma.kind::i8, TMEM accumulators). Rows of A (= U, or
 // its real L x 2N view) and columns of B (= Y, or its real expansion) are scaled by powers of two
-// (frexp: |x 2^-e| < 1) and split into kOzS signed 7-bit slices: x = 2^e sum_i q_i 2^{-7(i+1)}.
-// The slice products A_i B_j with i + j < kOzS are exact in int32 (|q| <= 127, K <= 4096); the CTA
-// keeps the kOzS partial sums D_d = sum_{i+j=d} A_i B_j of its 128 x 64 tile in kOzS TMEM
-// accumulators and the epilogue forms 2^(ea + eb) sum_d 2^{-7(d+2)} D_d in fp64. The dropped
-// terms (i + j >= kOzS) are below 2^-49 of the row/column scales: normwise weight error <= 2.2e-13
-// on the C2/C4/C5 panels (tools/ozaki_floor.py, profiles/ozaki_floor_r01.txt; bound 1e-10).
-// Operands reach shared memory by TMA (3-D tensor maps [kOzS][rows][Kp], 64-byte swizzle) issued
+// (frexp: |x 2^-e| < 1) and split into NS signed 7-bit slices: x = 2^e sum_i q_i 2^{-7(i+1)}.
+// The slice products A_i B_j with i + j < NS are exact in int32 (|q| <= 127; NS (K) 127^2 < 2^31
+// for K <= 16384); the CTA keeps the NS partial sums D_d = sum_{i+j=d} A_i B_j of its 128 x 64
+// tile in NS TMEM accumulators (NS x 64 <= 512 columns) and the epilogue forms
+// 2^(ea + eb) sum_d 2^{-7(d+2)} D_d in fp64. The dropped terms (i + j >= NS) are below
+// 2^-(7 NS) of the row/column scales: NS = 8 (the default) leaves a normwise panel error of
+// <= 1.3e-15, the level of a native fp64 GEMM; NS = 7 leaves <= 2.2e-13 (tools/ozaki_floor.py,
+// profiles/ozaki_floor_r01.txt).
+// Operands reach shared memory by TMA (3-D tensor maps [NS][rows][Kp], 64-byte swizzle) issued
 // by one thread; one thread issues the MMAs; full/empty mbarriers hand the two stages over.
-constexpr int kOzS = 7;
+constexpr int kOzMaxS = 8;
 constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64, kOzStages = 2, kOzThreads = 320;  // 8 epilogue warps + TMA + MMA
 constexpr int kOzTA = kOzBM * kOzBK, kOzTB = kOzBN * kOzBK;
-constexpr int kOzStageBytes = kOzS * (kOzTA + kOzTB);
-constexpr size_t kOzSmem = (size_t)kOzStages * kOzStageBytes + (2 * kOzStages + 1) * 8 + 16 + 1024;
+template <int NS> constexpr int oz_stage_bytes() { return NS * (kOzTA + kOzTB); }
+template <int NS>
+constexpr size_t oz_smem() { return (size_t)kOzStages * oz_stage_bytes<NS>() + (2 * kOzStages + 1) * 8 + 16 + 1024; }
+static_assert(oz_smem<kOzMaxS>() <= 227 * 1024, "two stages of 8 slices fit shared memory");
 
 struct OzakiParams {
   const int* ea;  // [M] row exponents of A
@@ -427,12 +438,13 @@ __device__ __forceinline__ void oz_mbar_wait(uint64_t* b, unsigned parity) {
       : "memory");
 }
 
+template <int NS>
 static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                             const __grid_constant__ CUtensorMap tmB,
                                                                             const OzakiParams p) {
   extern __shared__ __align__(1024) unsigned char oz_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kOzStages * kOzStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kOzStages * oz_stage_bytes<NS>());
   uint64_t* empty = full + kOzStages;
   uint64_t* done = empty + kOzStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
@@ -460,11 +472,11 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
     for (int kt = 0; kt < KT; ++kt) {
       const int st = kt % kOzStages;
       if (kt >= kOzStages) oz_mbar_wait(empty + st, ((kt / kOzStages) - 1) & 1);
-      unsigned char* sb = sm + st * kOzStageBytes;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)), "r"(kOzStageBytes)
+      unsigned char* sb = sm + st * oz_stage_bytes<NS>();
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)), "r"(oz_stage_bytes<NS>())
                    : "memory");
 #pragma unroll
-      for (int i = 0; i < kOzS; ++i) {
+      for (int i = 0; i < NS; ++i) {
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
                 oz_u32(sb + i * kOzTA)),
@@ -472,7 +484,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
             : "memory");
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                oz_u32(sb + kOzS * kOzTA + i * kOzTB)),
+                oz_u32(sb + NS * kOzTA + i * kOzTB)),
             "l"(&tmB), "r"(kt * kOzBK), "r"(n0), "r"(i), "r"(oz_u32(full + st))
             : "memory");
       }
@@ -483,15 +495,15 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
       const int st = kt % kOzStages;
       oz_mbar_wait(full + st, (kt / kOzStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned char* sb = sm + st * kOzStageBytes;
+      const unsigned char* sb = sm + st * oz_stage_bytes<NS>();
 #pragma unroll
-      for (int i = 0; i < kOzS; ++i)
+      for (int i = 0; i < NS; ++i)
 #pragma unroll
-        for (int j = 0; j < kOzS - i; ++j)
+        for (int j = 0; j < NS - i; ++j)
 #pragma unroll
           for (int ks = 0; ks < kOzBK / 32; ++ks) {
             const uint64_t da = oz_desc(sb + i * kOzTA + ks * 32);
-            const uint64_t db = oz_desc(sb + kOzS * kOzTA + j * kOzTB + ks * 32);
+            const uint64_t db = oz_desc(sb + NS * kOzTA + j * kOzTB + ks * 32);
             const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first write of D_{i+j}: i = 0
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
@@ -515,7 +527,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
 #pragma unroll
     for (int c = 0; c < kEC; ++c) acc[c] = 0.0;
 #pragma unroll
-    for (int d = kOzS - 1; d >= 0; --d) {  // smallest terms first
+    for (int d = NS - 1; d >= 0; --d) {  // smallest terms first
       const double sc = ldexp(1.0, -7 * (d + 2));
       {
         constexpr int cb = 0;
@@ -561,10 +573,11 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
 
 // x = 2^e sum_i q_i 2^{-7(i+1)}, |q_i| <= 127 (frexp exponent: |x 2^-e| < 1); q_i of element k of
 // row r goes to out[(i * rows + r) * Kp + k]; zero for k in [K, Kp)
-__device__ __forceinline__ void oz_split_value(double v, int ex, int8_t (&q)[kOzS]) {
+template <int NS>
+__device__ __forceinline__ void oz_split_value(double v, int ex, int8_t (&q)[NS]) {
   double r = ldexp(v, -ex);
 #pragma unroll
-  for (int i = 0; i < kOzS; ++i) {
+  for (int i = 0; i < NS; ++i) {
     const double f = trunc(r * 128.0);
     q[i] = (int8_t)f;
     r = r * 128.0 - f;
@@ -572,6 +585,7 @@ __device__ __forceinline__ void oz_split_value(double v, int ex, int8_t (&q)[kOz
 }
 
 // rows of a row-major [rows][ldx] fp64 matrix (one warp per row)
+template <int NS>
 static __global__ void ffs_ozaki_split_rows_kernel(const double* __restrict__ X, int rows, int K, int64_t ldx,
                                                    int8_t* __restrict__ out, int Kp, int* __restrict__ e) {
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -585,15 +599,16 @@ static __global__ void ffs_ozaki_split_rows_kernel(const double* __restrict__ X,
   if (mx > 0.0) frexp(mx, &ex);
   if (lane == 0) e[r] = ex;
   for (int k = lane; k < Kp; k += 32) {
-    int8_t q[kOzS];
-    oz_split_value(k < K ? xr[k] : 0.0, ex, q);
+    int8_t q[NS];
+    oz_split_value<NS>(k < K ? xr[k] : 0.0, ex, q);
 #pragma unroll
-    for (int i = 0; i < kOzS; ++i) out[((size_t)i * rows + r) * Kp + k] = q[i];
+    for (int i = 0; i < NS; ++i) out[((size_t)i * rows + r) * Kp + k] = q[i];
   }
 }
 
 // columns of a row-major [K][ldy] fp64 matrix (32 columns per CTA of 256 threads): column c's
 // slices are written K-major, out[(i * ncols + c) * Kp + k]
+template <int NS>
 static __global__ void __launch_bounds__(256) ffs_ozaki_split_cols_kernel(const double* __restrict__ Y, int K, int ncols,
                                                                          int64_t ldy, int8_t* __restrict__ out, int Kp,
                                                                          int* __restrict__ e) {
@@ -621,16 +636,16 @@ static __global__ void __launch_bounds__(256) ffs_ozaki_split_cols_kernel(const 
     {
       const int cc = t >> 3, k8 = (t & 7) * 8;  // 32 columns x 8 groups of 8 k
       const int ex = (int)red[0][cc];
-      int8_t q8[kOzS][8];
+      int8_t q8[NS][8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        int8_t q[kOzS];
-        oz_split_value(tile[k8 + u][cc], ex, q);
+        int8_t q[NS];
+        oz_split_value<NS>(tile[k8 + u][cc], ex, q);
 #pragma unroll
-        for (int i = 0; i < kOzS; ++i) q8[i][u] = q[i];
+        for (int i = 0; i < NS; ++i) q8[i][u] = q[i];
       }
 #pragma unroll
-      for (int i = 0; i < kOzS; ++i) {
+      for (int i = 0; i < NS; ++i) {
         uint64_t w = 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) w |= (uint64_t)(uint8_t)q8[i][u] << (8 * u);

@@ -38,11 +38,10 @@ struct Params {
   int32_t* positions;      // [M][Np]
   int32_t* flags;          // [M] or null
   double* wfull;           // per owner [Np][Np] scalars
-  int64_t S;               // debug trace: first S samples
+  int64_t S0, S;           // debug trace of samples S0 .. S0+S-1
   double* trace;           // [S][Np][L] or null
   size_t owner_smem;       // bytes of per-owner shared memory
   size_t ushared_smem;     // bytes of the shared U^T copy (shared-U path)
-  int dbg;                 // development switches (FFS_DEBUG_SKIP)
 };
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
@@ -320,7 +319,7 @@ ffs_sample_kernel(const Params p) {
         for (int r = 0; r < R; ++r) P[r][c] = v[r];
       }
 #pragma unroll 4
-      for (int ii = 0; ii < ((p.dbg & 1) ? 0 : k0); ++ii) {  // dbg bit0: development, WRONG results
+      for (int ii = 0; ii < k0; ++ii) {
         T v[R];
         load_col<T, R, USMEM>(p, Uts, perm[ii], t, v);
         T wb[B];
@@ -357,9 +356,9 @@ ffs_sample_kernel(const Params p) {
               }
             pos[k] = xk;
           }
-          if (p.trace != nullptr && i < p.S) {
+          if (p.trace != nullptr && (uint64_t)(i - p.S0) < (uint64_t)p.S) {
             double inv = Ttot > 0.0 ? 1.0 / Ttot : 0.0;
-            double* tr = p.trace + (i * Np + k) * (int64_t)L;
+            double* tr = p.trace + ((i - p.S0) * Np + k) * (int64_t)L;
 #pragma unroll
             for (int r = 0; r < R; ++r)
               if (t * R + r < L) tr[t * R + r] = w[r] * inv;
@@ -381,7 +380,7 @@ ffs_sample_kernel(const Params p) {
         }
       });
       // ---- Gauss-Jordan update of W with the nb new rows (only if later columns remain)
-      if (k0 + nb < Np && !(p.dbg & 4)) {  // dbg bit2: development, WRONG results
+      if (k0 + nb < Np) {
         gsync<WARP>();
         for (int idx = t; idx < nb * Np; idx += G) {
           const int tt = idx / Np, j = idx % Np;

@@ -5,22 +5,18 @@
 #include "ffs_kernel.cuh"
 #include "ffs_warp_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
-#include "ffs_mma_kernel.cuh"
 
 namespace ffsk {
 template <typename T, bool WARP, int R, int B, bool USMEM, int MAXT> const void* sample_kernel_ptr() {
   return reinterpret_cast<const void*>(&ffs_sample_kernel<T, WARP, R, B, USMEM, MAXT>);
 }
-template <int R, int B, int G, int MAXT, bool TIMING, int OPT> const void* seg_kernel_ptr() {
-  return reinterpret_cast<const void*>(&ffs_seg_kernel<R, B, G, MAXT, TIMING, OPT>);
+template <int R, int B, int G, int MAXT> const void* seg_kernel_ptr() {
+  return reinterpret_cast<const void*>(&ffs_seg_kernel<R, B, G, MAXT>);
 }
 template <typename T, int R, int B, int MAXT> const void* cluster_kernel_ptr() {
   return reinterpret_cast<const void*>(&ffs_cluster_kernel<T, R, B, MAXT>);
 }
 template <typename T, int R, int B, int MAXT> const void* cluster_step_kernel_ptr() {
   return reinterpret_cast<const void*>(&ffs_cluster_kernel<T, R, B, MAXT, true>);
-}
-template <int MAXT> const void* mma_kernel_ptr() {
-  return reinterpret_cast<const void*>(&ffs_mma_kernel<MAXT>);
 }
 }  // namespace ffsk

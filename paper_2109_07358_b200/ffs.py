@@ -17,6 +17,18 @@ from . import build as _build
 FFS_F64, FFS_C128 = 0, 1
 FFS_OK, FFS_EINVAL, FFS_ECUDA, FFS_ENOWS = 0, -1, -2, -3
 
+# include/ffs.h ffs_option
+OPTIONS = {
+    "dense_gemm": 1,        # 8 = Ozaki int8 x 8 slices (default), 7 = 7 slices, 0 = DMMA
+    "dense_theta": 2,       # gathered/GEMM crossover fraction (< 0: default)
+    "dense_batch": 3,       # samples per lockstep batch (0: default)
+    "block_step": 4,        # 1: large-L block-step paths (default); 0: per-sample cluster kernel
+    "large_l_marginal": 5,  # 1: large-L marginals on the block-step kernels (default)
+    "cluster": 6,           # 1: L >= 2048 on cluster kernels (default); 0: one CTA per sample
+    "graph": 7,             # 1: block-step launches replayed as a CUDA graph (default)
+    "force_generic": 8,     # 1: every shape on the per-sample warp/CTA-owner kernel
+}
+
 EXPORTED = (
     "ffs_workspace_bytes",
     "ffs_sample",
@@ -27,6 +39,8 @@ EXPORTED = (
     "ffs_last_launch_count",
     "ffs_profile_enable",
     "ffs_last_kernel_ms",
+    "ffs_set_option",
+    "ffs_get_option",
     "ffs_last_error",
 )
 
@@ -57,13 +71,16 @@ def load(build_if_missing: bool = True):
     L.ffs_workspace_bytes.restype = sz
     L.ffs_sample.argtypes = [vp, i64, i64, ci, i64, vp, vp, vp, vp, sz, vp]
     L.ffs_sample_marginal.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp]
-    L.ffs_debug_trace.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp, i64, vp]
+    L.ffs_debug_trace.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp, i64, i64, vp]
     L.ffs_host_workspace_bytes.argtypes = [i64, i64, i64, ci, i64]
     L.ffs_host_workspace_bytes.restype = sz
     L.ffs_sample_host.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp]
     L.ffs_last_launch_count.restype = ci
     L.ffs_profile_enable.argtypes = [ci]
     L.ffs_last_kernel_ms.restype = ctypes.c_float
+    L.ffs_set_option.argtypes = [ci, ctypes.c_double]
+    L.ffs_get_option.argtypes = [ci]
+    L.ffs_get_option.restype = ctypes.c_double
     L.ffs_last_error.restype = ctypes.c_char_p
     _lib = L
     return L
@@ -108,6 +125,20 @@ def ffs_last_kernel_ms() -> float:
     return float(load().ffs_last_kernel_ms())
 
 
+def set_option(name: str, value: float) -> None:
+    """ffs_set_option (include/ffs.h): a NaN value restores the default."""
+    _check(load().ffs_set_option(OPTIONS[name], float(value)))
+
+
+def get_option(name: str) -> float:
+    return float(load().ffs_get_option(OPTIONS[name]))
+
+
+def reset_options() -> None:
+    for name in OPTIONS:
+        set_option(name, float("nan"))
+
+
 class Workspace:
     """Caller-owned device workspace (torch allocation), grown on demand."""
 
@@ -121,6 +152,27 @@ class Workspace:
         if self.buf is None or self.buf.numel() < nbytes:
             self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         return self.buf.data_ptr(), self.buf.numel()
+
+
+def _check_out(t: Optional[torch.Tensor], shape, name: str, cuda: bool):
+    """Caller-supplied outputs: int32, contiguous, the exact shape, on the right side."""
+    if t is None:
+        return
+    if t.dtype != torch.int32 or tuple(t.shape) != tuple(shape) or not t.is_contiguous() or t.is_cuda != cuda:
+        where = "CUDA" if cuda else "host"
+        raise FFSError(f"{name} must be a contiguous int32 {where} tensor of shape {tuple(shape)}, "
+                       f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+
+
+def _keep_alive(stream, *tensors):
+    """The library works asynchronously on `stream`: tell the caching allocator that these
+    tensors (temporaries included) are in use there, so their memory is not handed to other work
+    on torch's current stream before the kernels finish."""
+    if stream is None:
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
 
 
 def _prep(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int):
@@ -143,6 +195,8 @@ def ffs_sample_marginal(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int,
     L, N = U.shape
     M = uniforms.shape[0]
     dt = _dtype_code(U)
+    _check_out(positions, (M, Nprime), "positions", True)
+    _check_out(flags, (M,), "flags", True)
     if positions is None:
         positions = torch.empty((M, Nprime), dtype=torch.int32, device=U.device)
     if flags is None and with_flags:
@@ -150,12 +204,13 @@ def ffs_sample_marginal(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int,
     ws = workspace if workspace is not None else Workspace(U.device)
     need = ffs_workspace_bytes(L, N, Nprime, dt, M)
     if need == 0 and M > 0:
-        _check(FFS_EINVAL)
+        _check(load().ffs_sample_marginal(U.data_ptr(), L, N, dt, M, Nprime, None, None, None, None, 0, None))
     wp, wn = ws.get(need)
     rc = load().ffs_sample_marginal(U.data_ptr(), L, N, dt, M, Nprime, uniforms.data_ptr(), positions.data_ptr(),
                                     flags.data_ptr() if flags is not None else None, wp, wn,
                                     _stream_handle(stream, U.device))
     _check(rc)
+    _keep_alive(stream, U, uniforms, positions, flags, ws.buf)
     return (positions, flags) if with_flags else positions
 
 
@@ -168,6 +223,8 @@ def ffs_sample(U: torch.Tensor, uniforms: torch.Tensor, positions: Optional[torc
     L = U.shape[0]
     M = uniforms.shape[0]
     dt = _dtype_code(U)
+    _check_out(positions, (M, N), "positions", True)
+    _check_out(flags, (M,), "flags", True)
     if positions is None:
         positions = torch.empty((M, N), dtype=torch.int32, device=U.device)
     if flags is None and with_flags:
@@ -178,25 +235,28 @@ def ffs_sample(U: torch.Tensor, uniforms: torch.Tensor, positions: Optional[torc
                            flags.data_ptr() if flags is not None else None, wp, wn,
                            _stream_handle(stream, U.device))
     _check(rc)
+    _keep_alive(stream, U, uniforms, positions, flags, ws.buf)
     return (positions, flags) if with_flags else positions
 
 
-def ffs_debug_trace(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int, S: int,
+def ffs_debug_trace(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int, S: int, S0: int = 0,
                     workspace: Optional[Workspace] = None, stream=None):
-    """Positions [M][N'], flags [M] and normalised weights [S][N'][L] of the first S samples."""
+    """Positions [M][N'], flags [M] and normalised weights [S][N'][L] of samples S0 .. S0+S-1."""
     U, uniforms = _prep(U, uniforms, Nprime)
     L, N = U.shape
     M = uniforms.shape[0]
     dt = _dtype_code(U)
-    S = min(S, M)
+    S = max(0, min(S, M - S0))
     positions = torch.empty((M, Nprime), dtype=torch.int32, device=U.device)
     flags = torch.empty(M, dtype=torch.int32, device=U.device)
     weights = torch.zeros((S, Nprime, L), dtype=torch.float64, device=U.device)
     ws = workspace if workspace is not None else Workspace(U.device)
     wp, wn = ws.get(ffs_workspace_bytes(L, N, Nprime, dt, M))
     rc = load().ffs_debug_trace(U.data_ptr(), L, N, dt, M, Nprime, uniforms.data_ptr(), positions.data_ptr(),
-                                flags.data_ptr(), wp, wn, _stream_handle(stream, U.device), S, weights.data_ptr())
+                                flags.data_ptr(), wp, wn, _stream_handle(stream, U.device), S0, S,
+                                weights.data_ptr())
     _check(rc)
+    _keep_alive(stream, U, uniforms, positions, flags, weights, ws.buf)
     return positions, flags, weights
 
 
@@ -211,6 +271,10 @@ def ffs_sample_host(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int,
     L, N = U.shape
     M = uniforms.shape[0]
     dt = _dtype_code(U)
+    if uniforms.dtype != torch.float64 or uniforms.dim() != 2 or uniforms.shape[1] != 2 * Nprime:
+        raise FFSError(f"uniforms must be float64 [M][2N'] with N'={Nprime}, got {tuple(uniforms.shape)}")
+    _check_out(positions, (M, Nprime), "positions", False)
+    _check_out(flags, (M,), "flags", False)
     if positions is None:
         positions = torch.empty((M, Nprime), dtype=torch.int32, pin_memory=True)
     ws = workspace if workspace is not None else Workspace(device)

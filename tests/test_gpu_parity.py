@@ -27,12 +27,22 @@ def _to_dev(U):
     return torch.from_numpy(np.ascontiguousarray(U)).cuda()
 
 
-def run_gpu(U, uni, Np, trace_S=0):
+@pytest.fixture(autouse=True)
+def _default_options():
+    """Every test starts and ends with the library's default tuning options."""
+    if torch.cuda.is_available():
+        _ffs().reset_options()
+    yield
+    if torch.cuda.is_available():
+        _ffs().reset_options()
+
+
+def run_gpu(U, uni, Np, trace_S=0, trace_S0=0):
     ffs = _ffs()
     Ud = _to_dev(U)
     ud = torch.from_numpy(uni).cuda()
     if trace_S:
-        pos, flags, w = ffs.ffs_debug_trace(Ud, ud, Np, trace_S)
+        pos, flags, w = ffs.ffs_debug_trace(Ud, ud, Np, trace_S, S0=trace_S0)
         torch.cuda.synchronize()
         return pos.cpu().numpy(), flags.cpu().numpy(), w.cpu().numpy()
     if Np == U.shape[1]:
@@ -88,15 +98,24 @@ def test_tiny_config_full_M_bitexact_and_chisquare():
     assert pval > 1e-3, (stat, dof, pval)
 
 
-# (config, N', oracle prefix size, trace samples)
+# (config, N', oracle sample indices, traced samples): the compared samples are spread over the
+# whole run (first / middle / last tiles, clusters and lockstep batches), and the traced samples
+# are the LAST ones of the full-size launch (ffs_debug_trace S0), so the weights are checked in
+# the last tiles too. Sizes: what the oracle on the GPU box's host cores finishes in ~1 minute.
+def _spread(M, n):
+    return sorted(set(np.linspace(0, M - 1, n).round().astype(int).tolist()))
+
+
 FULL = [
     ("dw", None, 3000, 4),
     ("anderson", None, 300, 2),
     ("anderson", 16, 4000, 8),
-    ("peierls", None, 6, 1),
-    ("dpp", None, 3, 1),
+    ("peierls", None, 12, 2),
+    ("dpp", None, 6, 1),
     ("dpp", 64, 400, 4),
 ]
+
+FULL_WEIGHT_TOL = 1e-11  # 10x inside the 1e-10 bound: emulation or blocking drift shows before parity breaks
 
 
 @pytest.mark.parametrize("name,Np,n_ref,n_trace", FULL)
@@ -106,19 +125,23 @@ def test_full_size_configs(name, Np, n_ref, n_trace):
     Np = cfg.N if Np is None else Np
     M = cfg.M if Np == cfg.N else cfg.marginal_M
     uni = inputs.uniforms(M, Np, cfg.uniform_seed + (0 if Np == cfg.N else 100))
-    gpos, gflags, _ = run_gpu(U, uni, Np)
+    gpos, gflags, tw = run_gpu(U, uni, Np, trace_S=n_trace, trace_S0=M - n_trace)
     assert (gflags == 0).all()
     assert gpos.min() >= 0 and gpos.max() < cfg.L
     srt = np.sort(gpos, axis=1)
     assert (np.diff(srt, axis=1) > 0).all()  # Pauli exclusion, every sample
-    rpos = ref.sample(U, uni[:n_ref], Np=Np)
-    r = compare_positions(U, uni, gpos, rpos, Np)
+    idx = np.array(_spread(M, n_ref))
+    rpos = ref.sample(U, uni[idx], Np=Np)
+    r = compare_positions(U, uni[idx], gpos[idx], rpos, Np)
+    print(f"\n{name} N'={Np}: {r['exact']}/{len(idx)} compared samples bit-exact "
+          f"(indices {idx[0]}..{idx[-1]}), {r['ties']} CDF-boundary ties")
     assert not r["failures"], r["failures"][:5]
-    # weights along the path for the first samples (debug trace of the same kernel)
-    tpos, _, tw = run_gpu(U, uni[:n_trace], Np, trace_S=n_trace)
-    assert (tpos == gpos[:n_trace]).all()
-    _, rw = ref.weights(U, uni[:n_trace], Np=Np)
-    assert compare_weights(tw, rw, tpos, rpos[:n_trace]) <= WEIGHT_TOL
+    # weights along the path of the last n_trace samples of the full-size launch
+    last = np.arange(M - n_trace, M)
+    rlast, rw = ref.weights(U, uni[last], Np=Np)
+    err = compare_weights(tw, rw, gpos[last], rlast)
+    print(f"{name} N'={Np}: max normwise weight error {err:.3e} over samples {last[0]}..{last[-1]}")
+    assert err <= FULL_WEIGHT_TOL
     # property at full size: occupation of each site = K_xx * N'/N (exchangeable order)
     K = np.sum(np.abs(U) ** 2, axis=1) * (Np / cfg.N)
     check_occupations(gpos, K, M)
@@ -151,8 +174,22 @@ def test_edge_cases():
     assert L.ffs_sample(Ud.data_ptr(), 10, 11, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
     assert L.ffs_sample_marginal(Ud.data_ptr(), 10, 3, 0, 4, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
     assert L.ffs_sample(Ud.data_ptr(), 10, 3, 9, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
-    assert L.ffs_sample(Ud.data_ptr(), 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    # no / too small workspace: FFS_ENOWS
+    assert L.ffs_sample(Ud.data_ptr(), 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == ffs.FFS_ENOWS
     assert L.ffs_sample(None, 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    # L beyond the supported range (16384 real, 8192 complex): FFS_EINVAL, never truncated
+    assert L.ffs_workspace_bytes(16385, 8, 8, 0, 4) == 0
+    assert L.ffs_workspace_bytes(8193, 8, 8, 1, 4) == 0
+    assert L.ffs_sample(Ud.data_ptr(), 16385, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    assert "unsupported L" in L.ffs_last_error().decode()
+    # trace range outside [0, M)
+    assert L.ffs_debug_trace(Ud.data_ptr(), 10, 3, 0, 4, 3, ud.data_ptr(), pos.data_ptr(), None, None, 0, None,
+                             3, 2, pos.data_ptr()) == -1
+    # caller-supplied outputs are validated by the binding
+    with pytest.raises(ffs.FFSError):
+        ffs.ffs_sample(Ud, ud, positions=torch.empty((4, 2), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ffs.FFSError):
+        ffs.ffs_sample(Ud, ud, positions=torch.empty((4, 3), dtype=torch.int64, device="cuda"))
     # N = 1, N' = 1, L = N (full filling)
     for (l, n, np_) in [(9, 1, 1), (12, 5, 1), (6, 6, 6), (33, 33, 33)]:
         Ue = inputs.random_orthonormal(l, n, l + n)
@@ -208,35 +245,68 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
     assert not (gfl & 1).any()
 
 
-# Lockstep-dense path schedules (ffs_abi.cu launch_dense): several batches with a ragged last one
-# (FFS_DENSE_S), all-GEMM (theta 0; Ozaki-emulated GEMM by default, the DMMA GEMM with
-# FFS_DENSE_GEMM=dmma), all-gathered (theta 1) and the default hybrid; real and complex; the
-# environment is read per call, so each case runs the same kernels in another order.
+# Lockstep-dense path schedules (ffs_abi.cu launch_dense): several batches with a ragged last one,
+# all-GEMM (theta 0) with each GEMM (Ozaki 8 slices = default, Ozaki 7, DMMA), all-gathered
+# (theta 1), the default hybrid, with and without the CUDA-graph driver; real and complex.
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("env", [{"FFS_DENSE_S": "16"}, {"FFS_DENSE_THETA": "0"}, {"FFS_DENSE_THETA": "1"},
-                                 {"FFS_DENSE_S": "7", "FFS_DENSE_THETA": "0.5"},
-                                 {"FFS_DENSE_THETA": "0", "FFS_DENSE_GEMM": "dmma"}])
-def test_dense_path_schedules(env, cplx, monkeypatch):
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+@pytest.mark.parametrize("opts", [{"dense_batch": 16}, {"dense_theta": 0}, {"dense_theta": 1},
+                                  {"dense_batch": 7, "dense_theta": 0.5},
+                                  {"dense_theta": 0, "dense_gemm": 7},
+                                  {"dense_theta": 0, "dense_gemm": 0},
+                                  {"dense_theta": 0.3, "graph": 0}])
+def test_dense_path_schedules(opts, cplx):
+    ffs = _ffs()
+    for k, v in opts.items():
+        ffs.set_option(k, v)
     L, N = 2100, 258  # L: 2 clusters' rows with a ragged tail; N' = N: ragged last panel block
     U = inputs.random_orthonormal(L, N, 77 + int(cplx), complex_=cplx)
-    uni = inputs.uniforms(40, N, 4242)
-    gpos, gflags, gw = run_gpu(U, uni, N, trace_S=2)
+    M = 40
+    uni = inputs.uniforms(M, N, 4242)
+    gpos, gflags, gw = run_gpu(U, uni, N, trace_S=2, trace_S0=M - 2)
     rpos = ref.sample(U, uni, Np=N)
     r = compare_positions(U, uni, gpos, rpos, N)
     assert not r["failures"], r["failures"][:3]
     assert (gflags == 0).all()
-    _, rw = ref.weights(U, uni[:2], Np=N)
-    assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
+    _, rw = ref.weights(U, uni[M - 2:], Np=N)
+    assert compare_weights(gw, rw, gpos[M - 2:], rpos[M - 2:]) <= WEIGHT_TOL
+
+
+def test_graph_replay_matches_direct_launches():
+    """The CUDA-graph driver replays the captured block loop: a second call with the same buffers
+    (graph reuse) and a call with new buffers (graph update) give the direct-launch result."""
+    ffs = _ffs()
+    L, N, M = 2100, 258, 24
+    U = _to_dev(inputs.random_orthonormal(L, N, 5))
+    outs = []
+    for graph in (0, 1, 1):
+        ffs.set_option("graph", graph)
+        ud = torch.from_numpy(inputs.uniforms(M, N, 11)).cuda()
+        outs.append(ffs.ffs_sample(U, ud).cpu().numpy())
+    assert (outs[0] == outs[1]).all() and (outs[1] == outs[2]).all()
+    assert ffs.ffs_last_launch_count() > 10  # kernel nodes of the replayed graph
+
+
+def test_options_api():
+    ffs = _ffs()
+    assert ffs.get_option("dense_gemm") == 8.0
+    ffs.set_option("dense_gemm", 7)
+    assert ffs.get_option("dense_gemm") == 7.0
+    ffs.set_option("dense_gemm", float("nan"))
+    assert ffs.get_option("dense_gemm") == 8.0
+    lib = ffs.load()
+    assert lib.ffs_set_option(99, 1.0) == ffs.FFS_EINVAL
+    ffs.set_option("dense_gemm", 5)  # accepted here, rejected when a plan is made
+    U = _to_dev(inputs.random_orthonormal(2100, 258, 5))
+    with pytest.raises(ffs.FFSError):
+        ffs.ffs_sample(U, torch.from_numpy(inputs.uniforms(4, 258, 1)).cuda())
 
 
 # Marginals at large L run the step + batched-GJ kernels with every block contracted gathered
-# (ffs_abi.cu dense_eligible); FFS_STEP_MARGINAL=0 keeps them on the per-sample cluster kernel.
+# (ffs_abi.cu dense_eligible); option large_l_marginal = 0 keeps them on the per-sample cluster kernel.
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("step", ["1", "0"])
-def test_large_L_marginal_paths(step, cplx, monkeypatch):
-    monkeypatch.setenv("FFS_STEP_MARGINAL", step)
+def test_large_L_marginal_paths(step, cplx):
+    _ffs().set_option("large_l_marginal", int(step))
     L, N, Np = 2100, 300, 42  # ragged last block (42 = 5 x 8 + 2)
     U = inputs.random_orthonormal(L, N, 91 + int(cplx), complex_=cplx)
     uni = inputs.uniforms(64, Np, 515)
@@ -285,3 +355,20 @@ def test_large_L_small_batches(L, N, M, cplx):
     assert (gflags == 0).all()
     _, rw = ref.weights(U, uni[:1], Np=N)
     assert compare_weights(gw, rw, gpos, rpos) <= WEIGHT_TOL
+
+
+# Odd N' on the block-step marginal path (the batched Gauss-Jordan kernel's W rows are then not
+# 16-byte aligned: element-wise accesses), several block counts and a ragged last block.
+@pytest.mark.parametrize("Np", [19, 21, 43])
+def test_block_step_odd_marginal(Np):
+    L, N = 2100, 300
+    U = inputs.random_orthonormal(L, N, 3 * Np)
+    M = 48
+    uni = inputs.uniforms(M, Np, 17 + Np)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=2, trace_S0=M - 2)
+    rpos = ref.sample(U, uni, Np=Np)
+    r = compare_positions(U, uni, gpos, rpos, Np)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    _, rw = ref.weights(U, uni[M - 2:], Np=Np)
+    assert compare_weights(gw, rw, gpos[M - 2:], rpos[M - 2:]) <= WEIGHT_TOL
