@@ -1,18 +1,21 @@
 #!/usr/bin/env python3
 """Benchmark of the FFS hot path (BASELINE.json metric: FFS samples/sec and effective FP64
-GFLOP/s at 1 B200; % of roofline).
+GFLOP/s vs (L,N) at 1 B200; % of roofline).
 
 One "step" = one ffs_sample call over the whole workload (permutation draw, candidate weights,
 inverse-CDF draws, panel/factor updates, positions out for all M samples) with inputs resident in
-HBM. Default workload: BASELINE.json configs[1] (1D double well, L=256, N=32, M=65536, fp64).
+HBM. Default workload: the largest single-GPU configuration of BASELINE.json, configs[4] (the
+DPP-shaped projection DPP, L=16384, N=1024, M=1024, fp64). The same JSON line carries a `sweep`
+with every BASELINE.json workload (C1, C2, C3, C3 marginal, C4, C5, C5 marginal), each timed the
+same way (device time, kernel time, roofline fraction, clocks, end-to-end through the host-buffer
+C-ABI call, and the CPU oracle on a bounded sample).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dw] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dpp] [--marginal] [--no-sweep]
+  python bench.py --impl reference     # the CPU oracle (oracle/) as the reference arm
 
 N>1: launched under torchrun (one process per GPU); every rank samples its own M samples (own
 uniform stream, "scaling": "weak"), no collective on the data path; the timed region is bracketed
-by a barrier + synchronize and the max over ranks is reported.
-`--impl reference` times the CPU oracle (oracle/, the paper's algorithm in C) on a bounded
-sample of the same workload on the host cores (rank 0 only).
+by a barrier + synchronize and the max over ranks is reported (the sweep runs at N=1 only).
 """
 from __future__ import annotations
 
@@ -33,23 +36,26 @@ sys.path.insert(0, ROOT)
 from paper_2109_07358_b200 import inputs  # noqa: E402
 
 METRIC = "FFS samples/sec and effective FP64 GFLOP/s vs (L,N) at 1 B200; % of roofline"
-PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# FP64 FMA pipe: 148 SMs x 64 FMA/clk x 2 flop x 1.965 GHz (measured: DMMA 36.9,
-# DFMA 34.1, cuBLAS DGEMM 35.5 TFLOP/s — profiles/fp64_peaks_r01.json)
+# FP64 FMA pipe: 148 SMs x 64 FMA/clk x 2 flop x 1.965 GHz (measured on this pool:
+# DMMA 36.9, DFMA 34.1, cuBLAS DGEMM 35.5 TFLOP/s, profiles/fp64_peaks_r01.json).
+# MEASURED_PEAKS.json has no FP64 entry, so the derived peak is the denominator.
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
-# dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel per launch, from one
-# `ncu --set full` capture of this bench command (profiles/r01_ncu_summary.md)
-TRAFFIC_BYTES = {"dw": 25294336}
+# ncu-measured per-launch numbers of this round (tools/gpu_r2_ncu.sh): DRAM traffic of the
+# dominant kernel and, for the dense path, the INT8 tensor-pipe activity of its GEMM
+ROOFLINE_FILE = os.path.join(ROOT, "profiles", "roofline_r02.json")
+SWEEP = [("tiny", False), ("dw", False), ("anderson", False), ("anderson", True), ("peierls", False),
+         ("dpp", False), ("dpp", True)]
+L2_NOTE = "flushed (256 MB write) before every timed GPU step"
 
 
-def paper_flops(cfg_L, Np, cplx):
+def paper_flops(L, Np, cplx):
     """Algorithmic flops per sample, PAPER.md:81/83 (L N'^2 + N'^3; x4 for complex)."""
-    return (4 if cplx else 1) * (cfg_L * Np * Np + Np ** 3)
+    return (4 if cplx else 1) * (L * Np * Np + Np ** 3)
 
 
-def weight_flops(cfg_L, Np, cplx):
+def weight_flops(L, Np, cplx):
     """Candidate-weight flops per sample: sum_k 2 L k."""
-    return (4 if cplx else 1) * cfg_L * Np * (Np + 1)
+    return (4 if cplx else 1) * L * Np * (Np + 1)
 
 
 class ClockSampler:
@@ -118,8 +124,43 @@ def workload(name, marginal, rank):
     return cfg, U, uni, M, Np
 
 
-def cpu_oracle_rate(U, uni, Np, budget_s=15.0, max_samples=None):
-    """Oracle samples/s on a bounded prefix of the workload (host cores, OpenMP)."""
+def wl_name(name, marginal):
+    return name + (":marginal" if marginal else "")
+
+
+def config_of(cfg, Np, M):
+    """The `config` object of both arms (identical keys and values)."""
+    return {"workload": wl_name(cfg.name, Np < cfg.N), "L": cfg.L, "N": cfg.N, "Nprime": Np, "M": M,
+            "l2": L2_NOTE}
+
+
+def path_of(cfg, Np, cplx):
+    """Kernel (sequence) libffs dispatches this shape to (ffs_abi.cu launch()) and its arithmetic."""
+    if (not cplx) and cfg.L <= 256 and Np <= 48:
+        return "ffs_seg_kernel (warp-segment owners)", "f64"
+    dt = "c128" if cplx else "f64"
+    if cfg.L >= 2048 and cfg.N >= 256 and cfg.N % 2 == 0:
+        if Np < cfg.N:
+            return ("block-step path (marginal): ffs_cluster_kernel<STEP> with gathered contraction + "
+                    "ffs_dense_gj_kernel per block, CUDA graph"), dt
+        return ("block-step path (hybrid dense): ffs_cluster_kernel<STEP>, ffs_ozaki_gemm_kernel<8> for "
+                "k0 >= theta N', ffs_dense_gj_kernel per block, CUDA graph"), \
+            dt + " (dense GEMM: Ozaki FP64 emulation, int8 x 8 slices on tcgen05; fp64-level, <= 1.3e-15 normwise)"
+    if cfg.L >= 2048:
+        return "ffs_cluster_kernel", dt
+    return "ffs_sample_kernel (CTA owners)", dt
+
+
+def load_roofline_file():
+    try:
+        with open(ROOFLINE_FILE) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def cpu_oracle_rate(U, uni, Np, budget_s=15.0):
+    """Oracle samples/s on a bounded prefix of the workload (host cores, OpenMP over samples)."""
     from oracle import ref
     ref.lib()
     L = U.shape[0]
@@ -127,17 +168,15 @@ def cpu_oracle_rate(U, uni, Np, budget_s=15.0, max_samples=None):
     # one sample per host thread first, except where one sample is already ~10+ s of CPU work
     # (C5 full: 1.8e10 flop per sample; 16 concurrent samples took 217 s, memory-bound)
     n = 1 if work > 8e9 else max(1, ref.num_threads())
-    t_used = 0.0
     while True:
-        n = min(n, uni.shape[0] if max_samples is None else min(uni.shape[0], max_samples))
+        n = min(n, uni.shape[0])
         t0 = time.perf_counter()
         ref.sample(U, uni[:n], Np=Np)
         t = time.perf_counter() - t0
-        if t > budget_s / 4 or n >= uni.shape[0] or (max_samples and n >= max_samples):
-            t_used = t
+        if t > budget_s / 4 or n >= uni.shape[0]:
             break
         n = int(n * max(2.0, min(16.0, (budget_s / 4) / max(t, 1e-3))))
-    return n / t_used, n, t_used, min(n, ref.num_threads())  # threads actually used (OpenMP over samples)
+    return n / t, n, t, min(n, ref.num_threads())  # threads actually used (OpenMP over samples)
 
 
 def run_reference(args):
@@ -146,42 +185,36 @@ def run_reference(args):
         return 0
     cfg, U, uni, M, Np = workload(args.config, args.marginal, 0)
     cplx = np.iscomplexobj(U)
-    rates = []
-    n_used = 0
+    rates, n_used, cores = [], 0, 1
     for step in range(args.warmup + args.steps):
         rate, n, t, cores = cpu_oracle_rate(U, uni, Np, budget_s=min(20.0, 60.0 / max(1, args.steps)))
         if step >= args.warmup:
             rates.append(rate)
             n_used = n
     v = statistics.median(rates)
-    ms = M / v * 1e3
+    _, dt = path_of(cfg, Np, cplx)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": M / v * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
-        "config": {"workload": cfg.name + (":marginal" if args.marginal else ""), "L": cfg.L, "N": cfg.N,
-                   "Nprime": Np, "M": M, "per_step_sample": f"first {n_used} of {M} samples"},
+        "config": config_of(cfg, Np, M),
         "effective_gflops": v * paper_flops(cfg.L, Np, cplx) / 1e9,
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {n_used} samples of the workload per step, OpenMP over samples"},
+                         "sample": f"first {n_used} of {M} samples per step (extrapolated to M), OpenMP over samples"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_gpu(args):
+def measure_gpu(name, marginal, steps, warmup, rank, world, dev, with_e2e=True):
+    """Device-time samples/s of one workload (inputs resident, L2 flushed before every step),
+    the libffs kernel time, clocks during the timed region, and the host-buffer e2e rate."""
     import torch
     import torch.distributed as dist
     from paper_2109_07358_b200 import ffs
 
-    rank, world, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    cfg, U, uni, M, Np = workload(args.config, args.marginal, rank)
+    cfg, U, uni, M, Np = workload(name, marginal, rank)
     cplx = np.iscomplexobj(U)
     Ud = torch.from_numpy(np.ascontiguousarray(U)).to(dev)
     ud = torch.from_numpy(uni).to(dev)
@@ -189,25 +222,22 @@ def run_gpu(args):
     flg = torch.empty(M, dtype=torch.int32, device=dev)
     ws = ffs.Workspace(dev)
     stream = torch.cuda.current_stream(dev)
-    # L2 flush buffer (> 126 MB L2): the workload's inputs are smaller than L2
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
         ffs.ffs_sample_marginal(Ud, ud, Np, positions=pos, flags=flg, workspace=ws, stream=stream)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     ffs.ffs_profile_enable(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev.index or 0)
     clk.start()
-    total_ms = 0.0
-    kern_ms = []
-    launches = 0
-    for _ in range(args.steps):
+    total_ms, kern_ms, launches = 0.0, [], 0
+    for _ in range(steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -221,69 +251,125 @@ def run_gpu(args):
     torch.cuda.synchronize(dev)
     clocks = clk.stop()
     ffs.ffs_profile_enable(False)
-    ms = total_ms / args.steps
+    ms = total_ms / steps
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
     flags_bad = int((flg != 0).sum().item())
+    kms = statistics.median([k for k in kern_ms if k > 0]) if any(k > 0 for k in kern_ms) else ms
+    fl = paper_flops(cfg.L, Np, cplx)
+    achieved = M * fl / (kms * 1e-3) / 1e12
+    out = {"cfg": cfg, "U": U, "uni": uni, "M": M, "Np": Np, "cplx": cplx, "ms": ms, "kernel_ms": kms,
+           "achieved": achieved, "frac": achieved / FP64_PEAK_TFLOPS, "clocks": clocks,
+           "launches": launches, "flags_bad": flags_bad, "steps": steps}
+    del flush
+    if with_e2e:
+        # end to end through the host-buffer C-ABI call (pinned host buffers, copies timed)
+        hU = torch.from_numpy(np.ascontiguousarray(U)).pin_memory()
+        hu = torch.from_numpy(uni).pin_memory()
+        hp = torch.empty((M, Np), dtype=torch.int32).pin_memory()
+        hf = torch.empty(M, dtype=torch.int32).pin_memory()
+        hws = ffs.Workspace(dev)
+        ffs.ffs_sample_host(hU, hu, Np, positions=hp, flags=hf, workspace=hws, stream=stream, device=dev)
+        e2e_ms = []
+        for _ in range(steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            ffs.ffs_sample_host(hU, hu, Np, positions=hp, flags=hf, workspace=hws, stream=stream, device=dev)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e = statistics.median(e2e_ms)
+        if world > 1:
+            t = torch.tensor([e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e = float(t.item())
+        assert (hp.to(dev) == pos).all().item(), "host path and device path disagree"
+        out["e2e"] = {"value": M * world / (e2e * 1e-3), "unit": "samples/s",
+                      "h2d_bytes_per_step": int(hU.numel() * hU.element_size() + hu.numel() * 8),
+                      "d2h_bytes_per_step": int(hp.numel() * 4 + hf.numel() * 4)}
+        del hws
+    del ws, Ud, ud
+    torch.cuda.empty_cache()
+    return out
 
-    # ---- end-to-end through the host-buffer C-ABI call (pinned host buffers, copies timed)
-    hU = torch.from_numpy(np.ascontiguousarray(U)).pin_memory()
-    hu = torch.from_numpy(uni).pin_memory()
-    hp = torch.empty((M, Np), dtype=torch.int32).pin_memory()
-    hf = torch.empty(M, dtype=torch.int32).pin_memory()
-    hws = ffs.Workspace(dev)
-    for _ in range(max(1, args.warmup // 2)):
-        ffs.ffs_sample_host(hU, hu, Np, positions=hp, flags=hf, workspace=hws, stream=stream, device=dev)
-    e2e_ms = []
-    for _ in range(args.steps):
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        ffs.ffs_sample_host(hU, hu, Np, positions=hp, flags=hf, workspace=hws, stream=stream, device=dev)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e = statistics.median(e2e_ms)
+
+def sweep_entry(r, cpu_budget, no_cpu):
+    cfg, M, Np, cplx = r["cfg"], r["M"], r["Np"], r["cplx"]
+    kern, dt = path_of(cfg, Np, cplx)
+    e = {"config": config_of(cfg, Np, M), "dtype": dt, "value": M / (r["ms"] * 1e-3), "unit": "samples/s",
+         "ms_per_step": r["ms"], "steps": r["steps"], "kernel": kern, "kernel_ms": r["kernel_ms"],
+         "effective_gflops": M * paper_flops(cfg.L, Np, cplx) / (r["ms"] * 1e-3) / 1e9,
+         "frac": r["frac"], "clocks": r["clocks"], "e2e": r.get("e2e"), "gpu_launches": r["launches"],
+         "sample_flags_nonzero": r["flags_bad"]}
+    if not no_cpu:
+        rate, n, t, cores = cpu_oracle_rate(r["U"], r["uni"], Np, budget_s=cpu_budget)
+        e["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                             "sample": f"first {n} of {M} samples ({t:.1f} s), OpenMP over samples"}
+    return e
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
     if world > 1:
-        t = torch.tensor([e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
-    assert (hp.to(dev) == pos).all().item(), "host path and device path disagree"
-
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    head = measure_gpu(args.config, args.marginal, args.steps, args.warmup, rank, world, dev)
+    sweep = None
+    if world == 1 and not args.no_sweep and rank == 0:
+        sweep = {}
+        for name, marg in SWEEP:
+            key = wl_name(name, marg)
+            if name == args.config and marg == args.marginal:
+                r = head
+            else:
+                r = measure_gpu(name, marg, max(3, min(args.steps, 10)), 3, rank, world, dev)
+            sweep[key] = sweep_entry(r, args.sweep_cpu_budget, args.no_cpu)
+            sys.stderr.write(f"sweep {key}: {sweep[key]['value']:.4g} samples/s, frac {sweep[key]['frac']:.3f}\n")
     if rank == 0:
+        cfg, M, Np, cplx = head["cfg"], head["M"], head["Np"], head["cplx"]
         units = M * world
-        value = units / (ms * 1e-3)
+        value = units / (head["ms"] * 1e-3)
         fl = paper_flops(cfg.L, Np, cplx)
-        kms = statistics.median([k for k in kern_ms if k > 0]) if any(k > 0 for k in kern_ms) else ms
-        achieved = M * fl / (kms * 1e-3) / 1e12
+        kern, dt = path_of(cfg, Np, cplx)
+        rf = load_roofline_file().get(wl_name(cfg.name, Np < cfg.N), {})
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
-            "config": {"workload": cfg.name + (":marginal" if args.marginal else ""), "L": cfg.L, "N": cfg.N,
-                       "Nprime": Np, "M_per_gpu": M, "l2": "flushed (256 MB write) before every timed step",
-                       "U_sha256": inputs.u_sha256(U)[:16]},
+            "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": config_of(cfg, Np, M),
+            "inputs": {"U_sha256": inputs.u_sha256(head["U"])[:16], "uniforms": "numpy Philox, seed 1000+index"},
             "effective_gflops": value * fl / 1e9,
             "weight_gflops": value * weight_flops(cfg.L, Np, cplx) / 1e9,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                         "kernel": ffs_path_kernel(cfg, Np, cplx),
-                         "kernel_ms": kms, "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"},
-            "gpu_launches": launches,
-            "sample_flags_nonzero": flags_bad,
-            "clocks": clocks,
-            "e2e": {"value": units / (e2e * 1e-3), "unit": "samples/s",
-                    "h2d_bytes_per_step": int(hU.numel() * hU.element_size() + hu.numel() * 8),
-                    "d2h_bytes_per_step": int(hp.numel() * 4 + hf.numel() * 4)},
+            "roofline": {"bound": "alu", "achieved": head["achieved"], "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": head["frac"], "traffic": rf.get("traffic"),
+                         "kernel": kern, "kernel_ms": head["kernel_ms"],
+                         "achieved_def": "M x F_paper (L N'^2 + N'^3, x4 complex; PAPER.md:81/83) / kernel_ms "
+                                         "(CUDA events on the launch stream around the sampling kernels)",
+                         "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)"},
+            "gpu_launches": head["launches"],
+            "sample_flags_nonzero": head["flags_bad"],
+            "clocks": head["clocks"],
+            "e2e": head["e2e"],
         }
-        if args.traffic is not None:
-            line["roofline"]["traffic"] = args.traffic
-        elif not args.marginal and cfg.name in TRAFFIC_BYTES:
-            line["roofline"]["traffic"] = TRAFFIC_BYTES[cfg.name]
-        if not args.no_cpu and world == 1:
-            rate, n, t, cores = cpu_oracle_rate(U, uni, Np, budget_s=args.cpu_budget)
-            line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                                    "sample": f"first {n} of {M} samples ({t:.1f} s), OpenMP over samples"}
+        for k in ("traffic_source", "gemm"):
+            if k in rf:
+                line["roofline"][k] = rf[k]
+        if world == 1 and not args.no_cpu:
+            if sweep and wl_name(cfg.name, Np < cfg.N) in sweep and "cpu_baseline" in sweep[wl_name(cfg.name, Np < cfg.N)]:
+                line["cpu_baseline"] = sweep[wl_name(cfg.name, Np < cfg.N)]["cpu_baseline"]
+            else:
+                rate, n, t, cores = cpu_oracle_rate(head["U"], head["uni"], Np, budget_s=args.cpu_budget)
+                line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                                        "sample": f"first {n} of {M} samples ({t:.1f} s), OpenMP over samples"}
+        if sweep is not None:
+            line["sweep"] = sweep
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -291,36 +377,18 @@ def run_gpu(args):
     return 0
 
 
-def ffs_uses_warp(cfg, Np, cplx):
-    return (not cplx) and cfg.L <= 256 and Np <= 48
-
-
-def ffs_path_kernel(cfg, Np, cplx):
-    """Name of the timed kernel (sequence) of the path libffs dispatches to (ffs_abi.cu launch())."""
-    if ffs_uses_warp(cfg, Np, cplx):
-        return "ffs_seg_kernel"
-    if cfg.L >= 2048:
-        if Np < cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
-            return "step path (marginal): ffs_cluster_kernel<STEP> (gathered contraction) + ffs_dense_gj_kernel per block"
-        if Np == cfg.N and cfg.N >= 256 and cfg.N % 2 == 0:
-            return ("dense path (hybrid): ffs_cluster_kernel<STEP> (+ ffs_ozaki_gemm_kernel for k0 >= theta N') "
-                    "+ ffs_dense_gj_kernel per block")
-        return "ffs_cluster_kernel"
-    return "ffs_sample_kernel"
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="dw", choices=sorted(inputs.CONFIGS))
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="dpp", choices=sorted(inputs.CONFIGS))
     ap.add_argument("--marginal", action="store_true", help="the config's marginal (N'<N) workload")
     ap.add_argument("--impl", default="ffs", choices=["ffs", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
+    ap.add_argument("--no-sweep", action="store_true", help="only the headline workload")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
+    ap.add_argument("--sweep-cpu-budget", type=float, default=6.0, help="seconds of oracle work per sweep entry")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

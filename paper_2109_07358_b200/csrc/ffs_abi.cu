@@ -565,6 +565,22 @@ size_t dense_gj_bytes(int k0) { return ffsk::dense_gj_smem<T, 8, gj_tj<T>()>(k0)
 template <int NS>
 const void* ozaki_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel<NS>); }
 
+// 3-D tensor map [NS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn tensor_map_encoder() {
+  // resolved once (thread-safe function-local static); first called when a plan is made, outside
+  // any stream capture
+  static const EncodeTiledFn enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) fn = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  return enc;
+}
+
 int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, DensePlan& d) {
   const bool cx = dtype == FFS_C128;
   d.c.fn = cx ? ffsk::cluster_step_kernel_ptr<cplx, 2, 8, 512>() : ffsk::cluster_step_kernel_ptr<double, 4, 8, 512>();
@@ -622,6 +638,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   d.ws_ea = ns ? align_up((size_t)L * 4) : 0;
   d.ws_ozb = ns ? align_up((size_t)ns * ncolsY * d.Kp) : 0;
   d.ws_eb = ns ? align_up((size_t)ncolsY * 4) : 0;
+  if (ns && !tensor_map_encoder()) return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if (ns == 8) {
     if (int rc = ffsh::ensure_max_smem(ozaki_fn<8>())) return rc;
   } else if (ns == 7) {
@@ -639,18 +656,8 @@ int make_dense_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Dens
                            [&](DensePlan& p) { return make_dense_plan_uncached(L, N, Np, dtype, M, p); });
 }
 
-// 3-D tensor map [NS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 int oz_tensor_map(CUtensorMap* m, const int8_t* base, int ns, int64_t rows, int Kp, int box_rows) {
-  // resolved once (thread-safe function-local static)
-  static const EncodeTiledFn enc = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) fn = nullptr;
-    return reinterpret_cast<EncodeTiledFn>(fn);
-  }();
+  const EncodeTiledFn enc = tensor_map_encoder();
   if (!enc) return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)ns};
   const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)Kp * (cuuint64_t)rows};
@@ -831,6 +838,7 @@ struct GraphEntry {
 };
 thread_local GraphEntry g_graphs[4];
 thread_local unsigned g_graph_next = 0;
+thread_local cudaStream_t g_capture_stream = nullptr;
 
 int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
                  int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
@@ -856,12 +864,16 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
     if (g.exec && g.key == key) ge = &g;
   if (!ge) {
     ge = &g_graphs[g_graph_next++ % 4];
+    // capture on a library-owned stream (the caller's may be the legacy default stream, which
+    // cannot be captured); the executable graph is then launched on the caller's stream
+    if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(FFS_ECUDA, "capture stream creation failed");
     cudaGraph_t graph_def = nullptr;
-    if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    if (cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return fail(FFS_ECUDA, "cudaStreamBeginCapture failed");
     const int l0 = ffsh::launches();
-    rc = issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, stream, S0, S, trace);
-    const cudaError_t ce = cudaStreamEndCapture(stream, &graph_def);
+    rc = issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, g_capture_stream, S0, S, trace);
+    const cudaError_t ce = cudaStreamEndCapture(g_capture_stream, &graph_def);
     if (rc != FFS_OK) {
       if (graph_def) cudaGraphDestroy(graph_def);
       return rc;
