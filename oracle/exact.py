@@ -96,3 +96,18 @@ def pooled_chisquare(observed: np.ndarray, expected: np.ndarray, min_expected: f
     stat = float(((bo - be) ** 2 / be).sum())
     dof = len(bo) - 1
     return stat, dof, float(stats.chi2.sf(stat, dof)), len(bo)
+
+
+def lensemble_set_probabilities(V: np.ndarray, lam: np.ndarray):
+    """L-ensemble law of the DPP pipeline by its definition: with the kernel
+    C = V diag(lam) V^dagger, P(S) = det(C_S) / det(I + C) for every subset S of the L items
+    (the empty set has det(C_empty) = 1). Returns (list of sorted index tuples, probabilities)."""
+    L = V.shape[0]
+    C = (V * lam[None, :]) @ V.conj().T
+    Z = float(np.real(np.linalg.det(np.eye(L) + C)))
+    subsets, p = [], []
+    for n in range(L + 1):
+        for S in itertools.combinations(range(L), n):
+            subsets.append(S)
+            p.append(1.0 if n == 0 else float(np.real(np.linalg.det(C[np.ix_(S, S)]))))
+    return subsets, np.array(p) / Z

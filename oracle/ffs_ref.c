@@ -171,6 +171,73 @@ int ffs_ref_chain(const double* U, int64_t L, int64_t N, int dtype, int64_t Np, 
     return r;
 }
 
+/* ---------------------------------------------------------------- L-ensemble front end
+ * PAPER.md:178-180 (text summarisation, step 2): the correlation matrix C = sum_j lambda_j u_j u_j^T
+ * is eigendecomposed, "Each eigenvector u_j is selected with probability lambda_j/(lambda_j+1)",
+ * and "The selected set of vectors ... form the matrix U in Eq. (1), according to which we perform
+ * the fermion sampling with fermion particle number N" -- so each sample has its own N_i and U_i.
+ *   V        : [L][K] eigenvectors (orthonormal columns), real or complex (dtype)
+ *   lam      : [K] eigenvalues >= 0
+ *   uniforms : [M][3K]: [0,K) keep draws (keep j iff u_j < lambda_j/(lambda_j+1), taken in fp64),
+ *              [K,2K) the FFS permutation draws of U_i (first N_i used, reading Q6 with N = N_i),
+ *              [2K,3K) the N_i selection draws (reading Q5)
+ *   positions: [M][K] out, sampling order, entries k >= N_i set to -1; counts [M] = N_i; flags [M]
+ * U_i = V[:, kept columns in ascending j] is built explicitly and sampled by run_one(). */
+int ffs_ref_sample_lensemble(const double* V, const double* lam, int64_t L, int64_t K, int dtype, int64_t M,
+                             const double* uniforms, int32_t* positions, int32_t* counts, int32_t* flags,
+                             int nthreads)
+{
+    if (M == 0) return 0;
+    if (!V || !lam || !uniforms || !positions || L < 1 || K < 1 || K > L) return -1;
+    if (dtype != FFS_REF_F64 && dtype != FFS_REF_C128) return -1;
+    size_t es = dtype == FFS_REF_C128 ? 16 : 8;
+    size_t sb = scratch_bytes(L, K, K, dtype) + es * (size_t)(L * K) + 8 * (size_t)(2 * K) + 4 * (size_t)K + 64;
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        char* buf = (char*)malloc(sb);
+        if (!buf) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = 1;
+        } else {
+            char* Ui = buf + scratch_bytes(L, K, K, dtype);
+            double* row = (double*)(Ui + es * (size_t)(L * K));
+            int32_t* kept = (int32_t*)(row + 2 * K);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 16)
+#endif
+            for (int64_t i = 0; i < M; ++i) {
+                const double* u = uniforms + i * 3 * K;
+                int64_t n = 0;
+                for (int64_t j = 0; j < K; ++j)
+                    if (u[j] < lam[j] / (lam[j] + 1.0)) kept[n++] = (int32_t)j;
+                for (int64_t k = 0; k < K; ++k) positions[i * K + k] = -1;
+                if (counts) counts[i] = (int32_t)n;
+                int f = 0;
+                if (n > 0) {
+                    for (int64_t x = 0; x < L; ++x)
+                        for (int64_t c = 0; c < n; ++c)
+                            memcpy(Ui + es * (size_t)(x * n + c), (const char*)V + es * (size_t)(x * K + kept[c]), es);
+                    for (int64_t k = 0; k < n; ++k) {
+                        row[k] = u[K + k];
+                        row[n + k] = u[2 * K + k];
+                    }
+                    f = run_one((const double*)Ui, L, n, dtype, n, row, NULL, NULL, positions + i * K, NULL, NULL,
+                                NULL, buf);
+                }
+                if (flags) flags[i] = f;
+            }
+            free(buf);
+        }
+    }
+    return bad ? -2 : 0;
+}
+
 int ffs_ref_num_threads(void)
 {
 #ifdef _OPENMP

@@ -42,6 +42,7 @@ def lib():
         L.ffs_ref_chain.argtypes = [vp, i64, i64, ctypes.c_int, i64, vp, vp, vp, vp, vp]
         L.ffs_ref_permutation.argtypes = [vp, i64, i64, vp]
         L.ffs_ref_permutation.restype = None
+        L.ffs_ref_sample_lensemble.argtypes = [vp, vp, i64, i64, ctypes.c_int, i64, vp, vp, vp, vp, ctypes.c_int]
         L.ffs_ref_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -111,6 +112,25 @@ def chain(U, m, x):
     if rc != 0:
         raise ValueError(f"ffs_ref_chain rc={rc}")
     return w, hn2, tot
+
+
+def sample_lensemble(V, lam, uniforms, nthreads=0):
+    """L-ensemble DPP: eigenvector j kept iff u_j < lambda_j/(lambda_j+1), then FFS
+    on the kept columns. uniforms [M][3K]; returns positions [M][K] (-1 padded), counts [M], flags [M]."""
+    Vb, dt = _u_bytes(V)
+    L, K = Vb.shape
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    uni = np.ascontiguousarray(uniforms, dtype=np.float64)
+    M = uni.shape[0]
+    assert lam.shape == (K,) and uni.shape == (M, 3 * K), (lam.shape, uni.shape)
+    pos = np.empty((M, K), dtype=np.int32)
+    cnt = np.empty(M, dtype=np.int32)
+    flags = np.empty(M, dtype=np.int32)
+    rc = lib().ffs_ref_sample_lensemble(_ptr(Vb), _ptr(lam), L, K, dt, M, _ptr(uni), _ptr(pos), _ptr(cnt),
+                                        _ptr(flags), nthreads)
+    if rc != 0:
+        raise ValueError(f"ffs_ref_sample_lensemble rc={rc}")
+    return pos, cnt, flags
 
 
 def num_threads() -> int:

@@ -275,3 +275,57 @@ def test_bad_arguments_rejected():
     assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 2, 0, 1, 3, uni.ctypes.data, pos.ctypes.data, None, 1) == -1
     assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 2, 7, 1, 2, uni.ctypes.data, pos.ctypes.data, None, 1) == -1
     assert L.ffs_ref_sample_marginal(U.ctypes.data, 4, 2, 0, 0, 2, None, None, None, 1) == 0
+
+
+# ---------------------------------------------------------------- L-ensemble front end
+def _lens_inputs(L, K, seed, cplx=False):
+    V = _rand_u(L, K, seed, cplx)
+    lam = np.random.default_rng(seed).uniform(0.05, 4.0, K)
+    return V, lam
+
+
+def _lens_uniforms(M, K, seed):
+    return np.random.Generator(np.random.Philox(seed)).random((M, 3 * K))
+
+
+@pytest.mark.parametrize("L,K,cplx", [(6, 6, False), (7, 4, False), (5, 5, True)])
+def test_lensemble_matches_brute_force_law(L, K, cplx):
+    """Sampled subsets follow P(S) = det(C_S)/det(I + C), C = V diag(lam) V^dagger: the L-ensemble
+    the paper's pipeline samples by keeping eigenvector j w.p. lam_j/(lam_j+1) and running FFS."""
+    V, lam = _lens_inputs(L, K, 100 + L + K, cplx)
+    M = 200000
+    pos, cnt, flags = ref.sample_lensemble(V, lam, _lens_uniforms(M, K, 5 + L))
+    assert (flags == 0).all()
+    assert (cnt <= K).all() and (pos[np.arange(K)[None, :] >= cnt[:, None]] == -1).all()
+    subsets, p = exact.lensemble_set_probabilities(V, lam)
+    assert abs(p.sum() - 1.0) < 1e-12  # normalisation of the definition
+    index = {s: i for i, s in enumerate(subsets)}
+    obs = np.bincount([index[tuple(sorted(r[:c]))] for r, c in zip(pos.tolist(), cnt.tolist())],
+                      minlength=len(subsets))
+    stat, dof, pval, _ = exact.pooled_chisquare(obs, p * M)
+    assert pval > 1e-3, (stat, dof, pval)
+
+
+def test_lensemble_size_distribution():
+    """N_i is a sum of independent Bernoulli(lam_j/(lam_j+1)): mean and variance."""
+    L, K = 40, 24
+    V, lam = _lens_inputs(L, K, 3)
+    M = 20000
+    _, cnt, _ = ref.sample_lensemble(V, lam, _lens_uniforms(M, K, 9))
+    q = lam / (lam + 1)
+    mu, var = q.sum(), (q * (1 - q)).sum()
+    assert abs(cnt.mean() - mu) < 4 * np.sqrt(var / M)
+    assert abs(cnt.var() / var - 1) < 0.1
+
+
+def test_lensemble_degenerate_spectra():
+    """lam = 0 keeps nothing (empty sample); lam -> inf keeps every eigenvector, and the sample is
+    then plain FFS of V driven by the permutation / selection blocks of the same uniform row."""
+    L, K = 12, 5
+    V = _rand_u(L, K, 21)
+    uni = _lens_uniforms(300, K, 4)
+    pos, cnt, _ = ref.sample_lensemble(V, np.zeros(K), uni)
+    assert (cnt == 0).all() and (pos == -1).all()
+    pos, cnt, _ = ref.sample_lensemble(V, np.full(K, 1e300), uni)
+    assert (cnt == K).all()
+    assert (pos == ref.sample(V, uni[:, K:])).all()
