@@ -87,6 +87,26 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_
                     const double* uniforms, int32_t* positions, int32_t* sample_flags,
                     void* workspace, size_t ws_bytes, void* stream);
 
+/* L-ensemble DPP front end (text-summarisation pipeline step 2). The caller has
+ * eigendecomposed the correlation matrix C = sum_j lambda_j v_j v_j^dagger (setup, not part of the
+ * path). Per sample i, eigenvector j is kept iff keep_u[j] < lambda_j/(lambda_j + 1) (the paper's
+ * "selected with probability lambda_j/(lambda_j+1)"; the decision is taken in fp64); the kept
+ * columns, in ascending j, form U_i (L x N_i), which is sampled by FFS exactly as ffs_sample
+ * samples U (Eq. 1-3) with N = N_i. The sampled subsets follow the L-ensemble law
+ * P(S) = det(C_S) / det(I + C).
+ *   V        : DEVICE [L][K] eigenvectors (orthonormal columns), dtype as ffs_sample; K <= L
+ *   lambda   : DEVICE double[K], eigenvalues >= 0
+ *   uniforms : DEVICE double[M][3K]: [0,K) keep draws, [K,2K) the permutation draws of U_i
+ *              (first N_i used, rule of ffs_sample with N = N_i), [2K,3K) the N_i selections
+ *   positions: DEVICE int32[M][K] out, sampling order; entries k >= N_i are -1
+ *   counts   : DEVICE int32[M] out (N_i) or NULL; sample_flags as ffs_sample (NULL allowed)
+ * Workspace: ffs_lensemble_workspace_bytes(L, K, dtype, M) bytes (0 = invalid arguments).
+ * Errors as ffs_sample (L <= 16384 real / 8192 complex). An empty kept set gives N_i = 0. */
+size_t ffs_lensemble_workspace_bytes(int64_t L, int64_t K, ffs_dtype dtype, int64_t M);
+int ffs_sample_lensemble(const void* V, const double* lambda, int64_t L, int64_t K, ffs_dtype dtype, int64_t M,
+                         const double* uniforms, int32_t* positions, int32_t* counts, int32_t* sample_flags,
+                         void* workspace, size_t ws_bytes, void* stream);
+
 /* Number of kernel launches the last successful sampling call on this thread issued. */
 int ffs_last_launch_count(void);
 

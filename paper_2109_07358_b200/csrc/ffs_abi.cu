@@ -21,6 +21,7 @@
 #include "ffs_warp_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
 #include "ffs_dense.cuh"
+#include "ffs_lens.cuh"
 #include "ffs_kptr.h"
 
 // ====================================================================== shared host helpers
@@ -937,6 +938,8 @@ int launch_generic(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
   p.trace = S > 0 ? trace : nullptr;
   p.owner_smem = pl.owner_smem;
   p.ushared_smem = pl.ushared_smem;
+  p.ustride = (int)(2 * Np);
+  p.usel = (int)Np;
   if (!pl.v.usmem) launch_transpose(U, const_cast<double*>(p.Ut), L, N, pl.Lp, dtype, stream);
   void* args[] = {&p};
   ffsh::prof_begin(stream);
@@ -1002,6 +1005,79 @@ size_t workspace_bytes(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
   return make_plan(L, N, Np, dtype, M, pl) == FFS_OK ? pl.ws_ut + pl.ws_wfull : 0;
 }
 
+
+// ------------------------------------------------------------------ L-ensemble front end
+// ffs_lens_prep_kernel (keep draws + permutation of the kept columns) then ffs_sample_kernel in
+// ragged mode (each sample its own N_i <= K steps). Workspace: [cols M x K | nps M | generic plan].
+struct LensLayout {
+  size_t cols, nps, plan, total;
+  Plan pl;
+  int prep_tpb;
+};
+int lens_layout(int64_t L, int64_t K, int dtype, int64_t M, LensLayout& y) {
+  if (int rc = check_shape(L, K, K, dtype, std::max<int64_t>(M, 1))) return rc;
+  if (int rc = make_plan(L, K, K, dtype, std::max<int64_t>(M, 1), y.pl)) return rc;
+  y.cols = 0;
+  y.nps = align_up((size_t)std::max<int64_t>(M, 1) * K * 4);
+  y.plan = y.nps + align_up((size_t)std::max<int64_t>(M, 1) * 4);
+  y.total = y.plan + y.pl.ws_ut + y.pl.ws_wfull;
+  y.prep_tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * K)));
+  return FFS_OK;
+}
+
+int launch_lensemble(const void* V, const double* lambda, int64_t L, int64_t K, int dtype, int64_t M,
+                     const double* uniforms, int32_t* positions, int32_t* counts, int32_t* flags, void* ws,
+                     size_t ws_bytes, cudaStream_t stream) {
+  ffsh::launches() = 0;
+  if (M == 0) return FFS_OK;
+  if (M < 0) return fail(FFS_EINVAL, "M=%lld < 0", (long long)M);
+  if (!V || !lambda || !uniforms || !positions) return fail(FFS_EINVAL, "null V/lambda/uniforms/positions");
+  LensLayout y;
+  if (int rc = lens_layout(L, K, dtype, M, y)) return rc;
+  if (!ws || ws_bytes < y.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, y.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  char* w = static_cast<char*>(ws);
+  int32_t* cols = reinterpret_cast<int32_t*>(w + y.cols);
+  int32_t* nps = reinterpret_cast<int32_t*>(w + y.nps);
+  char* pw = w + y.plan;
+  const Plan& pl = y.pl;
+  const int64_t pgrid = (M + y.prep_tpb - 1) / y.prep_tpb;
+  ffsk::ffs_lens_prep_kernel<<<(unsigned)pgrid, y.prep_tpb, (size_t)y.prep_tpb * K * 4, stream>>>(lambda, uniforms, cols,
+                                                                                              nps, M, (int)K);
+  ++ffsh::launches();
+  ffsk::Params p{};
+  p.U = static_cast<const double*>(V);
+  p.Ut = pl.v.usmem ? nullptr : reinterpret_cast<const double*>(pw);
+  p.L = (int)L;
+  p.N = (int)K;
+  p.Np = (int)K;
+  p.Lp = pl.Lp;
+  p.ut_stride = pl.ut_stride;
+  p.M = M;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.wfull = reinterpret_cast<double*>(pw + pl.ws_ut);
+  p.owner_smem = pl.owner_smem;
+  p.ushared_smem = pl.ushared_smem;
+  p.cols = cols;
+  p.nps = nps;
+  p.ustride = (int)(3 * K);
+  p.usel = (int)(2 * K);
+  if (!pl.v.usmem) launch_transpose(V, const_cast<double*>(p.Ut), L, K, pl.Lp, dtype, stream);
+  void* args[] = {&p};
+  ffsh::prof_begin(stream);
+  cudaError_t e = cudaLaunchKernel(pl.v.fn, dim3(pl.grid), dim3(pl.threads), args, pl.smem, stream);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  ffsh::prof_end(stream);
+  ++ffsh::launches();
+  if (counts && cudaMemcpyAsync(counts, nps, (size_t)M * 4, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+    return fail(FFS_ECUDA, "counts copy failed");
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  ffsh::clear_error();
+  return FFS_OK;
+}
 }  // namespace
 
 // ====================================================================== extern "C"
@@ -1140,6 +1216,18 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_
 #undef FFS_CK
   ffsh::launches() = launches;
   return FFS_OK;
+}
+
+size_t ffs_lensemble_workspace_bytes(int64_t L, int64_t K, ffs_dtype dtype, int64_t M) {
+  LensLayout y;
+  return lens_layout(L, K, dtype, M, y) == FFS_OK ? y.total : 0;
+}
+
+int ffs_sample_lensemble(const void* V, const double* lambda, int64_t L, int64_t K, ffs_dtype dtype, int64_t M,
+                         const double* uniforms, int32_t* positions, int32_t* counts, int32_t* sample_flags,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  return launch_lensemble(V, lambda, L, K, dtype, M, uniforms, positions, counts, sample_flags, workspace, ws_bytes,
+                          static_cast<cudaStream_t>(stream));
 }
 
 int ffs_last_launch_count(void) { return ffsh::launches(); }

@@ -42,6 +42,12 @@ struct Params {
   double* trace;           // [S][Np][L] or null
   size_t owner_smem;       // bytes of per-owner shared memory
   size_t ushared_smem;     // bytes of the shared U^T copy (shared-U path)
+  // ragged mode (L-ensemble front end, ffs_lens.cu): sample i runs nps[i] <= Np steps on the
+  // columns cols[i][0 .. nps[i]) (its kept eigenvectors, already permuted); null otherwise
+  const int32_t* cols;     // [M][N]
+  const int32_t* nps;      // [M]
+  int ustride;             // uniform row stride: 2 Np (ffs_sample), 3 N (L-ensemble)
+  int usel;                // offset of the selection uniforms within a row: Np, or 2 N
 };
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
@@ -278,30 +284,37 @@ ffs_sample_kernel(const Params p) {
   const T* Ug = reinterpret_cast<const T*>(p.U);
 
   for (int64_t i = gid; i < p.M; i += num_owners) {
-    const double* urow = p.uniforms + i * 2 * (int64_t)Np;
-    // ---- a1: permutation (reading Q6), forward partial Fisher-Yates
-    for (int j = t; j < N; j += G) perm[j] = j;
-    gsync<WARP>();
-    if (t == 0) {
-      for (int j = 0; j < Np; ++j) {
-        const int n = N - j;
-        int r = (int)floor(urow[j] * (double)n);
-        r = (r > n - 1 ? n - 1 : r) + j;
-        const int a = perm[j];
-        perm[j] = perm[r];
-        perm[r] = a;
+    const double* urow = p.uniforms + i * (int64_t)p.ustride;
+    const double* usel = urow + p.usel;
+    const int Npi = p.nps ? p.nps[i] : Np;  // steps of this sample (ragged mode: its N_i)
+    if (p.cols) {
+      // ragged mode: the permuted kept columns come precomputed
+      for (int j = t; j < Npi; j += G) perm[j] = p.cols[i * N + j];
+    } else {
+      // ---- a1: permutation (reading Q6), forward partial Fisher-Yates
+      for (int j = t; j < N; j += G) perm[j] = j;
+      gsync<WARP>();
+      if (t == 0) {
+        for (int j = 0; j < Np; ++j) {
+          const int n = N - j;
+          int r = (int)floor(urow[j] * (double)n);
+          r = (r > n - 1 ? n - 1 : r) + j;
+          const int a = perm[j];
+          perm[j] = perm[r];
+          perm[r] = a;
+        }
       }
     }
     gsync<WARP>();
     uint32_t chosen = 0;
     int flag = 0;
 
-    for (int k0 = 0; k0 < Np; k0 += B) {
-      const int nb = min(B, Np - k0);
+    for (int k0 = 0; k0 < Npi; k0 += B) {
+      const int nb = min(B, Npi - k0);
       // ---- stage Wb = W[0:k0, k0:k0+nb] (A^{-1} V[X, block cols])
       for (int idx = t; idx < k0 * B; idx += G) {
         const int ii = idx / B, c = idx % B;
-        Wb[idx] = c < nb ? Wf[(size_t)ii * Np + k0 + c] : S::zero();
+        Wb[idx] = c < nb ? Wf[(size_t)ii * Npi + k0 + c] : S::zero();
       }
       gsync<WARP>();
       // ---- a3: panel P = V[:, k0:k0+B] - V[:, 0:k0] Wb   (registers: R rows x B cols)
@@ -342,7 +355,7 @@ ffs_sample_kernel(const Params p) {
             w[r] = (x < L && !((chosen >> r) & 1u)) ? S::abs2(P[r][rr]) : 0.0;
           }
           double Ttot;
-          const int xk = select_site<WARP, R>(w, urow[Np + k], t, L, chosen, red, redi, Ttot);
+          const int xk = select_site<WARP, R>(w, usel[k], t, L, chosen, red, redi, Ttot);
           if (!((Ttot > 0.0) && isfinite(Ttot))) flag |= 1;
           const int own = xk / R, orow = xk % R;
           if (t == own) {
@@ -380,34 +393,34 @@ ffs_sample_kernel(const Params p) {
         }
       });
       // ---- Gauss-Jordan update of W with the nb new rows (only if later columns remain)
-      if (k0 + nb < Np) {
+      if (k0 + nb < Npi) {
         gsync<WARP>();
-        for (int idx = t; idx < nb * Np; idx += G) {
-          const int tt = idx / Np, j = idx % Np;
+        for (int idx = t; idx < nb * Npi; idx += G) {
+          const int tt = idx / Npi, j = idx % Npi;
           Vnew[idx] = Ug[(size_t)pos[k0 + tt] * N + perm[j]];
         }
         gsync<WARP>();
-        for (int j = k0 + nb + t; j < Np; j += G) {
+        for (int j = k0 + nb + t; j < Npi; j += G) {
           T z[B];
 #pragma unroll
-          for (int tt = 0; tt < B; ++tt) z[tt] = tt < nb ? Vnew[tt * Np + j] : S::zero();
+          for (int tt = 0; tt < B; ++tt) z[tt] = tt < nb ? Vnew[tt * Npi + j] : S::zero();
           // R_new = V[X_new, j] - V[X_new, 0:k0] W[0:k0, j]; 8 independent W loads in flight
           int ii = 0;
           for (; ii + 8 <= k0; ii += 8) {
             T w8[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) w8[u] = Wf[(size_t)(ii + u) * Np + j];
+            for (int u = 0; u < 8; ++u) w8[u] = Wf[(size_t)(ii + u) * Npi + j];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
 #pragma unroll
               for (int tt = 0; tt < B; ++tt)
-                if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii + u], w8[u], z[tt]);
+                if (tt < nb) z[tt] = S::fms(Vnew[tt * Npi + ii + u], w8[u], z[tt]);
           }
           for (; ii < k0; ++ii) {
-            const T wij = Wf[(size_t)ii * Np + j];
+            const T wij = Wf[(size_t)ii * Npi + j];
 #pragma unroll
             for (int tt = 0; tt < B; ++tt)
-              if (tt < nb) z[tt] = S::fms(Vnew[tt * Np + ii], wij, z[tt]);
+              if (tt < nb) z[tt] = S::fms(Vnew[tt * Npi + ii], wij, z[tt]);
           }
           // forward substitution with the unit-lower factor L[tt][s] = Row[tt][s] * Pinv[s]
 #pragma unroll
@@ -427,34 +440,34 @@ ffs_sample_kernel(const Params p) {
             }
 #pragma unroll
           for (int tt = 0; tt < B; ++tt)
-            if (tt < nb) Wf[(size_t)(k0 + tt) * Np + j] = z[tt];
+            if (tt < nb) Wf[(size_t)(k0 + tt) * Npi + j] = z[tt];
           // W[0:k0, j] -= Wb Z[:, j]; 8 rows per batch (independent loads, then stores)
           ii = 0;
           for (; ii + 8 <= k0; ii += 8) {
             T a8[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) a8[u] = Wf[(size_t)(ii + u) * Np + j];
+            for (int u = 0; u < 8; ++u) a8[u] = Wf[(size_t)(ii + u) * Npi + j];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
 #pragma unroll
               for (int tt = 0; tt < B; ++tt)
                 if (tt < nb) a8[u] = S::fms(Wb[(ii + u) * B + tt], z[tt], a8[u]);
-              Wf[(size_t)(ii + u) * Np + j] = a8[u];
+              Wf[(size_t)(ii + u) * Npi + j] = a8[u];
             }
           }
           for (; ii < k0; ++ii) {
-            T a = Wf[(size_t)ii * Np + j];
+            T a = Wf[(size_t)ii * Npi + j];
 #pragma unroll
             for (int tt = 0; tt < B; ++tt)
               if (tt < nb) a = S::fms(Wb[ii * B + tt], z[tt], a);
-            Wf[(size_t)ii * Np + j] = a;
+            Wf[(size_t)ii * Npi + j] = a;
           }
         }
       }
       gsync<WARP>();
     }
     // ---- a6: positions (sampling order) and flags
-    for (int j = t; j < Np; j += G) p.positions[i * Np + j] = pos[j];
+    for (int j = t; j < Np; j += G) p.positions[i * Np + j] = j < Npi ? pos[j] : -1;
     if constexpr (WARP) {
       flag = __reduce_or_sync(0xffffffffu, flag);
     } else {

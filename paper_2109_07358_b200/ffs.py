@@ -39,6 +39,8 @@ EXPORTED = (
     "ffs_last_launch_count",
     "ffs_profile_enable",
     "ffs_last_kernel_ms",
+    "ffs_lensemble_workspace_bytes",
+    "ffs_sample_lensemble",
     "ffs_set_option",
     "ffs_get_option",
     "ffs_last_error",
@@ -78,6 +80,9 @@ def load(build_if_missing: bool = True):
     L.ffs_last_launch_count.restype = ci
     L.ffs_profile_enable.argtypes = [ci]
     L.ffs_last_kernel_ms.restype = ctypes.c_float
+    L.ffs_lensemble_workspace_bytes.argtypes = [i64, i64, ci, i64]
+    L.ffs_lensemble_workspace_bytes.restype = sz
+    L.ffs_sample_lensemble.argtypes = [vp, vp, i64, i64, ci, i64, vp, vp, vp, vp, vp, sz, vp]
     L.ffs_set_option.argtypes = [ci, ctypes.c_double]
     L.ffs_get_option.argtypes = [ci]
     L.ffs_get_option.restype = ctypes.c_double
@@ -284,3 +289,39 @@ def ffs_sample_host(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int,
                                 _stream_handle(stream, ws.device))
     _check(rc)
     return positions
+
+
+def ffs_sample_lensemble(V: torch.Tensor, lam: torch.Tensor, uniforms: torch.Tensor,
+                         workspace: Optional[Workspace] = None, stream=None):
+    """L-ensemble DPP: eigenvector j of C kept iff u_j < lam_j/(lam_j+1), then
+    FFS on the kept columns. V [L][K] (float64/complex128), lam [K] float64, uniforms [M][3K].
+    Returns positions int32 [M][K] (-1 past N_i), counts int32 [M], flags int32 [M]."""
+    if not (V.is_cuda and lam.is_cuda and uniforms.is_cuda):
+        raise FFSError("V, lam and uniforms must be CUDA tensors")
+    if V.dim() != 2:
+        raise FFSError("V must be 2-D [L][K]")
+    V = V.contiguous()
+    L, K = V.shape
+    lam = lam.contiguous()
+    uniforms = uniforms.contiguous()
+    if lam.dtype != torch.float64 or tuple(lam.shape) != (K,):
+        raise FFSError(f"lam must be float64 [K={K}]")
+    if uniforms.dtype != torch.float64 or uniforms.dim() != 2 or uniforms.shape[1] != 3 * K:
+        raise FFSError(f"uniforms must be float64 [M][3K] with K={K}, got {tuple(uniforms.shape)}")
+    M = uniforms.shape[0]
+    dt = _dtype_code(V)
+    positions = torch.empty((M, K), dtype=torch.int32, device=V.device)
+    counts = torch.empty(M, dtype=torch.int32, device=V.device)
+    flags = torch.empty(M, dtype=torch.int32, device=V.device)
+    ws = workspace if workspace is not None else Workspace(V.device)
+    need = int(load().ffs_lensemble_workspace_bytes(L, K, dt, M))
+    if need == 0 and M > 0:
+        _check(load().ffs_sample_lensemble(V.data_ptr(), lam.data_ptr(), L, K, dt, M, None, None, None, None,
+                                           None, 0, None))
+    wp, wn = ws.get(need)
+    rc = load().ffs_sample_lensemble(V.data_ptr(), lam.data_ptr(), L, K, dt, M, uniforms.data_ptr(),
+                                     positions.data_ptr(), counts.data_ptr(), flags.data_ptr(), wp, wn,
+                                     _stream_handle(stream, V.device))
+    _check(rc)
+    _keep_alive(stream, V, lam, uniforms, positions, counts, flags, ws.buf)
+    return positions, counts, flags

@@ -138,7 +138,10 @@ _CACHE_DIR = os.environ.get("FFS_INPUT_CACHE", "/tmp/ffs_input_cache")
 
 def build_u(cfg: Config) -> np.ndarray:
     """U for a registered config; cached on disk (git-ignored) because C4's eigh takes ~1 min."""
-    path = os.path.join(_CACHE_DIR, f"U_{cfg.name}.npy")
+    # keyed by the config AND this file's recipe source, so an edited generator never serves a
+    # stale matrix
+    key = hashlib.sha256((repr(cfg) + open(__file__).read()).encode()).hexdigest()[:16]
+    path = os.path.join(_CACHE_DIR, f"U_{cfg.name}_{key}.npy")
     if os.path.exists(path):
         try:
             return np.load(path)
@@ -164,6 +167,57 @@ def build_u(cfg: Config) -> np.ndarray:
     except OSError:
         pass
     return U
+
+
+# ---------------------------------------------------------------- L-ensemble workload
+@dataclasses.dataclass(frozen=True)
+class LensConfig:
+    """A DPP-summarisation-shaped L-ensemble: L items with D-dimensional features B = diag(q) G,
+    G ~ N(0,1)^{L x D} (seed), quality q = exp(0.5 z), z ~ N(0,1) (the C5 recipe at L = 1024, the
+    paper's Fig. 3B chain length); C = s B B^T with the scale s chosen so that the expected sample
+    size sum_j lambda_j/(lambda_j+1) equals n_mean (the paper's summaries keep a few sentences per
+    article; here a larger n_mean so every sample runs tens of FFS steps). Eigenvectors / values
+    come from the SVD of B (setup, not timed)."""
+    name: str = "lens"
+    L: int = 1024
+    D: int = 256
+    n_mean: float = 64.0
+    M: int = 16384
+    seed: int = 0
+
+    @property
+    def uniform_seed(self) -> int:
+        return 1005
+
+
+LENS = LensConfig()
+
+
+def build_lensemble(cfg: LensConfig = LENS, L: Optional[int] = None, D: Optional[int] = None,
+                    n_mean: Optional[float] = None, seed: Optional[int] = None, complex_: bool = False):
+    """(V [L][D], lam [D]) of the L-ensemble kernel C = V diag(lam) V^dagger."""
+    L = cfg.L if L is None else L
+    D = cfg.D if D is None else D
+    n_mean = cfg.n_mean if n_mean is None else n_mean
+    rng = np.random.default_rng(cfg.seed if seed is None else seed)
+    G = rng.standard_normal((L, D))
+    if complex_:
+        G = G + 1j * rng.standard_normal((L, D))
+    q = np.exp(0.5 * rng.standard_normal(L))
+    V, sig, _ = np.linalg.svd(q[:, None] * G, full_matrices=False)
+    s2 = sig ** 2
+    lo, hi = -60.0, 60.0  # bisection on log s: expected size sum s s2/(1 + s s2) = n_mean
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        e = np.sum(np.exp(mid) * s2 / (1.0 + np.exp(mid) * s2))
+        lo, hi = (mid, hi) if e < n_mean else (lo, mid)
+    lam = np.exp(0.5 * (lo + hi)) * s2
+    return np.ascontiguousarray(V), np.ascontiguousarray(lam)
+
+
+def lens_uniforms(M: int, K: int, seed: int) -> np.ndarray:
+    """[M][3K] fp64 uniforms (keep draws | permutation draws | selections), numpy Philox."""
+    return np.random.Generator(np.random.Philox(seed)).random((M, 3 * K))
 
 
 def u_sha256(U: np.ndarray) -> str:
