@@ -111,3 +111,28 @@ def lensemble_set_probabilities(V: np.ndarray, lam: np.ndarray):
             subsets.append(S)
             p.append(1.0 if n == 0 else float(np.real(np.linalg.det(C[np.ix_(S, S)]))))
     return subsets, np.array(p) / Z
+
+
+def gutzwiller_exact(U: np.ndarray, V: float):
+    """Exact Gutzwiller-projected expectations by enumeration (Supp S5): every
+    spinful configuration (S_up, S_dn) of the free ensemble has P_0 = P(S_up) P(S_dn) with
+    P(S) = |det U_S|^2 (Eq. 1); the interacting distribution is P_J ∝ J^2 P_0, J^2 = exp(-V D),
+    D = |S_up ∩ S_dn| (Eq. 4). Returns dict with <J^2>_0, <D>_J, <n_x>_J, and the per-configuration
+    arrays (p0, J2, D, n) for error estimates."""
+    subsets, p = set_probabilities(U)
+    L = U.shape[0]
+    p0, J2, D, n = [], [], [], []
+    for a, pa in zip(subsets, p):
+        for b, pb in zip(subsets, p):
+            d = len(set(a) & set(b))
+            occ = np.zeros(L)
+            occ[list(a)] += 1
+            occ[list(b)] += 1
+            p0.append(pa * pb)
+            J2.append(np.exp(-V * d))
+            D.append(d)
+            n.append(occ)
+    p0, J2, D, n = map(np.array, (p0, J2, D, n))
+    Z = np.sum(p0 * J2)
+    return {"J2_0": Z, "D_J": np.sum(p0 * J2 * D) / Z, "n_J": (p0 * J2) @ n / Z,
+            "p0": p0, "J2": J2, "D": D, "n": n}

@@ -238,6 +238,75 @@ int ffs_ref_sample_lensemble(const double* V, const double* lam, int64_t L, int6
     return bad ? -2 : 0;
 }
 
+/* ---------------------------------------------------------------- observables of the samples
+ * Occupation numbers <n_x> (SPEC.md:201 occupation oracle; "occupation number on
+ * the site"), pair occupations <n_x n_y>, and the Slater-Jastrow / Gutzwiller reweighting of Supp S5
+ * (PAPER.md:336-350): <O> = <J^2 o_L>_0 / <J^2>_0 with the Gutzwiller factor of Eq. 4
+ * J(x) = exp(-V/2 sum_i n_{i,up} n_{i,down}), i.e. J^2 = exp(-V D), D = number of doubly occupied
+ * sites. A spinful sample is a pair of independent FFS samples of the same U: rows 2s (up) and
+ * 2s+1 (down) of positions (SPEC.md:387 N_up = N_down). Entries < 0 (L-ensemble padding) are
+ * skipped. Plain loops over the samples, in sample order. */
+int ffs_ref_occupation(const int32_t* positions, int64_t M, int64_t Np, int64_t L, uint64_t* occ)
+{
+    if (!positions || !occ || L < 1 || Np < 1 || M < 0) return -1;
+    for (int64_t x = 0; x < L; ++x) occ[x] = 0;
+    for (int64_t i = 0; i < M; ++i)
+        for (int64_t k = 0; k < Np; ++k) {
+            int32_t x = positions[i * Np + k];
+            if (x >= 0 && x < L) occ[x] += 1;
+        }
+    return 0;
+}
+
+/* pair[x][y] = number of samples with both x and y occupied, x, y < W (the diagonal is <n_x>) */
+int ffs_ref_pair_occupation(const int32_t* positions, int64_t M, int64_t Np, int64_t W, uint64_t* pair)
+{
+    if (!positions || !pair || W < 1 || Np < 1 || M < 0) return -1;
+    for (int64_t q = 0; q < W * W; ++q) pair[q] = 0;
+    for (int64_t i = 0; i < M; ++i)
+        for (int64_t a = 0; a < Np; ++a) {
+            int32_t x = positions[i * Np + a];
+            if (x < 0 || x >= W) continue;
+            for (int64_t b = 0; b < Np; ++b) {
+                int32_t y = positions[i * Np + b];
+                if (y >= 0 && y < W) pair[x * W + y] += 1;
+            }
+        }
+    return 0;
+}
+
+/* result[0] = <J^2>_0 = (1/Ms) sum_s J_s^2; result[1] = <D>_J; result[2 + x] = <n_x>_J (both spins),
+ * with <O>_J = sum_s J_s^2 O_s / sum_s J_s^2, Ms spinful samples. */
+int ffs_ref_gutzwiller(const int32_t* positions, int64_t Ms, int64_t Np, int64_t L, double V, double* result)
+{
+    if (!positions || !result || L < 1 || Np < 1 || Ms < 1) return -1;
+    char* up = (char*)calloc((size_t)L, 1);
+    double* num = (double*)calloc((size_t)L, sizeof(double));
+    if (!up || !num) { free(up); free(num); return -2; }
+    double Z = 0.0, Dsum = 0.0;
+    for (int64_t s = 0; s < Ms; ++s) {
+        const int32_t* xu = positions + (2 * s) * Np;
+        const int32_t* xd = positions + (2 * s + 1) * Np;
+        for (int64_t k = 0; k < Np; ++k) if (xu[k] >= 0 && xu[k] < L) up[xu[k]] = 1;
+        int64_t D = 0;
+        for (int64_t k = 0; k < Np; ++k) if (xd[k] >= 0 && xd[k] < L && up[xd[k]]) ++D;
+        const double J2 = exp(-V * (double)D);   /* J^2 = exp(2 * (-V/2) D) */
+        Z += J2;
+        Dsum += J2 * (double)D;
+        for (int64_t k = 0; k < Np; ++k) {
+            if (xu[k] >= 0 && xu[k] < L) num[xu[k]] += J2;
+            if (xd[k] >= 0 && xd[k] < L) num[xd[k]] += J2;
+        }
+        for (int64_t k = 0; k < Np; ++k) if (xu[k] >= 0 && xu[k] < L) up[xu[k]] = 0;
+    }
+    result[0] = Z / (double)Ms;
+    result[1] = Dsum / Z;
+    for (int64_t x = 0; x < L; ++x) result[2 + x] = num[x] / Z;
+    free(up);
+    free(num);
+    return 0;
+}
+
 int ffs_ref_num_threads(void)
 {
 #ifdef _OPENMP

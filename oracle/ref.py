@@ -42,6 +42,9 @@ def lib():
         L.ffs_ref_chain.argtypes = [vp, i64, i64, ctypes.c_int, i64, vp, vp, vp, vp, vp]
         L.ffs_ref_permutation.argtypes = [vp, i64, i64, vp]
         L.ffs_ref_permutation.restype = None
+        L.ffs_ref_occupation.argtypes = [vp, i64, i64, i64, vp]
+        L.ffs_ref_pair_occupation.argtypes = [vp, i64, i64, i64, vp]
+        L.ffs_ref_gutzwiller.argtypes = [vp, i64, i64, i64, ctypes.c_double, vp]
         L.ffs_ref_sample_lensemble.argtypes = [vp, vp, i64, i64, ctypes.c_int, i64, vp, vp, vp, vp, ctypes.c_int]
         L.ffs_ref_num_threads.restype = ctypes.c_int
         _lib = L
@@ -131,6 +134,32 @@ def sample_lensemble(V, lam, uniforms, nthreads=0):
     if rc != 0:
         raise ValueError(f"ffs_ref_sample_lensemble rc={rc}")
     return pos, cnt, flags
+
+
+def occupation(positions, L):
+    """occ[x] = number of samples with site x occupied (entries < 0 skipped)."""
+    pos = np.ascontiguousarray(positions, dtype=np.int32)
+    occ = np.empty(L, dtype=np.uint64)
+    assert lib().ffs_ref_occupation(_ptr(pos), pos.shape[0], pos.shape[1], L, _ptr(occ)) == 0
+    return occ
+
+
+def pair_occupation(positions, W):
+    """pair[x][y] = number of samples with x and y occupied (x, y < W)."""
+    pos = np.ascontiguousarray(positions, dtype=np.int32)
+    pair = np.empty((W, W), dtype=np.uint64)
+    assert lib().ffs_ref_pair_occupation(_ptr(pos), pos.shape[0], pos.shape[1], W, _ptr(pair)) == 0
+    return pair
+
+
+def gutzwiller(positions, L, V):
+    """Gutzwiller reweighting (Supp S5) of spinful samples (rows 2s up, 2s+1 down):
+    [<J^2>_0, <D>_J, <n_0>_J .. <n_{L-1}>_J] with J^2 = exp(-V D)."""
+    pos = np.ascontiguousarray(positions, dtype=np.int32)
+    assert pos.shape[0] % 2 == 0
+    res = np.empty(2 + L, dtype=np.float64)
+    assert lib().ffs_ref_gutzwiller(_ptr(pos), pos.shape[0] // 2, pos.shape[1], L, float(V), _ptr(res)) == 0
+    return res
 
 
 def num_threads() -> int:

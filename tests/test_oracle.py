@@ -329,3 +329,71 @@ def test_lensemble_degenerate_spectra():
     pos, cnt, _ = ref.sample_lensemble(V, np.full(K, 1e300), uni)
     assert (cnt == K).all()
     assert (pos == ref.sample(V, uni[:, K:])).all()
+
+
+# ---------------------------------------------------------------- observables and reweighting (Supp S5)
+def test_occupation_and_pair_closed_forms():
+    """Projection DPP identities (K = U U^dagger): <n_x> = K_xx and <n_x n_y> = K_xx K_yy - |K_xy|^2
+    (z-tests), the sum rule sum_x n_x = N per sample (exact), diagonal pair counts = occupations."""
+    L, N, M = 12, 4, 100000
+    U = _rand_u(L, N, 31)
+    pos = ref.sample(U, inputs.uniforms(M, N, 32))
+    occ = ref.occupation(pos, L)
+    assert int(occ.sum()) == M * N
+    K = U @ U.conj().T
+    kxx = np.real(np.diag(K))
+    z = (occ / M - kxx) / np.sqrt(kxx * (1 - kxx) / M)
+    assert np.abs(z).max() < 4.5
+    pair = ref.pair_occupation(pos, L)
+    assert (np.diag(pair) == occ).all() and (pair == pair.T).all()
+    assert (pair.sum(axis=1) == N * occ).all()
+    g = np.outer(kxx, kxx) - np.abs(K) ** 2
+    np.fill_diagonal(g, kxx)
+    zp = (pair / M - g) / np.sqrt(np.maximum(g * (1 - g), 1e-12) / M)
+    assert np.abs(zp).max() < 5.0
+
+
+def test_gutzwiller_reweighting_matches_enumeration():
+    """<O>_J = <J^2 O>_0/<J^2>_0 from free FFS samples equals the exact interacting expectation of
+    the Gutzwiller-projected state (enumeration over all spinful configurations), within 4.5 sigma
+    of the ratio estimator."""
+    L, N, V, Ms = 5, 2, 1.5, 100000
+    U = _rand_u(L, N, 41)
+    pos = ref.sample(U, inputs.uniforms(2 * Ms, N, 42))
+    res = ref.gutzwiller(pos, L, V)
+    ex = exact.gutzwiller_exact(U, V)
+    w = ex["p0"] * ex["J2"] / ex["J2_0"]
+
+    def se(o, mean):  # delta-method s.e. of sum J2 O / sum J2 under P_0
+        return np.sqrt(np.sum(ex["p0"] * (ex["J2"] / ex["J2_0"]) ** 2 * (o - mean) ** 2) / Ms)
+
+    assert abs(res[0] - ex["J2_0"]) < 4.5 * np.sqrt(np.sum(ex["p0"] * (ex["J2"] - ex["J2_0"]) ** 2) / Ms)
+    assert abs(res[1] - ex["D_J"]) < 4.5 * se(ex["D"], ex["D_J"])
+    for x in range(L):
+        assert abs(res[2 + x] - ex["n_J"][x]) < 4.5 * se(ex["n"][:, x], ex["n_J"][x])
+    # the reweighting moves the estimate: <D>_J < <D>_0 for V > 0
+    assert ex["D_J"] < np.sum(ex["p0"] * ex["D"]) - 0.05
+    assert abs(w.sum() - 1) < 1e-12
+
+
+def test_gutzwiller_special_cases():
+    """V = 0: unit weights, <n_x>_J is the plain sample mean (both spins), <J^2>_0 = 1; a
+    hand-built pair set with known double occupancies gives the closed-form weighted mean."""
+    L, N = 10, 3
+    U = _rand_u(L, N, 51)
+    pos = ref.sample(U, inputs.uniforms(400, N, 52))
+    r0 = ref.gutzwiller(pos, L, 0.0)
+    assert r0[0] == 1.0
+    np.testing.assert_allclose(r0[2:], ref.occupation(pos, L) / 200.0, rtol=0, atol=1e-14)
+    # two spinful samples: D = 2 (x = 0, 1 doubly occupied) and D = 0
+    pos = np.array([[0, 1, 2], [1, 0, 5], [3, 4, 6], [7, 8, 9]], dtype=np.int32)
+    V = 0.7
+    r = ref.gutzwiller(pos, L, V)
+    w1, w2 = np.exp(-2 * V), 1.0
+    assert abs(r[0] - (w1 + w2) / 2) < 1e-15
+    assert abs(r[1] - 2 * w1 / (w1 + w2)) < 1e-15
+    n = np.zeros(L)
+    n[[0, 1]] = 2 * w1
+    n[[2, 5]] = w1
+    n[[3, 4, 6, 7, 8, 9]] = w2
+    np.testing.assert_allclose(r[2:], n / (w1 + w2), rtol=1e-15)
