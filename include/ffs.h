@@ -107,6 +107,32 @@ int ffs_sample_lensemble(const void* V, const double* lambda, int64_t L, int64_t
                          const double* uniforms, int32_t* positions, int32_t* counts, int32_t* sample_flags,
                          void* workspace, size_t ws_bytes, void* stream);
 
+/* Observables of FFS samples, on the device (Supp S5).
+ * positions: DEVICE int32[M][N'] as written by the sampling calls; entries < 0 (the L-ensemble's
+ * padding) are skipped. Outputs are DEVICE arrays, zeroed and filled by the call (async on stream).
+ *   ffs_occupation      : occ[x] = number of samples with site x occupied, x < L (uint64[L]);
+ *                         <n_x> = occ[x] / M ("occupation number").
+ *   ffs_pair_occupation : pair[x][y] = number of samples with x and y both occupied, x, y < W
+ *                         (uint64[W][W]; the diagonal is occ); <n_x n_y> = pair / M.
+ *   ffs_gutzwiller_reweight: Slater-Jastrow reweighting with the Gutzwiller factor of Eq. 4,
+ *                         J = exp(-V/2 sum_i n_{i,up} n_{i,down}): a spinful sample s is the pair of
+ *                         rows (2s, 2s+1) = (up, down), D_s = number of sites in both rows,
+ *                         J_s^2 = exp(-V D_s); result (DOUBLE[2 + L]): [0] = <J^2>_0 =
+ *                         (1/Ms) sum_s J_s^2, [1] = <D>_J, [2 + x] = <n_x>_J (both spins), with
+ *                         <O>_J = sum_s J_s^2 O_s / sum_s J_s^2 (the paper's <J^2 o_L>_0/<J^2>_0).
+ *                         dcount (uint64[N'+1], or NULL) receives the histogram of D_s. The sums
+ *                         are formed from exact integer histograms by D (order-independent).
+ *                         Ms >= 1 spinful samples (2 Ms rows); workspace of
+ *                         ffs_gutzwiller_workspace_bytes(N', L) bytes (FFS_ENOWS if smaller).
+ * Errors: FFS_EINVAL for null pointers / invalid sizes (W <= 46340, N' <= 8192 for pairs), FFS_ECUDA. */
+int ffs_occupation(const int32_t* positions, int64_t M, int64_t Nprime, int64_t L, unsigned long long* occ,
+                   void* stream);
+int ffs_pair_occupation(const int32_t* positions, int64_t M, int64_t Nprime, int64_t W, unsigned long long* pair,
+                        void* stream);
+size_t ffs_gutzwiller_workspace_bytes(int64_t Nprime, int64_t L);
+int ffs_gutzwiller_reweight(const int32_t* positions, int64_t Ms, int64_t Nprime, int64_t L, double V, double* result,
+                            unsigned long long* dcount, void* workspace, size_t ws_bytes, void* stream);
+
 /* Number of kernel launches the last successful sampling call on this thread issued. */
 int ffs_last_launch_count(void);
 

@@ -22,6 +22,7 @@
 #include "ffs_cluster_kernel.cuh"
 #include "ffs_dense.cuh"
 #include "ffs_lens.cuh"
+#include "ffs_observe.cuh"
 #include "ffs_kptr.h"
 
 // ====================================================================== shared host helpers
@@ -1228,6 +1229,92 @@ int ffs_sample_lensemble(const void* V, const double* lambda, int64_t L, int64_t
                          void* workspace, size_t ws_bytes, void* stream) {
   return launch_lensemble(V, lambda, L, K, dtype, M, uniforms, positions, counts, sample_flags, workspace, ws_bytes,
                           static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- observables (ffs_observe.cuh)
+static int obs_grid(int64_t work_items, int per_cta) {
+  const int sms = ffsh::sm_count(ffsh::device());
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work_items + per_cta - 1) / per_cta, (int64_t)sms * 8));
+}
+
+int ffs_occupation(const int32_t* positions, int64_t M, int64_t Nprime, int64_t L, unsigned long long* occ,
+                   void* stream) {
+  ffsh::launches() = 0;
+  if (M < 0 || Nprime < 1 || L < 1 || L > INT32_MAX) return fail(FFS_EINVAL, "invalid shape M=%lld N'=%lld L=%lld",
+                                                              (long long)M, (long long)Nprime, (long long)L);
+  if (!occ || (M > 0 && !positions)) return fail(FFS_EINVAL, "null positions/occ");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(occ, 0, (size_t)L * 8, s) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
+  if (M == 0) return FFS_OK;
+  const int64_t n = M * Nprime;
+  const int grid = obs_grid(n, ffsk::kObsThreads * 16);
+  const bool sm = L * 4 <= 48 * 1024 * 4;
+  ffsh::prof_begin(s);
+  if (sm) {
+    if (int rc = ffsh::ensure_max_smem(reinterpret_cast<const void*>(&ffsk::ffs_occupation_kernel<true>))) return rc;
+    ffsk::ffs_occupation_kernel<true><<<grid, ffsk::kObsThreads, (size_t)L * 4, s>>>(positions, n, (int)L, occ);
+  } else {
+    ffsk::ffs_occupation_kernel<false><<<grid, ffsk::kObsThreads, 0, s>>>(positions, n, (int)L, occ);
+  }
+  ffsh::prof_end(s);
+  ++ffsh::launches();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FFS_OK : fail(FFS_ECUDA, "occupation kernel: %s", cudaGetErrorString(e));
+}
+
+int ffs_pair_occupation(const int32_t* positions, int64_t M, int64_t Nprime, int64_t W, unsigned long long* pair,
+                        void* stream) {
+  ffsh::launches() = 0;
+  if (M < 0 || Nprime < 1 || Nprime > 8192 || W < 1 || W > 46340)
+    return fail(FFS_EINVAL, "invalid shape M=%lld N'=%lld W=%lld", (long long)M, (long long)Nprime, (long long)W);
+  if (!pair || (M > 0 && !positions)) return fail(FFS_EINVAL, "null positions/pair");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(pair, 0, (size_t)W * W * 8, s) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
+  if (M == 0) return FFS_OK;
+  const int warps = ffsk::kObsThreads / 32;
+  if (int rc = ffsh::ensure_max_smem(reinterpret_cast<const void*>(&ffsk::ffs_pair_kernel))) return rc;
+  ffsh::prof_begin(s);
+  ffsk::ffs_pair_kernel<<<obs_grid(M, warps), ffsk::kObsThreads, (size_t)warps * Nprime * 4, s>>>(positions, M, (int)Nprime,
+                                                                                               (int)W, pair);
+  ffsh::prof_end(s);
+  ++ffsh::launches();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FFS_OK : fail(FFS_ECUDA, "pair kernel: %s", cudaGetErrorString(e));
+}
+
+size_t ffs_gutzwiller_workspace_bytes(int64_t Nprime, int64_t L) {
+  if (Nprime < 1 || L < 1 || L > INT32_MAX) return 0;
+  return align_up((size_t)(Nprime + 1) * 8) + align_up((size_t)(Nprime + 1) * L * 8);
+}
+
+int ffs_gutzwiller_reweight(const int32_t* positions, int64_t Ms, int64_t Nprime, int64_t L, double V, double* result,
+                            unsigned long long* dcount, void* workspace, size_t ws_bytes, void* stream) {
+  ffsh::launches() = 0;
+  if (Ms < 1 || Nprime < 1 || L < 1 || L > INT32_MAX || !std::isfinite(V))
+    return fail(FFS_EINVAL, "invalid arguments Ms=%lld N'=%lld L=%lld", (long long)Ms, (long long)Nprime, (long long)L);
+  if (!positions || !result) return fail(FFS_EINVAL, "null positions/result");
+  const size_t need = ffs_gutzwiller_workspace_bytes(Nprime, L);
+  if (!workspace || ws_bytes < need) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dc = static_cast<unsigned long long*>(workspace);
+  unsigned long long* od = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) +
+                                                                 align_up((size_t)(Nprime + 1) * 8));
+  if (cudaMemsetAsync(workspace, 0, need, s) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
+  const int warps = ffsk::kObsThreads / 32;
+  const size_t smem = (size_t)warps * ((L + 31) / 32) * 4;
+  if (smem > kMaxSmem) return fail(FFS_EINVAL, "L=%lld too large for the per-warp site bitmap", (long long)L);
+  if (int rc = ffsh::ensure_max_smem(reinterpret_cast<const void*>(&ffsk::ffs_gutzwiller_kernel))) return rc;
+  ffsh::prof_begin(s);
+  ffsk::ffs_gutzwiller_kernel<<<obs_grid(Ms, warps), ffsk::kObsThreads, smem, s>>>(positions, Ms, (int)Nprime, (int)L,
+                                                                                  dc, od);
+  ffsk::ffs_reweight_finalize_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((L + 255) / 256, 1024)), 256, 0, s>>>(
+      dc, od, (int)Nprime, (int)L, Ms, V, result);
+  ffsh::prof_end(s);
+  ffsh::launches() += 2;
+  if (dcount && cudaMemcpyAsync(dcount, dc, (size_t)(Nprime + 1) * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(FFS_ECUDA, "dcount copy failed");
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FFS_OK : fail(FFS_ECUDA, "gutzwiller kernels: %s", cudaGetErrorString(e));
 }
 
 int ffs_last_launch_count(void) { return ffsh::launches(); }

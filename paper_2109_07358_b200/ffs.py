@@ -41,6 +41,10 @@ EXPORTED = (
     "ffs_last_kernel_ms",
     "ffs_lensemble_workspace_bytes",
     "ffs_sample_lensemble",
+    "ffs_occupation",
+    "ffs_pair_occupation",
+    "ffs_gutzwiller_workspace_bytes",
+    "ffs_gutzwiller_reweight",
     "ffs_set_option",
     "ffs_get_option",
     "ffs_last_error",
@@ -83,6 +87,11 @@ def load(build_if_missing: bool = True):
     L.ffs_lensemble_workspace_bytes.argtypes = [i64, i64, ci, i64]
     L.ffs_lensemble_workspace_bytes.restype = sz
     L.ffs_sample_lensemble.argtypes = [vp, vp, i64, i64, ci, i64, vp, vp, vp, vp, vp, sz, vp]
+    L.ffs_occupation.argtypes = [vp, i64, i64, i64, vp, vp]
+    L.ffs_pair_occupation.argtypes = [vp, i64, i64, i64, vp, vp]
+    L.ffs_gutzwiller_workspace_bytes.argtypes = [i64, i64]
+    L.ffs_gutzwiller_workspace_bytes.restype = sz
+    L.ffs_gutzwiller_reweight.argtypes = [vp, i64, i64, i64, ctypes.c_double, vp, vp, vp, sz, vp]
     L.ffs_set_option.argtypes = [ci, ctypes.c_double]
     L.ffs_get_option.argtypes = [ci]
     L.ffs_get_option.restype = ctypes.c_double
@@ -325,3 +334,49 @@ def ffs_sample_lensemble(V: torch.Tensor, lam: torch.Tensor, uniforms: torch.Ten
     _check(rc)
     _keep_alive(stream, V, lam, uniforms, positions, counts, flags, ws.buf)
     return positions, counts, flags
+
+
+def _positions_arg(positions: torch.Tensor):
+    if not positions.is_cuda or positions.dtype != torch.int32 or positions.dim() != 2:
+        raise FFSError("positions must be a CUDA int32 tensor [M][N']")
+    return positions.contiguous()
+
+
+def ffs_occupation(positions: torch.Tensor, L: int, stream=None) -> torch.Tensor:
+    """occ[x] = number of samples with site x occupied (int64 [L]; uint64 counts in the library)."""
+    positions = _positions_arg(positions)
+    M, Np = positions.shape
+    occ = torch.empty(L, dtype=torch.int64, device=positions.device)
+    _check(load().ffs_occupation(positions.data_ptr(), M, Np, L, occ.data_ptr(),
+                                 _stream_handle(stream, positions.device)))
+    _keep_alive(stream, positions, occ)
+    return occ
+
+
+def ffs_pair_occupation(positions: torch.Tensor, W: int, stream=None) -> torch.Tensor:
+    """pair[x][y] = number of samples with x and y occupied, x, y < W (int64 [W][W])."""
+    positions = _positions_arg(positions)
+    M, Np = positions.shape
+    pair = torch.empty((W, W), dtype=torch.int64, device=positions.device)
+    _check(load().ffs_pair_occupation(positions.data_ptr(), M, Np, W, pair.data_ptr(),
+                                      _stream_handle(stream, positions.device)))
+    _keep_alive(stream, positions, pair)
+    return pair
+
+
+def ffs_gutzwiller_reweight(positions: torch.Tensor, L: int, V: float, workspace: Optional[Workspace] = None,
+                            stream=None):
+    """Gutzwiller reweighting (Supp S5) of spinful samples (rows 2s up, 2s+1 down): returns
+    result float64 [2 + L] = [<J^2>_0, <D>_J, <n_x>_J ...] and the D histogram int64 [N'+1]."""
+    positions = _positions_arg(positions)
+    M, Np = positions.shape
+    if M % 2 or M == 0:
+        raise FFSError("positions must hold an even, nonzero number of rows (up/down pairs)")
+    res = torch.empty(2 + L, dtype=torch.float64, device=positions.device)
+    dcount = torch.empty(Np + 1, dtype=torch.int64, device=positions.device)
+    ws = workspace if workspace is not None else Workspace(positions.device)
+    wp, wn = ws.get(int(load().ffs_gutzwiller_workspace_bytes(Np, L)))
+    _check(load().ffs_gutzwiller_reweight(positions.data_ptr(), M // 2, Np, L, float(V), res.data_ptr(),
+                                          dcount.data_ptr(), wp, wn, _stream_handle(stream, positions.device)))
+    _keep_alive(stream, positions, res, dcount, ws.buf)
+    return res, dcount
