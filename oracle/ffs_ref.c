@@ -307,6 +307,59 @@ int ffs_ref_gutzwiller(const int32_t* positions, int64_t Ms, int64_t Np, int64_t
     return 0;
 }
 
+/* ffs_ref_sample_metropolis: M samples of the Supp S7 variant (sample_metropolis above), Np steps,
+ * Mc Metropolis updates per step. uniforms [M][Np + Np (1 + 2 Mc)], positions [M][Np], flags [M],
+ * margins [M][Np] or NULL. */
+int ffs_ref_sample_metropolis(const double* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, int64_t Mc,
+                              const double* uniforms, int32_t* positions, int32_t* flags, double* margins,
+                              int nthreads)
+{
+    if (M == 0) return 0;
+    if (check_args(U, L, N, dtype, Np) || Mc < 0 || !uniforms || !positions) return -1;
+    const int64_t stride = Np + Np * (1 + 2 * Mc);
+    size_t sb = scratch_bytes(L, N, Np, dtype);
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        char* buf = (char*)malloc(sb);
+        if (!buf) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = 1;
+        } else {
+            size_t es = dtype == FFS_REF_C128 ? 16 : 8;
+            char* p = buf;
+            void* R = p;      p += es * (size_t)(Np * Np);
+            void* h = p;      p += es * (size_t)Np;
+            p += 8 * (size_t)L;
+            char* chosen = p; p += (size_t)L;
+            int32_t* m = (int32_t*)(((uintptr_t)p + 3) & ~(uintptr_t)3);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 16)
+#endif
+            for (int64_t i = 0; i < M; ++i) {
+                const double* u = uniforms + i * stride;
+                ffs_ref_permutation(u, N, Np, m);
+                int f;
+                if (dtype == FFS_REF_F64)
+                    f = sample_metropolis_f64(U, L, N, Np, Mc, m, u, positions + i * Np,
+                                              margins ? margins + i * Np : NULL, (double*)R, (double*)h, chosen);
+                else
+                    f = sample_metropolis_c128((const double _Complex*)U, L, N, Np, Mc, m, u, positions + i * Np,
+                                               margins ? margins + i * Np : NULL, (double _Complex*)R,
+                                               (double _Complex*)h, chosen);
+                if (flags) flags[i] = f;
+            }
+            free(buf);
+        }
+    }
+    return bad ? -2 : 0;
+}
+
 int ffs_ref_num_threads(void)
 {
 #ifdef _OPENMP

@@ -116,3 +116,62 @@ static int SFX(sample_chain)(const SCALAR* U, int64_t L, int64_t N, int64_t Np, 
     }
     return flags;
 }
+
+/* Continuous / large-L variant (Supp S7): the same permutation, elimination and
+ * normal vector h as sample_chain, but x_k is drawn by a Metropolis chain of Mc updates instead of
+ * the explicit inverse-CDF draw over all L candidates: "A trial random ... update is proposed
+ * (x_k -> x_k + dx), and then accepted with probability |u_{x_k+dx}^T h|^2 / |u_{x_k}^T h|^2"
+ * (PAPER.md:385-386); "The update is iterated for M_cond times"; for problems with
+ * large L "replace the continuous update x_k -> x_k + dx by a discrete update x_k -> x_k'"
+ * (PAPER.md:393). Readings (Q16-Q18): the chain starts at x = floor(u_init L); the
+ * discrete update proposes x' = floor(u_prop L) (uniform over the sites: a symmetric proposal);
+ * the move is accepted iff u_acc * w(x) < w(x') (= u_acc < min(1, w(x')/w(x)), and a zero-weight
+ * start moves to the first positive-weight proposal); chosen sites have w = 0 (Pauli exclusion).
+ *   u       : [Np perm draws | Np x (1 + 2 Mc) chain draws: init, (prop, acc) x Mc]
+ *   margin  : if non-NULL, [Np] the smallest |u_acc - w(x')/w(x)| over the step's decisions with
+ *             w(x) > 0 (how close a decision came to flipping; tie detection in the parity tests)
+ * Returns flags: bit0 = some h had a non-finite norm, bit2 = a chain ended on a zero-weight site. */
+static int SFX(sample_metropolis)(const SCALAR* U, int64_t L, int64_t N, int64_t Np, int64_t Mc, const int32_t* m,
+                                  const double* u, int32_t* x_out, double* margin, SCALAR* R, SCALAR* h, char* chosen)
+{
+    const int64_t ncols = Np;
+    int flags = 0;
+    memset(chosen, 0, (size_t)L);
+    for (int64_t k = 1; k <= Np; ++k) {
+        if (k >= 2) SFX(advance_elimination)(U, N, m, x_out[k - 2], R, ncols, k);
+        double hn2;
+        SFX(normal_vector)(R, ncols, k, h, &hn2);
+        if (!isfinite(hn2)) flags |= 1;
+        const double* uc = u + Np + (k - 1) * (1 + 2 * Mc);
+        double mg = INFINITY;
+        int64_t x = (int64_t)floor(uc[0] * (double)L);
+        if (x > L - 1) x = L - 1;
+        double wx = 0.0;
+        if (!chosen[x]) {
+            SCALAR s = 0.0;
+            for (int64_t j = 0; j < k; ++j) s += U[x * N + m[j]] * h[j];
+            wx = ABS2(s);
+        }
+        for (int64_t t = 0; t < Mc; ++t) {
+            int64_t xp = (int64_t)floor(uc[1 + 2 * t] * (double)L);
+            if (xp > L - 1) xp = L - 1;
+            double wp = 0.0;
+            if (!chosen[xp]) {
+                SCALAR s = 0.0;
+                for (int64_t j = 0; j < k; ++j) s += U[xp * N + m[j]] * h[j];
+                wp = ABS2(s);
+            }
+            const double ua = uc[2 + 2 * t];
+            if (wx > 0.0 && fabs(ua - wp / wx) < mg) mg = fabs(ua - wp / wx);
+            if (ua * wx < wp) {
+                x = xp;
+                wx = wp;
+            }
+        }
+        if (!(wx > 0.0)) flags |= 4;
+        x_out[k - 1] = (int32_t)x;
+        chosen[x] = 1;
+        if (margin) margin[k - 1] = mg;
+    }
+    return flags;
+}

@@ -45,6 +45,8 @@ def lib():
         L.ffs_ref_occupation.argtypes = [vp, i64, i64, i64, vp]
         L.ffs_ref_pair_occupation.argtypes = [vp, i64, i64, i64, vp]
         L.ffs_ref_gutzwiller.argtypes = [vp, i64, i64, i64, ctypes.c_double, vp]
+        L.ffs_ref_sample_metropolis.argtypes = [vp, i64, i64, ctypes.c_int, i64, i64, i64, vp, vp, vp, vp,
+                                                ctypes.c_int]
         L.ffs_ref_sample_lensemble.argtypes = [vp, vp, i64, i64, ctypes.c_int, i64, vp, vp, vp, vp, ctypes.c_int]
         L.ffs_ref_num_threads.restype = ctypes.c_int
         _lib = L
@@ -160,6 +162,25 @@ def gutzwiller(positions, L, V):
     res = np.empty(2 + L, dtype=np.float64)
     assert lib().ffs_ref_gutzwiller(_ptr(pos), pos.shape[0] // 2, pos.shape[1], L, float(V), _ptr(res)) == 0
     return res
+
+
+def sample_metropolis(U, uniforms, Np, Mc, nthreads=0, return_margins=False):
+    """Supp S7 variant: Mc Metropolis updates per step with uniform discrete
+    proposals. uniforms [M][Np + Np (1 + 2 Mc)]; returns positions [M][Np], flags [M] (and the
+    per-step decision margins [M][Np])."""
+    Ub, dt = _u_bytes(U)
+    L, N = Ub.shape
+    uni = np.ascontiguousarray(uniforms, dtype=np.float64)
+    M = uni.shape[0]
+    assert uni.shape == (M, Np + Np * (1 + 2 * Mc)), (uni.shape, Np, Mc)
+    pos = np.empty((M, Np), dtype=np.int32)
+    flags = np.empty(M, dtype=np.int32)
+    mg = np.empty((M, Np), dtype=np.float64) if return_margins else None
+    rc = lib().ffs_ref_sample_metropolis(_ptr(Ub), L, N, dt, M, Np, Mc, _ptr(uni), _ptr(pos), _ptr(flags), _ptr(mg),
+                                         nthreads)
+    if rc != 0:
+        raise ValueError(f"ffs_ref_sample_metropolis rc={rc}")
+    return (pos, flags, mg) if return_margins else (pos, flags)
 
 
 def num_threads() -> int:

@@ -397,3 +397,68 @@ def test_gutzwiller_special_cases():
     n[[2, 5]] = w1
     n[[3, 4, 6, 7, 8, 9]] = w2
     np.testing.assert_allclose(r[2:], n / (w1 + w2), rtol=1e-15)
+
+
+# ---------------------------------------------------------------- Supp S7 Metropolis variant
+def _metro_uniforms(M, Np, Mc, seed):
+    return np.random.Generator(np.random.Philox(seed)).random((M, Np + Np * (1 + 2 * Mc)))
+
+
+def test_metropolis_without_updates_keeps_the_initial_draw():
+    """M_cond = 0: x_k is the chain's start floor(u_init L) (PAPER.md:388 with no iteration)."""
+    L, N = 30, 3
+    U = _rand_u(L, N, 61)
+    uni = _metro_uniforms(500, N, 0, 62)
+    pos, flags = ref.sample_metropolis(U, uni, N, 0)
+    starts = np.floor(uni[:, N:] * L).astype(int)
+    assert (pos == starts).all()
+
+
+def test_metropolis_accept_rule():
+    """u_acc = 0 accepts every proposal with positive weight (0 * w(x) < w(x')), so the chain ends
+    on the last proposal that is not an already chosen site (those have weight 0, Pauli)."""
+    L, N, Mc = 25, 4, 6
+    U = _rand_u(L, N, 63)
+    uni = _metro_uniforms(300, N, Mc, 64)
+    for k in range(N):
+        uni[:, N + k * (1 + 2 * Mc) + 2:N + (k + 1) * (1 + 2 * Mc):2] = 0.0
+    pos, flags = ref.sample_metropolis(U, uni, N, Mc)
+    for i in range(300):
+        chosen = set()
+        for k in range(N):
+            c = uni[i, N + k * (1 + 2 * Mc):N + (k + 1) * (1 + 2 * Mc)]
+            x = int(np.floor(c[0] * L))
+            for t in range(Mc):
+                xp = int(np.floor(c[1 + 2 * t] * L))
+                if xp not in chosen:
+                    x = xp
+            assert pos[i, k] == x
+            chosen.add(x)
+
+
+def test_metropolis_single_particle_stationary_law():
+    """N = 1: the chain targets w(x) = |U[x,0]|^2 (Eq. 3 with k = 1); after Mc = 100 independent
+    uniform proposals the draws follow it (chi-square), as the paper's N = 1 continuous example."""
+    from scipy import stats
+    L, M = 20, 100000
+    U = _rand_u(L, 1, 65)
+    pos, _ = ref.sample_metropolis(U, _metro_uniforms(M, 1, 100, 66), 1, 100)
+    p = np.abs(U[:, 0]) ** 2
+    obs = np.bincount(pos[:, 0], minlength=L)
+    assert stats.chisquare(obs, p * M).pvalue > 1e-3
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_metropolis_tiny_law(cplx):
+    """SPEC.md:193 acceptance example: L = 6, N = 2, M_cond = 500 discrete updates -> the sampled
+    sets follow |det U_S|^2 (Eq. 1): chi-square and TV <= 0.02 (100 000 samples)."""
+    L, N, M, Mc = 6, 2, 100000, 200
+    U = _rand_u(L, N, 67, cplx)
+    pos, flags = ref.sample_metropolis(U, _metro_uniforms(M, N, Mc, 68), N, Mc)
+    assert (flags == 0).all()
+    subsets, p = exact.set_probabilities(U)
+    index = {s: i for i, s in enumerate(subsets)}
+    obs = np.bincount([index[tuple(sorted(q))] for q in pos.tolist()], minlength=len(subsets))
+    stat, dof, pval, _ = exact.pooled_chisquare(obs, p * M)
+    assert pval > 1e-3, (stat, dof, pval)
+    assert 0.5 * np.abs(obs / M - p).sum() <= 0.02
