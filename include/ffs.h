@@ -107,6 +107,25 @@ int ffs_sample_lensemble(const void* V, const double* lambda, int64_t L, int64_t
                          const double* uniforms, int32_t* positions, int32_t* counts, int32_t* sample_flags,
                          void* workspace, size_t ws_bytes, void* stream);
 
+/* Continuous / large-L variant (Supp S7): the permutation, elimination and
+ * normal vector of ffs_sample, but x_k is drawn by a Metropolis chain of Mcond updates instead of
+ * the inverse-CDF draw over all L sites ("accepted with probability |u_{x_k+dx}^T h|^2 /
+ * |u_{x_k}^T h|^2", "iterated for M_cond times"; for large L "a discrete update x_k -> x_k'"), so
+ * the cost per sample is O(N'^3 + Mcond N'^2), independent of L. Readings shared with the oracle
+ * (Q16-Q18): the chain of step k starts at x = floor(u_init L); each update proposes
+ * x' = floor(u_prop L) (uniform, symmetric) and accepts iff u_acc w(x) < w(x'); chosen sites have
+ * w = 0. The result approaches Eq. 1 as Mcond grows (exact only in that limit).
+ *   uniforms : DEVICE double[M][N' + N'(1 + 2 Mcond)]: [0, N') permutation draws (rule of
+ *              ffs_sample), then per step k: u_init, (u_prop, u_acc) x Mcond
+ *   positions: DEVICE int32[M][N'] out; sample_flags (or NULL): bit0 = non-finite pivot,
+ *              bit2 = a chain ended on a zero-weight site (Mcond too small)
+ * Any L <= 2^31-1 (U is only read at the proposed rows); N' <= N <= L; Mcond <= 4096.
+ * Workspace: ffs_metropolis_workspace_bytes(...) bytes. Errors as ffs_sample. */
+size_t ffs_metropolis_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int64_t Mcond, ffs_dtype dtype, int64_t M);
+int ffs_sample_metropolis(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
+                          int64_t Mcond, const double* uniforms, int32_t* positions, int32_t* sample_flags,
+                          void* workspace, size_t ws_bytes, void* stream);
+
 /* Observables of FFS samples, on the device (Supp S5).
  * positions: DEVICE int32[M][N'] as written by the sampling calls; entries < 0 (the L-ensemble's
  * padding) are skipped. Outputs are DEVICE arrays, zeroed and filled by the call (async on stream).

@@ -23,6 +23,7 @@
 #include "ffs_dense.cuh"
 #include "ffs_lens.cuh"
 #include "ffs_observe.cuh"
+#include "ffs_metro.cuh"
 #include "ffs_kptr.h"
 
 // ====================================================================== shared host helpers
@@ -288,6 +289,20 @@ int make_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, Plan& pl) 
                      [&](Plan& p) { return make_plan_uncached(L, N, Np, dtype, M, p); });
 }
 
+// a1 for the paths that take precomputed permutation prefixes: one thread per sample, its
+// working permutation of N entries in shared memory (ffs_permute_kernel)
+int launch_permute(const double* uniforms, int64_t ustride, int32_t* perm, int64_t M, int64_t N, int64_t Np,
+                   cudaStream_t s) {
+  const int tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
+  const size_t smem = (size_t)tpb * N * 4;
+  if (smem > kMaxSmem) return fail(FFS_EINVAL, "N=%lld too large for the permutation kernel", (long long)N);
+  if (int rc = ffsh::ensure_max_smem(reinterpret_cast<const void*>(&ffsk::ffs_permute_kernel))) return rc;
+  const int64_t pgrid = (M + tpb - 1) / tpb;
+  ffsk::ffs_permute_kernel<<<(unsigned)pgrid, tpb, smem, s>>>(uniforms, ustride, perm, M, (int)N, (int)Np);
+  ++ffsh::launches();
+  return FFS_OK;
+}
+
 // ------------------------------------------------------------------ fast warp-owner path
 // Real U, L <= 256, N' <= kMaxNpWarp, U^T small enough for shared memory: ffs_seg_kernel
 // (one CTA per SM, G-lane segments of warps = sample owners) after ffs_permute_kernel.
@@ -295,8 +310,6 @@ struct WarpPlan {
   const void* fn;
   int R, B, S, G = 32, maxt, warps, grid, Lp, ut_stride;
   size_t ushared, owner, smem, ws_perm;
-  int perm_tpb;
-  size_t perm_smem;
 };
 
 template <int R, int B, int G, int MAXT>
@@ -345,8 +358,6 @@ int make_warp_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, WarpPla
   const int64_t ctas = (M + (int64_t)warps * w.S - 1) / ((int64_t)warps * w.S);
   w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, sms));
   w.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-  w.perm_tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
-  w.perm_smem = (size_t)w.perm_tpb * N * 4;
   return FFS_OK;
 }
 
@@ -366,9 +377,7 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
     return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, w.ws_perm);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
   int32_t* perm = static_cast<int32_t*>(ws);
-  const int64_t pgrid = (M + w.perm_tpb - 1) / w.perm_tpb;
-  ffsk::ffs_permute_kernel<<<(unsigned)pgrid, w.perm_tpb, w.perm_smem, stream>>>(uniforms, perm, M, (int)N, (int)Np);
-  ++ffsh::launches();
+  if (int rc2 = launch_permute(uniforms, 2 * Np, perm, M, N, Np, stream)) return rc2;
   ffsk::WarpParams p{};
   p.U = static_cast<const double*>(U);
   p.perm = perm;
@@ -709,12 +718,7 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
     ++ffsh::launches();
   }
   if (d.k_gather > 0) launch_transpose(U, Ut, L, N, d.c.Lpt, dtype, stream);
-  {
-    const int tpb = (int)std::max<int64_t>(1, std::min<int64_t>(128, 40960 / (4 * N)));
-    const int64_t pgrid = (M + tpb - 1) / tpb;
-    ffsk::ffs_permute_kernel<<<(unsigned)pgrid, tpb, (size_t)tpb * N * 4, stream>>>(uniforms, perm, M, (int)N, (int)Np);
-    ++ffsh::launches();
-  }
+  if (int rc = launch_permute(uniforms, 2 * Np, perm, M, N, Np, stream)) return rc;
   const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
   const int gjt = cx ? gj_tj<cplx>() : gj_tj<double>();
   double* Y = d.ws_y ? reinterpret_cast<double*>(Yb) : nullptr;
@@ -1079,6 +1083,79 @@ int launch_lensemble(const void* V, const double* lambda, int64_t L, int64_t K, 
   ffsh::clear_error();
   return FFS_OK;
 }
+
+// ------------------------------------------------------------------ Supp S7 Metropolis variant
+// ffs_permute_kernel (a1) then ffs_metro_kernel (one warp per sample, W per warp slot).
+// Workspace: [perm M x N' | W slots x N'^2].
+struct MetroLayout {
+  size_t perm, wbuf, total, smem;
+  int grid;
+};
+int metro_layout(int64_t L, int64_t N, int64_t Np, int64_t Mc, int dtype, int64_t M, MetroLayout& y) {
+  if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0 || Mc < 0 || Mc > 4096)
+    return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M_cond=%lld", (long long)L, (long long)N,
+                (long long)Np, (long long)Mc);
+  if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
+  const bool cx = dtype == FFS_C128;
+  const size_t es = cx ? 16 : 8;
+  y.smem = (size_t)ffsk::kMetroWarps * (cx ? ffsk::metro_warp_smem<cplx>((int)Np, (int)Mc)
+                                           : ffsk::metro_warp_smem<double>((int)Np, (int)Mc));
+  if (y.smem > kMaxSmem) return fail(FFS_EINVAL, "N'=%lld / M_cond=%lld too large for the Metropolis kernel",
+                                     (long long)Np, (long long)Mc);
+  const void* fn = cx ? reinterpret_cast<const void*>(&ffsk::ffs_metro_kernel<cplx>)
+                      : reinterpret_cast<const void*>(&ffsk::ffs_metro_kernel<double>);
+  if (int rc = ffsh::ensure_max_smem(fn)) return rc;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ffsk::kMetroWarps * 32, y.smem) != cudaSuccess ||
+      per_sm < 1)
+    return fail(FFS_EINVAL, "Metropolis kernel does not fit on an SM");
+  const int64_t M1 = std::max<int64_t>(M, 1);
+  y.grid = (int)std::max<int64_t>(1, std::min<int64_t>((M1 + ffsk::kMetroWarps - 1) / ffsk::kMetroWarps,
+                                                       (int64_t)per_sm * ffsh::sm_count(ffsh::device())));
+  y.perm = 0;
+  y.wbuf = align_up((size_t)M1 * Np * 4);
+  y.total = y.wbuf + align_up((size_t)y.grid * ffsk::kMetroWarps * Np * Np * es);
+  return FFS_OK;
+}
+
+int launch_metropolis(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, int64_t Mc,
+                      const double* uniforms, int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes,
+                      cudaStream_t stream) {
+  ffsh::launches() = 0;
+  if (M == 0) return FFS_OK;
+  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions");
+  MetroLayout y;
+  if (int rc = metro_layout(L, N, Np, Mc, dtype, M, y)) return rc;
+  if (!ws || ws_bytes < y.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, y.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  char* w = static_cast<char*>(ws);
+  int32_t* perm = reinterpret_cast<int32_t*>(w + y.perm);
+  const int64_t ustride = Np + Np * (1 + 2 * Mc);
+  if (int rc = launch_permute(uniforms, ustride, perm, M, N, Np, stream)) return rc;
+  ffsk::MetroParams p{};
+  p.U = static_cast<const double*>(U);
+  p.perm = perm;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.wbuf = reinterpret_cast<double*>(w + y.wbuf);
+  p.M = M;
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  p.Mc = (int)Mc;
+  ffsh::prof_begin(stream);
+  if (dtype == FFS_C128)
+    ffsk::ffs_metro_kernel<cplx><<<y.grid, ffsk::kMetroWarps * 32, y.smem, stream>>>(p);
+  else
+    ffsk::ffs_metro_kernel<double><<<y.grid, ffsk::kMetroWarps * 32, y.smem, stream>>>(p);
+  ffsh::prof_end(stream);
+  ++ffsh::launches();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  ffsh::clear_error();
+  return FFS_OK;
+}
 }  // namespace
 
 // ====================================================================== extern "C"
@@ -1315,6 +1392,18 @@ int ffs_gutzwiller_reweight(const int32_t* positions, int64_t Ms, int64_t Nprime
     return fail(FFS_ECUDA, "dcount copy failed");
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FFS_OK : fail(FFS_ECUDA, "gutzwiller kernels: %s", cudaGetErrorString(e));
+}
+
+size_t ffs_metropolis_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, int64_t Mcond, ffs_dtype dtype, int64_t M) {
+  MetroLayout y;
+  return metro_layout(L, N, Nprime, Mcond, dtype, M, y) == FFS_OK ? y.total : 0;
+}
+
+int ffs_sample_metropolis(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
+                          int64_t Mcond, const double* uniforms, int32_t* positions, int32_t* sample_flags,
+                          void* workspace, size_t ws_bytes, void* stream) {
+  return launch_metropolis(U, L, N, dtype, M, Nprime, Mcond, uniforms, positions, sample_flags, workspace, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
 }
 
 int ffs_last_launch_count(void) { return ffsh::launches(); }

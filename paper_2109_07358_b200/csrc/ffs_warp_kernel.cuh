@@ -64,8 +64,8 @@ struct Draw {
 };
 
 // U [L][N] -> per-sample permutation prefix [M][Np] (a1 rule, reading Q6); one thread per sample.
-static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, int32_t* __restrict__ perm, int64_t M,
-                                   int N, int Np) {
+static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, int64_t ustride,
+                                          int32_t* __restrict__ perm, int64_t M, int N, int Np) {
   extern __shared__ int pscratch[];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // per-thread working permutation, interleaved across the block ([N][blockDim]): the threads of
@@ -74,7 +74,7 @@ static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, i
   const int bs = blockDim.x;
   if (i >= M) return;
   for (int j = 0; j < N; ++j) m[j * bs] = j;
-  const double* u = uniforms + i * 2 * (int64_t)Np;
+  const double* u = uniforms + i * ustride;
   for (int j = 0; j < Np; ++j) {
     const int n = N - j;
     int r = (int)floor(u[j] * (double)n);

@@ -41,6 +41,8 @@ EXPORTED = (
     "ffs_last_kernel_ms",
     "ffs_lensemble_workspace_bytes",
     "ffs_sample_lensemble",
+    "ffs_metropolis_workspace_bytes",
+    "ffs_sample_metropolis",
     "ffs_occupation",
     "ffs_pair_occupation",
     "ffs_gutzwiller_workspace_bytes",
@@ -87,6 +89,9 @@ def load(build_if_missing: bool = True):
     L.ffs_lensemble_workspace_bytes.argtypes = [i64, i64, ci, i64]
     L.ffs_lensemble_workspace_bytes.restype = sz
     L.ffs_sample_lensemble.argtypes = [vp, vp, i64, i64, ci, i64, vp, vp, vp, vp, vp, sz, vp]
+    L.ffs_metropolis_workspace_bytes.argtypes = [i64, i64, i64, i64, ci, i64]
+    L.ffs_metropolis_workspace_bytes.restype = sz
+    L.ffs_sample_metropolis.argtypes = [vp, i64, i64, ci, i64, i64, i64, vp, vp, vp, vp, sz, vp]
     L.ffs_occupation.argtypes = [vp, i64, i64, i64, vp, vp]
     L.ffs_pair_occupation.argtypes = [vp, i64, i64, i64, vp, vp]
     L.ffs_gutzwiller_workspace_bytes.argtypes = [i64, i64]
@@ -380,3 +385,31 @@ def ffs_gutzwiller_reweight(positions: torch.Tensor, L: int, V: float, workspace
                                           dcount.data_ptr(), wp, wn, _stream_handle(stream, positions.device)))
     _keep_alive(stream, positions, res, dcount, ws.buf)
     return res, dcount
+
+
+def ffs_sample_metropolis(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int, Mcond: int,
+                          workspace: Optional[Workspace] = None, stream=None):
+    """Supp S7 variant: Mcond Metropolis updates per step (uniform discrete proposals).
+    uniforms [M][N' + N'(1 + 2 Mcond)]; returns positions int32 [M][N'] and flags int32 [M]."""
+    if not (U.is_cuda and uniforms.is_cuda) or U.dim() != 2:
+        raise FFSError("U [L][N] and uniforms must be CUDA tensors")
+    U = U.contiguous()
+    uniforms = uniforms.contiguous()
+    L, N = U.shape
+    width = Nprime + Nprime * (1 + 2 * Mcond)
+    if uniforms.dtype != torch.float64 or uniforms.dim() != 2 or uniforms.shape[1] != width:
+        raise FFSError(f"uniforms must be float64 [M][{width}], got {tuple(uniforms.shape)}")
+    M = uniforms.shape[0]
+    dt = _dtype_code(U)
+    positions = torch.empty((M, Nprime), dtype=torch.int32, device=U.device)
+    flags = torch.empty(M, dtype=torch.int32, device=U.device)
+    ws = workspace if workspace is not None else Workspace(U.device)
+    need = int(load().ffs_metropolis_workspace_bytes(L, N, Nprime, Mcond, dt, M))
+    if need == 0 and M > 0:
+        _check(load().ffs_sample_metropolis(U.data_ptr(), L, N, dt, M, Nprime, Mcond, None, None, None, None, 0, None))
+    wp, wn = ws.get(need)
+    _check(load().ffs_sample_metropolis(U.data_ptr(), L, N, dt, M, Nprime, Mcond, uniforms.data_ptr(),
+                                        positions.data_ptr(), flags.data_ptr(), wp, wn,
+                                        _stream_handle(stream, U.device)))
+    _keep_alive(stream, U, uniforms, positions, flags, ws.buf)
+    return positions, flags

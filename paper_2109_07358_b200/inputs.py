@@ -220,6 +220,40 @@ def lens_uniforms(M: int, K: int, seed: int) -> np.ndarray:
     return np.random.Generator(np.random.Philox(seed)).random((M, 3 * K))
 
 
+# ---------------------------------------------------------------- Supp S7 workload (continuous models)
+@dataclasses.dataclass(frozen=True)
+class MetroConfig:
+    """Continuous-model stand-in for the Supp S7 variant: N fermions in a box,
+    discretised on a fine grid of L sites (the "large number of lattice sites L" that makes the
+    explicit sampler inefficient); U = the N lowest box orbitals
+    U[x, n] = sqrt(2/(L+1)) sin(pi (n+1)(x+1)/(L+1)) (exact eigenvectors of the open chain, so
+    orthonormal without a factorisation). M_cond updates per step, N' = N."""
+    name: str = "metro"
+    L: int = 1 << 20
+    N: int = 64
+    Mc: int = 32
+    M: int = 16384
+
+    @property
+    def uniform_seed(self) -> int:
+        return 1006
+
+
+METRO = MetroConfig()
+
+
+def build_box_orbitals(L: int, N: int) -> np.ndarray:
+    x = np.arange(1, L + 1, dtype=np.float64)[:, None]
+    n = np.arange(1, N + 1, dtype=np.float64)[None, :]
+    return np.ascontiguousarray(np.sqrt(2.0 / (L + 1)) * np.sin(np.pi * n * x / (L + 1)))
+
+
+def metro_uniforms(M: int, Np: int, Mc: int, seed: int) -> np.ndarray:
+    """[M][N' + N'(1 + 2 Mc)] fp64 uniforms: permutation draws, then per step u_init and
+    (u_prop, u_acc) x Mc (numpy Philox)."""
+    return np.random.Generator(np.random.Philox(seed)).random((M, Np + Np * (1 + 2 * Mc)))
+
+
 def u_sha256(U: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(U).tobytes()).hexdigest()
 
