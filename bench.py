@@ -309,6 +309,134 @@ def sweep_entry(r, cpu_budget, no_cpu):
     return e
 
 
+def measure_extensions(dev, steps, no_cpu, cpu_budget):
+    """The §8(f) rows beyond the BASELINE workloads, each timed like a sweep entry (device time
+    with inputs resident, L2 flushed, kernel events, clocks, e2e where a host path exists):
+    the L-ensemble front end (`lens`), the Supp S7 Metropolis variant (`metro`), and the
+    Gutzwiller reweighting of C2 spinful samples (`gutzwiller`, HBM-bound)."""
+    import torch
+    from paper_2109_07358_b200 import ffs
+
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(fn, K):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        ffs.ffs_profile_enable(True)
+        clk = ClockSampler(dev.index or 0)
+        clk.start()
+        tot, kms = 0.0, []
+        for _ in range(K):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+            kms.append(ffs.ffs_last_kernel_ms())
+        clocks = clk.stop()
+        ffs.ffs_profile_enable(False)
+        return tot / K, statistics.median(kms), clocks, ffs.ffs_last_launch_count()
+
+    # L-ensemble (PAPER.md:178-180)
+    cfg = inputs.LENS
+    V, lam = inputs.build_lensemble(cfg)
+    uni = inputs.lens_uniforms(cfg.M, cfg.D, cfg.uniform_seed)
+    Vd, ld, ud = (torch.from_numpy(a).to(dev) for a in (V, lam, uni))
+    ws = ffs.Workspace(dev)
+    res = {}
+
+    def lens_step():
+        res["out"] = ffs.ffs_sample_lensemble(Vd, ld, ud, workspace=ws, stream=stream)
+
+    ms, kms, clocks, nl = timed(lens_step, steps)
+    nmean = float(res["out"][1].double().mean().item())
+    fl = cfg.L * nmean ** 2 + nmean ** 3  # PAPER.md:81 at the sample's own N_i (mean)
+    out["lens"] = {"config": {"workload": "lens", "L": cfg.L, "K": cfg.D, "mean_N": nmean, "M": cfg.M,
+                              "l2": L2_NOTE},
+                   "dtype": "f64", "value": cfg.M / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms,
+                   "kernel": "ffs_lens_prep_kernel + ffs_sample_kernel (ragged mode, CTA owners)",
+                   "kernel_ms": kms, "effective_gflops": cfg.M * fl / (ms * 1e-3) / 1e9,
+                   "frac": cfg.M * fl / (kms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, "clocks": clocks, "gpu_launches": nl}
+    if not no_cpu:
+        from oracle import ref
+        n = 2048
+        t0 = time.perf_counter()
+        ref.sample_lensemble(V, lam, uni[:n])
+        t = time.perf_counter() - t0
+        out["lens"]["cpu_baseline"] = {"value": n / t, "unit": "samples/s", "cores": min(n, ref.num_threads()),
+                                       "kind": "oracle", "sample": f"first {n} of {cfg.M} samples ({t:.1f} s)"}
+    del Vd, ld, ud, ws
+
+    # Supp S7 Metropolis variant, continuous-model stand-in (L = 2^20 grid)
+    mc = inputs.METRO
+    U = inputs.build_box_orbitals(mc.L, mc.N)
+    uni = inputs.metro_uniforms(mc.M, mc.N, mc.Mc, mc.uniform_seed)
+    Ud, ud = torch.from_numpy(U).to(dev), torch.from_numpy(uni).to(dev)
+    ws = ffs.Workspace(dev)
+
+    def metro_step():
+        ffs.ffs_sample_metropolis(Ud, ud, mc.N, mc.Mc, workspace=ws, stream=stream)
+
+    ms, kms, clocks, nl = timed(metro_step, steps)
+    N = mc.N
+    fl = N ** 3 / 3 + 2 * mc.Mc * N * (N + 1) / 2      # GJ rank-1 updates + Mc weights per step
+    byts = 8 * mc.Mc * N * (N + 1) / 2 + 16 * N * (1 + 2 * mc.Mc)  # gathered U entries + uniforms
+    out["metro"] = {"config": {"workload": "metro", "L": mc.L, "N": N, "Nprime": N, "Mcond": mc.Mc, "M": mc.M,
+                               "l2": L2_NOTE},
+                    "dtype": "f64", "value": mc.M / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms,
+                    "kernel": "ffs_permute_kernel + ffs_metro_kernel (warp per sample)", "kernel_ms": kms,
+                    "roofline": {"bound": "hbm", "achieved": mc.M * byts / (kms * 1e-3) / 1e9,
+                                 "peak": measured_hbm(), "unit": "GB/s",
+                                 "frac": mc.M * byts / (kms * 1e-3) / 1e9 / measured_hbm(),
+                                 "bytes_def": "algorithmic: the gathered U entries of every chain state "
+                                              "(8 (k+1) B per state) + the chain uniforms, per sample"},
+                    "effective_gflops": mc.M * fl / (ms * 1e-3) / 1e9, "clocks": clocks, "gpu_launches": nl}
+    if not no_cpu:
+        from oracle import ref
+        n = 256
+        t0 = time.perf_counter()
+        ref.sample_metropolis(U, uni[:n], N, mc.Mc)
+        t = time.perf_counter() - t0
+        out["metro"]["cpu_baseline"] = {"value": n / t, "unit": "samples/s", "cores": min(n, ref.num_threads()),
+                                        "kind": "oracle", "sample": f"first {n} of {mc.M} samples ({t:.1f} s)"}
+    del Ud, ud, ws
+
+    # Gutzwiller reweighting (Supp S5) of C2 spinful samples: an HBM-bound reduction
+    cfg, U, uni, M, Np = workload("dw", False, 0)
+    pos = ffs.ffs_sample(torch.from_numpy(U).to(dev), torch.from_numpy(uni).to(dev))
+    ws = ffs.Workspace(dev)
+
+    def gw_step():
+        ffs.ffs_gutzwiller_reweight(pos, cfg.L, 1.0, workspace=ws, stream=stream)
+
+    ms, kms, clocks, nl = timed(gw_step, steps)
+    byts = M * Np * 4
+    out["gutzwiller"] = {"config": {"workload": "gutzwiller(dw)", "L": cfg.L, "Nprime": Np, "spinful_samples": M // 2,
+                                    "V": 1.0, "l2": L2_NOTE},
+                         "value": (M // 2) / (ms * 1e-3), "unit": "spinful samples/s", "ms_per_step": ms,
+                         "kernel": "ffs_gutzwiller_kernel + ffs_reweight_finalize_kernel", "kernel_ms": kms,
+                         "roofline": {"bound": "hbm", "achieved": byts / (kms * 1e-3) / 1e9, "peak": measured_hbm(),
+                                      "unit": "GB/s", "frac": byts / (kms * 1e-3) / 1e9 / measured_hbm(),
+                                      "bytes_def": "positions read once: 4 N' B per sample"},
+                         "clocks": clocks, "gpu_launches": nl}
+    del flush
+    return out
+
+
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6547.5  # MEASURED_PEAKS.json value of round 1 (same pool)
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -370,6 +498,8 @@ def run_gpu(args):
                                         "sample": f"first {n} of {M} samples ({t:.1f} s), OpenMP over samples"}
         if sweep is not None:
             line["sweep"] = sweep
+        if world == 1 and not args.no_sweep:
+            line["extensions"] = measure_extensions(dev, max(3, min(args.steps, 10)), args.no_cpu, args.sweep_cpu_budget)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
