@@ -30,20 +30,24 @@
 /* ---- real instantiation ---- */
 #define SCALAR double
 #define ABS2(z) ((z) * (z))
+#define CONJ(z) (z)
 #define SFX(name) name##_f64
 #include "ffs_ref_core.h"
 #undef SCALAR
 #undef ABS2
+#undef CONJ
 #undef SFX
 
 /* ---- complex instantiation ---- */
 static inline double abs2_c(double _Complex z) { return creal(z) * creal(z) + cimag(z) * cimag(z); }
 #define SCALAR double _Complex
 #define ABS2(z) abs2_c(z)
+#define CONJ(z) conj(z)
 #define SFX(name) name##_c128
 #include "ffs_ref_core.h"
 #undef SCALAR
 #undef ABS2
+#undef CONJ
 #undef SFX
 
 /* Permutation draw ("generate a vector m as a random permutation of n"; reading Q6):
@@ -352,6 +356,54 @@ int ffs_ref_sample_metropolis(const double* U, int64_t L, int64_t N, int dtype, 
                     f = sample_metropolis_c128((const double _Complex*)U, L, N, Np, Mc, m, u, positions + i * Np,
                                                margins ? margins + i * Np : NULL, (double _Complex*)R,
                                                (double _Complex*)h, chosen);
+                if (flags) flags[i] = f;
+            }
+            free(buf);
+        }
+    }
+    return bad ? -2 : 0;
+}
+
+/* ffs_ref_sample_hkpv: M samples of the modified HKPV sampler (hkpv_chain above), Np steps.
+ * uniforms [M][Np] selection draws; positions [M][Np]; flags [M]; weights [S][Np][L] and totals
+ * [S][Np] of the first S samples (either may be NULL; S <= M). */
+int ffs_ref_sample_hkpv(const double* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np,
+                        const double* uniforms, int32_t* positions, int32_t* flags, int64_t S, double* weights,
+                        double* totals, int nthreads)
+{
+    if (M == 0) return 0;
+    if (check_args(U, L, N, dtype, Np) || !uniforms || !positions || S < 0 || S > M) return -1;
+    size_t es = dtype == FFS_REF_C128 ? 16 : 8;
+    size_t sb = es * (size_t)(Np * N) + 8 * (size_t)L + (size_t)L + 64;
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        char* buf = (char*)malloc(sb);
+        if (!buf) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = 1;
+        } else {
+            void* E = buf;
+            double* r = (double*)(buf + es * (size_t)(Np * N));
+            char* chosen = (char*)(r + L);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 16)
+#endif
+            for (int64_t i = 0; i < M; ++i) {
+                double* wt = (weights && i < S) ? weights + i * Np * L : NULL;
+                double* tt = (totals && i < S) ? totals + i * Np : NULL;
+                int f;
+                if (dtype == FFS_REF_F64)
+                    f = hkpv_chain_f64(U, L, N, Np, uniforms + i * Np, positions + i * Np, wt, tt, (double*)E, r,
+                                       chosen);
+                else
+                    f = hkpv_chain_c128((const double _Complex*)U, L, N, Np, uniforms + i * Np, positions + i * Np,
+                                        wt, tt, (double _Complex*)E, r, chosen);
                 if (flags) flags[i] = f;
             }
             free(buf);

@@ -175,3 +175,76 @@ static int SFX(sample_metropolis)(const SCALAR* U, int64_t L, int64_t N, int64_t
     }
     return flags;
 }
+
+/* Modified HKPV sampler (the paper's comparison method: "improved from O(N^3 L) to
+ * O(N^2 L) with certain modification", "the modified HPKV algorithm requires 2LN^2
+ * operations"; its steps as SPEC.md:238-246 states them): the chain rule on the projection kernel
+ * K = U U^dagger without forming K. r_1(x) = |u_x|^2; at step k, x_k ~ r_k (inverse CDF with the
+ * selection rule of reading Q5; chosen sites 0, rounding residues below 0 clamped to 0); then
+ * e_k = u_{x_k} orthonormalised against e_1..e_{k-1} (modified Gram-Schmidt, Hermitian inner
+ * product <a, b> = sum_n a_n conj(b_n)) and r_{k+1}(x) = r_k(x) - |<u_x, e_k>|^2 for every x
+ * (L N multiply-adds per step: 2 L N^2 operations in total).
+ *   u_sel : Np selection uniforms;  w_trace / tot_out as sample_chain (normalised r_k, and T_k)
+ *   E     : scratch Np x N SCALAR, r : scratch L doubles */
+static int SFX(hkpv_chain)(const SCALAR* U, int64_t L, int64_t N, int64_t Np, const double* u_sel, int32_t* x_out,
+                           double* w_trace, double* tot_out, SCALAR* E, double* r, char* chosen)
+{
+    int flags = 0;
+    memset(chosen, 0, (size_t)L);
+    for (int64_t x = 0; x < L; ++x) {
+        double a = 0.0;
+        for (int64_t n = 0; n < N; ++n) a += ABS2(U[x * N + n]);
+        r[x] = a;
+    }
+    for (int64_t k = 1; k <= Np; ++k) {
+        double T = 0.0;
+        for (int64_t x = 0; x < L; ++x) {
+            double wx = (chosen[x] || !(r[x] > 0.0)) ? 0.0 : r[x];
+            T += wx;
+        }
+        int64_t sel = -1;
+        if (!(T > 0.0) || !isfinite(T)) {
+            flags |= 1;
+            for (int64_t x = 0; x < L; ++x) if (!chosen[x]) { sel = x; break; }
+        } else {
+            double t = u_sel[k - 1] * T, C = 0.0;
+            for (int64_t x = 0; x < L; ++x) {
+                double wx = (chosen[x] || !(r[x] > 0.0)) ? 0.0 : r[x];
+                C += wx;
+                if (wx > 0.0 && C > t) { sel = x; break; }
+            }
+            if (sel < 0)
+                for (int64_t x = L - 1; x >= 0; --x)
+                    if (!chosen[x] && r[x] > 0.0) { sel = x; break; }
+        }
+        if (sel < 0) sel = 0;
+        if (w_trace)
+            for (int64_t x = 0; x < L; ++x)
+                w_trace[(k - 1) * L + x] = (T > 0.0 && !chosen[x] && r[x] > 0.0) ? r[x] / T : 0.0;
+        if (tot_out) tot_out[k - 1] = T;
+        if (T > 0.0 && r[sel] / T < 1e-12) flags |= 2;
+        x_out[k - 1] = (int32_t)sel;
+        chosen[sel] = 1;
+        if (k == Np) break;
+        /* e_k: modified Gram-Schmidt of u_{x_k} against e_1..e_{k-1} */
+        SCALAR* e = E + (k - 1) * N;
+        for (int64_t n = 0; n < N; ++n) e[n] = U[sel * N + n];
+        for (int64_t j = 0; j < k - 1; ++j) {
+            const SCALAR* ej = E + j * N;
+            SCALAR c = 0.0;
+            for (int64_t n = 0; n < N; ++n) c += e[n] * CONJ(ej[n]);
+            for (int64_t n = 0; n < N; ++n) e[n] -= c * ej[n];
+        }
+        double nrm = 0.0;
+        for (int64_t n = 0; n < N; ++n) nrm += ABS2(e[n]);
+        nrm = sqrt(nrm);
+        for (int64_t n = 0; n < N; ++n) e[n] /= nrm;
+        /* residual update for every candidate */
+        for (int64_t x = 0; x < L; ++x) {
+            SCALAR c = 0.0;
+            for (int64_t n = 0; n < N; ++n) c += U[x * N + n] * CONJ(e[n]);
+            r[x] -= ABS2(c);
+        }
+    }
+    return flags;
+}

@@ -47,6 +47,8 @@ def lib():
         L.ffs_ref_gutzwiller.argtypes = [vp, i64, i64, i64, ctypes.c_double, vp]
         L.ffs_ref_sample_metropolis.argtypes = [vp, i64, i64, ctypes.c_int, i64, i64, i64, vp, vp, vp, vp,
                                                 ctypes.c_int]
+        L.ffs_ref_sample_hkpv.argtypes = [vp, i64, i64, ctypes.c_int, i64, i64, vp, vp, vp, i64, vp, vp,
+                                          ctypes.c_int]
         L.ffs_ref_sample_lensemble.argtypes = [vp, vp, i64, i64, ctypes.c_int, i64, vp, vp, vp, vp, ctypes.c_int]
         L.ffs_ref_num_threads.restype = ctypes.c_int
         _lib = L
@@ -181,6 +183,27 @@ def sample_metropolis(U, uniforms, Np, Mc, nthreads=0, return_margins=False):
     if rc != 0:
         raise ValueError(f"ffs_ref_sample_metropolis rc={rc}")
     return (pos, flags, mg) if return_margins else (pos, flags)
+
+
+def sample_hkpv(U, uniforms, Np=None, S=0, nthreads=0):
+    """Modified HKPV sampler (the paper's comparator).
+    uniforms [M][Np] selection draws. Returns positions [M][Np], flags [M], and for S > 0 the
+    normalised weights [S][Np][L] and totals [S][Np] of the first S samples."""
+    Ub, dt = _u_bytes(U)
+    L, N = Ub.shape
+    uni = np.ascontiguousarray(uniforms, dtype=np.float64)
+    M = uni.shape[0]
+    Np = uni.shape[1] if Np is None else Np
+    assert uni.shape == (M, Np), (uni.shape, Np)
+    pos = np.empty((M, Np), dtype=np.int32)
+    flags = np.empty(M, dtype=np.int32)
+    w = np.empty((S, Np, L), dtype=np.float64) if S else None
+    tot = np.empty((S, Np), dtype=np.float64) if S else None
+    rc = lib().ffs_ref_sample_hkpv(_ptr(Ub), L, N, dt, M, Np, _ptr(uni), _ptr(pos), _ptr(flags), S, _ptr(w),
+                                   _ptr(tot), nthreads)
+    if rc != 0:
+        raise ValueError(f"ffs_ref_sample_hkpv rc={rc}")
+    return (pos, flags, w, tot) if S else (pos, flags)
 
 
 def num_threads() -> int:

@@ -462,3 +462,53 @@ def test_metropolis_tiny_law(cplx):
     stat, dof, pval, _ = exact.pooled_chisquare(obs, p * M)
     assert pval > 1e-3, (stat, dof, pval)
     assert 0.5 * np.abs(obs / M - p).sum() <= 0.02
+
+
+# ---------------------------------------------------------------- modified HKPV comparator
+@pytest.mark.parametrize("cplx", [False, True])
+def test_hkpv_conditionals_are_schur_complements_of_K(cplx):
+    """The HKPV chain rule on K = U U^dagger: the step-k weight of x is the Schur complement
+    K_xx - K_{x,X} K_XX^{-1} K_{X,x} of the chosen set X (normalised by its trace N - k + 1),
+    and the totals obey the trace identity sum_x r_k(x) = N - (k-1)."""
+    L, N = 11, 5
+    U = _rand_u(L, N, 71, cplx)
+    uni = np.random.Generator(np.random.Philox(72)).random((6, N))
+    pos, _, w, tot = ref.sample_hkpv(U, uni, S=6)
+    K = U @ U.conj().T
+    for i in range(6):
+        for k in range(N):
+            X = list(pos[i, :k])
+            r = np.real(np.diag(K)).copy()
+            if X:
+                KX = K[np.ix_(range(L), X)]
+                r -= np.real(np.einsum("xa,ab,xb->x", KX, np.linalg.inv(K[np.ix_(X, X)]), KX.conj()))
+                r[X] = 0.0
+            np.testing.assert_allclose(w[i, k], np.maximum(r, 0) / (N - k), atol=1e-12)
+            assert abs(tot[i, k] - (N - k)) < 1e-12
+
+
+@pytest.mark.parametrize("L,N,cplx", [(6, 3, False), (16, 4, False), (5, 2, True)])
+def test_hkpv_matches_brute_force_law(L, N, cplx):
+    U = _rand_u(L, N, 73 + L, cplx) if (L, N) != (16, 4) else inputs.build_u(inputs.CONFIGS["tiny"])
+    M = 200000
+    pos, flags = ref.sample_hkpv(U, np.random.Generator(np.random.Philox(74)).random((M, N)))
+    assert (flags == 0).all()
+    subsets, p = exact.set_probabilities(U)
+    index = {s: i for i, s in enumerate(subsets)}
+    obs = np.bincount([index[tuple(sorted(q))] for q in pos.tolist()], minlength=len(subsets))
+    stat, dof, pval, _ = exact.pooled_chisquare(obs, p * M)
+    assert pval > 1e-3, (stat, dof, pval)
+
+
+def test_hkpv_special_cases():
+    """Point mass (U = e_3 column), full filling (L = N), first step K_xx / N."""
+    U = np.zeros((5, 1))
+    U[2, 0] = 1.0
+    pos, _ = ref.sample_hkpv(U, np.random.default_rng(1).random((50, 1)))
+    assert (pos == 2).all()
+    U = _rand_u(4, 4, 75)
+    pos, _ = ref.sample_hkpv(U, np.random.default_rng(2).random((50, 4)))
+    assert all(sorted(p) == [0, 1, 2, 3] for p in pos.tolist())
+    U = _rand_u(9, 3, 76)
+    _, _, w, _ = ref.sample_hkpv(U, np.random.default_rng(3).random((1, 3)), S=1)
+    np.testing.assert_allclose(w[0, 0], np.sum(U ** 2, axis=1) / 3, atol=1e-15)

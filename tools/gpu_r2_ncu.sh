@@ -14,6 +14,11 @@ done
 full() {  # name workload kernel-regex skip
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$3 -s $4 -c 1 -o $O/full_$1 \
     python tools/run_once.py $2 2 > $O/full_$1.log 2>&1
+  ncu -i $O/full_$1.ncu-rep --page raw --csv > $O/full_$1_raw.csv 2>/dev/null
+  ncu -i $O/full_$1.ncu-rep --page details --csv > $O/full_$1_details.csv 2>/dev/null
+  ncu -i $O/full_$1.ncu-rep --page source --csv --print-source sass > $O/full_$1_sass.csv 2>/dev/null
+  gzip -f $O/full_$1_sass.csv
+  rm -f $O/full_$1.ncu-rep
 }
 full ozaki8_dpp dpp ffs_ozaki_gemm_kernel 60
 full step_dpp dpp "ffs_cluster_kernel" 100
