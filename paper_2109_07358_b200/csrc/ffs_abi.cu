@@ -801,7 +801,10 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
           op.N = (int)oz_ncols;
           op.K = d.Kp;
           op.panel = gp.panel;
-          const dim3 og((unsigned)(oz_ncols / ffsk::kOzBN), (unsigned)((L + ffsk::kOzBM - 1) / ffsk::kOzBM));
+          // stream the smaller slice set (keeps the other operand L2-resident)
+          op.m_fast = (int64_t)L * d.Kp < oz_ncols * d.Kp ? 1 : 0;
+          const unsigned mt = (unsigned)((L + ffsk::kOzBM - 1) / ffsk::kOzBM), nt = (unsigned)(oz_ncols / ffsk::kOzBN);
+          const dim3 og = op.m_fast ? dim3(mt, nt) : dim3(nt, mt);
           if (ns == 8)
             ffsk::ffs_ozaki_gemm_kernel<8><<<og, ffsk::kOzThreads, ffsk::oz_smem<8>(), stream>>>(oz_ta, oz_tb, op);
           else

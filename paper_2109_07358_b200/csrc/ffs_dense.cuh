@@ -414,6 +414,11 @@ struct OzakiParams {
   double* C;      // per-sample panel layout (see DgemmParams::panel)
   int M, N, K;    // K padded to a multiple of kOzBK (zero slices)
   int panel;
+  // tile raster: consecutive CTAs share one operand tile and stream the other one, which must
+  // stay L2-resident across the sweep. m_fast = 1: blockIdx.x walks the M-tiles (A streamed,
+  // B tile shared; for B >> A, e.g. C4's 512 MB of Y slices vs 32 MB of U slices);
+  // m_fast = 0: blockIdx.x walks the N-tiles (B streamed; C5: 64 MB of Y vs 128 MB of U)
+  int m_fast;
 };
 
 __device__ __forceinline__ unsigned oz_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -449,7 +454,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
   uint64_t* done = empty + kOzStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int m0 = blockIdx.y * kOzBM, n0 = blockIdx.x * kOzBN;
+  const int m0 = (p.m_fast ? blockIdx.x : blockIdx.y) * kOzBM, n0 = (p.m_fast ? blockIdx.y : blockIdx.x) * kOzBN;
   const int KT = p.K / kOzBK;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_u32(tmem_slot)), "r"(512)
