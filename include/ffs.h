@@ -126,6 +126,22 @@ int ffs_sample_metropolis(const void* U, int64_t L, int64_t N, ffs_dtype dtype, 
                           int64_t Mcond, const double* uniforms, int32_t* positions, int32_t* sample_flags,
                           void* workspace, size_t ws_bytes, void* stream);
 
+/* Modified-HKPV sampler, the paper's comparison method ("O(N^2 L) with certain
+ * modification", :81 "the modified HPKV algorithm requires 2LN^2 operations"; its steps as
+ * SPEC.md:238-246): the chain rule on K = U U^dagger. Residuals r(x) = |u_x|^2 - sum_j |<u_x, e_j>|^2;
+ * step k draws x_k ∝ r (selection rule of ffs_sample: strict C(x) > u T, chosen sites and
+ * non-positive residuals weigh 0), orthonormalises u_{x_k} against the earlier e_j (Gram-Schmidt,
+ * Hermitian inner product) and subtracts |<u_x, e_k>|^2 from every residual. It samples the same
+ * law as ffs_sample (Eq. 1) with different conditionals and no permutation; provided to measure
+ * the paper's "about 100% more efficient" claim on the same GPU (bench.py extensions).
+ *   uniforms : DEVICE double[M][N'] selection draws; positions DEVICE int32[M][N'] out (sampling
+ *              order); sample_flags as ffs_sample (NULL allowed)
+ * Same shapes and errors as ffs_sample_marginal; workspace ffs_hkpv_workspace_bytes(...) bytes. */
+size_t ffs_hkpv_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M);
+int ffs_sample_hkpv(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
+                    const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
+                    size_t ws_bytes, void* stream);
+
 /* Observables of FFS samples, on the device (Supp S5).
  * positions: DEVICE int32[M][N'] as written by the sampling calls; entries < 0 (the L-ensemble's
  * padding) are skipped. Outputs are DEVICE arrays, zeroed and filled by the call (async on stream).

@@ -14,6 +14,7 @@
 #include <set>
 #include <tuple>
 #include <utility>
+#include <vector>
 
 #include "ffs.h"
 #include "ffs_host.h"
@@ -24,6 +25,7 @@
 #include "ffs_lens.cuh"
 #include "ffs_observe.cuh"
 #include "ffs_metro.cuh"
+#include "ffs_hkpv.cuh"
 #include "ffs_kptr.h"
 
 // ====================================================================== shared host helpers
@@ -835,53 +837,46 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
   return FFS_OK;
 }
 
-// CUDA-graph driver (north_star (d)): the block loop is captured once per (arguments, options)
-// and replayed with one cudaGraphLaunch; a change of pointers or sizes re-captures and updates
-// the executable graph in place. Per host thread, the last few argument sets are kept.
+// CUDA-graph driver (north_star (d)): a multi-launch schedule is captured once per (arguments,
+// options) and replayed with one cudaGraphLaunch; a change of pointers or sizes re-captures and
+// updates the executable graph in place. Per host thread, the last few argument sets are kept.
+// Capture happens on a library-owned stream (the caller's may be the legacy default stream, which
+// cannot be captured); the executable is launched on the caller's stream. When the caller's stream
+// is itself being captured, or the option is off, the launches are issued directly.
 struct GraphEntry {
-  std::tuple<const void*, int64_t, int64_t, int, int64_t, int64_t, const double*, int32_t*, int32_t*, void*, int64_t,
-             int64_t, double*, uint64_t, int>
-      key;
+  std::vector<int64_t> key;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
 };
-thread_local GraphEntry g_graphs[4];
+thread_local GraphEntry g_graphs[8];
 thread_local unsigned g_graph_next = 0;
 thread_local cudaStream_t g_capture_stream = nullptr;
 
-int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
-                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
-                 double* trace) {
-  DensePlan d;
-  int rc = make_dense_plan(L, N, Np, dtype, M, d);
-  if (rc != FFS_OK) return rc;
-  if (!ws || ws_bytes < d.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, d.total);
-  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+template <typename Issue>
+int run_graph(const std::vector<int64_t>& key0, cudaStream_t stream, Issue&& issue) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return fail(FFS_ECUDA, "cudaStreamIsCapturing failed");
-  const bool graph = ffsh::option(FFS_OPT_GRAPH) != 0.0 && cs == cudaStreamCaptureStatusNone;
-  if (!graph) {
+  if (ffsh::option(FFS_OPT_GRAPH) == 0.0 || cs != cudaStreamCaptureStatusNone) {
     ffsh::prof_begin(stream);
-    rc = issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, stream, S0, S, trace);
+    const int rc = issue(stream);
     ffsh::prof_end(stream);
     return rc;
   }
-  const auto key = std::make_tuple(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, S0, S, trace,
-                                   ffsh::options_version(), ffsh::device());
+  std::vector<int64_t> key = key0;
+  key.push_back((int64_t)ffsh::options_version());
+  key.push_back(ffsh::device());
   GraphEntry* ge = nullptr;
   for (auto& g : g_graphs)
     if (g.exec && g.key == key) ge = &g;
   if (!ge) {
-    ge = &g_graphs[g_graph_next++ % 4];
-    // capture on a library-owned stream (the caller's may be the legacy default stream, which
-    // cannot be captured); the executable graph is then launched on the caller's stream
+    ge = &g_graphs[g_graph_next++ % 8];
     if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
       return fail(FFS_ECUDA, "capture stream creation failed");
     cudaGraph_t graph_def = nullptr;
     if (cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return fail(FFS_ECUDA, "cudaStreamBeginCapture failed");
     const int l0 = ffsh::launches();
-    rc = issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, g_capture_stream, S0, S, trace);
+    const int rc = issue(g_capture_stream);
     const cudaError_t ce = cudaStreamEndCapture(g_capture_stream, &graph_def);
     if (rc != FFS_OK) {
       if (graph_def) cudaGraphDestroy(graph_def);
@@ -914,6 +909,22 @@ int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int6
   if (e != cudaSuccess) return fail(FFS_ECUDA, "cudaGraphLaunch failed: %s", cudaGetErrorString(e));
   ffsh::prof_end(stream);
   return FFS_OK;
+}
+
+int launch_dense(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
+                 double* trace) {
+  DensePlan d;
+  int rc = make_dense_plan(L, N, Np, dtype, M, d);
+  if (rc != FFS_OK) return rc;
+  if (!ws || ws_bytes < d.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, d.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  const std::vector<int64_t> key = {1, (int64_t)(uintptr_t)U, L, N, dtype, M, Np, (int64_t)(uintptr_t)uniforms,
+                                    (int64_t)(uintptr_t)positions, (int64_t)(uintptr_t)flags, (int64_t)(uintptr_t)ws,
+                                    S0, S, (int64_t)(uintptr_t)trace};
+  return run_graph(key, stream, [&](cudaStream_t s) {
+    return issue_dense(d, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, s, S0, S, trace);
+  });
 }
 
 // ------------------------------------------------------------------ generic CTA/warp-owner path
@@ -1154,6 +1165,127 @@ int launch_metropolis(const void* U, int64_t L, int64_t N, int dtype, int64_t M,
     ffsk::ffs_metro_kernel<double><<<y.grid, ffsk::kMetroWarps * 32, y.smem, stream>>>(p);
   ffsh::prof_end(stream);
   ++ffsh::launches();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+  ffsh::clear_error();
+  return FFS_OK;
+}
+
+// ------------------------------------------------------------------ modified-HKPV comparator
+// Lockstep batches of S samples: per step one ffs_hkpv_step_kernel launch (CTA per sample: draw +
+// Gram-Schmidt) and one DMMA GEMM with the residual-update epilogue; replayed as a CUDA graph.
+// Workspace: [U padded L x ldu | r S x L | chosen | E S x N' x N | Eb].
+struct HkpvPlan {
+  int64_t S, ldu, ldE, fK;
+  size_t u, r, ch, e, eb, total, step_smem;
+};
+int hkpv_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HkpvPlan& h) {
+  if (int rc = check_shape(L, N, Np, dtype, std::max<int64_t>(M, 1))) return rc;
+  const bool cx = dtype == FFS_C128;
+  const size_t es = cx ? 16 : 8;
+  const int64_t f = cx ? 2 : 1;
+  h.ldu = cx ? N : ((N + 1) & ~int64_t(1));  // 16-byte aligned rows of the GEMM's A operand
+  h.fK = f * h.ldu;
+  // batch: residuals, e-vectors and the GEMM operand of S samples within ~16 GB
+  const double per = (double)L * 8 + (double)Np * N * es + (double)f * h.fK * 8 + ((L + 31) / 32) * 4.0;
+  h.S = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(M, 1), (int64_t)(16e9 / per)));
+  const double ob = ffsh::option(FFS_OPT_DENSE_BATCH);
+  if (ob >= 1.0) h.S = std::min<int64_t>(h.S, (int64_t)ob);
+  const int64_t q = ffsk::kGN / f;
+  h.ldE = (h.S + q - 1) / q * q;
+  h.u = 0;
+  h.r = align_up((size_t)L * h.ldu * es);
+  h.ch = h.r + align_up((size_t)h.S * L * 8);
+  h.e = h.ch + align_up((size_t)h.S * ((L + 31) / 32) * 4);
+  h.eb = h.e + align_up((size_t)h.S * Np * N * es);
+  h.total = h.eb + align_up((size_t)h.fK * f * h.ldE * 8);
+  h.step_smem = 32 * 8 + 96 * 4 + (size_t)(N + Np) * es;
+  if (h.step_smem > kMaxSmem || N > 16384) return fail(FFS_EINVAL, "N=%lld too large for the HKPV step kernel", (long long)N);
+  const void* sf = cx ? reinterpret_cast<const void*>(&ffsk::ffs_hkpv_step_kernel<cplx>)
+                      : reinterpret_cast<const void*>(&ffsk::ffs_hkpv_step_kernel<double>);
+  if (int rc = ffsh::ensure_max_smem(sf)) return rc;
+  return ffsh::ensure_max_smem(reinterpret_cast<const void*>(&ffsk::ffs_dgemm_kernel<32, 3, 1>));
+}
+
+int issue_hkpv(const HkpvPlan& h, const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np,
+               const double* uniforms, int32_t* positions, int32_t* flags, void* ws, cudaStream_t s) {
+  const bool cx = dtype == FFS_C128;
+  const size_t es = cx ? 16 : 8;
+  const int64_t f = cx ? 2 : 1;
+  char* w = static_cast<char*>(ws);
+  double* Up = reinterpret_cast<double*>(w + h.u);
+  if (cudaMemcpy2DAsync(Up, h.ldu * es, U, N * es, N * es, L, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(FFS_ECUDA, "U copy failed");
+  if (h.ldu > N && cudaMemset2DAsync(reinterpret_cast<char*>(Up) + N * es, h.ldu * es, 0, (h.ldu - N) * es, L, s) != cudaSuccess)
+    return fail(FFS_ECUDA, "U pad failed");
+  ffsk::HkpvParams p{};
+  p.U = Up;
+  p.ldu = h.ldu;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.r = reinterpret_cast<double*>(w + h.r);
+  p.chosen = reinterpret_cast<uint32_t*>(w + h.ch);
+  p.E = reinterpret_cast<double*>(w + h.e);
+  p.Eb = reinterpret_cast<double*>(w + h.eb);
+  p.ldE = h.ldE;
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  ffsk::DgemmParams gp{};
+  gp.A = Up;
+  gp.B = p.Eb;
+  gp.C = nullptr;
+  gp.lda = h.fK;
+  gp.ldb = f * h.ldE;
+  gp.ldc = 0;
+  gp.M = (int)L;
+  gp.N = (int)(f * h.ldE);
+  gp.K = (int)h.fK;
+  gp.panel = 0;
+  gp.r = p.r;
+  gp.rld = L;
+  gp.cplx = cx ? 1 : 0;
+  const dim3 ggrid((unsigned)(f * h.ldE / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
+  for (int64_t base = 0; base < M; base += h.S) {
+    const int64_t Sb = std::min<int64_t>(h.S, M - base);
+    p.base = base;
+    p.Sb = (int)Sb;
+    gp.nsamp = (int)Sb;
+    if (cudaMemsetAsync(p.Eb, 0, (size_t)h.fK * f * h.ldE * 8, s) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
+    const unsigned ig = (unsigned)std::min<int64_t>((Sb * L + 255) / 256, 65535);
+    if (cx) ffsk::ffs_hkpv_init_kernel<cplx><<<ig, 256, 0, s>>>(p);
+    else ffsk::ffs_hkpv_init_kernel<double><<<ig, 256, 0, s>>>(p);
+    ++ffsh::launches();
+    for (int k = 0; k < Np; ++k) {
+      p.k = k;
+      if (cx) ffsk::ffs_hkpv_step_kernel<cplx><<<(unsigned)Sb, ffsk::kHkpvThreads, h.step_smem, s>>>(p);
+      else ffsk::ffs_hkpv_step_kernel<double><<<(unsigned)Sb, ffsk::kHkpvThreads, h.step_smem, s>>>(p);
+      ++ffsh::launches();
+      if (k + 1 < Np) {
+        ffsk::ffs_dgemm_kernel<32, 3, 1><<<ggrid, ffsk::kGThreads, ffsk::gemm_smem<32, 3>(), s>>>(gp);
+        ++ffsh::launches();
+      }
+    }
+  }
+  return FFS_OK;
+}
+
+int launch_hkpv(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+                int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  ffsh::launches() = 0;
+  if (M == 0) return FFS_OK;
+  if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions");
+  HkpvPlan h;
+  if (int rc = hkpv_plan(L, N, Np, dtype, M, h)) return rc;
+  if (!ws || ws_bytes < h.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, h.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  const std::vector<int64_t> key = {2, (int64_t)(uintptr_t)U, L, N, dtype, M, Np, (int64_t)(uintptr_t)uniforms,
+                                    (int64_t)(uintptr_t)positions, (int64_t)(uintptr_t)flags, (int64_t)(uintptr_t)ws};
+  int rc = run_graph(key, stream, [&](cudaStream_t s) {
+    return issue_hkpv(h, U, L, N, dtype, M, Np, uniforms, positions, flags, ws, s);
+  });
+  if (rc != FFS_OK) return rc;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FFS_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
   ffsh::clear_error();
@@ -1407,6 +1539,18 @@ int ffs_sample_metropolis(const void* U, int64_t L, int64_t N, ffs_dtype dtype, 
                           void* workspace, size_t ws_bytes, void* stream) {
   return launch_metropolis(U, L, N, dtype, M, Nprime, Mcond, uniforms, positions, sample_flags, workspace, ws_bytes,
                            static_cast<cudaStream_t>(stream));
+}
+
+size_t ffs_hkpv_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M) {
+  HkpvPlan h;
+  return hkpv_plan(L, N, Nprime, dtype, M, h) == FFS_OK ? h.total : 0;
+}
+
+int ffs_sample_hkpv(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_t M, int64_t Nprime,
+                    const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
+                    size_t ws_bytes, void* stream) {
+  return launch_hkpv(U, L, N, dtype, M, Nprime, uniforms, positions, sample_flags, workspace, ws_bytes,
+                     static_cast<cudaStream_t>(stream));
 }
 
 int ffs_last_launch_count(void) { return ffsh::launches(); }

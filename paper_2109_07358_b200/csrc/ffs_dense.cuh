@@ -40,6 +40,12 @@ struct DgemmParams {
   int64_t lda, ldb, ldc;
   int M, N, K;
   int panel;  // > 0: C in per-sample panel layout, column n -> C[(n / panel) * M * panel + row * panel + n % panel]
+  // EPI = 1 (modified-HKPV residual update, ffs_hkpv.cuh): instead of storing C, subtract |C|^2
+  // from the residuals r[sample][row] (row stride rld); real: column n is sample n; complex
+  // (cplx = 1): columns 2s, 2s+1 are Re, Im of sample s; samples >= nsamp are padding
+  double* r;
+  int64_t rld;
+  int nsamp, cplx;
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -59,7 +65,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int
 // the fragment loads (g = 0..3 or 4..7, t4 = 0..3) hits 16 distinct 8-byte bank slots.
 // <32, 3>: 192 KB smem, 255 registers (fastest alone); <16, 4>: 128 KB, ~200 registers, which leaves
 // room on each SM for a co-resident ffs_dense_gj_kernel CTA of the other half-batch (2-stream mode)
-template <int kGK, int kGStages>
+template <int kGK, int kGStages, int EPI = 0>
 static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const DgemmParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* As = reinterpret_cast<double*>(smem);
@@ -127,6 +133,38 @@ static __global__ void __launch_bounds__(kGThreads, 1) ffs_dgemm_kernel(const Dg
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if constexpr (EPI == 1) {
+    // |C|^2 of the tile staged transposed in shared memory ([sample][row], row stride 129), then
+    // subtracted from r with each column's rows contiguous across the threads (coalesced)
+    static_assert(kGStages * (kGM * kGK + kGK * kGN) >= kGN * (kGM + 1), "staging tile fits the pipeline buffers");
+    __syncthreads();
+    double* Ts = reinterpret_cast<double*>(smem);
+    constexpr int kLd = kGM + 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = wm * 32 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int cl = wn * 64 + j * 8 + 2 * t4;
+        const double a = acc[i][j][0], b = acc[i][j][1];
+        if (p.cplx) {
+          Ts[(cl >> 1) * kLd + rl] = fma(a, a, b * b);
+        } else {
+          Ts[cl * kLd + rl] = a * a;
+          Ts[(cl + 1) * kLd + rl] = b * b;
+        }
+      }
+    }
+    __syncthreads();
+    const int ns = p.cplx ? kGN / 2 : kGN;
+    const int s0 = p.cplx ? n0 / 2 : n0;
+    for (int idx = t; idx < ns * kGM; idx += kGThreads) {
+      const int sl = idx / kGM, rl = idx % kGM;
+      const int row = m0 + rl, smp = s0 + sl;
+      if (row < p.M && smp < p.nsamp) p.r[(size_t)smp * p.rld + row] -= Ts[sl * kLd + rl];
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + wm * 32 + i * 8 + g;

@@ -43,6 +43,8 @@ EXPORTED = (
     "ffs_sample_lensemble",
     "ffs_metropolis_workspace_bytes",
     "ffs_sample_metropolis",
+    "ffs_hkpv_workspace_bytes",
+    "ffs_sample_hkpv",
     "ffs_occupation",
     "ffs_pair_occupation",
     "ffs_gutzwiller_workspace_bytes",
@@ -92,6 +94,9 @@ def load(build_if_missing: bool = True):
     L.ffs_metropolis_workspace_bytes.argtypes = [i64, i64, i64, i64, ci, i64]
     L.ffs_metropolis_workspace_bytes.restype = sz
     L.ffs_sample_metropolis.argtypes = [vp, i64, i64, ci, i64, i64, i64, vp, vp, vp, vp, sz, vp]
+    L.ffs_hkpv_workspace_bytes.argtypes = [i64, i64, i64, ci, i64]
+    L.ffs_hkpv_workspace_bytes.restype = sz
+    L.ffs_sample_hkpv.argtypes = [vp, i64, i64, ci, i64, i64, vp, vp, vp, vp, sz, vp]
     L.ffs_occupation.argtypes = [vp, i64, i64, i64, vp, vp]
     L.ffs_pair_occupation.argtypes = [vp, i64, i64, i64, vp, vp]
     L.ffs_gutzwiller_workspace_bytes.argtypes = [i64, i64]
@@ -411,5 +416,32 @@ def ffs_sample_metropolis(U: torch.Tensor, uniforms: torch.Tensor, Nprime: int, 
     _check(load().ffs_sample_metropolis(U.data_ptr(), L, N, dt, M, Nprime, Mcond, uniforms.data_ptr(),
                                         positions.data_ptr(), flags.data_ptr(), wp, wn,
                                         _stream_handle(stream, U.device)))
+    _keep_alive(stream, U, uniforms, positions, flags, ws.buf)
+    return positions, flags
+
+
+def ffs_sample_hkpv(U: torch.Tensor, uniforms: torch.Tensor, Nprime: Optional[int] = None,
+                    workspace: Optional[Workspace] = None, stream=None):
+    """Modified-HKPV comparator (PAPER.md:45-46, 81): uniforms [M][N'] selection draws;
+    returns positions int32 [M][N'] and flags int32 [M]."""
+    if not (U.is_cuda and uniforms.is_cuda) or U.dim() != 2:
+        raise FFSError("U [L][N] and uniforms must be CUDA tensors")
+    U = U.contiguous()
+    uniforms = uniforms.contiguous()
+    L, N = U.shape
+    Np = uniforms.shape[1] if Nprime is None else Nprime
+    if uniforms.dtype != torch.float64 or uniforms.dim() != 2 or uniforms.shape[1] != Np:
+        raise FFSError(f"uniforms must be float64 [M][N'={Np}], got {tuple(uniforms.shape)}")
+    M = uniforms.shape[0]
+    dt = _dtype_code(U)
+    positions = torch.empty((M, Np), dtype=torch.int32, device=U.device)
+    flags = torch.empty(M, dtype=torch.int32, device=U.device)
+    ws = workspace if workspace is not None else Workspace(U.device)
+    need = int(load().ffs_hkpv_workspace_bytes(L, N, Np, dt, M))
+    if need == 0 and M > 0:
+        _check(load().ffs_sample_hkpv(U.data_ptr(), L, N, dt, M, Np, None, None, None, None, 0, None))
+    wp, wn = ws.get(need)
+    _check(load().ffs_sample_hkpv(U.data_ptr(), L, N, dt, M, Np, uniforms.data_ptr(), positions.data_ptr(),
+                                  flags.data_ptr(), wp, wn, _stream_handle(stream, U.device)))
     _keep_alive(stream, U, uniforms, positions, flags, ws.buf)
     return positions, flags
