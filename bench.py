@@ -425,6 +425,34 @@ def measure_extensions(dev, steps, no_cpu, cpu_budget):
                                       "unit": "GB/s", "frac": byts / (kms * 1e-3) / 1e9 / measured_hbm(),
                                       "bytes_def": "positions read once: 4 N' B per sample"},
                          "clocks": clocks, "gpu_launches": nl}
+    # the paper's comparator on the same GPU: modified HKPV (2 L N^2) vs FFS (L N^2 + N^3),
+    # PAPER.md:81 "nearly the twice" / Fig. 3B (L = 1024 random U, N sweep); same uniforms layout
+    hk = {}
+    cases = [("dw", None), ("anderson", None), ("dpp", None)] + [("fig3b", n) for n in (16, 32, 64, 128)]
+    for name, n in cases:
+        if name == "fig3b":
+            L, N, M = 1024, n, 16384
+            U = inputs.random_orthonormal(L, N, 3000 + N)
+        else:
+            cfg = inputs.CONFIGS[name]
+            L, N, M = cfg.L, cfg.N, cfg.M
+            U = inputs.build_u(cfg)
+        uni = inputs.uniforms(M, N, 4000 + N)
+        Ud = torch.from_numpy(U).to(dev)
+        ud = torch.from_numpy(uni).to(dev)
+        us = torch.from_numpy(np.ascontiguousarray(uni[:, N:])).to(dev)
+        ws1, ws2 = ffs.Workspace(dev), ffs.Workspace(dev)
+        K = 2 if name == "dpp" else max(3, min(steps, 5))
+        ms_f, _, clk_f, _ = timed(lambda: ffs.ffs_sample(Ud, ud, workspace=ws1, stream=stream), K)
+        ms_h, _, clk_h, nl = timed(lambda: ffs.ffs_sample_hkpv(Ud, us, workspace=ws2, stream=stream), K)
+        key = f"{name}_N{N}" if name == "fig3b" else name
+        hk[key] = {"L": L, "N": N, "M": M, "ffs_ms": ms_f, "hkpv_ms": ms_h, "time_ratio_hkpv_over_ffs": ms_h / ms_f,
+                   "flop_ratio_paper": 2 * L * N ** 2 / (L * N ** 2 + N ** 3),
+                   "hkpv_samples_per_s": M / (ms_h * 1e-3), "ffs_samples_per_s": M / (ms_f * 1e-3),
+                   "clocks": clk_h, "hkpv_gpu_launches": nl}
+        del Ud, ud, us, ws1, ws2
+        torch.cuda.empty_cache()
+    out["hkpv_comparator"] = hk
     del flush
     return out
 
