@@ -1271,11 +1271,71 @@ int issue_hkpv(const HkpvPlan& h, const void* U, int64_t L, int64_t N, int dtype
   return FFS_OK;
 }
 
+// small real L: the fused warp-per-sample kernel (U^T and e-vectors in shared memory)
+struct HkpvWarpPlan {
+  const void* fn;
+  int R, maxt, warps, grid, Lp, ut_stride;
+  size_t ushared, owner, smem;
+};
+template <int R, int MAXT>
+void hkpv_warp_fn(HkpvWarpPlan& w) {
+  w.fn = reinterpret_cast<const void*>(&ffsk::ffs_hkpv_warp_kernel<R, MAXT>);
+  w.R = R;
+  w.maxt = MAXT;
+}
+bool hkpv_warp_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, HkpvWarpPlan& w) {
+  if (dtype != FFS_F64 || L > 256 || ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0) return false;
+  if (L <= 32) hkpv_warp_fn<1, 512>(w);
+  else if (L <= 64) hkpv_warp_fn<2, 512>(w);
+  else if (L <= 128) hkpv_warp_fn<4, 512>(w);
+  else hkpv_warp_fn<8, 512>(w);
+  w.Lp = 32 * w.R;
+  w.ut_stride = w.Lp + 2;
+  w.ushared = ffsk::align16((size_t)N * w.ut_stride * 8);
+  w.owner = ffsk::hkpv_warp_owner_bytes((int)N, (int)Np);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, w.fn) != cudaSuccess) return false;
+  const int by_regs = 4 * std::max(1, 16384 / (((std::max(fa.numRegs, 1) * 32 + 255) / 256) * 256));
+  int warps = std::min(w.maxt / 32, by_regs);
+  while (warps > 1 && w.ushared + (size_t)warps * w.owner > kMaxSmem) --warps;
+  w.warps = warps;
+  w.smem = w.ushared + (size_t)warps * w.owner;
+  if (w.smem > kMaxSmem || ffsh::ensure_max_smem(w.fn) != FFS_OK) return false;
+  const int64_t ctas = (std::max<int64_t>(M, 1) + warps - 1) / warps;
+  w.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, ffsh::sm_count(ffsh::device())));
+  return true;
+}
+
 int launch_hkpv(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream) {
   ffsh::launches() = 0;
   if (M == 0) return FFS_OK;
   if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions");
+  if (int rc = check_shape(L, N, Np, dtype, M)) return rc;
+  HkpvWarpPlan wp;
+  if (hkpv_warp_plan(L, N, Np, dtype, M, wp)) {
+    ffsk::HkpvWarpParams q{};
+    q.U = static_cast<const double*>(U);
+    q.uniforms = uniforms;
+    q.positions = positions;
+    q.flags = flags;
+    q.M = M;
+    q.L = (int)L;
+    q.N = (int)N;
+    q.Np = (int)Np;
+    q.Lp = wp.Lp;
+    q.ut_stride = wp.ut_stride;
+    q.ushared = wp.ushared;
+    q.owner_bytes = wp.owner;
+    void* args[] = {&q};
+    ffsh::prof_begin(stream);
+    cudaError_t e = cudaLaunchKernel(wp.fn, dim3(wp.grid), dim3(32 * wp.warps), args, wp.smem, stream);
+    if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+    ffsh::prof_end(stream);
+    ++ffsh::launches();
+    ffsh::clear_error();
+    return FFS_OK;
+  }
   HkpvPlan h;
   if (int rc = hkpv_plan(L, N, Np, dtype, M, h)) return rc;
   if (!ws || ws_bytes < h.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, h.total);

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include "ffs_dense.cuh"
+#include "ffs_kernel.cuh"
 
 namespace ffsk {
 
@@ -197,6 +198,119 @@ static __global__ void __launch_bounds__(kHkpvThreads) ffs_hkpv_step_kernel(cons
     else es = {e.re * inv, e.im * inv};
     Ek[n] = es;
     dense_y_store<T>(p.Eb, p.ldE, n, (int64_t)sl, conj_t(es));
+  }
+}
+
+// Small L (real, L <= 32 R): one warp per sample for all N' steps, U^T once per CTA in shared
+// memory (the swizzled layout of ffs_sample_kernel's warp owners), the sample's residuals in
+// registers (lane l owns sites l R .. l R + R - 1), its e-vectors in its shared-memory slice.
+// Per step: the draw (select_site), Gram-Schmidt with lanes over the e-vectors / components, and
+// the residual update r_x -= |u_x . e_k|^2 (R x N FMAs per lane from the shared U^T).
+struct HkpvWarpParams {
+  const double* U;         // [L][N]
+  const double* uniforms;  // [M][Np]
+  int32_t* positions;      // [M][Np]
+  int32_t* flags;
+  int64_t M;
+  int L, N, Np, Lp, ut_stride;
+  size_t ushared, owner_bytes;
+};
+
+__host__ __device__ inline size_t hkpv_warp_owner_bytes(int N, int Np) {
+  return align16(sizeof(double) * (size_t)Np * N) + align16(sizeof(double) * 2 * (size_t)N) +
+         align16(sizeof(double) * (size_t)Np) + align16(sizeof(double) * 32 + sizeof(int) * 96);
+}
+
+template <int R, int MAXT>
+static __global__ void __launch_bounds__(MAXT, 1) ffs_hkpv_warp_kernel(const HkpvWarpParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int L = p.L, N = p.N, Np = p.Np;
+  double* Uts = reinterpret_cast<double*>(smem);
+  for (int idx = threadIdx.x; idx < N * p.Lp; idx += blockDim.x) {
+    const int x = idx / N, c = idx % N;
+    Uts[(size_t)c * p.ut_stride + Swz<double, R>::phys(x)] = (x < L) ? p.U[(size_t)x * N + c] : 0.0;
+  }
+  __syncthreads();
+  unsigned char* ob = smem + p.ushared + (size_t)wid * p.owner_bytes;
+  double* E = reinterpret_cast<double*>(ob);                                      // [Np][N]
+  double* v = reinterpret_cast<double*>(ob + align16(sizeof(double) * (size_t)Np * N));  // [N] (+ [N] scratch)
+  double* cf = v + 2 * N;                                                          // [Np]
+  double* red = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(cf) + align16(sizeof(double) * Np));
+  int* redi = reinterpret_cast<int*>(red + 32);
+  Params lp{};  // load_col needs only the shared-U^T stride
+  lp.ut_stride = p.ut_stride;
+  for (int64_t i = (int64_t)blockIdx.x * nwarps + wid; i < p.M; i += (int64_t)gridDim.x * nwarps) {
+    double res[R];
+    for (int r = 0; r < R; ++r) res[r] = 0.0;
+    for (int c = 0; c < N; ++c) {
+      double u[R];
+      load_col<double, R, true>(lp, Uts, c, lane, u);
+#pragma unroll
+      for (int r = 0; r < R; ++r) res[r] = fma(u[r], u[r], res[r]);
+    }
+    uint32_t chosen = 0;
+    int flag = 0;
+    for (int k = 0; k < Np; ++k) {
+      double w[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = (((chosen >> r) & 1u) || !(res[r] > 0.0)) ? 0.0 : res[r];
+      double T;
+      const int xs = select_site<true, R>(w, p.uniforms[i * Np + k], lane, L, chosen, red, redi, T);
+      if (!(T > 0.0 && isfinite(T))) flag |= 1;
+      const int own = xs / R, orow = xs % R;
+      if (lane == own) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r == orow) {
+            if (T > 0.0 && w[r] / T < 1e-12) flag |= 2;
+            chosen |= 1u << r;
+          }
+        p.positions[i * Np + k] = xs;
+      }
+      if (k + 1 == Np) break;
+      // e_k: two classical Gram-Schmidt passes of u_{x_k} against e_0 .. e_{k-1}
+      for (int n = lane; n < N; n += 32) v[n] = Uts[(size_t)n * p.ut_stride + Swz<double, R>::phys(xs)];
+      __syncwarp();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int j = lane; j < k; j += 32) {
+          double a = 0.0;
+          for (int n = 0; n < N; ++n) a = fma(v[n], E[(size_t)j * N + n], a);
+          cf[j] = a;
+        }
+        __syncwarp();
+        for (int n = lane; n < N; n += 32) {
+          double a = v[n];
+          for (int j = 0; j < k; ++j) a = fma(-cf[j], E[(size_t)j * N + n], a);
+          v[n] = a;
+        }
+        __syncwarp();
+      }
+      double nl = 0.0;
+      for (int n = lane; n < N; n += 32) nl = fma(v[n], v[n], nl);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, o);
+      const double inv = 1.0 / sqrt(nl);
+      for (int n = lane; n < N; n += 32) E[(size_t)k * N + n] = v[n] * inv;
+      __syncwarp();
+      // r_x -= |u_x . e_k|^2 for this lane's sites
+      double c[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) c[r] = 0.0;
+      const double* ek = E + (size_t)k * N;
+      for (int n = 0; n < N; ++n) {
+        double u[R];
+        load_col<double, R, true>(lp, Uts, n, lane, u);
+        const double e = ek[n];
+#pragma unroll
+        for (int r = 0; r < R; ++r) c[r] = fma(u[r], e, c[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) res[r] = fma(-c[r], c[r], res[r]);
+    }
+    flag = __reduce_or_sync(0xffffffffu, flag);
+    if (lane == 0 && p.flags) p.flags[i] = flag;
+    __syncwarp();
   }
 }
 

@@ -80,3 +80,18 @@ def test_hkpv_tiny_law_chisquare():
     obs = np.bincount([index[tuple(sorted(q))] for q in gpos.tolist()], minlength=len(subsets))
     stat, dof, pval, _ = exact.pooled_chisquare(obs, p * M)
     assert pval > 1e-3, (stat, dof, pval)
+
+
+@pytest.mark.parametrize("L,N", [(16, 4), (256, 32), (100, 45)])
+def test_hkpv_lockstep_path_at_small_L(L, N):
+    """The lockstep GEMM path (option force_generic) on the shapes the warp kernel takes by default."""
+    ffs = _ffs()
+    ffs.set_option("force_generic", 1)
+    try:
+        U = inputs.random_orthonormal(L, N, 7 * L + N)
+        uni = np.random.Generator(np.random.Philox(L)).random((150, N))
+        gpos, gfl = run_gpu(U, uni)
+        ex, ties, _ = compare(U, uni, gpos)
+        assert ex + ties == 150 and (gfl == 0).all()
+    finally:
+        ffs.reset_options()
