@@ -144,13 +144,18 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
     // across the block-step launches)
     T* Wf = reinterpret_cast<T*>(p.wfull) + (STEP ? sl : cid) * (int64_t)Np * Np;
     const double* urow = p.uniforms + i * 2 * (int64_t)Np;
-    // ---- a1 permutation (every CTA computes the same one; STEP: precomputed prefix)
+    // ---- a1 permutation (every CTA computes the same one; STEP: precomputed prefix, and only the
+    // entries this block step reads: the gathered columns m_0 .. m_{k0+B-1} when it contracts
+    // them itself, and its own B selection uniforms)
     if constexpr (STEP) {
-      for (int j = t; j < Np; j += blockDim.x) perm[j] = p.permg[i * Np + j];
+      const int kend = min(Np, p.k0 + B);
+      if (p.gather)
+        for (int j = t; j < kend; j += blockDim.x) perm[j] = p.permg[i * Np + j];
+      for (int j = p.k0 + t; j < kend; j += blockDim.x) usel[j] = urow[Np + j];
     } else {
       for (int j = t; j < N; j += blockDim.x) perm[j] = j;
+      for (int j = t; j < Np; j += blockDim.x) usel[j] = urow[Np + j];
     }
-    for (int j = t; j < Np; j += blockDim.x) usel[j] = urow[Np + j];
     __syncthreads();
     if (!STEP && t == 0) {
       for (int j = 0; j < Np; ++j) {
