@@ -12,7 +12,7 @@
  *   u_x     : the k-dimensional row vector U_{x,(m_1..m_k)}
  *   R       : the iteratively Gauss-eliminated rows of u_{x_1..x_{k-1}}, kept in the permuted
  *             column order over ncols columns ("always carry out Gaussian elimination in the full
- *             N-dimensional space"; ncols = Np, reading R2 in DESIGN.md)
+ *             N-dimensional space"; ncols = Np, reading Q11 in DESIGN.md)
  *   h       : k-dim unit normal vector, perpendicular to u_{x_1..x_{k-1}} (Eq. 3)
  *   w(x)    : |u_x^T h|^2  (Eq. 3; bilinear u^T h, no conjugation: reading Q3)
  */
