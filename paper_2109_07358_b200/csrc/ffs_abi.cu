@@ -577,10 +577,6 @@ template <typename T>
 size_t dense_gj_bytes(int k0) { return ffsk::dense_gj_smem<T, 8, gj_tj<T>()>(k0); }
 template <int NS>
 const void* ozaki_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel<NS>); }
-template <typename T>
-const void* dense_gj1_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj1_kernel<T, 8>); }
-// the one-pass GJ kernel reads W through a tensor map: 16-byte row strides (N' even for real)
-bool gj1_ok(int dtype, int64_t Np) { return dtype == FFS_C128 || (Np % 2) == 0; }
 
 // 3-D tensor map [NS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -664,11 +660,6 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut + d.ws_oza + d.ws_ea + d.ws_ozb + d.ws_eb;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "block-step path: N'=%lld too large for the GJ tile", (long long)Np);
-  if (gj1_ok(dtype, Np)) {
-    const size_t g1 = cx ? ffsk::dense_gj1_smem<cplx, 8>((int)Np) : ffsk::dense_gj1_smem<double, 8>((int)Np);
-    if (g1 > kMaxSmem) return fail(FFS_EINVAL, "block-step path: N'=%lld too large for the one-pass GJ tile", (long long)Np);
-    if (int rc = ffsh::ensure_max_smem(cx ? dense_gj1_fn<cplx>() : dense_gj1_fn<double>())) return rc;
-  }
   return ffsh::ensure_max_smem(cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>());
 }
 
@@ -689,23 +680,6 @@ int oz_tensor_map(CUtensorMap* m, const int8_t* base, int ns, int64_t rows, int 
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(FFS_ECUDA, "cuTensorMapEncodeTiled failed");
-  return FFS_OK;
-}
-
-// 3-D tensor map over the batch's W [S][N'][N'] (doubles; complex rows are 2N' doubles), boxes of
-// 64 rows x 128 bytes, 128-byte swizzle (ffs_dense_gj1_kernel)
-int gj_tensor_map(CUtensorMap* m, const double* W, int64_t S, int64_t Np, bool cx) {
-  const EncodeTiledFn enc = tensor_map_encoder();
-  if (!enc) return fail(FFS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const int64_t rowd = (cx ? 2 : 1) * Np;  // doubles per row
-  const cuuint64_t dims[3] = {(cuuint64_t)rowd, (cuuint64_t)Np, (cuuint64_t)S};
-  const cuuint64_t strides[2] = {(cuuint64_t)rowd * 8, (cuuint64_t)rowd * 8 * (cuuint64_t)Np};
-  const cuuint32_t box[3] = {16, (cuuint32_t)ffsk::kGj1Chunk, 1};
-  const cuuint32_t es[3] = {1, 1, 1};
-  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(W), dims, strides, box, es,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return fail(FFS_ECUDA, "cuTensorMapEncodeTiled (W) failed");
   return FFS_OK;
 }
 
@@ -749,11 +723,6 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
   if (int rc = launch_permute(uniforms, 2 * Np, perm, M, N, Np, stream)) return rc;
   const void* gjf = cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>();
   const int gjt = cx ? gj_tj<cplx>() : gj_tj<double>();
-  const bool one_pass = gj1_ok(dtype, Np);
-  const void* gj1f = cx ? dense_gj1_fn<cplx>() : dense_gj1_fn<double>();
-  const int gj1t = cx ? ffsk::gj1_tj<cplx>() : ffsk::gj1_tj<double>();
-  CUtensorMap tmW;
-  if (one_pass && gj_tensor_map(&tmW, reinterpret_cast<const double*>(Wb), d.S, Np, cx) != FFS_OK) return FFS_ECUDA;
   double* Y = d.ws_y ? reinterpret_cast<double*>(Yb) : nullptr;
   double* Pd = reinterpret_cast<double*>(Pb);
   double* Wd = reinterpret_cast<double*>(Wb);
@@ -856,17 +825,10 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
       if (k0 + B < Np) {
         q.k0 = k0;
         const int nc = (int)Np - k0 - B;
-        if (one_pass && k0 > 0) {
-          const dim3 jg((unsigned)((nc + gj1t - 1) / gj1t), (unsigned)nh);
-          const size_t gsm = cx ? ffsk::dense_gj1_smem<cplx, 8>(k0) : ffsk::dense_gj1_smem<double, 8>(k0);
-          void* qargs[] = {&tmW, &q};
-          e = cudaLaunchKernel(gj1f, jg, dim3(ffsk::kGj1Threads), qargs, gsm, stream);
-        } else {
-          const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
-          const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
-          void* qargs[] = {&q};
-          e = cudaLaunchKernel(gjf, jg, dim3(256), qargs, gsm, stream);
-        }
+        const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
+        const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
+        void* qargs[] = {&q};
+        e = cudaLaunchKernel(gjf, jg, dim3(256), qargs, gsm, stream);
         if (e != cudaSuccess) return fail(FFS_ECUDA, "gj launch failed: %s", cudaGetErrorString(e));
         ++ffsh::launches();
       }

@@ -699,153 +699,4 @@ static __global__ void __launch_bounds__(256) ffs_ozaki_split_cols_kernel(const 
   }
 }
 
-// ---------------------------------------------------------------- batched Gauss-Jordan, one DRAM pass
-// The same update as ffs_dense_gj_kernel, with each CTA's W tile W[0:k0, j0:j0+TJ] (TJ = 128 bytes
-// of columns) brought into shared memory ONCE by TMA (a 3-D tensor map over the batch's W
-// [S][N'][N'], boxes of 64 rows x 128 bytes, 128-byte swizzle, one mbarrier per box so step (1)
-// starts on the first rows while the rest stream in), reduced in step (1), updated in place in
-// step (3) and written back once with coalesced 128-byte rows: W crosses HBM once each way (the
-// kernel above re-reads the rows that fell out of L2 between its two passes). The tensor map needs
-// 16-byte row strides: N' even for real T (always for complex).
-constexpr int kGj1Threads = 256, kGj1Chunk = 64;
-template <typename T> constexpr int gj1_tj() { return 128 / (int)sizeof(T); }
-template <typename T, int B>
-__host__ __device__ inline size_t dense_gj1_smem(int k0) {
-  constexpr int TJ = 128 / (int)sizeof(T), NSL = kGj1Threads / TJ;
-  const size_t nch = (size_t)(k0 + kGj1Chunk - 1) / kGj1Chunk;
-  return 1024 + nch * kGj1Chunk * 128 + 8 * (nch + 1) +
-         sizeof(T) * (2 * (size_t)kGj1Chunk * B + (size_t)NSL * B * TJ + 2 * B * TJ + B * B + B) + sizeof(int) * 2 * B + 64;
-}
-
-template <typename T, int B>
-static __global__ void __launch_bounds__(kGj1Threads, 1) ffs_dense_gj1_kernel(const __grid_constant__ CUtensorMap tmW,
-                                                                             const DenseGjParams q) {
-  using S = Sc<T>;
-  constexpr int TJ = 128 / (int)sizeof(T), NSL = kGj1Threads / TJ;
-  extern __shared__ __align__(1024) unsigned char graw[];
-  unsigned char* tile = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(graw) + 1023) & ~uintptr_t(1023));
-  const int k0 = q.k0, k1 = k0 + B, Np = q.Np, N = q.N;
-  const int sl = blockIdx.y;
-  const int64_t i_s = q.base + sl;
-  const int t = threadIdx.x, jl = t % TJ, slice = t / TJ;
-  const int j0 = k1 + blockIdx.x * TJ;
-  const int ncol = min(TJ, Np - j0);
-  const int j = j0 + jl;
-  const bool has = jl < ncol;
-  const int nch = (k0 + kGj1Chunk - 1) / kGj1Chunk;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tile + (size_t)nch * kGj1Chunk * 128);  // [nch]
-  T* Vn = reinterpret_cast<T*>(bar + nch + 1);                                         // [64][B]
-  T* Wbc = Vn + kGj1Chunk * B;                                                         // [64][B]
-  T* Zp = Wbc + kGj1Chunk * B;                                                         // [NSL][B][TJ]
-  T* Zs = Zp + NSL * B * TJ;                                                           // [B][TJ]
-  T* Zu = Zs + B * TJ;                                                                 // [B][TJ]
-  T* RP = Zu + B * TJ;                                                                 // Row [B][B], Pinv [B]
-  int* xn = reinterpret_cast<int*>(RP + B * B + B);
-  const int32_t* pm = q.perm + i_s * Np;
-  const T* Ug = reinterpret_cast<const T*>(q.U);
-  T* W = reinterpret_cast<T*>(q.W) + (size_t)sl * Np * Np;
-  // element (row r, column jl) of the 128-byte-swizzled tile: 16-byte chunk c of row r sits at c ^ (r & 7)
-  auto tel = [&](int r) -> T& {
-    constexpr int per = 16 / (int)sizeof(T);
-    const int c = jl / per, e = jl % per;
-    return *reinterpret_cast<T*>(tile + (size_t)r * 128 + ((c ^ (r & 7)) << 4) + e * sizeof(T));
-  };
-  if (t == 0) {
-    for (int c = 0; c < nch; ++c) oz_mbar_init(bar + c, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (t < B) xn[t] = q.positions[i_s * Np + k0 + t];
-  if (t < B * B + B) RP[t] = reinterpret_cast<const T*>(q.rowg)[(size_t)sl * (B * B + B) + t];
-  __syncthreads();
-  if (t == 0) {
-    constexpr unsigned kBox = kGj1Chunk * 128;
-    const int cx = j0 * (int)(sizeof(T) / 8);  // the map's inner dimension counts doubles
-    for (int c = 0; c < nch; ++c) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(bar + c)), "r"(kBox) : "memory");
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-              oz_u32(tile + (size_t)c * kBox)),
-          "l"(&tmW), "r"(cx), "r"(c * kGj1Chunk), "r"(sl), "r"(oz_u32(bar + c))
-          : "memory");
-    }
-  }
-  // (1) minus the partial sums V[X_new, i] W[i, j] over this thread's rows i = slice (mod NSL)
-  T acc[B];
-#pragma unroll
-  for (int tt = 0; tt < B; ++tt) acc[tt] = S::zero();
-  for (int c = 0; c < nch; ++c) {
-    const int r0 = c * kGj1Chunk, nr = min(k0, r0 + kGj1Chunk) - r0;
-    for (int idx = t; idx < nr * B; idx += blockDim.x) Vn[idx] = Ug[(size_t)xn[idx % B] * N + pm[r0 + idx / B]];
-    __syncthreads();
-    oz_mbar_wait(bar + c, 0);
-    if (has)
-      for (int r = slice; r < nr; r += NSL) {
-        const T w = tel(r0 + r);
-#pragma unroll
-        for (int tt = 0; tt < B; ++tt) acc[tt] = S::fms(Vn[r * B + tt], w, acc[tt]);
-      }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int tt = 0; tt < B; ++tt) Zp[(slice * B + tt) * TJ + jl] = acc[tt];
-  __syncthreads();
-  for (int idx = t; idx < B * TJ; idx += blockDim.x) {
-    T a = S::zero();
-    for (int s2 = 0; s2 < NSL; ++s2) a = S::add(a, Zp[s2 * B * TJ + idx]);
-    Zu[idx] = a;
-  }
-  __syncthreads();
-  // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
-  if (t < TJ && has) {
-    T z[B];
-#pragma unroll
-    for (int tt = 0; tt < B; ++tt) z[tt] = S::add(Ug[(size_t)xn[tt] * N + pm[j]], Zu[tt * TJ + t]);
-    const T* Row = RP;
-    const T* Pinv = RP + B * B;
-#pragma unroll
-    for (int tt = 1; tt < B; ++tt)
-#pragma unroll
-      for (int s2 = 0; s2 < tt; ++s2) z[tt] = S::fms(S::mul(Row[tt * B + s2], Pinv[s2]), z[s2], z[tt]);
-#pragma unroll
-    for (int tt = B - 1; tt >= 0; --tt) {
-#pragma unroll
-      for (int s2 = tt + 1; s2 < B; ++s2) z[tt] = S::fms(Row[tt * B + s2], z[s2], z[tt]);
-      z[tt] = S::mul(z[tt], Pinv[tt]);
-    }
-#pragma unroll
-    for (int tt = 0; tt < B; ++tt) {
-      Zs[tt * TJ + t] = z[tt];
-      W[(size_t)(k0 + tt) * Np + j] = z[tt];
-    }
-  }
-  __syncthreads();
-  // (3) W[0:k0, j] -= W[0:k0, k0:k1] Z[:, j] from the tile, one coalesced 128-byte write per row
-  T z[B];
-#pragma unroll
-  for (int tt = 0; tt < B; ++tt) z[tt] = Zs[tt * TJ + jl];
-  for (int c = 0; c < nch; ++c) {
-    const int r0 = c * kGj1Chunk, nr = min(k0, r0 + kGj1Chunk) - r0;
-    for (int idx = t; idx < nr * B; idx += blockDim.x) Wbc[idx] = W[(size_t)(r0 + idx / B) * Np + k0 + idx % B];
-    __syncthreads();
-    if (has)
-      for (int r = slice; r < nr; r += NSL) {
-        T a = tel(r0 + r);
-#pragma unroll
-        for (int tt = 0; tt < B; ++tt) a = S::fms(Wbc[r * B + tt], z[tt], a);
-        W[(size_t)(r0 + r) * Np + j] = a;
-      }
-    __syncthreads();
-  }
-  // next block's Y_s columns (the tile holding columns k1 .. k1+B-1)
-  if (blockIdx.x == 0 && q.Y != nullptr) {
-    const int nb1 = min(B, Np - k1);
-    const int64_t col0 = (int64_t)sl * B;
-    for (int idx = t; idx < k1 * B; idx += blockDim.x) {
-      const int ii = idx / B, c = idx % B;
-      dense_y_store<T>(q.Y, q.ldY, pm[ii], col0 + c, c < nb1 ? S::neg(W[(size_t)ii * Np + k1 + c]) : S::zero());
-    }
-    if (t < nb1) dense_y_store<T>(q.Y, q.ldY, pm[k1 + t], col0 + t, S::one());
-  }
-}
-
 }  // namespace ffsk
