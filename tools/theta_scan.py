@@ -8,25 +8,26 @@ import torch  # noqa: E402
 
 from paper_2109_07358_b200 import ffs, inputs  # noqa: E402
 
-name = sys.argv[1]
+name, _, marg = sys.argv[1].partition(":")
 cfg = inputs.CONFIGS[name]
 U = torch.from_numpy(inputs.build_u(cfg)).cuda()
-u = torch.from_numpy(inputs.workload_uniforms(cfg)).cuda()
+u = torch.from_numpy(inputs.workload_uniforms(cfg, bool(marg))).cuda()
+Np = cfg.marginal_Np if marg else cfg.N
 ws = ffs.Workspace("cuda")
 for th in sys.argv[2:]:
     key, _, val = th.partition("=")
     if val:
         ffs.set_option(key, float(val))
-    else:
+    elif key != "-":
         ffs.set_option("dense_theta", float(key))
     for _ in range(2):
-        ffs.ffs_sample(U, u, workspace=ws)
+        ffs.ffs_sample_marginal(U, u, Np, workspace=ws)
     torch.cuda.synchronize()
     ts = []
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ffs.ffs_sample(U, u, workspace=ws)
+        ffs.ffs_sample_marginal(U, u, Np, workspace=ws)
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
