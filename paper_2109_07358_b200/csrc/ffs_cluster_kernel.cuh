@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             xsel_k = *xsel;
             xr = xrow;
           }
+          FFS_CHECK(xsel_k >= 0 && xsel_k < L);
           if (t == 0) pos[k] = xsel_k;
           if (t < B) Row[rr * B + t] = xr[t];
           const T piv = xr[rr];

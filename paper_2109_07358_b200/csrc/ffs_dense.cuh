@@ -418,6 +418,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     const int64_t col0 = (int64_t)sl * B;
     for (int idx = t; idx < k1 * B; idx += blockDim.x) {
       const int ii = idx / B, c = idx % B;
+      FFS_CHECK(pm[ii] >= 0 && pm[ii] < N);
       dense_y_store<T>(q.Y, q.ldY, pm[ii], col0 + c, c < nb1 ? S::neg(W[(size_t)ii * Np + k1 + c]) : S::zero());
     }
     if (t < nb1) dense_y_store<T>(q.Y, q.ldY, pm[k1 + t], col0 + t, S::one());
@@ -600,6 +601,7 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
 #pragma unroll
       for (int c = 0; c < kEC; c += 2) {
         const int col = n0 + ch + c;
+        FFS_CHECK(col + 1 < p.N);
         const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
         const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;  // biased exponents
         const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);

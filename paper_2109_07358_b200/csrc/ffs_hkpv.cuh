@@ -144,6 +144,7 @@ static __global__ void __launch_bounds__(kHkpvThreads) ffs_hkpv_step_kernel(cons
     }
     xs = !ok ? c : (a != kNone ? a : b);
   }
+  FFS_CHECK(xs >= 0 && xs < L);
   if (xs < 0 || xs >= L) xs = 0;  // unreachable for N' <= N <= L
   const double wsel = wgt(xs);
   __syncthreads();  // every thread has read the residuals / bitmap before the update below
@@ -268,6 +269,7 @@ static __global__ void __launch_bounds__(MAXT, 1) ffs_hkpv_warp_kernel(const Hkp
           }
         p.positions[i * Np + k] = xs;
       }
+      FFS_CHECK(xs >= 0 && xs < L);
       if (k + 1 == Np) break;
       // e_k: two classical Gram-Schmidt passes of u_{x_k} against e_0 .. e_{k-1}
       for (int n = lane; n < N; n += 32) v[n] = Uts[(size_t)n * p.ut_stride + Swz<double, R>::phys(xs)];

@@ -289,7 +289,10 @@ ffs_sample_kernel(const Params p) {
     const int Npi = p.nps ? p.nps[i] : Np;  // steps of this sample (ragged mode: its N_i)
     if (p.cols) {
       // ragged mode: the permuted kept columns come precomputed
-      for (int j = t; j < Npi; j += G) perm[j] = p.cols[i * N + j];
+      for (int j = t; j < Npi; j += G) {
+        FFS_CHECK(p.cols[i * N + j] >= 0 && p.cols[i * N + j] < N);
+        perm[j] = p.cols[i * N + j];
+      }
     } else {
       // ---- a1: permutation (reading Q6), forward partial Fisher-Yates
       for (int j = t; j < N; j += G) perm[j] = j;
@@ -467,7 +470,10 @@ ffs_sample_kernel(const Params p) {
       gsync<WARP>();
     }
     // ---- a6: positions (sampling order) and flags
-    for (int j = t; j < Np; j += G) p.positions[i * Np + j] = j < Npi ? pos[j] : -1;
+    for (int j = t; j < Np; j += G) {
+      FFS_CHECK(j >= Npi || (pos[j] >= 0 && pos[j] < L));
+      p.positions[i * Np + j] = j < Npi ? pos[j] : -1;
+    }
     if constexpr (WARP) {
       flag = __reduce_or_sync(0xffffffffu, flag);
     } else {

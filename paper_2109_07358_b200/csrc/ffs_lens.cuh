@@ -37,6 +37,7 @@ static __global__ void ffs_lens_prep_kernel(const double* __restrict__ lambda, c
     a[r * bs] = t;
     cols[i * K + j] = a[j * bs];
   }
+  FFS_CHECK(n >= 0 && n <= K);
   nps[i] = n;
 }
 

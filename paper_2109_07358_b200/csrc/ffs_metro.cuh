@@ -124,6 +124,7 @@ static __global__ void __launch_bounds__(kMetroWarps * 32) ffs_metro_kernel(cons
           }
         }
         if (!(wc > 0.0)) flag |= 4;
+        FFS_CHECK(ex[cur] >= 0 && ex[cur] < L);
         pos[k] = ex[cur];
         *pivot = es[cur];  // s(x_k): the new diagonal entry of the factorization
       }

@@ -2,7 +2,27 @@
 // Complex products are BILINEAR (u_x^T h; reading Q3): no conjugation anywhere
 // except in |z|^2 and in the reciprocal of a pivot.
 #pragma once
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Device-side bounds checks of the checked build (python -m paper_2109_07358_b200.build --checked
+// -> libffs_checked.so, compiled with -DFFS_CHECKED): a failed check prints its condition and
+// traps. compute-sanitizer is closed on this GPU pool (profiles/r02/compute_sanitizer_closed.log);
+// these checks guard every index the kernels derive from data (sites, permuted columns).
+#ifdef FFS_CHECKED
+#define FFS_CHECK(cond)                                                                   \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("FFS_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define FFS_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 struct cplx {
   double re, im;

@@ -79,6 +79,7 @@ static __global__ void ffs_permute_kernel(const double* __restrict__ uniforms, i
     const int n = N - j;
     int r = (int)floor(u[j] * (double)n);
     r = (r > n - 1 ? n - 1 : r) + j;
+    FFS_CHECK(r >= j && r < N);
     const int a = m[j * bs];
     const int b = m[r * bs];
     m[r * bs] = a;
@@ -295,6 +296,7 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
     const int64_t id = g * SEGS + seg;
     const int64_t i = id < p.M ? id : p.M - 1;  // a short last group recomputes a sample
     for (int j = sl; j < Np; j += G) {
+      FFS_CHECK(p.perm[i * Np + j] >= 0 && p.perm[i * Np + j] < N);
       perm[j] = p.perm[i * Np + j] * stride;  // U^T column offset of m_j
       usel[j] = p.uniforms[i * 2 * (int64_t)Np + Np + j];
     }
@@ -440,7 +442,10 @@ __device__ __forceinline__ void ffs_seg_body(const WarpParams& p) {
     // ---- a6: positions and flags
     unsigned fl = __reduce_or_sync(0xffffffffu, (unsigned)flag << (seg * 2));
     if (id < p.M) {
-      for (int j = sl; j < Np; j += G) p.positions[id * Np + j] = pos[j];
+      for (int j = sl; j < Np; j += G) {
+        FFS_CHECK(pos[j] >= 0 && pos[j] < L);
+        p.positions[id * Np + j] = pos[j];
+      }
       if (sl == 0 && p.flags != nullptr) p.flags[id] = (fl >> (seg * 2)) & 3u;
     }
     __syncwarp();

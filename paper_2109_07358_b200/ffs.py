@@ -62,7 +62,9 @@ class FFSError(RuntimeError):
 
 
 def lib_path() -> str:
-    return _build.SO
+    """libffs.so in the package directory; FFS_LIBRARY=checked selects the bounds-checked build
+    (libffs_checked.so, -DFFS_CHECKED) for the checked test runs."""
+    return _build.SO_CHECKED if os.environ.get("FFS_LIBRARY") == "checked" else _build.SO
 
 
 def load(build_if_missing: bool = True):
@@ -70,11 +72,12 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.SO):
+    so = lib_path()
+    if not os.path.exists(so):
         if not build_if_missing:
-            raise FFSError(f"{_build.SO} missing: run python -m paper_2109_07358_b200.build")
-        _build.build()
-    L = ctypes.CDLL(_build.SO)
+            raise FFSError(f"{so} missing: run python -m paper_2109_07358_b200.build")
+        _build.build(checked=so == _build.SO_CHECKED)
+    L = ctypes.CDLL(so)
     i64, vp, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
     ci = ctypes.c_int
     L.ffs_workspace_bytes.argtypes = [i64, i64, i64, ci, i64]
