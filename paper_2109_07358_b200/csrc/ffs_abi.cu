@@ -1112,8 +1112,8 @@ int metro_layout(int64_t L, int64_t N, int64_t Np, int64_t Mc, int dtype, int64_
   if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
   const bool cx = dtype == FFS_C128;
   const size_t es = cx ? 16 : 8;
-  y.smem = (size_t)ffsk::kMetroWarps * (cx ? ffsk::metro_warp_smem<cplx>((int)Np, (int)Mc)
-                                           : ffsk::metro_warp_smem<double>((int)Np, (int)Mc));
+  y.smem = (size_t)ffsk::kMetroWarps * (cx ? ffsk::metro_warp_smem<cplx>((int)Np, (int)Mc, (int)N)
+                                           : ffsk::metro_warp_smem<double>((int)Np, (int)Mc, (int)N));
   if (y.smem > kMaxSmem) return fail(FFS_EINVAL, "N'=%lld / M_cond=%lld too large for the Metropolis kernel",
                                      (long long)Np, (long long)Mc);
   const void* fn = cx ? reinterpret_cast<const void*>(&ffsk::ffs_metro_kernel<cplx>)

@@ -8,9 +8,10 @@
 // One warp per sample. The coefficients W = A^{-1} V[X, later columns] live in global memory per
 // warp slot and get a rank-1 Gauss-Jordan update after every step (O(k N') per step, lanes over
 // columns, coalesced rows). The chain's weights s(x) = V[x, 0:k+1] . (-W[0:k, k]; 1) of all
-// M_cond + 1 states (start + proposals) are independent of the acceptance history, so lane e
-// evaluates entry e (a k+1 term gathered dot product from U's row x_e); one lane then runs the
-// sequential accept/reject chain over the stored weights.
+// M_cond + 1 states (start + proposals) are independent of the acceptance history: with h
+// scattered into U's column order each is one coalesced read of row x by the warp and a warp
+// reduction, 8 states' reads in flight together; one lane then runs the sequential accept/reject
+// chain over the stored weights.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -41,12 +42,13 @@ __device__ __forceinline__ cplx ldg_t(const cplx* p) {
 __host__ __device__ inline size_t metro_align(size_t v) { return (v + 15) & ~size_t(15); }
 
 // per-warp shared memory: m [Np] int, pos [Np] int, h [Np] T, vrow [Np] T, chain entries [Mc + 1]
-// of (s T, w double, x int), pivot T
+// of (s T, w double, x int), pivot T, hp [N] T
 template <typename T>
-__host__ __device__ inline size_t metro_warp_smem(int Np, int Mc) {
+__host__ __device__ inline size_t metro_warp_smem(int Np, int Mc, int N) {
   const size_t e = (size_t)Mc + 1;
   return 2 * metro_align(sizeof(int) * Np) + 2 * metro_align(sizeof(T) * Np) +
-         metro_align(e * (sizeof(int) + sizeof(double) + sizeof(T))) + metro_align(sizeof(T));
+         metro_align(e * (sizeof(int) + sizeof(double) + sizeof(T))) + metro_align(sizeof(T)) +
+         metro_align(sizeof(T) * N);
 }
 
 template <typename T>
@@ -56,7 +58,7 @@ static __global__ void __launch_bounds__(kMetroWarps * 32) ffs_metro_kernel(cons
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int L = p.L, N = p.N, Np = p.Np, Mc = p.Mc;
   const int E = Mc + 1;
-  unsigned char* b = msm + (size_t)wid * metro_warp_smem<T>(Np, Mc);
+  unsigned char* b = msm + (size_t)wid * metro_warp_smem<T>(Np, Mc, N);
   int* perm = reinterpret_cast<int*>(b);
   b += metro_align(sizeof(int) * Np);
   int* pos = reinterpret_cast<int*>(b);
@@ -70,6 +72,8 @@ static __global__ void __launch_bounds__(kMetroWarps * 32) ffs_metro_kernel(cons
   int* ex = reinterpret_cast<int*>(ew + E);   // [E] sites
   b += metro_align((size_t)E * (sizeof(int) + sizeof(double) + sizeof(T)));
   T* pivot = reinterpret_cast<T*>(b);
+  b += metro_align(sizeof(T));
+  T* hp = reinterpret_cast<T*>(b);
   const T* Ug = reinterpret_cast<const T*>(p.U);
   const int64_t slot = (int64_t)blockIdx.x * kMetroWarps + wid;
   const int64_t nslots = (int64_t)gridDim.x * kMetroWarps;
@@ -87,29 +91,63 @@ static __global__ void __launch_bounds__(kMetroWarps * 32) ffs_metro_kernel(cons
       if (lane == 0) h[k] = S::one();
       __syncwarp();
       const double* uc = urow + Np + (int64_t)k * (1 + 2 * Mc);
-      // weights of the start (e = 0) and the Mc proposals (e >= 1), one lane per entry
-      for (int e = lane; e < E; e += 32) {
-        int x = (int)floor(uc[e == 0 ? 0 : 2 * e - 1] * (double)L);
-        x = x > L - 1 ? L - 1 : x;
-        bool chosen = false;
-        for (int j = 0; j < k; ++j) chosen |= (pos[j] == x);
-        T s = S::zero();
-        double w = 0.0;
-        if (!chosen) {
-          const T* ur = Ug + (size_t)x * N;
-          T a0 = S::zero(), a1 = S::zero();
-          int j = 0;
-          for (; j + 1 <= k; j += 2) {
-            a0 = S::fms(S::neg(ldg_t(ur + perm[j])), h[j], a0);
-            a1 = S::fms(S::neg(ldg_t(ur + perm[j + 1])), h[j + 1], a1);
+      // h scattered into U's column order (hp[m_j] = h[j] for j <= k, 0 elsewhere): a chain state's
+      // s(x) = U[x, :] . hp is then one coalesced read of row x by the warp and a warp reduction
+      for (int c = lane; c < N; c += 32) hp[c] = S::zero();
+      __syncwarp();
+      for (int j = lane; j <= k; j += 32) hp[perm[j]] = h[j];
+      __syncwarp();
+      // weights of the start (e = 0) and the Mc proposals (e >= 1), kBatch states at a time (their
+      // row reads in flight together)
+      constexpr int kBatch = 8;
+      for (int e0 = 0; e0 < E; e0 += kBatch) {
+        int xb[kBatch];
+        bool live[kBatch];
+        T part[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+          const int e = e0 + b;
+          int x = 0;
+          bool chosen = true;
+          if (e < E) {
+            x = (int)floor(uc[e == 0 ? 0 : 2 * e - 1] * (double)L);
+            x = x > L - 1 ? L - 1 : x;
+            bool hit = false;
+            for (int j = lane; j < k; j += 32) hit |= (pos[j] == x);
+            chosen = __any_sync(0xffffffffu, hit);
           }
-          for (; j <= k; ++j) a0 = S::fms(S::neg(ldg_t(ur + perm[j])), h[j], a0);
-          s = S::add(a0, a1);
-          w = S::abs2(s);
+          xb[b] = x;
+          live[b] = !chosen;
+          part[b] = S::zero();
         }
-        ex[e] = x;
-        ew[e] = w;
-        es[e] = s;
+        for (int c = lane; c < N; c += 32) {
+          const T hc = hp[c];
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b)
+            if (live[b]) part[b] = S::fms(S::neg(ldg_t(Ug + (size_t)xb[b] * N + c)), hc, part[b]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) {
+            if constexpr (sizeof(T) == 8) {
+              part[b] = S::add(part[b], __shfl_xor_sync(0xffffffffu, part[b], o));
+            } else {
+              cplx y;
+              y.re = __shfl_xor_sync(0xffffffffu, part[b].re, o);
+              y.im = __shfl_xor_sync(0xffffffffu, part[b].im, o);
+              part[b] = S::add(part[b], y);
+            }
+          }
+        if (lane == 0) {
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b)
+            if (e0 + b < E) {
+              ex[e0 + b] = xb[b];
+              ew[e0 + b] = live[b] ? S::abs2(part[b]) : 0.0;
+              es[e0 + b] = live[b] ? part[b] : S::zero();
+            }
+        }
       }
       __syncwarp();
       // the sequential accept / reject chain
