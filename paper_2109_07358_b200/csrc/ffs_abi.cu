@@ -805,8 +805,8 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
           op.panel = gp.panel;
           // stream the smaller slice set (keeps the other operand L2-resident)
           op.m_fast = (int64_t)L * d.Kp < oz_ncols * d.Kp ? 1 : 0;
-          const unsigned mt = (unsigned)((L + ffsk::kOzBM - 1) / ffsk::kOzBM), nt = (unsigned)(oz_ncols / ffsk::kOzBN);
-          const dim3 og = op.m_fast ? dim3(mt, nt) : dim3(nt, mt);
+          const int64_t ntiles = ((L + ffsk::kOzBM - 1) / ffsk::kOzBM) * (oz_ncols / ffsk::kOzBN);
+          const dim3 og((unsigned)std::min<int64_t>(ntiles, ffsh::sm_count(ffsh::device())));  // persistent
           if (ns == 8)
             ffsk::ffs_ozaki_gemm_kernel<8><<<og, ffsk::kOzThreads, ffsk::oz_smem<8>(), stream>>>(oz_ta, oz_tb, op);
           else

@@ -444,7 +444,7 @@ constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64, kOzStages = 2, kOzThreads = 3
 constexpr int kOzTA = kOzBM * kOzBK, kOzTB = kOzBN * kOzBK;
 template <int NS> constexpr int oz_stage_bytes() { return NS * (kOzTA + kOzTB); }
 template <int NS>
-constexpr size_t oz_smem() { return (size_t)kOzStages * oz_stage_bytes<NS>() + (2 * kOzStages + 1) * 8 + 16 + 1024; }
+constexpr size_t oz_smem() { return (size_t)kOzStages * oz_stage_bytes<NS>() + (2 * kOzStages + 2) * 8 + 16 + 1024; }
 static_assert(oz_smem<kOzMaxS>() <= 227 * 1024, "two stages of 8 slices fit shared memory");
 
 struct OzakiParams {
@@ -482,6 +482,11 @@ __device__ __forceinline__ void oz_mbar_wait(uint64_t* b, unsigned parity) {
       : "memory");
 }
 
+// Persistent: one CTA per SM walks the tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... (the
+// raster of OzakiParams::m_fast). TMEM is allocated and the barriers initialised once; the TMA
+// producer streams the K chunks of consecutive tiles through the two stages without a break; the
+// MMA issuer starts a tile as soon as the epilogue has drained the accumulators of the previous one
+// (tmem_empty), and the epilogue's fp64 scaling and global stores overlap the next tile's MMAs.
 template <int NS>
 static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                             const __grid_constant__ CUtensorMap tmB,
@@ -490,11 +495,18 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kOzStages * oz_stage_bytes<NS>());
   uint64_t* empty = full + kOzStages;
-  uint64_t* done = empty + kOzStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + kOzStages;  // MMA -> epilogue: the tile's accumulators are complete
+  uint64_t* tempty = tfull + 1;         // epilogue -> MMA: the accumulators have been read
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int m0 = (p.m_fast ? blockIdx.x : blockIdx.y) * kOzBM, n0 = (p.m_fast ? blockIdx.y : blockIdx.x) * kOzBN;
   const int KT = p.K / kOzBK;
+  const int mt = (p.M + kOzBM - 1) / kOzBM, nt = p.N / kOzBN;
+  const int ntiles = mt * nt;
+  auto tile_origin = [&](int tt, int& m0, int& n0) {
+    const int a = p.m_fast ? tt % mt : tt / nt, b = p.m_fast ? tt / mt : tt % nt;
+    m0 = a * kOzBM;
+    n0 = b * kOzBN;
+  };
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_u32(tmem_slot)), "r"(512)
                  : "memory");
@@ -505,7 +517,8 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
       oz_mbar_init(full + s, 1);
       oz_mbar_init(empty + s, 1);
     }
-    oz_mbar_init(done, 1);
+    oz_mbar_init(tfull, 1);
+    oz_mbar_init(tempty, 256);  // the 8 epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -513,68 +526,81 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   if (warp == 8 && lane == 0) {  // TMA producer
-    for (int kt = 0; kt < KT; ++kt) {
-      const int st = kt % kOzStages;
-      if (kt >= kOzStages) oz_mbar_wait(empty + st, ((kt / kOzStages) - 1) & 1);
-      unsigned char* sb = sm + st * oz_stage_bytes<NS>();
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)), "r"(oz_stage_bytes<NS>())
-                   : "memory");
+    int g = 0;                   // K chunks issued so far (all tiles)
+    for (int tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+      int m0, n0;
+      tile_origin(tt, m0, n0);
+      for (int kt = 0; kt < KT; ++kt, ++g) {
+        const int st = g % kOzStages;
+        if (g >= kOzStages) oz_mbar_wait(empty + st, ((g / kOzStages) - 1) & 1);
+        unsigned char* sb = sm + st * oz_stage_bytes<NS>();
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)),
+                     "r"(oz_stage_bytes<NS>())
+                     : "memory");
 #pragma unroll
-      for (int i = 0; i < NS; ++i) {
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                oz_u32(sb + i * kOzTA)),
-            "l"(&tmA), "r"(kt * kOzBK), "r"(m0), "r"(i), "r"(oz_u32(full + st))
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                oz_u32(sb + NS * kOzTA + i * kOzTB)),
-            "l"(&tmB), "r"(kt * kOzBK), "r"(n0), "r"(i), "r"(oz_u32(full + st))
-            : "memory");
+        for (int i = 0; i < NS; ++i) {
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                  oz_u32(sb + i * kOzTA)),
+              "l"(&tmA), "r"(kt * kOzBK), "r"(m0), "r"(i), "r"(oz_u32(full + st))
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                  oz_u32(sb + NS * kOzTA + i * kOzTB)),
+              "l"(&tmB), "r"(kt * kOzBK), "r"(n0), "r"(i), "r"(oz_u32(full + st))
+              : "memory");
+        }
       }
     }
   } else if (warp == 9 && lane == 0) {  // MMA issuer
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) | ((uint32_t)(kOzBM >> 4) << 24);
-    for (int kt = 0; kt < KT; ++kt) {
-      const int st = kt % kOzStages;
-      oz_mbar_wait(full + st, (kt / kOzStages) & 1);
+    int g = 0, it = 0;
+    for (int tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++it) {
+      if (it > 0) oz_mbar_wait(tempty, (it - 1) & 1);  // the previous tile's accumulators were read
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned char* sb = sm + st * oz_stage_bytes<NS>();
+      for (int kt = 0; kt < KT; ++kt, ++g) {
+        const int st = g % kOzStages;
+        oz_mbar_wait(full + st, (g / kOzStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const unsigned char* sb = sm + st * oz_stage_bytes<NS>();
 #pragma unroll
-      for (int i = 0; i < NS; ++i)
+        for (int i = 0; i < NS; ++i)
 #pragma unroll
-        for (int j = 0; j < NS - i; ++j)
+          for (int j = 0; j < NS - i; ++j)
 #pragma unroll
-          for (int ks = 0; ks < kOzBK / 32; ++ks) {
-            const uint64_t da = oz_desc(sb + i * kOzTA + ks * 32);
-            const uint64_t db = oz_desc(sb + NS * kOzTA + j * kOzTB + ks * 32);
-            const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first write of D_{i+j}: i = 0
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)((i + j) * kOzBN)),
-                "l"(da), "l"(db), "r"(idesc), "r"(acc)
-                : "memory");
-          }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(empty + st))
+            for (int ks = 0; ks < kOzBK / 32; ++ks) {
+              const uint64_t da = oz_desc(sb + i * kOzTA + ks * 32);
+              const uint64_t db = oz_desc(sb + NS * kOzTA + j * kOzTB + ks * 32);
+              const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first write of D_{i+j}: i = 0
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)((i + j) * kOzBN)),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                  : "memory");
+            }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(empty + st))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(tfull))
                    : "memory");
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oz_u32(done))
-                 : "memory");
   }
   if (warp < 8) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. (tile rows), columns 32 (w / 4) ..
-    oz_mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     constexpr int kEC = kOzBN / 2;  // columns per epilogue warp
     const int q = warp & 3, ch = (warp >> 2) * kEC;
-    double acc[kEC];
+    int it = 0;
+    for (int tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++it) {
+      int m0, n0;
+      tile_origin(tt, m0, n0);
+      oz_mbar_wait(tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double acc[kEC];
 #pragma unroll
-    for (int c = 0; c < kEC; ++c) acc[c] = 0.0;
+      for (int c = 0; c < kEC; ++c) acc[c] = 0.0;
 #pragma unroll
-    for (int d = NS - 1; d >= 0; --d) {  // smallest terms first
-      const double sc = ldexp(1.0, -7 * (d + 2));
-      {
-        constexpr int cb = 0;
+      for (int d = NS - 1; d >= 0; --d) {  // smallest terms first
+        const double sc = ldexp(1.0, -7 * (d + 2));
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * kOzBN + ch);
         asm volatile(
@@ -587,27 +613,30 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[cb + c] = fma((double)(int)v[c], sc, acc[cb + c]);
+        for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], sc, acc[c]);
       }
-    }
-    const int row = m0 + q * 32 + lane;
-    if (row < p.M) {
-      // 2^(ea + eb) as one multiply by an exact power of two built from its biased exponent
-      // (ldexp outside the normal range); panel (8 or 16) is a power of two
-      const int er = p.ea[row];
-      const int lp = __ffs(p.panel) - 1;
-      double* crow = p.C + (size_t)row * p.panel;
-      const size_t sstride = (size_t)p.M * p.panel;
+      // every accumulator of this tile is in registers: hand TMEM back to the MMA issuer
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(oz_u32(tempty)) : "memory");
+      const int row = m0 + q * 32 + lane;
+      if (row < p.M) {
+        // 2^(ea + eb) as one multiply by an exact power of two built from its biased exponent
+        // (ldexp outside the normal range); panel (8 or 16) is a power of two
+        const int er = p.ea[row];
+        const int lp = __ffs(p.panel) - 1;
+        double* crow = p.C + (size_t)row * p.panel;
+        const size_t sstride = (size_t)p.M * p.panel;
 #pragma unroll
-      for (int c = 0; c < kEC; c += 2) {
-        const int col = n0 + ch + c;
-        FFS_CHECK(col + 1 < p.N);
-        const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
-        const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;  // biased exponents
-        const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
-        const double s1 = (b1 > 0 && b1 < 2047) ? __longlong_as_double((long long)b1 << 52) : ldexp(1.0, er + e2.y);
-        *reinterpret_cast<double2*>(crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1))) =
-            make_double2(acc[c] * s0, acc[c + 1] * s1);
+        for (int c = 0; c < kEC; c += 2) {
+          const int col = n0 + ch + c;
+          FFS_CHECK(col + 1 < p.N);
+          const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
+          const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;  // biased exponents
+          const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
+          const double s1 = (b1 > 0 && b1 < 2047) ? __longlong_as_double((long long)b1 << 52) : ldexp(1.0, er + e2.y);
+          *reinterpret_cast<double2*>(crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1))) =
+              make_double2(acc[c] * s0, acc[c + 1] * s1);
+        }
       }
     }
   }
