@@ -217,8 +217,9 @@ struct HkpvWarpParams {
   size_t ushared, owner_bytes;
 };
 
+// e-vector rows are N + 1 doubles apart: lanes over j reading E[j][n] hit distinct banks
 __host__ __device__ inline size_t hkpv_warp_owner_bytes(int N, int Np) {
-  return align16(sizeof(double) * (size_t)Np * N) + align16(sizeof(double) * 2 * (size_t)N) +
+  return align16(sizeof(double) * (size_t)Np * (N + 1)) + align16(sizeof(double) * 2 * (size_t)N) +
          align16(sizeof(double) * (size_t)Np) + align16(sizeof(double) * 32 + sizeof(int) * 96);
 }
 
@@ -234,8 +235,9 @@ static __global__ void __launch_bounds__(MAXT, 1) ffs_hkpv_warp_kernel(const Hkp
   }
   __syncthreads();
   unsigned char* ob = smem + p.ushared + (size_t)wid * p.owner_bytes;
-  double* E = reinterpret_cast<double*>(ob);                                      // [Np][N]
-  double* v = reinterpret_cast<double*>(ob + align16(sizeof(double) * (size_t)Np * N));  // [N] (+ [N] scratch)
+  const int ldE = N + 1;
+  double* E = reinterpret_cast<double*>(ob);                                           // [Np][N + 1]
+  double* v = reinterpret_cast<double*>(ob + align16(sizeof(double) * (size_t)Np * ldE));  // [N] (+ [N] scratch)
   double* cf = v + 2 * N;                                                          // [Np]
   double* red = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(cf) + align16(sizeof(double) * Np));
   int* redi = reinterpret_cast<int*>(red + 32);
@@ -277,13 +279,13 @@ static __global__ void __launch_bounds__(MAXT, 1) ffs_hkpv_warp_kernel(const Hkp
       for (int pass = 0; pass < 2; ++pass) {
         for (int j = lane; j < k; j += 32) {
           double a = 0.0;
-          for (int n = 0; n < N; ++n) a = fma(v[n], E[(size_t)j * N + n], a);
+          for (int n = 0; n < N; ++n) a = fma(v[n], E[(size_t)j * ldE + n], a);
           cf[j] = a;
         }
         __syncwarp();
         for (int n = lane; n < N; n += 32) {
           double a = v[n];
-          for (int j = 0; j < k; ++j) a = fma(-cf[j], E[(size_t)j * N + n], a);
+          for (int j = 0; j < k; ++j) a = fma(-cf[j], E[(size_t)j * ldE + n], a);
           v[n] = a;
         }
         __syncwarp();
@@ -293,13 +295,13 @@ static __global__ void __launch_bounds__(MAXT, 1) ffs_hkpv_warp_kernel(const Hkp
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, o);
       const double inv = 1.0 / sqrt(nl);
-      for (int n = lane; n < N; n += 32) E[(size_t)k * N + n] = v[n] * inv;
+      for (int n = lane; n < N; n += 32) E[(size_t)k * ldE + n] = v[n] * inv;
       __syncwarp();
       // r_x -= |u_x . e_k|^2 for this lane's sites
       double c[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) c[r] = 0.0;
-      const double* ek = E + (size_t)k * N;
+      const double* ek = E + (size_t)k * ldE;
       for (int n = 0; n < N; ++n) {
         double u[R];
         load_col<double, R, true>(lp, Uts, n, lane, u);
