@@ -112,9 +112,11 @@ def dist_env():
     return rank, world, local
 
 
-def workload(name, marginal, rank):
+def workload(name, marginal, rank, world=1):
     cfg = inputs.CONFIGS[name]
-    U = inputs.build_u(cfg)
+    # multi-GPU: U is built once, on rank 0, and broadcast (broadcast_u); every rank
+    # draws its own uniform stream
+    U = inputs.build_u(cfg) if rank == 0 or world == 1 else None
     if marginal:
         M, Np = cfg.marginal_M, cfg.marginal_Np
         uni = inputs.uniforms(M, Np, cfg.uniform_seed + 100 + 7919 * rank)
@@ -207,6 +209,25 @@ def run_reference(args):
     return 0
 
 
+def broadcast_u(U, cfg, dev, world):
+    """U on this rank's device: rank 0's bytes, sent to the others with one broadcast (NCCL on the
+    GPU box; any torch.distributed backend), outside every timed region."""
+    import torch
+    if world == 1:
+        return torch.from_numpy(np.ascontiguousarray(U)).to(dev)
+    import torch.distributed as dist
+    dt = torch.complex128 if cfg.dtype == inputs.C128 else torch.float64
+    if U is not None:
+        Ud = torch.from_numpy(np.ascontiguousarray(U)).to(dev)
+    else:
+        Ud = torch.empty((cfg.L, cfg.N), dtype=dt, device=dev)
+    if dt == torch.complex128:
+        dist.broadcast(torch.view_as_real(Ud), src=0)
+    else:
+        dist.broadcast(Ud, src=0)
+    return Ud
+
+
 def measure_gpu(name, marginal, steps, warmup, rank, world, dev, with_e2e=True):
     """Device-time samples/s of one workload (inputs resident, L2 flushed before every step),
     the libffs kernel time, clocks during the timed region, and the host-buffer e2e rate."""
@@ -214,9 +235,11 @@ def measure_gpu(name, marginal, steps, warmup, rank, world, dev, with_e2e=True):
     import torch.distributed as dist
     from paper_2109_07358_b200 import ffs
 
-    cfg, U, uni, M, Np = workload(name, marginal, rank)
+    cfg, U, uni, M, Np = workload(name, marginal, rank, world)
+    Ud = broadcast_u(U, cfg, dev, world)
+    if U is None:
+        U = Ud.cpu().numpy()  # the host copy for the e2e leg (the bytes rank 0 built)
     cplx = np.iscomplexobj(U)
-    Ud = torch.from_numpy(np.ascontiguousarray(U)).to(dev)
     ud = torch.from_numpy(uni).to(dev)
     pos = torch.empty((M, Np), dtype=torch.int32, device=dev)
     flg = torch.empty(M, dtype=torch.int32, device=dev)

@@ -110,8 +110,8 @@ FULL = [
     ("dw", None, 3000, 4),
     ("anderson", None, 300, 2),
     ("anderson", 16, 4000, 8),
-    ("peierls", None, 12, 2),
-    ("dpp", None, 6, 1),
+    ("peierls", None, 24, 2),
+    ("dpp", None, 8, 1),
     ("dpp", 64, 400, 4),
 ]
 

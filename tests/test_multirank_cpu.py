@@ -55,3 +55,32 @@ def test_two_rank_sharding_matches_single_process(tmp_path):
     out = str(tmp_path / "pos.npy")
     mp.spawn(_worker, args=(2, _free_port(), U, uni, out), nprocs=2, join=True)
     assert (np.load(out) == ref.sample(U, uni)).all()
+
+
+def _bcast_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    cfg = inputs.CONFIGS["tiny"]
+    cfg_c = inputs.Config("cplx_small", 12, 3, 8, 3, inputs.C128, 0, "none")
+    U = inputs.build_u(cfg) if rank == 0 else None
+    Ud = bench.broadcast_u(U, cfg, torch.device("cpu"), world)
+    Uc = inputs.random_orthonormal(12, 3, 5, complex_=True) if rank == 0 else None
+    Ucd = bench.broadcast_u(Uc, cfg_c, torch.device("cpu"), world)
+    np.save(out_path + f".{rank}.npy", Ud.numpy())
+    np.save(out_path + f".c{rank}.npy", Ucd.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_u_broadcast(tmp_path):
+    """bench.py's multi-GPU input path: rank 0 builds U once and broadcasts it (real and complex);
+    every rank ends with rank 0's bytes."""
+    out = str(tmp_path / "u")
+    mp.spawn(_bcast_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    U0 = inputs.build_u(inputs.CONFIGS["tiny"])
+    Uc = inputs.random_orthonormal(12, 3, 5, complex_=True)
+    for r in range(2):
+        assert (np.load(out + f".{r}.npy") == U0).all()
+        assert (np.load(out + f".c{r}.npy") == Uc).all()
