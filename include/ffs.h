@@ -199,7 +199,9 @@ typedef enum {
                                    replayed as a CUDA graph (not while the caller's stream is being
                                    captured); 0: direct launches */
   FFS_OPT_FORCE_GENERIC = 8,    /* 1: every shape on the per-sample warp/CTA-owner kernel (testing) */
-  FFS_OPT_LAST = 8
+  FFS_OPT_GEMM_2SM = 9,         /* 1 (default): the 8-slice Ozaki GEMM runs as CTA pairs (tcgen05
+                                   cta_group::2, 256 x 64 tiles); 0: one CTA per 128 x 64 tile */
+  FFS_OPT_LAST = 9
 } ffs_option;
 int ffs_set_option(int option, double value);
 double ffs_get_option(int option);

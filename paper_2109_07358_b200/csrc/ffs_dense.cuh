@@ -469,6 +469,13 @@ __device__ __forceinline__ uint64_t oz_desc(const void* base) {  // K-major, 64-
   d |= (uint64_t)4 << 61;
   return d;
 }
+// descriptor of an operand `off` bytes past the one `base` describes: the start address (>> 4)
+// is the low 14-bit field and shared memory is < 256 KB, so the offset adds to the low word
+// without a carry (one uniform add per MMA instead of recomputing the descriptor)
+__device__ __forceinline__ uint64_t oz_desc_add(uint64_t base, uint32_t off) {
+  const uint32_t lo = (uint32_t)base + (off >> 4), hi = (uint32_t)(base >> 32);
+  return ((uint64_t)hi << 32) | lo;
+}
 __device__ __forceinline__ void oz_mbar_init(uint64_t* b, unsigned n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(oz_u32(b)), "r"(n) : "memory");
 }
@@ -563,14 +570,15 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
         oz_mbar_wait(full + st, (g / kOzStages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const unsigned char* sb = sm + st * oz_stage_bytes<NS>();
+        const uint64_t da0 = oz_desc(sb), db0 = oz_desc(sb + NS * kOzTA);
 #pragma unroll
         for (int i = 0; i < NS; ++i)
 #pragma unroll
           for (int j = 0; j < NS - i; ++j)
 #pragma unroll
             for (int ks = 0; ks < kOzBK / 32; ++ks) {
-              const uint64_t da = oz_desc(sb + i * kOzTA + ks * 32);
-              const uint64_t db = oz_desc(sb + NS * kOzTA + j * kOzTB + ks * 32);
+              const uint64_t da = oz_desc_add(da0, i * kOzTA + ks * 32);
+              const uint64_t db = oz_desc_add(db0, j * kOzTB + ks * 32);
               const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first write of D_{i+j}: i = 0
               asm volatile(
                   "{\n\t.reg .pred p;\n\t"
@@ -643,6 +651,201 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm_kernel(co
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+// ---- 2-SM variant (tcgen05 cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 64
+// tile. Each CTA loads its 128 rows of the A slices and HALF (32 columns) of the B slices; the
+// leader CTA issues M = 256 MMAs that read A from each CTA's own shared memory and B from both,
+// writing rows 0-127 to the leader's TMEM and 128-255 to the peer's. Per SM and K chunk that is
+// 80 KB of TMA loads and 5 KB of shared-memory operand reads per MMA instead of 96 KB / 6 KB for
+// the one-SM tile, at the same MMA count (B300_MICROARCH: one-SM MMA with both operands in shared
+// memory is limited by the operand reads). Barriers: the leader's full barrier expects both CTAs'
+// bytes (both CTAs' TMA loads signal it); the leader's MMA commits release the stage and the
+// accumulators in both CTAs; both CTAs' epilogues hand the TMEM back to the leader.
+constexpr int kOz2TB = (kOzBN / 2) * kOzBK;  // one CTA's half of the B tile (32 columns)
+template <int NS> constexpr int oz2_stage_bytes() { return NS * (kOzTA + kOz2TB); }
+template <int NS>
+constexpr size_t oz2_smem() { return (size_t)kOzStages * oz2_stage_bytes<NS>() + (2 * kOzStages + 2) * 8 + 16 + 1024; }
+
+__device__ __forceinline__ unsigned oz2_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void oz2_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NS>
+static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                             const __grid_constant__ CUtensorMap tmB,
+                                                                             const OzakiParams p) {
+  extern __shared__ __align__(1024) unsigned char oz_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kOzStages * oz2_stage_bytes<NS>());
+  uint64_t* empty = full + kOzStages;
+  uint64_t* tfull = empty + kOzStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const unsigned crank = oz2_rank();
+  const bool leader = crank == 0;
+  const int KT = p.K / kOzBK;
+  const int mt = (p.M + 2 * kOzBM - 1) / (2 * kOzBM), nt = p.N / kOzBN;  // pair tiles: 256 x 64
+  const int ntiles = mt * nt;
+  const int pfirst = (int)(blockIdx.x >> 1), pstep = (int)(gridDim.x >> 1);
+  auto tile_origin = [&](int tt, int& m0, int& n0) {  // this CTA's 128 rows of the pair tile
+    const int a = p.m_fast ? tt % mt : tt / nt, b = p.m_fast ? tt / mt : tt % nt;
+    m0 = a * 2 * kOzBM + (int)crank * kOzBM;
+    n0 = b * kOzBN;
+  };
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (t == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      oz_mbar_init(full + s, 1);
+      oz_mbar_init(empty + s, 1);
+    }
+    oz_mbar_init(tfull, 1);
+    oz_mbar_init(tempty, 2 * 256);  // both CTAs' epilogue threads
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  oz2_cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+  if (warp == 8 && lane == 0) {  // TMA producer (both CTAs)
+    int g = 0;
+    for (int tt = pfirst; tt < ntiles; tt += pstep) {
+      int m0, n0;
+      tile_origin(tt, m0, n0);
+      const int nb0 = n0 + (int)crank * (kOzBN / 2);
+      for (int kt = 0; kt < KT; ++kt, ++g) {
+        const int st = g % kOzStages;
+        if (g >= kOzStages) oz_mbar_wait(empty + st, ((g / kOzStages) - 1) & 1);
+        unsigned char* sb = sm + st * oz2_stage_bytes<NS>();
+        const uint32_t fb = oz_u32(full + st) & kPeerMask;
+        if (leader)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)),
+                       "r"(2 * oz2_stage_bytes<NS>())
+                       : "memory");
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+          asm volatile(
+              "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                  oz_u32(sb + i * kOzTA)),
+              "l"(&tmA), "r"(kt * kOzBK), "r"(m0), "r"(i), "r"(fb)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                  oz_u32(sb + NS * kOzTA + i * kOz2TB)),
+              "l"(&tmB), "r"(kt * kOzBK), "r"(nb0), "r"(i), "r"(fb)
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == 9 && lane == 0 && leader) {  // MMA issuer: the leader CTA only
+    const uint32_t idesc =
+        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) | ((uint32_t)((2 * kOzBM) >> 4) << 24);
+    const uint16_t mask = 0x3;
+    int g = 0, it = 0;
+    for (int tt = pfirst; tt < ntiles; tt += pstep, ++it) {
+      if (it > 0) oz_mbar_wait(tempty, (it - 1) & 1);  // both CTAs read the previous accumulators
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kt = 0; kt < KT; ++kt, ++g) {
+        const int st = g % kOzStages;
+        oz_mbar_wait(full + st, (g / kOzStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const unsigned char* sb = sm + st * oz2_stage_bytes<NS>();
+        const uint64_t da0 = oz_desc(sb), db0 = oz_desc(sb + NS * kOzTA);
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+#pragma unroll
+          for (int j = 0; j < NS - i; ++j)
+#pragma unroll
+            for (int ks = 0; ks < kOzBK / 32; ++ks) {
+              const uint64_t da = oz_desc_add(da0, i * kOzTA + ks * 32);
+              const uint64_t db = oz_desc_add(db0, j * kOz2TB + ks * 32);
+              const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)((i + j) * kOzBN)),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                  : "memory");
+            }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         oz_u32(empty + st)),
+                     "h"(mask)
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                       oz_u32(tfull)),
+                   "h"(mask)
+                   : "memory");
+    }
+  }
+  if (warp < 8) {  // epilogue (both CTAs): this CTA's 128 rows of the pair tile
+    constexpr int kEC = kOzBN / 2;
+    const int q = warp & 3, ch = (warp >> 2) * kEC;
+    const uint32_t te = oz_u32(tempty) & kPeerMask;
+    int it = 0;
+    for (int tt = pfirst; tt < ntiles; tt += pstep, ++it) {
+      int m0, n0;
+      tile_origin(tt, m0, n0);
+      oz_mbar_wait(tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double acc[kEC];
+#pragma unroll
+      for (int c = 0; c < kEC; ++c) acc[c] = 0.0;
+#pragma unroll
+      for (int d = NS - 1; d >= 0; --d) {
+        const double sc = ldexp(1.0, -7 * (d + 2));
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * kOzBN + ch);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], sc, acc[c]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(te) : "memory");
+      const int row = m0 + q * 32 + lane;
+      if (row < p.M) {
+        const int er = p.ea[row];
+        const int lp = __ffs(p.panel) - 1;
+        double* crow = p.C + (size_t)row * p.panel;
+        const size_t sstride = (size_t)p.M * p.panel;
+#pragma unroll
+        for (int c = 0; c < kEC; c += 2) {
+          const int col = n0 + ch + c;
+          FFS_CHECK(col + 1 < p.N);
+          const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
+          const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;
+          const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
+          const double s1 = (b1 > 0 && b1 < 2047) ? __longlong_as_double((long long)b1 << 52) : ldexp(1.0, er + e2.y);
+          *reinterpret_cast<double2*>(crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1))) =
+              make_double2(acc[c] * s0, acc[c + 1] * s1);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  oz2_cluster_sync();  // neither CTA leaves while the other may still signal it or read its TMEM
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
 // x = 2^e sum_i q_i 2^{-7(i+1)}, |q_i| <= 127 (frexp exponent: |x 2^-e| < 1); q_i of element k of

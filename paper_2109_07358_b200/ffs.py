@@ -27,6 +27,7 @@ OPTIONS = {
     "cluster": 6,           # 1: L >= 2048 on cluster kernels (default); 0: one CTA per sample
     "graph": 7,             # 1: block-step launches replayed as a CUDA graph (default)
     "force_generic": 8,     # 1: every shape on the per-sample warp/CTA-owner kernel
+    "gemm_2sm": 9,          # 1: the 8-slice Ozaki GEMM as tcgen05 CTA pairs (default)
 }
 
 EXPORTED = (

@@ -246,14 +246,16 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
 
 
 # Lockstep-dense path schedules (ffs_abi.cu launch_dense): several batches with a ragged last one,
-# all-GEMM (theta 0) with each GEMM (Ozaki 8 slices = default, Ozaki 7, DMMA), all-gathered
-# (theta 1), the default hybrid, with and without the CUDA-graph driver; real and complex.
+# all-GEMM (theta 0) with each GEMM (Ozaki 8 slices as CTA pairs = default, Ozaki 8 slices one CTA
+# per tile, Ozaki 7, DMMA), all-gathered (theta 1), the default hybrid, with and without the
+# CUDA-graph driver; real and complex.
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("opts", [{"dense_batch": 16}, {"dense_theta": 0}, {"dense_theta": 1},
                                   {"dense_batch": 7, "dense_theta": 0.5},
                                   {"dense_theta": 0, "dense_gemm": 7},
                                   {"dense_theta": 0, "dense_gemm": 0},
-                                  {"dense_theta": 0.3, "graph": 0}])
+                                  {"dense_theta": 0.3, "graph": 0},
+                                  {"dense_theta": 0, "gemm_2sm": 0}])
 def test_dense_path_schedules(opts, cplx):
     ffs = _ffs()
     for k, v in opts.items():
