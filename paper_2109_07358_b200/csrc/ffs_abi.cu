@@ -640,7 +640,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   double theta;
   if (d.gemm == 0) theta = cx ? 0.6 : 0.3;
   else if (d.gemm == 7) theta = cx ? 0.35 : 0.15;
-  else theta = cx ? 0.4 : 0.2;
+  else theta = cx ? 0.3 : 0.15;  // 8 slices, 2-SM GEMM (tools/theta_scan.py: C5 0.1-0.25, C4 0.25-0.4)
   const double ot = ffsh::option(FFS_OPT_DENSE_THETA);
   if (ot >= 0.0) theta = ot;
   d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
