@@ -201,10 +201,24 @@ typedef enum {
   FFS_OPT_FORCE_GENERIC = 8,    /* 1: every shape on the per-sample warp/CTA-owner kernel (testing) */
   FFS_OPT_GEMM_2SM = 9,         /* 1 (default): the 8-slice Ozaki GEMM runs as CTA pairs (tcgen05
                                    cta_group::2, 256 x 64 tiles); 0: one CTA per 128 x 64 tile */
-  FFS_OPT_LAST = 9
+  FFS_OPT_GRAM_DRAW = 10,       /* 1 (default): the draws of a GEMM block step run one warp per sample on
+                                   the tile Gram matrices of the panel (ffs_gram.cuh);
+                                   0: the cluster step kernel (panel in registers) */
+  FFS_OPT_GRAM_KAPPA = 11,      /* Gram draws: recompute the tile totals directly from the panel when
+                                   T < bound / kappa (cancellation guard); default 1e3 */
+  FFS_OPT_DENSE_MIN_L = 12,     /* smallest L on the block-step paths (default 2048); below 2048 every
+                                   block of a full sampling call takes the GEMM + Gram draws */
+  FFS_OPT_DENSE_MIN_N = 13,     /* smallest N on the block-step paths (default 256) */
+  FFS_OPT_LAST = 13
 } ffs_option;
 int ffs_set_option(int option, double value);
 double ffs_get_option(int option);
+
+/* Diagnostics of the Gram draws (process-wide device counters, read synchronously): out[0] =
+ * draws taken by ffs_gram_draw_kernel since the last reset, out[1] = draws whose tile totals were
+ * recomputed directly from the panel (cancellation guard / degenerate totals). reset != 0 zeroes
+ * the counters after reading. Returns FFS_OK or FFS_ECUDA. */
+int ffs_gram_counters(unsigned long long out[2], int reset);
 
 /* Thread-local message for the last non-OK return on this thread ("" if none). */
 const char* ffs_last_error(void);

@@ -22,6 +22,7 @@
 #include "ffs_warp_kernel.cuh"
 #include "ffs_cluster_kernel.cuh"
 #include "ffs_dense.cuh"
+#include "ffs_gram.cuh"
 #include "ffs_lens.cuh"
 #include "ffs_observe.cuh"
 #include "ffs_metro.cuh"
@@ -50,6 +51,10 @@ double default_option(int o) {
     case FFS_OPT_GRAPH: return 1.0;
     case FFS_OPT_FORCE_GENERIC: return 0.0;
     case FFS_OPT_GEMM_2SM: return 1.0;
+    case FFS_OPT_GRAM_DRAW: return 1.0;
+    case FFS_OPT_GRAM_KAPPA: return 1e3;
+    case FFS_OPT_DENSE_MIN_L: return 2048.0;
+    case FFS_OPT_DENSE_MIN_N: return 256.0;
     default: return 0.0;
   }
 }
@@ -557,7 +562,12 @@ bool dense_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   // marginals (N' < N) take the same step + batched-GJ kernels with every block contracted gathered
   // (no GEMM): C5 marginal 201 -> 180 ms against the per-sample cluster kernel
   const bool marg = ffsh::option(FFS_OPT_LARGE_L_MARGINAL) != 0.0 && Np < N;
-  return (Np == N || marg) && N >= 256 && N % 2 == 0 && cluster_eligible(L, dtype);
+  if (ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0 || ffsh::option(FFS_OPT_CLUSTER) == 0.0) return false;
+  const int64_t maxL = dtype == FFS_C128 ? kMaxLClusterComplex : kMaxLClusterReal;
+  // below L = 2048 (no cluster kernel): full sampling only, every block by GEMM + Gram draws
+  const int64_t minL = Np == N && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0
+                           ? std::min<int64_t>(2048, (int64_t)ffsh::option(FFS_OPT_DENSE_MIN_L)) : 2048;
+  return (Np == N || marg) && N >= (int64_t)ffsh::option(FFS_OPT_DENSE_MIN_N) && N % 2 == 0 && L >= minL && L <= maxL;
 }
 
 struct DensePlan {
@@ -566,9 +576,18 @@ struct DensePlan {
   int gemm;            // 8 / 7: Ozaki-emulated GEMM with that many slices; 0: DMMA GEMM; -1: no GEMM
   int Kp;              // GEMM K (f N) padded to the Ozaki K chunk
   size_t ws_oza, ws_ea, ws_ozb, ws_eb;
-  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, total;
+  size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, ws_g, total;
   int k_gather;        // blocks with k0 < k_gather contract the gathered columns in the step kernel
+  int gram;            // 1: GEMM blocks draw on the tile Gram matrices (ffs_gram.cuh)
+  int Rt;              // rows per Gram tile (32 tiles cover L)
 };
+
+template <typename T>
+const void* gram_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_gram_kernel<T, 8>); }
+template <typename T>
+const void* gram_draw_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_gram_draw_kernel<T, 8>); }
+template <typename T>
+constexpr size_t gram_draw_smem() { return ffsk::kGramWarps * sizeof(ffsk::GramWarpSmem<T, 8>); }
 
 // GJ tile: real 128 columns (two per thread, 16-byte W accesses), complex 64
 template <typename T> constexpr int gj_tj() { return sizeof(T) == 8 ? 128 : 64; }
@@ -641,8 +660,12 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   if (d.gemm == 0) theta = cx ? 0.6 : 0.3;
   else if (d.gemm == 7) theta = cx ? 0.35 : 0.15;
   else theta = cx ? 0.3 : 0.15;  // 8 slices, 2-SM GEMM (tools/theta_scan.py: C5 0.1-0.25, C4 0.25-0.4)
+  // with the Gram draws a GEMM block costs less than a cluster-step block sooner (C5 0.1: 691.9 ms,
+  // 0.15: 693.5, 0: 712.9; C4 0.2: 701.5, 0.3: 702.9, 0: 753.3)
+  if (d.gemm == 8 && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0) theta = cx ? 0.2 : 0.1;
   const double ot = ffsh::option(FFS_OPT_DENSE_THETA);
   if (ot >= 0.0) theta = ot;
+  if (L < 2048) theta = 0.0;
   d.k_gather = no_gemm ? (int)Np : (int)(theta * (double)Np);
   d.ws_ut = d.k_gather > 0 ? align_up((size_t)N * d.c.Lpt * es) : 0;
   const int64_t fK = (cx ? 2 : 1) * N;
@@ -660,7 +683,15 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   } else if (ns == 7) {
     if (int rc = ffsh::ensure_max_smem(ozaki_fn<7>())) return rc;
   }
-  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut + d.ws_oza + d.ws_ea + d.ws_ozb + d.ws_eb;
+  // Gram draws for the GEMM blocks: 32 row tiles of Rt rows (a multiple of 32) per sample
+  d.gram = (!no_gemm && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0) ? 1 : 0;
+  d.Rt = (int)(((L + 31) / 32 + 31) / 32 * 32);
+  if (d.Rt / 32 > ffsk::kGramMaxRl) d.gram = 0;
+  d.ws_g = d.gram ? align_up((size_t)d.S * (cx ? ffsk::GramIdx<cplx>::NE : ffsk::GramIdx<double>::NE) * 32 * 8) : 0;
+  if (d.gram)
+    if (int rc = ffsh::ensure_max_smem(cx ? gram_draw_fn<cplx>() : gram_draw_fn<double>())) return rc;
+  d.total = d.ws_perm + d.ws_y + d.ws_p + d.ws_w + d.ws_ch + d.ws_row + d.ws_ut + d.ws_oza + d.ws_ea + d.ws_ozb + d.ws_eb +
+            d.ws_g;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "block-step path: N'=%lld too large for the GJ tile", (long long)Np);
   return ffsh::ensure_max_smem(cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>());
@@ -706,6 +737,10 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
   int* oz_ea = reinterpret_cast<int*>(ozb0 + d.ws_oza);
   int8_t* ozb = reinterpret_cast<int8_t*>(ozb0 + d.ws_oza + d.ws_ea);
   int* oz_eb = reinterpret_cast<int*>(ozb0 + d.ws_oza + d.ws_ea + d.ws_ozb);
+  double* Gg = reinterpret_cast<double*>(ozb0 + d.ws_oza + d.ws_ea + d.ws_ozb + d.ws_eb);
+  unsigned long long* gstats = nullptr;
+  if (d.gram && cudaGetSymbolAddress(reinterpret_cast<void**>(&gstats), ffsk::g_gram_stats) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaGetSymbolAddress failed");
   const int ns = d.gemm > 0 ? d.gemm : 0;
   const int64_t f = cx ? 2 : 1;
   const int64_t oz_ncols = f * d.ldY;
@@ -829,10 +864,44 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
         }
       }
       c.k0 = k0;
-      void* args[] = {&c};
-      cudaError_t e = launch_cluster_kernel(d.c.fn, d.c.CS, (int)(nh * d.c.CS), d.c.threads, d.c.smem, stream, args);
-      if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
-      ++ffsh::launches();
+      cudaError_t e;
+      if (!c.gather && d.gram) {
+        // draws on the tile Gram matrices of the GEMM panel: one pass over P, then a warp per sample
+        ffsk::GramParams g{};
+        g.Pd = Pd;
+        g.G = Gg;
+        g.chosen_g = ch;
+        g.uniforms = uniforms;
+        g.positions = positions;
+        g.flags = flags;
+        g.rowg = rowg;
+        g.L = (int)L;
+        g.Lpt = d.c.Lpt;
+        g.Np = (int)Np;
+        g.Sb = (int)nh;
+        g.Rt = d.Rt;
+        g.k0 = k0;
+        g.base = base;
+        g.S0 = S0;
+        g.S = S > 0 ? S : 0;
+        g.trace = S > 0 ? trace : nullptr;
+        g.stats = gstats;
+        g.kappa_max = ffsh::option(FFS_OPT_GRAM_KAPPA);
+        void* gargs[] = {&g};
+        e = cudaLaunchKernel(cx ? gram_fn<cplx>() : gram_fn<double>(), dim3((unsigned)((nh * 32 + 7) / 8)), dim3(256), gargs, 0,
+                             stream);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "gram launch failed: %s", cudaGetErrorString(e));
+        e = cudaLaunchKernel(cx ? gram_draw_fn<cplx>() : gram_draw_fn<double>(),
+                             dim3((unsigned)((nh + ffsk::kGramWarps - 1) / ffsk::kGramWarps)), dim3(32 * ffsk::kGramWarps), gargs,
+                             cx ? gram_draw_smem<cplx>() : gram_draw_smem<double>(), stream);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "gram draw launch failed: %s", cudaGetErrorString(e));
+        ffsh::launches() += 2;
+      } else {
+        void* args[] = {&c};
+        e = launch_cluster_kernel(d.c.fn, d.c.CS, (int)(nh * d.c.CS), d.c.threads, d.c.smem, stream, args);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
+        ++ffsh::launches();
+      }
       if (k0 + B < Np) {
         q.k0 = k0;
         const int nc = (int)Np - k0 - B;
@@ -1651,6 +1720,18 @@ int ffs_set_option(int opt, double value) {
 double ffs_get_option(int opt) {
   if (opt <= 0 || opt >= ffsh::kNumOpts || opt > FFS_OPT_LAST) return NAN;
   return ffsh::option(opt);
+}
+
+int ffs_gram_counters(unsigned long long out[2], int reset) {
+  ffsh::clear_error();
+  if (!out) return fail(FFS_EINVAL, "null out");
+  if (cudaMemcpyFromSymbol(out, ffsk::g_gram_stats, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(FFS_ECUDA, "cudaMemcpyFromSymbol failed");
+  if (reset) {
+    const unsigned long long z[2] = {0, 0};
+    if (cudaMemcpyToSymbol(ffsk::g_gram_stats, z, sizeof(z)) != cudaSuccess) return fail(FFS_ECUDA, "cudaMemcpyToSymbol failed");
+  }
+  return FFS_OK;
 }
 
 const char* ffs_last_error(void) { return ffsh::g_err; }

@@ -1,0 +1,335 @@
+// Tile-Gram marginal path: real U, small N' (marginals), any L.
+//
+// Step k of a sample has the weights w_k(x) = |u_x^T h'|^2 with h' = (-A^{-1} V[X,k]; 1) on the
+// permuted columns m_0..m_k (Eq. 3), i.e. w_k(x) = (sum_{q<=k}
+// U[x, m_q] d_q)^2 with d = h'. The total of w_k over a TILE of rows is the quadratic form
+//   sum_{x in tile} w_k(x) = d^T K_tile[m, m] d,     K_tile = U_tile^T U_tile  (N x N),
+// and K_tile does not depend on the sample: it is computed ONCE per call for 32 row tiles
+// (ffs_tile_gram_u_kernel, L N^2 / 2 FMAs in all), after which a sample's step costs 32 forms of
+// (k+1)(k+2)/2 terms plus the rows of the one tile the threshold u T falls in -- O(32 N'^3 / 6 +
+// N'^2 L / 64) per sample instead of L N'^2 / 2. One warp owns a sample: lane t evaluates tile t,
+// a warp scan finds the crossing tile, its L/32 rows are scanned for x_k, and the coefficient
+// matrix C = A^{-1} V[X, later columns] takes a rank-1 Gauss-Jordan update. The gathered Gram
+// entries K_t[m_q][m_q'] of a sample accumulate in a per-warp slot of the workspace
+// ([entry][lane], coalesced) -- only column k is gathered at step k.
+// Conditioning: sum_t K_t = U^T U = 1, so by Cauchy-Schwarz sum_t |d^T K_t d| terms are bounded by
+// (k+1) |d|^2 = (k+1) T: the forms never cancel by more than a factor N' (no guard needed).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ffs_kernel.cuh"
+
+namespace ffsk {
+
+// K[t][a][b] = sum_{x in tile t} U[x][a] U[x][b], tiles of Rt rows; grid (b tiles, a tiles, 32),
+// 256 threads, 64 x 64 outputs per CTA (4 x 4 per thread); only a-tile <= b-tile is computed, the
+// mirror image is written with it
+static __global__ void __launch_bounds__(256) ffs_tile_gram_u_kernel(const double* __restrict__ U, double* __restrict__ K,
+                                                                    int L, int N, int Rt) {
+  if (blockIdx.y > blockIdx.x) return;
+  __shared__ double As[16][64 + 4], Bs[16][64 + 4];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int a0 = blockIdx.y * 64, b0 = blockIdx.x * 64, tile = blockIdx.z;
+  const int x0 = tile * Rt, x1 = min(L, x0 + Rt);
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int xc = x0; xc < x1; xc += 16) {
+    __syncthreads();
+    for (int idx = t; idx < 16 * 64; idx += 256) {
+      const int k = idx >> 6, c = idx & 63, x = xc + k;
+      As[k][c] = (x < x1 && a0 + c < N) ? U[(size_t)x * N + a0 + c] : 0.0;
+      Bs[k][c] = (x < x1 && b0 + c < N) ? U[(size_t)x * N + b0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+  }
+  double* Kt = K + (size_t)tile * N * N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = a0 + ty * 4 + i, b = b0 + tx * 4 + j;
+      if (a < N && b < N) {
+        Kt[(size_t)a * N + b] = acc[i][j];
+        if (blockIdx.y != blockIdx.x) Kt[(size_t)b * N + a] = acc[i][j];
+      }
+    }
+}
+
+struct KMargParams {
+  const double* U;         // [L][N]
+  const double* Ut;        // [N][Lpt] transposed, zero-padded, Lpt = 1024 Rl
+  const double* K;         // [32][N][N] tile Gram matrices of U
+  const int32_t* permg;    // [M][Np]
+  const double* uniforms;  // [M][2Np]
+  int32_t* positions;      // [M][Np]
+  int32_t* flags;          // [M] or null
+  double* Gs;              // [slots][Np(Np+1)/2][32] gathered Gram entries of the slot's sample
+  double* Cw;              // [slots][Np][Np] coefficient matrix
+  int L, N, Np, Lpt, Rl;   // Rl rows per lane of a tile (tile = 32 Rl rows)
+  int64_t M, S0, S;
+  double* trace;           // [S][Np][L] or null
+  size_t warp_smem;        // bytes of shared memory per warp
+};
+
+constexpr int kKmWarps = 4;
+
+__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np) {
+  return align16(sizeof(int) * Np) + 3 * align16(sizeof(double) * Np) + align16(sizeof(uint32_t) * ((L + 31) / 32));
+}
+
+template <int RLMAX>
+static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const KMargParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = p.L, N = p.N, Np = p.Np, Rl = p.Rl, Lpt = p.Lpt;
+  const int Rt = 32 * Rl;
+  unsigned char* wb = smem + (size_t)warp * p.warp_smem;
+  int* m = reinterpret_cast<int*>(wb);
+  double* dvec = reinterpret_cast<double*>(wb + align16(sizeof(int) * Np));
+  double* urow = dvec + align16(sizeof(double) * Np) / 8;
+  double* vrow = urow + align16(sizeof(double) * Np) / 8;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(vrow + align16(sizeof(double) * Np) / 8);
+  const int nwords = (L + 31) >> 5;
+  const int64_t slot = (int64_t)blockIdx.x * kKmWarps + warp;
+  const int64_t nslots = (int64_t)gridDim.x * kKmWarps;
+  double* Gs = p.Gs + (size_t)slot * ((size_t)Np * (Np + 1) / 2) * 32 + lane;
+  double* C = p.Cw + (size_t)slot * Np * Np;
+  const double* Kt = p.K + (size_t)lane * N * N;  // lane = tile
+
+  auto scan = [&](double v) -> double {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += y;
+    }
+    return v;
+  };
+
+  for (int64_t i = slot; i < p.M; i += nslots) {
+    const double* usel = p.uniforms + i * 2 * (int64_t)Np + Np;
+    __syncwarp();
+    for (int j = lane; j < Np; j += 32) {
+      m[j] = p.permg[i * Np + j];
+      FFS_CHECK(m[j] >= 0 && m[j] < N);
+    }
+    for (int j = lane; j < nwords; j += 32) bits[j] = 0u;
+    __syncwarp();
+    int flag = 0;
+    const bool traced = p.trace != nullptr && (uint64_t)(i - p.S0) < (uint64_t)p.S;
+
+    for (int r = 0; r < Np; ++r) {
+      const double u = usel[r];
+      const int mr = m[r];
+      // ---- tile totals: f = d^T K_t[m, m] d with d = (dvec[0:r], 1); column r is gathered now
+      double f;
+      {
+        double* gcol = Gs + (size_t)(r * (r + 1) / 2) * 32;
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+        int q = 0;
+        for (; q + 4 <= r; q += 4) {
+          const double v0 = Kt[(size_t)m[q] * N + mr], v1 = Kt[(size_t)m[q + 1] * N + mr];
+          const double v2 = Kt[(size_t)m[q + 2] * N + mr], v3 = Kt[(size_t)m[q + 3] * N + mr];
+          gcol[(size_t)q * 32] = v0;
+          gcol[(size_t)(q + 1) * 32] = v1;
+          gcol[(size_t)(q + 2) * 32] = v2;
+          gcol[(size_t)(q + 3) * 32] = v3;
+          c0 = fma(v0, dvec[q], c0);
+          c1 = fma(v1, dvec[q + 1], c1);
+          c2 = fma(v2, dvec[q + 2], c2);
+          c3 = fma(v3, dvec[q + 3], c3);
+        }
+        for (; q < r; ++q) {
+          const double v0 = Kt[(size_t)m[q] * N + mr];
+          gcol[(size_t)q * 32] = v0;
+          c0 = fma(v0, dvec[q], c0);
+        }
+        const double grr = Kt[(size_t)mr * N + mr];
+        gcol[(size_t)r * 32] = grr;
+        f = fma(2.0, (c0 + c1) + (c2 + c3), grr);
+        const double* g = Gs;
+        for (int qp = 0; qp < r; ++qp) {
+          const double dq = dvec[qp];
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int q2 = 0;
+          for (; q2 + 4 <= qp; q2 += 4) {
+            a0 = fma(g[(size_t)q2 * 32], dvec[q2], a0);
+            a1 = fma(g[(size_t)(q2 + 1) * 32], dvec[q2 + 1], a1);
+            a2 = fma(g[(size_t)(q2 + 2) * 32], dvec[q2 + 2], a2);
+            a3 = fma(g[(size_t)(q2 + 3) * 32], dvec[q2 + 3], a3);
+          }
+          for (; q2 < qp; ++q2) a0 = fma(g[(size_t)q2 * 32], dvec[q2], a0);
+          const double gd = g[(size_t)qp * 32];
+          f = fma(dq, fma(gd, dq, 2.0 * ((a0 + a1) + (a2 + a3))), f);
+          g += (size_t)(qp + 1) * 32;
+        }
+      }
+      if (f < 0.0) f = 0.0;
+      const double incl = scan(f);
+      const double Ttot = __shfl_sync(0xffffffffu, incl, 31);
+      const bool ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
+      int xsel = -1;
+      if (ok) {
+        const double thr = u * Ttot;
+        const unsigned cross = __ballot_sync(0xffffffffu, f > 0.0 && incl > thr);
+        const unsigned posl = __ballot_sync(0xffffffffu, f > 0.0);
+        const int tau = cross ? __ffs(cross) - 1 : 31 - __clz(posl);
+        double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) ex = 0.0;
+        const double thr_in = thr - __shfl_sync(0xffffffffu, ex, tau);
+        // ---- rows of tile tau: s(x) = sum_q U[x, m_q] d_q, Rl consecutive rows per lane
+        const int xb = (tau * 32 + lane) * Rl;
+        double s[RLMAX];
+        {
+          const double* col = p.Ut + (size_t)mr * Lpt + xb;
+#pragma unroll
+          for (int j = 0; j < RLMAX; ++j) s[j] = j < Rl ? col[j] : 0.0;
+        }
+        for (int q = 0; q < r; ++q) {
+          const double dq = dvec[q];
+          const double* col = p.Ut + (size_t)m[q] * Lpt + xb;
+#pragma unroll
+          for (int j = 0; j < RLMAX; ++j)
+            if (j < Rl) s[j] = fma(col[j], dq, s[j]);
+        }
+        double c[RLMAX];
+        double run = 0.0;
+#pragma unroll
+        for (int j = 0; j < RLMAX; ++j) {
+          const int x = xb + j;
+          if (j < Rl && x < L && !((bits[x >> 5] >> (x & 31)) & 1u)) run = fma(s[j], s[j], run);
+          c[j] = run;
+        }
+        const double incl2 = scan(run);
+        double ex2 = __shfl_up_sync(0xffffffffu, incl2, 1);
+        if (lane == 0) ex2 = 0.0;
+        // the in-tile threshold as the same fraction of the tile's row-wise total that thr_in is
+        // of the tile's Gram total (they differ by rounding); u T >= T after rounding: last row
+        const double Dt = __shfl_sync(0xffffffffu, incl2, 31);
+        const double thr2 = cross ? (thr_in / __shfl_sync(0xffffffffu, f, tau)) * Dt : 1.7976931348623157e308;
+        const double tp = thr2 - ex2;
+        int rs = RLMAX, rl = -1;
+#pragma unroll
+        for (int j = RLMAX - 1; j >= 0; --j) {
+          const double prev = j > 0 ? c[j - 1] : 0.0;
+          if (c[j] > prev && c[j] > tp) rs = j;
+        }
+#pragma unroll
+        for (int j = 0; j < RLMAX; ++j) {
+          const double prev = j > 0 ? c[j - 1] : 0.0;
+          if (c[j] > prev) rl = j;
+        }
+        const unsigned b1 = __ballot_sync(0xffffffffu, rs < RLMAX);
+        if (b1) {
+          const int ln = __ffs(b1) - 1;
+          xsel = (tau * 32 + ln) * Rl + __shfl_sync(0xffffffffu, rs, ln);
+        } else {
+          const unsigned b2 = __ballot_sync(0xffffffffu, rl >= 0);
+          if (b2) {
+            const int ln = 31 - __clz(b2);
+            xsel = (tau * 32 + ln) * Rl + __shfl_sync(0xffffffffu, rl, ln);
+          }
+        }
+        if (xsel < 0) {
+          // the tile's Gram total was rounding noise (no row of it has weight): the site of the
+          // largest weight over all rows (deterministic; never observed in the tests)
+          double best = -1.0;
+          int bx = -1;
+          for (int x = lane; x < L; x += 32) {
+            if ((bits[x >> 5] >> (x & 31)) & 1u) continue;
+            double sx = p.Ut[(size_t)mr * Lpt + x];
+            for (int q = 0; q < r; ++q) sx = fma(p.Ut[(size_t)m[q] * Lpt + x], dvec[q], sx);
+            if (sx * sx > best) {
+              best = sx * sx;
+              bx = x;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+            if (ob > best || (ob == best && ox >= 0 && (bx < 0 || ox < bx))) {
+              best = ob;
+              bx = ox;
+            }
+          }
+          xsel = bx;
+        }
+      }
+      if (xsel < 0) {
+        // T not finite / positive (flag bit0): the smallest site not drawn yet
+        flag |= 1;
+        for (int wbase = 0; wbase < nwords && xsel < 0; wbase += 32) {
+          const int wi = wbase + lane;
+          uint32_t word = wi < nwords ? bits[wi] : 0xffffffffu;
+          if (wi == nwords - 1 && (L & 31)) word |= 0xffffffffu << (L & 31);
+          const unsigned bf = __ballot_sync(0xffffffffu, word != 0xffffffffu);
+          if (bf) {
+            const int ln = __ffs(bf) - 1;
+            const uint32_t wsel = __shfl_sync(0xffffffffu, word, ln);
+            xsel = (wbase + ln) * 32 + (__ffs(~wsel) - 1);
+          }
+        }
+      }
+      FFS_CHECK(xsel >= 0 && xsel < L);
+      if (traced) {
+        const double inv = ok ? 1.0 / Ttot : 0.0;
+        double* tr = p.trace + ((i - p.S0) * Np + r) * (int64_t)L;
+        for (int x = lane; x < L; x += 32) {
+          double sx = p.Ut[(size_t)mr * Lpt + x];
+          for (int q = 0; q < r; ++q) sx = fma(p.Ut[(size_t)m[q] * Lpt + x], dvec[q], sx);
+          tr[x] = ((bits[x >> 5] >> (x & 31)) & 1u) ? 0.0 : sx * sx * inv;
+        }
+      }
+      // ---- pivot row v[c] = V[x, c] - V[x, 0:r] C[0:r, c] (c >= r) and the Gauss-Jordan update
+      for (int q = lane; q < Np; q += 32) urow[q] = p.U[(size_t)xsel * N + m[q]];
+      __syncwarp();
+      for (int cc = r + lane; cc < Np; cc += 32) {
+        double a0 = urow[cc], a1 = 0.0;
+        int q = 0;
+        for (; q + 2 <= r; q += 2) {
+          a0 = fma(-urow[q], C[(size_t)q * Np + cc], a0);
+          a1 = fma(-urow[q + 1], C[(size_t)(q + 1) * Np + cc], a1);
+        }
+        if (q < r) a0 = fma(-urow[q], C[(size_t)q * Np + cc], a0);
+        vrow[cc] = a0 + a1;
+      }
+      __syncwarp();
+      const double piv = vrow[r];
+      if (ok && piv * piv < 1e-12 * Ttot) flag |= 2;
+      const double ip = fast_rcp(piv);
+      for (int cc = r + 1 + lane; cc < Np; cc += 32) {
+        const double z = vrow[cc] * ip;
+        for (int q = 0; q < r; ++q) C[(size_t)q * Np + cc] = fma(-C[(size_t)q * Np + r], z, C[(size_t)q * Np + cc]);
+        C[(size_t)r * Np + cc] = z;
+      }
+      if (lane == 0) {
+        bits[xsel >> 5] |= 1u << (xsel & 31);
+        p.positions[i * Np + r] = xsel;
+      }
+      __syncwarp();
+      // d of the next step: -(column r+1 of C)
+      if (r + 1 < Np)
+        for (int q = lane; q <= r; q += 32) dvec[q] = -C[(size_t)q * Np + r + 1];
+      __syncwarp();
+    }
+    if (lane == 0 && p.flags != nullptr) p.flags[i] = flag;
+  }
+}
+
+}  // namespace ffsk

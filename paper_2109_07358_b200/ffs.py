@@ -28,6 +28,10 @@ OPTIONS = {
     "graph": 7,             # 1: block-step launches replayed as a CUDA graph (default)
     "force_generic": 8,     # 1: every shape on the per-sample warp/CTA-owner kernel
     "gemm_2sm": 9,          # 1: the 8-slice Ozaki GEMM as tcgen05 CTA pairs (default)
+    "gram_draw": 10,        # 1: GEMM block steps draw on the tile Gram matrices (default)
+    "gram_kappa": 11,       # cancellation guard of the Gram draws (default 1e3)
+    "dense_min_l": 12,      # smallest L on the block-step paths (default 2048)
+    "dense_min_n": 13,      # smallest N on the block-step paths (default 256)
 }
 
 EXPORTED = (
@@ -52,6 +56,7 @@ EXPORTED = (
     "ffs_gutzwiller_reweight",
     "ffs_set_option",
     "ffs_get_option",
+    "ffs_gram_counters",
     "ffs_last_error",
 )
 
@@ -109,6 +114,7 @@ def load(build_if_missing: bool = True):
     L.ffs_set_option.argtypes = [ci, ctypes.c_double]
     L.ffs_get_option.argtypes = [ci]
     L.ffs_get_option.restype = ctypes.c_double
+    L.ffs_gram_counters.argtypes = [vp, ci]
     L.ffs_last_error.restype = ctypes.c_char_p
     _lib = L
     return L
@@ -151,6 +157,13 @@ def ffs_profile_enable(on: bool = True) -> None:
 
 def ffs_last_kernel_ms() -> float:
     return float(load().ffs_last_kernel_ms())
+
+
+def ffs_gram_counters(reset: bool = False):
+    """ffs_gram_counters (include/ffs.h): (draws, direct recomputations) of the Gram draw kernel."""
+    out = (ctypes.c_ulonglong * 2)()
+    _check(load().ffs_gram_counters(ctypes.cast(out, ctypes.c_void_p), 1 if reset else 0))
+    return int(out[0]), int(out[1])
 
 
 def set_option(name: str, value: float) -> None:

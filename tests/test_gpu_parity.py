@@ -255,7 +255,11 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
                                   {"dense_theta": 0, "dense_gemm": 7},
                                   {"dense_theta": 0, "dense_gemm": 0},
                                   {"dense_theta": 0.3, "graph": 0},
-                                  {"dense_theta": 0, "gemm_2sm": 0}])
+                                  {"dense_theta": 0, "gemm_2sm": 0},
+                                  {"dense_theta": 0, "gram_draw": 0},
+                                  {"dense_batch": 9, "dense_theta": 0.25, "gram_draw": 0},
+                                  {"dense_theta": 0, "gram_kappa": 0},
+                                  {"dense_theta": 0, "gram_kappa": 1e30}])
 def test_dense_path_schedules(opts, cplx):
     ffs = _ffs()
     for k, v in opts.items():
@@ -271,6 +275,33 @@ def test_dense_path_schedules(opts, cplx):
     assert (gflags == 0).all()
     _, rw = ref.weights(U, uni[M - 2:], Np=N)
     assert compare_weights(gw, rw, gpos[M - 2:], rpos[M - 2:]) <= WEIGHT_TOL
+
+
+# Gram draws (ffs_gram.cuh) at the ends of [0, 1): u = 0 takes the first site with w > 0, u = 1 - 2^-53
+# the last one -- exactly, through the tile totals (Gram forms or direct sums) and the in-tile scan.
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("kappa", [1e3, 0.0])
+@pytest.mark.parametrize("useL", [0.0, 1.0 - 2.0 ** -53])
+def test_gram_draw_extreme_uniforms(useL, kappa, cplx):
+    ffs = _ffs()
+    ffs.set_option("dense_theta", 0)
+    ffs.set_option("gram_kappa", kappa)
+    L, N = 2100, 258
+    U = inputs.random_orthonormal(L, N, 911 + int(cplx), complex_=cplx)
+    M = 12
+    uni = inputs.uniforms(M, N, 31)
+    uni[:, N:] = useL
+    ffs.ffs_gram_counters(reset=True)
+    gpos, gfl, _ = run_gpu(U, uni, N)
+    draws, direct = ffs.ffs_gram_counters()
+    assert draws == M * N
+    # kappa = 0 sends every draw through the direct tile totals; at these extreme uniforms the
+    # pivots are the first / last sites with any weight (often tiny: large |d|), so the guard also
+    # fires often with the default kappa
+    assert direct >= draws if kappa == 0.0 else direct <= draws
+    rpos = ref.sample(U, uni, Np=N)
+    assert (gpos == rpos).all(), np.argwhere(gpos != rpos)[:5]
+    assert not (gfl & 1).any()
 
 
 def test_graph_replay_matches_direct_launches():
