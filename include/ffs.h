@@ -205,11 +205,14 @@ typedef enum {
                                    the tile Gram matrices of the panel (ffs_gram.cuh);
                                    0: the cluster step kernel (panel in registers) */
   FFS_OPT_GRAM_KAPPA = 11,      /* Gram draws: recompute the tile totals directly from the panel when
-                                   T < bound / kappa (cancellation guard); default 1e3 */
+                                   T < bound / kappa (cancellation guard); default 1e4 */
   FFS_OPT_DENSE_MIN_L = 12,     /* smallest L on the block-step paths (default 2048); below 2048 every
                                    block of a full sampling call takes the GEMM + Gram draws */
   FFS_OPT_DENSE_MIN_N = 13,     /* smallest N on the block-step paths (default 256) */
-  FFS_OPT_LAST = 13
+  FFS_OPT_TILE_GRAM = 14,       /* 1 (default): real U, N' <= 64 and 64 N' <= 3 L (L > 256): the tile-Gram
+                                   path (ffs_kmarg.cuh): tile totals as quadratic forms of the 32 tile
+                                   Gram matrices of U, one warp per sample; 0: the panel kernels */
+  FFS_OPT_LAST = 14
 } ffs_option;
 int ffs_set_option(int option, double value);
 double ffs_get_option(int option);

@@ -23,6 +23,7 @@
 #include "ffs_cluster_kernel.cuh"
 #include "ffs_dense.cuh"
 #include "ffs_gram.cuh"
+#include "ffs_kmarg.cuh"
 #include "ffs_lens.cuh"
 #include "ffs_observe.cuh"
 #include "ffs_metro.cuh"
@@ -52,9 +53,10 @@ double default_option(int o) {
     case FFS_OPT_FORCE_GENERIC: return 0.0;
     case FFS_OPT_GEMM_2SM: return 1.0;
     case FFS_OPT_GRAM_DRAW: return 1.0;
-    case FFS_OPT_GRAM_KAPPA: return 1e3;
+    case FFS_OPT_GRAM_KAPPA: return 1e4;
     case FFS_OPT_DENSE_MIN_L: return 2048.0;
     case FFS_OPT_DENSE_MIN_N: return 256.0;
+    case FFS_OPT_TILE_GRAM: return 1.0;
     default: return 0.0;
   }
 }
@@ -406,6 +408,116 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
   void* args[] = {&p};
   ffsh::prof_begin(stream);
   cudaError_t e = cudaLaunchKernel(w.fn, dim3(w.grid), dim3(32 * w.warps), args, w.smem, stream);
+  if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
+  ffsh::prof_end(stream);
+  ++ffsh::launches();
+  return FFS_OK;
+}
+
+// ------------------------------------------------------------------ tile-Gram path (small N')
+// Real U, N' <= 128, 64 N' <= 3 L: the 32 tile Gram matrices of U once per call, then one warp per
+// sample (ffs_kmarg.cuh). Workspace: [perm | U^T | K | Gs slots | C slots].
+struct KmPlan {
+  const void* fn;
+  int Rl, Lpt, grid, warps;
+  bool gs_smem, c_smem;
+  size_t warp_smem, smem, ws_perm, ws_ut, ws_k, ws_gs, ws_c, total;
+};
+
+bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
+  if (ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0 || ffsh::option(FFS_OPT_TILE_GRAM) == 0.0) return false;
+  return dtype == FFS_F64 && Np <= ffsk::kKmMaxNp && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
+}
+
+template <int WARPS>
+const void* km_fn(int Rl) {
+  return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<1, WARPS>)
+       : Rl <= 4 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<4, WARPS>)
+                 : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<16, WARPS>);
+}
+
+int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k) {
+  k.Rl = (int)((L + 1023) / 1024);
+  k.Lpt = 1024 * k.Rl;
+  // small N': the sample's Gram entries (N'(N'+1)/2 x 256 B) and C live in shared memory, one
+  // 6-warp CTA per SM; otherwise in per-warp slots of the workspace (at most ~1 GB of slots)
+  const size_t gs_slot = (size_t)Np * (Np + 1) / 2 * 32 * 8;
+  // (option value 3: Gram entries in shared memory when they fit, 6 warps per SM -- measured slower
+  // than 24 warps per SM reading them from L2: C3 marginal 1.8 vs 1.0 ms)
+  k.gs_smem = ffsh::option(FFS_OPT_TILE_GRAM) == 3.0 &&
+              6 * ffsk::kmarg_warp_smem((int)L, (int)Np, true, true) + ffsk::align16((size_t)Np * (Np + 1)) <= kMaxSmem;
+  k.c_smem = k.gs_smem || Np <= 32;
+  k.warps = k.gs_smem ? 6 : 4;
+  k.fn = k.gs_smem ? km_fn<6>(k.Rl) : km_fn<4>(k.Rl);
+  k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.gs_smem, k.c_smem);
+  k.smem = k.warps * k.warp_smem + ffsk::align16((size_t)Np * (Np + 1));  // + the entry/pair table
+  if (k.smem > kMaxSmem) return fail(FFS_EINVAL, "tile-Gram path: shared memory %zu too large", k.smem);
+  if (int rc = ffsh::ensure_max_smem(k.fn)) return rc;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, 32 * k.warps, k.smem) != cudaSuccess || per_sm < 1)
+    return fail(FFS_EINVAL, "tile-Gram kernel does not fit on an SM (smem=%zu)", k.smem);
+  const int sms = ffsh::sm_count(ffsh::device());
+  int64_t ctas = (int64_t)std::min(per_sm, 6) * sms;
+  if (!k.gs_smem) ctas = std::min<int64_t>(ctas, std::max<int64_t>(sms, (int64_t)((1024u << 20) / gs_slot) / k.warps));
+  ctas = std::min<int64_t>(ctas, (M + k.warps - 1) / k.warps);
+  k.grid = (int)std::max<int64_t>(1, ctas);
+  const size_t slots = (size_t)k.grid * k.warps;
+  k.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
+  k.ws_ut = align_up((size_t)N * k.Lpt * 8);
+  k.ws_k = align_up((size_t)32 * N * N * 8);
+  k.ws_gs = k.gs_smem ? 0 : align_up(slots * gs_slot);
+  k.ws_c = k.c_smem ? 0 : align_up(slots * (size_t)Np * Np * 8);
+  k.total = k.ws_perm + k.ws_ut + k.ws_k + k.ws_gs + k.ws_c;
+  return FFS_OK;
+}
+
+PlanCache<KmPlan> g_km_plans;
+int make_km_plan(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k) {
+  return g_km_plans.get(plan_key(4, L, N, Np, M, FFS_F64), k,
+                        [&](KmPlan& p) { return make_km_plan_uncached(L, N, Np, M, p); });
+}
+
+void launch_transpose(const void* U, double* Ut, int64_t L, int64_t N, int Lpt, int dtype, cudaStream_t s);
+
+int launch_kmarg(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, const double* uniforms, int32_t* positions,
+                 int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S, double* trace) {
+  KmPlan k;
+  int rc = make_km_plan(L, N, Np, M, k);
+  if (rc != FFS_OK) return rc;
+  if (!ws || ws_bytes < k.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, k.total);
+  if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
+  char* w = static_cast<char*>(ws);
+  int32_t* perm = reinterpret_cast<int32_t*>(w);
+  double* Ut = reinterpret_cast<double*>(w + k.ws_perm);
+  double* K = reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut);
+  ffsh::prof_begin(stream);
+  launch_transpose(U, Ut, L, N, k.Lpt, FFS_F64, stream);
+  const dim3 kg((unsigned)((N + 63) / 64), (unsigned)((N + 63) / 64), 32);
+  ffsk::ffs_tile_gram_u_kernel<<<kg, 256, 0, stream>>>(static_cast<const double*>(U), K, (int)L, (int)N, 32 * k.Rl);
+  ++ffsh::launches();
+  if (int rc2 = launch_permute(uniforms, 2 * Np, perm, M, N, Np, stream)) return rc2;
+  ffsk::KMargParams p{};
+  p.U = static_cast<const double*>(U);
+  p.Ut = Ut;
+  p.K = K;
+  p.permg = perm;
+  p.uniforms = uniforms;
+  p.positions = positions;
+  p.flags = flags;
+  p.Gs = k.gs_smem ? nullptr : reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut + k.ws_k);
+  p.Cw = k.c_smem ? nullptr : reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut + k.ws_k + k.ws_gs);
+  p.L = (int)L;
+  p.N = (int)N;
+  p.Np = (int)Np;
+  p.Lpt = k.Lpt;
+  p.Rl = k.Rl;
+  p.M = M;
+  p.S0 = S0;
+  p.S = S > 0 ? S : 0;
+  p.trace = S > 0 ? trace : nullptr;
+  p.warp_smem = k.warp_smem;
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchKernel(k.fn, dim3(k.grid), dim3(32 * k.warps), args, k.smem, stream);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));
   ffsh::prof_end(stream);
   ++ffsh::launches();
@@ -1072,6 +1184,8 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   int rc;
   if (warp_eligible(L, N, Np, dtype))
     rc = launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
+  else if (kmarg_eligible(L, N, Np, dtype))
+    rc = launch_kmarg(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
   else if (dense_eligible(L, N, Np, dtype))
     rc = launch_dense(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
   else if (cluster_eligible(L, dtype))
@@ -1091,6 +1205,10 @@ size_t workspace_bytes(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
   if (warp_eligible(L, N, Np, dtype)) {
     WarpPlan w;
     return make_warp_plan(L, N, Np, M, w) == FFS_OK ? w.ws_perm : 0;
+  }
+  if (kmarg_eligible(L, N, Np, dtype)) {
+    KmPlan k;
+    return make_km_plan(L, N, Np, M, k) == FFS_OK ? k.total : 0;
   }
   if (dense_eligible(L, N, Np, dtype)) {
     DensePlan d;

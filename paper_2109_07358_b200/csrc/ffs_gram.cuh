@@ -18,7 +18,7 @@
 // per draw, half of it in cluster barriers).
 //
 // Rounding: the quadratic form cancels when |d| is large (a small in-block pivot). Its absolute
-// error is bounded by ~eps sum_e |coef_e| |G_e| =: eps * bound; when T < bound / kappa_max the
+// error is bounded by ~eps (sum_q |d_q| sqrt(G[q][q]))^2 =: eps * bound; when T < bound / kappa_max the
 // warp recomputes the 32 tile totals directly from the panel rows (exact to summation rounding)
 // before it selects -- so the CDF the draw uses is within ~36 eps kappa_max T of the exact one,
 // inside the 1e-9 tie window of reading Q10. Rows already drawn weigh exactly 0 (bitmap /
@@ -162,6 +162,11 @@ static __global__ void __launch_bounds__(32 * kGramWarps) ffs_gram_draw_kernel(c
     if (lane < B) sm.Pinv[lane] = S::zero();
   }
   __syncwarp();
+  // sqrt(G[q][q]) of this lane's tile: the rounding scale of the forms (|G[q][q']| <= sg[q] sg[q'], and
+  // the accumulated entries carry errors of that size)
+  double sg[B];
+#pragma unroll
+  for (int q = 0; q < B; ++q) sg[q] = sqrt(fmax(sm.Gs[kD == 1 ? q * (q + 1) / 2 + q : q * q][lane], 0.0));
   int xsv[B];
 #pragma unroll
   for (int q = 0; q < B; ++q) xsv[q] = -1;
@@ -198,14 +203,15 @@ static __global__ void __launch_bounds__(32 * kGramWarps) ffs_gram_draw_kernel(c
       }
       __syncwarp();
       // ---- tile totals f (lane = tile) and their rounding scale
-      double f = 0.0, bd = 0.0;
+      double f = 0.0;
 #pragma unroll
-      for (int e = 0; e < GI::count(r); ++e) {
-        const double c = sm.coef[e], g = sm.Gs[e][lane];
-        f = fma(c, g, f);
-        bd = fma(fabs(c), fabs(g), bd);
-      }
+      for (int e = 0; e < GI::count(r); ++e) f = fma(sm.coef[e], sm.Gs[e][lane], f);
       if (f < 0.0) f = 0.0;
+      // bound of sum |d_q||d_q'||G[q][q']| for this tile: (sum_q |d_q| sqrt(G[q][q]))^2
+      double bd = sg[r];
+#pragma unroll
+      for (int q = 0; q < r; ++q) bd = fma(sqrt(S::abs2(dn[q])), sg[q], bd);
+      bd *= bd;
 
       auto masked = [&](int x) -> bool {
         bool m = ((ch[x >> 5] >> (x & 31)) & 1u) != 0u;
@@ -254,6 +260,10 @@ static __global__ void __launch_bounds__(32 * kGramWarps) ffs_gram_draw_kernel(c
           // tile totals from the panel rows themselves, in row order
           double sum = 0.0;
           const int x1 = min(L, (lane + 1) * Rt);
+          // the tile's rows into L2 first (no registers held): the dependent batches below then
+          // pay an L2 instead of a DRAM round trip each
+          for (int x = lane * Rt; x < x1; x += 128 / (int)(sizeof(T) * B))
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(Ps + (size_t)x * B));
           for (int x = lane * Rt; x < x1; x += 4) {
             double w4[4];
 #pragma unroll

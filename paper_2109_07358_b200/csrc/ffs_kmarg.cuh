@@ -9,9 +9,9 @@
 // (k+1)(k+2)/2 terms plus the rows of the one tile the threshold u T falls in -- O(32 N'^3 / 6 +
 // N'^2 L / 64) per sample instead of L N'^2 / 2. One warp owns a sample: lane t evaluates tile t,
 // a warp scan finds the crossing tile, its L/32 rows are scanned for x_k, and the coefficient
-// matrix C = A^{-1} V[X, later columns] takes a rank-1 Gauss-Jordan update. The gathered Gram
-// entries K_t[m_q][m_q'] of a sample accumulate in a per-warp slot of the workspace
-// ([entry][lane], coalesced) -- only column k is gathered at step k.
+// matrix C = A^{-1} V[X, later columns] takes a rank-1 Gauss-Jordan update. The Gram entries
+// K_t[m_q][m_q'] of a sample are gathered once, into shared memory ([entry][lane]) when
+// N'(N'+1)/2 x 256 B fits (N' <= ~18), else into a per-warp slot of the workspace.
 // Conditioning: sum_t K_t = U^T U = 1, so by Cauchy-Schwarz sum_t |d^T K_t d| terms are bounded by
 // (k+1) |d|^2 = (k+1) T: the forms never cancel by more than a factor N' (no guard needed).
 #pragma once
@@ -79,38 +79,64 @@ struct KMargParams {
   const double* uniforms;  // [M][2Np]
   int32_t* positions;      // [M][Np]
   int32_t* flags;          // [M] or null
-  double* Gs;              // [slots][Np(Np+1)/2][32] gathered Gram entries of the slot's sample
-  double* Cw;              // [slots][Np][Np] coefficient matrix
+  double* Gs;              // [slots][Np(Np+1)/2][32] gathered Gram entries (null: in shared memory)
+  double* Cw;              // [slots][Np][Np] coefficient matrix (null: in shared memory)
   int L, N, Np, Lpt, Rl;   // Rl rows per lane of a tile (tile = 32 Rl rows)
   int64_t M, S0, S;
   double* trace;           // [S][Np][L] or null
   size_t warp_smem;        // bytes of shared memory per warp
 };
 
-constexpr int kKmWarps = 4;
+constexpr int kKmMaxNp = 64;
 
-__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np) {
-  return align16(sizeof(int) * Np) + 3 * align16(sizeof(double) * Np) + align16(sizeof(uint32_t) * ((L + 31) / 32));
+// per-warp shared memory: m, selection uniforms, d, U[x_k, m], pivot row, coefficients of the form,
+// the drawn-row bitmap, and (small N') the gathered Gram entries and C
+__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np, bool gs_smem, bool c_smem) {
+  const size_t ne = (size_t)Np * (Np + 1) / 2;
+  return align16(sizeof(int) * Np) + 4 * align16(sizeof(double) * Np) + align16(sizeof(double) * ne) +
+         align16(sizeof(uint32_t) * ((L + 31) / 32)) + (gs_smem ? ne * 32 * sizeof(double) : 0) +
+         (c_smem ? align16(sizeof(double) * Np * Np) : 0);
 }
 
-template <int RLMAX>
-static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const KMargParams p) {
+template <int RLMAX, int WARPS>
+static __global__ void __launch_bounds__(32 * WARPS) ffs_kmarg_kernel(const KMargParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.L, N = p.N, Np = p.Np, Rl = p.Rl, Lpt = p.Lpt;
   const int Rt = 32 * Rl;
+  const int ne_all = Np * (Np + 1) / 2;
   unsigned char* wb = smem + (size_t)warp * p.warp_smem;
+  const size_t dsz = align16(sizeof(double) * Np);
   int* m = reinterpret_cast<int*>(wb);
-  double* dvec = reinterpret_cast<double*>(wb + align16(sizeof(int) * Np));
-  double* urow = dvec + align16(sizeof(double) * Np) / 8;
-  double* vrow = urow + align16(sizeof(double) * Np) / 8;
-  uint32_t* bits = reinterpret_cast<uint32_t*>(vrow + align16(sizeof(double) * Np) / 8);
+  double* uselv = reinterpret_cast<double*>(wb + align16(sizeof(int) * Np));
+  double* dvec = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(uselv) + dsz);
+  double* urow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(dvec) + dsz);
+  double* vrow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(urow) + dsz);
+  double* coef = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(vrow) + dsz);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(coef) + align16(sizeof(double) * ne_all));
+  unsigned char* extra = reinterpret_cast<unsigned char*>(bits) + align16(sizeof(uint32_t) * ((L + 31) / 32));
   const int nwords = (L + 31) >> 5;
-  const int64_t slot = (int64_t)blockIdx.x * kKmWarps + warp;
-  const int64_t nslots = (int64_t)gridDim.x * kKmWarps;
-  double* Gs = p.Gs + (size_t)slot * ((size_t)Np * (Np + 1) / 2) * 32 + lane;
-  double* C = p.Cw + (size_t)slot * Np * Np;
+  const int64_t slot = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t nslots = (int64_t)gridDim.x * WARPS;
+  // this lane's column of the gathered Gram entries, [entry][lane]; C [Np][Np]
+  double* Gs;
+  if (p.Gs != nullptr) {
+    Gs = p.Gs + (size_t)slot * ne_all * 32 + lane;
+  } else {
+    Gs = reinterpret_cast<double*>(extra) + lane;
+    extra += (size_t)ne_all * 32 * sizeof(double);
+  }
+  double* C = p.Cw != nullptr ? p.Cw + (size_t)slot * Np * Np : reinterpret_cast<double*>(extra);
   const double* Kt = p.K + (size_t)lane * N * N;  // lane = tile
+  // entry e <-> (q, q'), q <= q', e = q'(q'+1)/2 + q: one table per CTA
+  uint16_t* pairs = reinterpret_cast<uint16_t*>(smem + (size_t)WARPS * p.warp_smem);
+  for (int e = threadIdx.x; e < ne_all; e += blockDim.x) {
+    int qp = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while ((qp + 1) * (qp + 2) / 2 <= e) ++qp;
+    while (qp * (qp + 1) / 2 > e) --qp;
+    pairs[e] = (uint16_t)((e - qp * (qp + 1) / 2) | (qp << 8));
+  }
+  __syncthreads();
 
   auto scan = [&](double v) -> double {
 #pragma unroll
@@ -122,69 +148,106 @@ static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const K
   };
 
   for (int64_t i = slot; i < p.M; i += nslots) {
-    const double* usel = p.uniforms + i * 2 * (int64_t)Np + Np;
     __syncwarp();
     for (int j = lane; j < Np; j += 32) {
       m[j] = p.permg[i * Np + j];
       FFS_CHECK(m[j] >= 0 && m[j] < N);
+      uselv[j] = p.uniforms[i * 2 * (int64_t)Np + Np + j];
     }
     for (int j = lane; j < nwords; j += 32) bits[j] = 0u;
     __syncwarp();
+    // ---- the sample's Gram entries G[q][q'] = K_t[m_q][m_q'] (q <= q'), gathered once (16 in flight)
+    for (int e0 = 0; e0 < ne_all; e0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const unsigned pr = pairs[min(e0 + j, ne_all - 1)];
+        v[j] = Kt[(size_t)m[pr & 255u] * N + m[pr >> 8]];
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (e0 + j < ne_all) Gs[(size_t)(e0 + j) * 32] = v[j];
+    }
     int flag = 0;
     const bool traced = p.trace != nullptr && (uint64_t)(i - p.S0) < (uint64_t)p.S;
 
     for (int r = 0; r < Np; ++r) {
-      const double u = usel[r];
+      const double u = uselv[r];
       const int mr = m[r];
-      // ---- tile totals: f = d^T K_t[m, m] d with d = (dvec[0:r], 1); column r is gathered now
+      const int ne = (r + 1) * (r + 2) / 2;
+      // ---- coefficients of the form d^T G d, d = (dvec[0:r], 1): column q' by lane q' (mod 32)
+      for (int qp = lane; qp <= r; qp += 32) {
+        const double dq = qp == r ? 1.0 : dvec[qp];
+        double* cc = coef + qp * (qp + 1) / 2;
+        for (int q = 0; q < qp; ++q) cc[q] = 2.0 * dq * dvec[q];
+        cc[qp] = dq * dq;
+      }
+      __syncwarp();
+      // ---- tile totals f (lane = tile)
       double f;
       {
-        double* gcol = Gs + (size_t)(r * (r + 1) / 2) * 32;
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-        int q = 0;
-        for (; q + 4 <= r; q += 4) {
-          const double v0 = Kt[(size_t)m[q] * N + mr], v1 = Kt[(size_t)m[q + 1] * N + mr];
-          const double v2 = Kt[(size_t)m[q + 2] * N + mr], v3 = Kt[(size_t)m[q + 3] * N + mr];
-          gcol[(size_t)q * 32] = v0;
-          gcol[(size_t)(q + 1) * 32] = v1;
-          gcol[(size_t)(q + 2) * 32] = v2;
-          gcol[(size_t)(q + 3) * 32] = v3;
-          c0 = fma(v0, dvec[q], c0);
-          c1 = fma(v1, dvec[q + 1], c1);
-          c2 = fma(v2, dvec[q + 2], c2);
-          c3 = fma(v3, dvec[q + 3], c3);
+        double a[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = 0.0;
+        int e = 0;
+        for (; e + 32 <= ne; e += 32) {
+          double g[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) g[j] = Gs[(size_t)(e + j) * 32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) a[j & 7] = fma(g[j], coef[e + j], a[j & 7]);
         }
-        for (; q < r; ++q) {
-          const double v0 = Kt[(size_t)m[q] * N + mr];
-          gcol[(size_t)q * 32] = v0;
-          c0 = fma(v0, dvec[q], c0);
+        if (e + 16 <= ne) {
+          double g[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) g[j] = Gs[(size_t)(e + j) * 32];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) a[j & 7] = fma(g[j], coef[e + j], a[j & 7]);
+          e += 16;
         }
-        const double grr = Kt[(size_t)mr * N + mr];
-        gcol[(size_t)r * 32] = grr;
-        f = fma(2.0, (c0 + c1) + (c2 + c3), grr);
-        const double* g = Gs;
-        for (int qp = 0; qp < r; ++qp) {
-          const double dq = dvec[qp];
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          int q2 = 0;
-          for (; q2 + 4 <= qp; q2 += 4) {
-            a0 = fma(g[(size_t)q2 * 32], dvec[q2], a0);
-            a1 = fma(g[(size_t)(q2 + 1) * 32], dvec[q2 + 1], a1);
-            a2 = fma(g[(size_t)(q2 + 2) * 32], dvec[q2 + 2], a2);
-            a3 = fma(g[(size_t)(q2 + 3) * 32], dvec[q2 + 3], a3);
-          }
-          for (; q2 < qp; ++q2) a0 = fma(g[(size_t)q2 * 32], dvec[q2], a0);
-          const double gd = g[(size_t)qp * 32];
-          f = fma(dq, fma(gd, dq, 2.0 * ((a0 + a1) + (a2 + a3))), f);
-          g += (size_t)(qp + 1) * 32;
+        if (e < ne) {  // the last < 16 entries, loaded together
+          double g[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) g[j] = Gs[(size_t)min(e + j, ne - 1) * 32];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (e + j < ne) a[j & 7] = fma(g[j], coef[e + j], a[j & 7]);
+          e = ne;
         }
+        double at = 0.0;
+        for (; e < ne; ++e) at = fma(Gs[(size_t)e * 32], coef[e], at);
+        f = (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]))) + at;
       }
       if (f < 0.0) f = 0.0;
-      const double incl = scan(f);
-      const double Ttot = __shfl_sync(0xffffffffu, incl, 31);
-      const bool ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
+
+      // s(x) = sum_q U[x, m_q] d_q for one row (fallbacks, trace)
+      auto srow = [&](int x) -> double {
+        double sx = p.Ut[(size_t)mr * Lpt + x];
+        for (int q = 0; q < r; ++q) sx = fma(p.Ut[(size_t)m[q] * Lpt + x], dvec[q], sx);
+        return sx;
+      };
+      auto drawn = [&](int x) -> bool { return ((bits[x >> 5] >> (x & 31)) & 1u) != 0u; };
+
+      double Ttot = 0.0;
+      bool ok = true;
       int xsel = -1;
-      if (ok) {
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        if (attempt == 1) {
+          // the tile totals from the rows themselves (the form of a tile was rounding noise, or T
+          // is degenerate): rare
+          double sum = 0.0;
+          const int x1 = min(L, (lane + 1) * Rt);
+          for (int x = lane * Rt; x < x1; ++x)
+            if (!drawn(x)) {
+              const double sx = srow(x);
+              sum = fma(sx, sx, sum);
+            }
+          f = sum;
+        }
+        const double incl = scan(f);
+        Ttot = __shfl_sync(0xffffffffu, incl, 31);
+        ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
+        if (!ok) continue;
         const double thr = u * Ttot;
         const unsigned cross = __ballot_sync(0xffffffffu, f > 0.0 && incl > thr);
         const unsigned posl = __ballot_sync(0xffffffffu, f > 0.0);
@@ -192,7 +255,7 @@ static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const K
         double ex = __shfl_up_sync(0xffffffffu, incl, 1);
         if (lane == 0) ex = 0.0;
         const double thr_in = thr - __shfl_sync(0xffffffffu, ex, tau);
-        // ---- rows of tile tau: s(x) = sum_q U[x, m_q] d_q, Rl consecutive rows per lane
+        // ---- rows of tile tau, Rl consecutive rows per lane
         const int xb = (tau * 32 + lane) * Rl;
         double s[RLMAX];
         {
@@ -200,26 +263,46 @@ static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const K
 #pragma unroll
           for (int j = 0; j < RLMAX; ++j) s[j] = j < Rl ? col[j] : 0.0;
         }
-        for (int q = 0; q < r; ++q) {
-          const double dq = dvec[q];
-          const double* col = p.Ut + (size_t)m[q] * Lpt + xb;
+        {
+          constexpr int QB = RLMAX == 1 ? 8 : RLMAX <= 4 ? 4 : 2;  // columns in flight
+          int q = 0;
+          for (; q + QB <= r; q += QB) {
+            double cv[QB][RLMAX];
 #pragma unroll
-          for (int j = 0; j < RLMAX; ++j)
-            if (j < Rl) s[j] = fma(col[j], dq, s[j]);
+            for (int b = 0; b < QB; ++b) {
+              const double* col = p.Ut + (size_t)m[q + b] * Lpt + xb;
+#pragma unroll
+              for (int j = 0; j < RLMAX; ++j) cv[b][j] = j < Rl ? col[j] : 0.0;
+            }
+#pragma unroll
+            for (int b = 0; b < QB; ++b) {
+              const double dq = dvec[q + b];
+#pragma unroll
+              for (int j = 0; j < RLMAX; ++j) s[j] = fma(cv[b][j], dq, s[j]);
+            }
+          }
+          for (; q < r; ++q) {
+            const double dq = dvec[q];
+            const double* col = p.Ut + (size_t)m[q] * Lpt + xb;
+#pragma unroll
+            for (int j = 0; j < RLMAX; ++j)
+              if (j < Rl) s[j] = fma(col[j], dq, s[j]);
+          }
         }
         double c[RLMAX];
         double run = 0.0;
 #pragma unroll
         for (int j = 0; j < RLMAX; ++j) {
           const int x = xb + j;
-          if (j < Rl && x < L && !((bits[x >> 5] >> (x & 31)) & 1u)) run = fma(s[j], s[j], run);
+          if (j < Rl && x < L && !drawn(x)) run = fma(s[j], s[j], run);
           c[j] = run;
         }
         const double incl2 = scan(run);
         double ex2 = __shfl_up_sync(0xffffffffu, incl2, 1);
         if (lane == 0) ex2 = 0.0;
         // the in-tile threshold as the same fraction of the tile's row-wise total that thr_in is
-        // of the tile's Gram total (they differ by rounding); u T >= T after rounding: last row
+        // of the tile total used by the tile scan (they differ by rounding); u T >= T after
+        // rounding: the last row with w > 0
         const double Dt = __shfl_sync(0xffffffffu, incl2, 31);
         const double thr2 = cross ? (thr_in / __shfl_sync(0xffffffffu, f, tau)) * Dt : 1.7976931348623157e308;
         const double tp = thr2 - ex2;
@@ -245,31 +328,7 @@ static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const K
             xsel = (tau * 32 + ln) * Rl + __shfl_sync(0xffffffffu, rl, ln);
           }
         }
-        if (xsel < 0) {
-          // the tile's Gram total was rounding noise (no row of it has weight): the site of the
-          // largest weight over all rows (deterministic; never observed in the tests)
-          double best = -1.0;
-          int bx = -1;
-          for (int x = lane; x < L; x += 32) {
-            if ((bits[x >> 5] >> (x & 31)) & 1u) continue;
-            double sx = p.Ut[(size_t)mr * Lpt + x];
-            for (int q = 0; q < r; ++q) sx = fma(p.Ut[(size_t)m[q] * Lpt + x], dvec[q], sx);
-            if (sx * sx > best) {
-              best = sx * sx;
-              bx = x;
-            }
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int ox = __shfl_xor_sync(0xffffffffu, bx, o);
-            if (ob > best || (ob == best && ox >= 0 && (bx < 0 || ox < bx))) {
-              best = ob;
-              bx = ox;
-            }
-          }
-          xsel = bx;
-        }
+        if (xsel >= 0) break;
       }
       if (xsel < 0) {
         // T not finite / positive (flag bit0): the smallest site not drawn yet
@@ -291,23 +350,26 @@ static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const K
         const double inv = ok ? 1.0 / Ttot : 0.0;
         double* tr = p.trace + ((i - p.S0) * Np + r) * (int64_t)L;
         for (int x = lane; x < L; x += 32) {
-          double sx = p.Ut[(size_t)mr * Lpt + x];
-          for (int q = 0; q < r; ++q) sx = fma(p.Ut[(size_t)m[q] * Lpt + x], dvec[q], sx);
-          tr[x] = ((bits[x >> 5] >> (x & 31)) & 1u) ? 0.0 : sx * sx * inv;
+          const double sx = srow(x);
+          tr[x] = drawn(x) ? 0.0 : sx * sx * inv;
         }
       }
       // ---- pivot row v[c] = V[x, c] - V[x, 0:r] C[0:r, c] (c >= r) and the Gauss-Jordan update
       for (int q = lane; q < Np; q += 32) urow[q] = p.U[(size_t)xsel * N + m[q]];
       __syncwarp();
       for (int cc = r + lane; cc < Np; cc += 32) {
-        double a0 = urow[cc], a1 = 0.0;
+        double a0 = urow[cc], a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int q = 0;
-        for (; q + 2 <= r; q += 2) {
-          a0 = fma(-urow[q], C[(size_t)q * Np + cc], a0);
-          a1 = fma(-urow[q + 1], C[(size_t)(q + 1) * Np + cc], a1);
+        for (; q + 4 <= r; q += 4) {
+          const double w0 = C[(size_t)q * Np + cc], w1 = C[(size_t)(q + 1) * Np + cc];
+          const double w2 = C[(size_t)(q + 2) * Np + cc], w3 = C[(size_t)(q + 3) * Np + cc];
+          a0 = fma(-urow[q], w0, a0);
+          a1 = fma(-urow[q + 1], w1, a1);
+          a2 = fma(-urow[q + 2], w2, a2);
+          a3 = fma(-urow[q + 3], w3, a3);
         }
-        if (q < r) a0 = fma(-urow[q], C[(size_t)q * Np + cc], a0);
-        vrow[cc] = a0 + a1;
+        for (; q < r; ++q) a0 = fma(-urow[q], C[(size_t)q * Np + cc], a0);
+        vrow[cc] = (a0 + a1) + (a2 + a3);
       }
       __syncwarp();
       const double piv = vrow[r];
@@ -315,7 +377,18 @@ static __global__ void __launch_bounds__(32 * kKmWarps) ffs_kmarg_kernel(const K
       const double ip = fast_rcp(piv);
       for (int cc = r + 1 + lane; cc < Np; cc += 32) {
         const double z = vrow[cc] * ip;
-        for (int q = 0; q < r; ++q) C[(size_t)q * Np + cc] = fma(-C[(size_t)q * Np + r], z, C[(size_t)q * Np + cc]);
+        int q = 0;
+        for (; q + 4 <= r; q += 4) {
+          double w[4], cr[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            w[j] = C[(size_t)(q + j) * Np + cc];
+            cr[j] = C[(size_t)(q + j) * Np + r];
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) C[(size_t)(q + j) * Np + cc] = fma(-cr[j], z, w[j]);
+        }
+        for (; q < r; ++q) C[(size_t)q * Np + cc] = fma(-C[(size_t)q * Np + r], z, C[(size_t)q * Np + cc]);
         C[(size_t)r * Np + cc] = z;
       }
       if (lane == 0) {

@@ -29,9 +29,10 @@ OPTIONS = {
     "force_generic": 8,     # 1: every shape on the per-sample warp/CTA-owner kernel
     "gemm_2sm": 9,          # 1: the 8-slice Ozaki GEMM as tcgen05 CTA pairs (default)
     "gram_draw": 10,        # 1: GEMM block steps draw on the tile Gram matrices (default)
-    "gram_kappa": 11,       # cancellation guard of the Gram draws (default 1e3)
+    "gram_kappa": 11,       # cancellation guard of the Gram draws (default 1e4)
     "dense_min_l": 12,      # smallest L on the block-step paths (default 2048)
     "dense_min_n": 13,      # smallest N on the block-step paths (default 256)
+    "tile_gram": 14,        # 1: small-N' real shapes on the tile-Gram path (default)
 }
 
 EXPORTED = (

@@ -405,3 +405,59 @@ def test_block_step_odd_marginal(Np):
     assert (gflags == 0).all()
     _, rw = ref.weights(U, uni[M - 2:], Np=Np)
     assert compare_weights(gw, rw, gpos[M - 2:], rpos[M - 2:]) <= WEIGHT_TOL
+
+
+# The tile-Gram path (ffs_kmarg.cuh) takes every real shape with N' <= 64 and 64 N' <= 3 L by
+# default; with the option off the same shapes run on the panel kernels (CTA owner, cluster,
+# block-step), which stay covered here -- including the extreme selection uniforms.
+PANEL_SHAPES = [(1024, 40, 21), (1500, 19, 19), (5000, 11, 11), (9000, 7, 7), (2100, 300, 42), (2100, 300, 19),
+                (2100, 300, 1), (4096, 256, 9)]
+
+
+@pytest.mark.parametrize("L,N,Np", PANEL_SHAPES)
+def test_panel_paths_without_tile_gram(L, N, Np):
+    _ffs().set_option("tile_gram", 0)
+    U = inputs.random_orthonormal(L, N, 31 * L + N)
+    M = 48
+    uni = inputs.uniforms(M, Np, L + N + Np)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=2, trace_S0=M - 2)
+    rpos = ref.sample(U, uni, Np=Np)
+    r = compare_positions(U, uni, gpos, rpos, Np)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    _, rw = ref.weights(U, uni[M - 2:], Np=Np)
+    assert compare_weights(gw, rw, gpos[M - 2:], rpos[M - 2:]) <= WEIGHT_TOL
+    for useL in (0.0, 1.0 - 2.0 ** -53):
+        uni[:, Np:] = useL
+        gpos, gfl, _ = run_gpu(U, uni, Np)
+        assert (gpos == ref.sample(U, uni, Np=Np)).all()
+        assert not (gfl & 1).any()
+
+
+# Tile-Gram path: tile sizes of 1, 3, 4 and 16 rows per lane (L = 1024 .. 16384, ragged last tiles),
+# N' from 1 to 64, full sampling (N' = N) and marginals, many samples per warp slot.
+@pytest.mark.parametrize("L,N,Np", [(600, 20, 20), (1024, 128, 16), (2500, 64, 48), (3000, 300, 57), (4096, 140, 64),
+                                   (16384, 96, 33), (7000, 12, 1)])
+def test_tile_gram_path(L, N, Np):
+    ffs = _ffs()
+    assert ffs.ffs_workspace_bytes(L, N, Np, ffs.FFS_F64, 1) > 32 * N * N * 8  # the tile-Gram plan (holds K)
+    U = inputs.random_orthonormal(L, N, 13 * L + N)
+    M = 3000 if L * Np <= 40000 else 96
+    uni = inputs.uniforms(M, Np, 5 * L + Np)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=2, trace_S0=M - 2)
+    n_ref = min(M, 96)
+    idx = np.array(_spread(M, n_ref))
+    rpos = ref.sample(U, uni[idx], Np=Np)
+    r = compare_positions(U, uni[idx], gpos[idx], rpos, Np)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    assert all(len(set(q)) == Np for q in gpos.tolist())
+    last = np.arange(M - 2, M)
+    rlast, rw = ref.weights(U, uni[last], Np=Np)
+    assert compare_weights(gw, rw, gpos[last], rlast) <= WEIGHT_TOL
+    for useL in (0.0, 1.0 - 2.0 ** -53):
+        uni2 = uni[:32].copy()
+        uni2[:, Np:] = useL
+        gpos2, gfl2, _ = run_gpu(U, uni2, Np)
+        assert (gpos2 == ref.sample(U, uni2, Np=Np)).all()
+        assert not (gfl2 & 1).any()
