@@ -420,8 +420,8 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
 struct KmPlan {
   const void* fn;
   int Rl, Lpt, grid, warps;
-  bool gs_smem, c_smem;
-  size_t warp_smem, smem, ws_perm, ws_ut, ws_k, ws_gs, ws_c, total;
+  bool c_smem, blocked;
+  size_t warp_smem, smem, ws_perm, ws_ut, ws_k, ws_c, total;
 };
 
 bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
@@ -429,27 +429,25 @@ bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   return dtype == FFS_F64 && Np <= ffsk::kKmMaxNp && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
 }
 
-template <int WARPS>
+template <int WARPS, bool BLK>
 const void* km_fn(int Rl) {
-  return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<1, WARPS>)
-       : Rl <= 4 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<4, WARPS>)
-                 : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<16, WARPS>);
+  return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<1, WARPS, BLK>)
+       : Rl <= 4 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<4, WARPS, BLK>)
+                 : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<16, WARPS, BLK>);
 }
 
 int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k) {
   k.Rl = (int)((L + 1023) / 1024);
   k.Lpt = 1024 * k.Rl;
-  // small N': the sample's Gram entries (N'(N'+1)/2 x 256 B) and C live in shared memory, one
-  // 6-warp CTA per SM; otherwise in per-warp slots of the workspace (at most ~1 GB of slots)
-  const size_t gs_slot = (size_t)Np * (Np + 1) / 2 * 32 * 8;
-  // (option value 3: Gram entries in shared memory when they fit, 6 warps per SM -- measured slower
-  // than 24 warps per SM reading them from L2: C3 marginal 1.8 vs 1.0 ms)
-  k.gs_smem = ffsh::option(FFS_OPT_TILE_GRAM) == 3.0 &&
-              6 * ffsk::kmarg_warp_smem((int)L, (int)Np, true, true) + ffsk::align16((size_t)Np * (Np + 1)) <= kMaxSmem;
-  k.c_smem = k.gs_smem || Np <= 32;
-  k.warps = k.gs_smem ? 6 : 4;
-  k.fn = k.gs_smem ? km_fn<6>(k.Rl) : km_fn<4>(k.Rl);
-  k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.gs_smem, k.c_smem);
+  k.c_smem = Np <= 32;  // C [N'][N'] in shared memory (8 KB per warp at most), else a workspace slot per warp
+  k.warps = 4;
+  // N' > 24: blocked evaluation of the forms (K entries read once per block of 8 draws instead of
+  // once per draw: C5 marginal 3.3 instead of 11.7 MB of K rows per sample); option value 2 / 3
+  // forces flat / blocked
+  const double ot = ffsh::option(FFS_OPT_TILE_GRAM);
+  k.blocked = ot == 3.0 || (ot != 2.0 && Np > 24);
+  k.fn = k.blocked ? km_fn<4, true>(k.Rl) : km_fn<4, false>(k.Rl);
+  k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.c_smem, k.blocked);
   k.smem = k.warps * k.warp_smem + ffsk::align16((size_t)Np * (Np + 1));  // + the entry/pair table
   if (k.smem > kMaxSmem) return fail(FFS_EINVAL, "tile-Gram path: shared memory %zu too large", k.smem);
   if (int rc = ffsh::ensure_max_smem(k.fn)) return rc;
@@ -457,17 +455,15 @@ int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, 32 * k.warps, k.smem) != cudaSuccess || per_sm < 1)
     return fail(FFS_EINVAL, "tile-Gram kernel does not fit on an SM (smem=%zu)", k.smem);
   const int sms = ffsh::sm_count(ffsh::device());
-  int64_t ctas = (int64_t)std::min(per_sm, 6) * sms;
-  if (!k.gs_smem) ctas = std::min<int64_t>(ctas, std::max<int64_t>(sms, (int64_t)((1024u << 20) / gs_slot) / k.warps));
+  int64_t ctas = (int64_t)std::min(per_sm, 8) * sms;
   ctas = std::min<int64_t>(ctas, (M + k.warps - 1) / k.warps);
   k.grid = (int)std::max<int64_t>(1, ctas);
   const size_t slots = (size_t)k.grid * k.warps;
   k.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
   k.ws_ut = align_up((size_t)N * k.Lpt * 8);
   k.ws_k = align_up((size_t)32 * N * N * 8);
-  k.ws_gs = k.gs_smem ? 0 : align_up(slots * gs_slot);
   k.ws_c = k.c_smem ? 0 : align_up(slots * (size_t)Np * Np * 8);
-  k.total = k.ws_perm + k.ws_ut + k.ws_k + k.ws_gs + k.ws_c;
+  k.total = k.ws_perm + k.ws_ut + k.ws_k + k.ws_c;
   return FFS_OK;
 }
 
@@ -504,8 +500,7 @@ int launch_kmarg(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, con
   p.uniforms = uniforms;
   p.positions = positions;
   p.flags = flags;
-  p.Gs = k.gs_smem ? nullptr : reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut + k.ws_k);
-  p.Cw = k.c_smem ? nullptr : reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut + k.ws_k + k.ws_gs);
+  p.Cw = k.c_smem ? nullptr : reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut + k.ws_k);
   p.L = (int)L;
   p.N = (int)N;
   p.Np = (int)Np;
@@ -516,6 +511,7 @@ int launch_kmarg(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, con
   p.S = S > 0 ? S : 0;
   p.trace = S > 0 ? trace : nullptr;
   p.warp_smem = k.warp_smem;
+  p.kappa_max = ffsh::option(FFS_OPT_GRAM_KAPPA);
   void* args[] = {&p};
   cudaError_t e = cudaLaunchKernel(k.fn, dim3(k.grid), dim3(32 * k.warps), args, k.smem, stream);
   if (e != cudaSuccess) return fail(FFS_ECUDA, "launch failed: %s", cudaGetErrorString(e));

@@ -9,9 +9,11 @@
 // (k+1)(k+2)/2 terms plus the rows of the one tile the threshold u T falls in -- O(32 N'^3 / 6 +
 // N'^2 L / 64) per sample instead of L N'^2 / 2. One warp owns a sample: lane t evaluates tile t,
 // a warp scan finds the crossing tile, its L/32 rows are scanned for x_k, and the coefficient
-// matrix C = A^{-1} V[X, later columns] takes a rank-1 Gauss-Jordan update. The Gram entries
-// K_t[m_q][m_q'] of a sample are gathered once, into shared memory ([entry][lane]) when
-// N'(N'+1)/2 x 256 B fits (N' <= ~18), else into a per-warp slot of the workspace.
+// matrix C = A^{-1} V[X, later columns] takes a rank-1 Gauss-Jordan update. K is stored TILE-MINOR,
+// K[a][b][t]: the 32 tile values of one entry are 256 contiguous bytes, so the warp's read of a
+// sample's entry K_t[m_q][m_q'] (lane = t) is one coalesced row, straight from the shared K -- no
+// per-sample copy of the gathered Gram matrix is kept (measured: gathering it into a per-warp
+// slot cost 20 % of the instructions and wrote 35 KB per C3 sample back to DRAM).
 // Conditioning: sum_t K_t = U^T U = 1, so by Cauchy-Schwarz sum_t |d^T K_t d| terms are bounded by
 // (k+1) |d|^2 = (k+1) T: the forms never cancel by more than a factor N' (no guard needed).
 #pragma once
@@ -22,7 +24,7 @@
 
 namespace ffsk {
 
-// K[t][a][b] = sum_{x in tile t} U[x][a] U[x][b], tiles of Rt rows; grid (b tiles, a tiles, 32),
+// K[a][b][t] = sum_{x in tile t} U[x][a] U[x][b], tiles of Rt rows; grid (b tiles, a tiles, 32),
 // 256 threads, 64 x 64 outputs per CTA (4 x 4 per thread); only a-tile <= b-tile is computed, the
 // mirror image is written with it
 static __global__ void __launch_bounds__(256) ffs_tile_gram_u_kernel(const double* __restrict__ U, double* __restrict__ K,
@@ -58,15 +60,15 @@ static __global__ void __launch_bounds__(256) ffs_tile_gram_u_kernel(const doubl
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
   }
-  double* Kt = K + (size_t)tile * N * N;
+  double* Kt = K + tile;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int a = a0 + ty * 4 + i, b = b0 + tx * 4 + j;
       if (a < N && b < N) {
-        Kt[(size_t)a * N + b] = acc[i][j];
-        if (blockIdx.y != blockIdx.x) Kt[(size_t)b * N + a] = acc[i][j];
+        Kt[((size_t)a * N + b) * 32] = acc[i][j];
+        if (blockIdx.y != blockIdx.x) Kt[((size_t)b * N + a) * 32] = acc[i][j];
       }
     }
 }
@@ -74,37 +76,41 @@ static __global__ void __launch_bounds__(256) ffs_tile_gram_u_kernel(const doubl
 struct KMargParams {
   const double* U;         // [L][N]
   const double* Ut;        // [N][Lpt] transposed, zero-padded, Lpt = 1024 Rl
-  const double* K;         // [32][N][N] tile Gram matrices of U
+  const double* K;         // [N][N][32] tile Gram matrices of U, tile-minor
   const int32_t* permg;    // [M][Np]
   const double* uniforms;  // [M][2Np]
   int32_t* positions;      // [M][Np]
   int32_t* flags;          // [M] or null
-  double* Gs;              // [slots][Np(Np+1)/2][32] gathered Gram entries (null: in shared memory)
   double* Cw;              // [slots][Np][Np] coefficient matrix (null: in shared memory)
   int L, N, Np, Lpt, Rl;   // Rl rows per lane of a tile (tile = 32 Rl rows)
   int64_t M, S0, S;
   double* trace;           // [S][Np][L] or null
   size_t warp_smem;        // bytes of shared memory per warp
+  double kappa_max;        // blocked forms: cancellation guard (as ffs_gram.cuh)
 };
 
 constexpr int kKmMaxNp = 64;
 
-// per-warp shared memory: m, selection uniforms, d, U[x_k, m], pivot row, coefficients of the form,
-// the drawn-row bitmap, and (small N') the gathered Gram entries and C
-__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np, bool gs_smem, bool c_smem) {
-  const size_t ne = (size_t)Np * (Np + 1) / 2;
-  return align16(sizeof(int) * Np) + 4 * align16(sizeof(double) * Np) + align16(sizeof(double) * ne) +
-         align16(sizeof(uint32_t) * ((L + 31) / 32)) + (gs_smem ? ne * 32 * sizeof(double) : 0) +
-         (c_smem ? align16(sizeof(double) * Np * Np) : 0);
+// per-warp shared memory: m, selection uniforms, d, U[x_k, m], pivot row, the drawn-row bitmap,
+// (small N') C, and for the forms either the offsets of the sample's entries in K + their
+// coefficients (flat evaluation), or the block's D, tile Gram entries and their sqrt-diagonal
+// (blocked evaluation)
+__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np, bool c_smem, bool blocked) {
+  const size_t ne = ((size_t)Np * (Np + 1) / 2 + 15) & ~size_t(15);  // padded to the form's batch of 16
+  const size_t forms = blocked ? sizeof(double) * (48 + (size_t)Np * 8 + 36 * 32 + 8 * 32)
+                               : align16(sizeof(double) * ne) + align16(sizeof(int) * ne);
+  return align16(sizeof(int) * Np) + 4 * align16(sizeof(double) * Np) + forms +
+         align16(sizeof(uint32_t) * ((L + 31) / 32)) + (c_smem ? align16(sizeof(double) * Np * Np) : 0);
 }
 
-template <int RLMAX, int WARPS>
-static __global__ void __launch_bounds__(32 * WARPS) ffs_kmarg_kernel(const KMargParams p) {
+template <int RLMAX, int WARPS, bool BLK>
+static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 1) ffs_kmarg_kernel(const KMargParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.L, N = p.N, Np = p.Np, Rl = p.Rl, Lpt = p.Lpt;
   const int Rt = 32 * Rl;
   const int ne_all = Np * (Np + 1) / 2;
+  const int ne_pad = (ne_all + 15) & ~15;
   unsigned char* wb = smem + (size_t)warp * p.warp_smem;
   const size_t dsz = align16(sizeof(double) * Np);
   int* m = reinterpret_cast<int*>(wb);
@@ -113,21 +119,19 @@ static __global__ void __launch_bounds__(32 * WARPS) ffs_kmarg_kernel(const KMar
   double* urow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(dvec) + dsz);
   double* vrow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(urow) + dsz);
   double* coef = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(vrow) + dsz);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(coef) + align16(sizeof(double) * ne_all));
+  // flat: coef [ne_pad], koff [ne_pad]; blocked: coef [48], Dm [Np][8], gbs [36][32], sgs [8][32]
+  int* koff = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(coef) + align16(sizeof(double) * ne_pad));
+  double* Dm = coef + 48;
+  double* gbs = Dm + (size_t)Np * 8;
+  double* sgs = gbs + 36 * 32;
+  uint32_t* bits = BLK ? reinterpret_cast<uint32_t*>(sgs + 8 * 32)
+                       : reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(koff) + align16(sizeof(int) * ne_pad));
   unsigned char* extra = reinterpret_cast<unsigned char*>(bits) + align16(sizeof(uint32_t) * ((L + 31) / 32));
   const int nwords = (L + 31) >> 5;
   const int64_t slot = (int64_t)blockIdx.x * WARPS + warp;
   const int64_t nslots = (int64_t)gridDim.x * WARPS;
-  // this lane's column of the gathered Gram entries, [entry][lane]; C [Np][Np]
-  double* Gs;
-  if (p.Gs != nullptr) {
-    Gs = p.Gs + (size_t)slot * ne_all * 32 + lane;
-  } else {
-    Gs = reinterpret_cast<double*>(extra) + lane;
-    extra += (size_t)ne_all * 32 * sizeof(double);
-  }
   double* C = p.Cw != nullptr ? p.Cw + (size_t)slot * Np * Np : reinterpret_cast<double*>(extra);
-  const double* Kt = p.K + (size_t)lane * N * N;  // lane = tile
+  const double* Kl = p.K + lane;  // lane = tile
   // entry e <-> (q, q'), q <= q', e = q'(q'+1)/2 + q: one table per CTA
   uint16_t* pairs = reinterpret_cast<uint16_t*>(smem + (size_t)WARPS * p.warp_smem);
   for (int e = threadIdx.x; e < ne_all; e += blockDim.x) {
@@ -156,17 +160,14 @@ static __global__ void __launch_bounds__(32 * WARPS) ffs_kmarg_kernel(const KMar
     }
     for (int j = lane; j < nwords; j += 32) bits[j] = 0u;
     __syncwarp();
-    // ---- the sample's Gram entries G[q][q'] = K_t[m_q][m_q'] (q <= q'), gathered once (16 in flight)
-    for (int e0 = 0; e0 < ne_all; e0 += 16) {
-      double v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const unsigned pr = pairs[min(e0 + j, ne_all - 1)];
-        v[j] = Kt[(size_t)m[pr & 255u] * N + m[pr >> 8]];
+    // ---- offsets of the sample's Gram entries G[q][q'] = K[m_q][m_q'][:] in K (entry e by lane e mod 32)
+    if constexpr (!BLK) {
+      for (int e = lane; e < ne_all; e += 32) {
+        const unsigned pr = pairs[e];
+        koff[e] = (m[pr & 255u] * N + m[pr >> 8]) * 32;
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (e0 + j < ne_all) Gs[(size_t)(e0 + j) * 32] = v[j];
+      for (int e = ne_all + lane; e < ne_pad; e += 32) koff[e] = 0;
+      __syncwarp();
     }
     int flag = 0;
     const bool traced = p.trace != nullptr && (uint64_t)(i - p.S0) < (uint64_t)p.S;
@@ -175,48 +176,142 @@ static __global__ void __launch_bounds__(32 * WARPS) ffs_kmarg_kernel(const KMar
       const double u = uselv[r];
       const int mr = m[r];
       const int ne = (r + 1) * (r + 2) / 2;
-      // ---- coefficients of the form d^T G d, d = (dvec[0:r], 1): column q' by lane q' (mod 32)
-      for (int qp = lane; qp <= r; qp += 32) {
-        const double dq = qp == r ? 1.0 : dvec[qp];
-        double* cc = coef + qp * (qp + 1) / 2;
-        for (int q = 0; q < qp; ++q) cc[q] = 2.0 * dq * dvec[q];
-        cc[qp] = dq * dq;
-      }
-      __syncwarp();
-      // ---- tile totals f (lane = tile)
-      double f;
-      {
-        double a[8];
+      double f = 0.0;
+      if constexpr (BLK) {
+        // ---- blocked evaluation: at a block start k0 the tile Gram matrix of the block's 8 Schur
+        // columns, G_blk = D^T G D with D = (-C[0:k0, k0:k0+8]; I) -- every entry of
+        // G[0:k0+8, 0:k0+8] is read once per BLOCK; the draws of the block then use 36-term forms
+        // with the in-block coefficients d_blk = (-C[k0:k, k]; 1)
+        const int rb = r & 7, k0 = r - rb;
+        if (rb == 0) {
+          const int nb = min(8, Np - k0), na = k0 + nb;
+          for (int idx = lane; idx < na * 8; idx += 32) {
+            const int a = idx >> 3, c = idx & 7;
+            Dm[idx] = a < k0 ? (c < nb ? -C[(size_t)a * Np + k0 + c] : 0.0) : (a - k0 == c ? 1.0 : 0.0);
+          }
+          __syncwarp();
+          double gb[36];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = 0.0;
-        int e = 0;
-        for (; e + 32 <= ne; e += 32) {
-          double g[32];
+          for (int e = 0; e < 36; ++e) gb[e] = 0.0;
+          for (int a = 0; a < na; a += 2) {
+            const int a1 = min(a + 1, na - 1);
+            const double* Ka = Kl + (size_t)m[a] * N * 32;
+            const double* Kb = Kl + (size_t)m[a1] * N * 32;
+            double t0[8], t1[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) g[j] = Gs[(size_t)(e + j) * 32];
+            for (int c = 0; c < 8; ++c) t0[c] = t1[c] = 0.0;
+            for (int b = 0; b < na; b += 8) {
+              double g0[8], g1[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) a[j & 7] = fma(g[j], coef[e + j], a[j & 7]);
+              for (int j = 0; j < 8; ++j) {
+                const int mb = m[min(b + j, na - 1)] * 32;
+                g0[j] = Ka[mb];
+                g1[j] = Kb[mb];
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (b + j < na) {
+                  const double2* dr = reinterpret_cast<const double2*>(Dm + (size_t)(b + j) * 8);
+#pragma unroll
+                  for (int c2 = 0; c2 < 4; ++c2) {
+                    const double2 d2 = dr[c2];
+                    t0[2 * c2] = fma(g0[j], d2.x, t0[2 * c2]);
+                    t0[2 * c2 + 1] = fma(g0[j], d2.y, t0[2 * c2 + 1]);
+                    t1[2 * c2] = fma(g1[j], d2.x, t1[2 * c2]);
+                    t1[2 * c2 + 1] = fma(g1[j], d2.y, t1[2 * c2 + 1]);
+                  }
+                }
+            }
+            const double* da = Dm + (size_t)a * 8;
+            const double* db = Dm + (size_t)a1 * 8;
+            const bool two = a + 1 < na;
+#pragma unroll
+            for (int c1 = 0; c1 < 8; ++c1)
+#pragma unroll
+              for (int c = 0; c <= c1; ++c) {
+                gb[c1 * (c1 + 1) / 2 + c] = fma(da[c], t0[c1], gb[c1 * (c1 + 1) / 2 + c]);
+                if (two) gb[c1 * (c1 + 1) / 2 + c] = fma(db[c], t1[c1], gb[c1 * (c1 + 1) / 2 + c]);
+              }
+          }
+#pragma unroll
+          for (int e = 0; e < 36; ++e) gbs[e * 32 + lane] = gb[e];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) sgs[q * 32 + lane] = sqrt(fmax(gb[q * (q + 1) / 2 + q], 0.0));
         }
-        if (e + 16 <= ne) {
-          double g[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) g[j] = Gs[(size_t)(e + j) * 32];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) a[j & 7] = fma(g[j], coef[e + j], a[j & 7]);
-          e += 16;
+        if (lane <= rb) {
+          const int qp = lane;
+          const double dq = qp == rb ? 1.0 : dvec[k0 + qp];
+          double* cc = coef + qp * (qp + 1) / 2;
+          for (int q = 0; q < qp; ++q) cc[q] = 2.0 * dq * dvec[k0 + q];
+          cc[qp] = dq * dq;
         }
-        if (e < ne) {  // the last < 16 entries, loaded together
-          double g[16];
+        __syncwarp();
+        const int neb = (rb + 1) * (rb + 2) / 2;
+        for (int e = 0; e < neb; ++e) f = fma(coef[e], gbs[e * 32 + lane], f);
+        // cancellation guard (as ffs_gram.cuh): bound (sum_q |d_q| sqrt(G_blk[q][q]))^2 against the total
+        double bd = sgs[rb * 32 + lane];
+        for (int q = 0; q < rb; ++q) bd = fma(fabs(dvec[k0 + q]), sgs[q * 32 + lane], bd);
+        bd *= bd;
+        double ft = f > 0.0 ? f : 0.0;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) g[j] = Gs[(size_t)min(e + j, ne - 1) * 32];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (e + j < ne) a[j & 7] = fma(g[j], coef[e + j], a[j & 7]);
-          e = ne;
+        for (int o = 16; o > 0; o >>= 1) {
+          ft += __shfl_xor_sync(0xffffffffu, ft, o);
+          bd += __shfl_xor_sync(0xffffffffu, bd, o);
         }
-        double at = 0.0;
-        for (; e < ne; ++e) at = fma(Gs[(size_t)e * 32], coef[e], at);
-        f = (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]))) + at;
+        if (!(ft * p.kappa_max >= bd)) {
+          // rare: the form on the ORIGINAL columns (conditioned within a factor N'), entry by entry
+          f = 0.0;
+          for (int qp = 0; qp <= r; ++qp) {
+            const double dq = qp == r ? 1.0 : dvec[qp];
+            const double* Kc = Kl + (size_t)m[qp] * 32;
+            double acc = 0.0;
+            for (int q = 0; q < qp; ++q) acc = fma(Kc[(size_t)m[q] * N * 32], dvec[q], acc);
+            f = fma(dq, fma(Kc[(size_t)m[qp] * N * 32], dq, 2.0 * acc), f);
+          }
+        }
+      } else {
+        // ---- coefficients of the form d^T G d, d = (dvec[0:r], 1): column q' by lane q' (mod 32)
+        for (int qp = lane; qp <= r; qp += 32) {
+          const double dq = qp == r ? 1.0 : dvec[qp];
+          double* cc = coef + qp * (qp + 1) / 2;
+          for (int q = 0; q < qp; ++q) cc[q] = 2.0 * dq * dvec[q];
+          cc[qp] = dq * dq;
+        }
+        __syncwarp();
+        // ---- tile totals f (lane = tile)
+        {
+          double a[8];
+  #pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] = 0.0;
+          // batches of 16 entries: offsets and coefficients by 16-byte broadcast reads, the 16 K rows
+          // in flight together (the arrays are padded to a multiple of 16 entries: coefficient 0)
+          const int ne16 = (ne + 15) & ~15;
+          for (int e = lane + ne; e < ne16; e += 32) coef[e] = 0.0;
+          __syncwarp();
+          for (int e = 0; e < ne16; e += 16) {
+            int ko[16];
+            double g[16], cf[16];
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int4 k4 = *reinterpret_cast<const int4*>(koff + e + 4 * j);
+              ko[4 * j] = k4.x;
+              ko[4 * j + 1] = k4.y;
+              ko[4 * j + 2] = k4.z;
+              ko[4 * j + 3] = k4.w;
+            }
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) g[j] = Kl[ko[j]];
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const double2 c2 = *reinterpret_cast<const double2*>(coef + e + 2 * j);
+              cf[2 * j] = c2.x;
+              cf[2 * j + 1] = c2.y;
+            }
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) a[j & 7] = fma(g[j], cf[j], a[j & 7]);
+          }
+          f = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        }
       }
       if (f < 0.0) f = 0.0;
 

@@ -31,4 +31,4 @@ for th in sys.argv[2:]:
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
-    print(name, th, f"{min(ts):.1f} ms", flush=True)
+    print(name, th, f"{min(ts):.3f} ms", flush=True)
