@@ -141,12 +141,17 @@ def path_of(cfg, Np, cplx):
     if (not cplx) and cfg.L <= 256 and Np <= 48:
         return "ffs_seg_kernel (warp-segment owners)", "f64"
     dt = "c128" if cplx else "f64"
+    if (not cplx) and Np <= 64 and 64 * Np <= 3 * cfg.L and cfg.N <= 2048:
+        return ("tile-Gram path: ffs_tile_gram_u_kernel (32 tile Gram matrices of U, once per call) + "
+                "ffs_kmarg_kernel (warp per sample, tile totals as quadratic forms"
+                + (", blocked)" if Np > 24 else ")")), dt
     if cfg.L >= 2048 and cfg.N >= 256 and cfg.N % 2 == 0:
         if Np < cfg.N:
             return ("block-step path (marginal): ffs_cluster_kernel<STEP> with gathered contraction + "
                     "ffs_dense_gj_kernel per block, CUDA graph"), dt
-        return ("block-step path (hybrid dense): ffs_cluster_kernel<STEP>, ffs_ozaki_gemm_kernel<8> for "
-                "k0 >= theta N', ffs_dense_gj_kernel per block, CUDA graph"), \
+        return ("block-step path (hybrid dense): per block ffs_ozaki_gemm2_kernel<8> (P = U Y), ffs_gram_kernel + "
+                "ffs_gram_draw_kernel (draws on tile Gram matrices, warp per sample), ffs_dense_gj_kernel; "
+                "ffs_cluster_kernel<STEP> for k0 < theta N'; CUDA graph"), \
             dt + " (dense GEMM: Ozaki FP64 emulation, int8 x 8 slices on tcgen05; fp64-level, <= 1.3e-15 normwise)"
     if cfg.L >= 2048:
         return "ffs_cluster_kernel", dt

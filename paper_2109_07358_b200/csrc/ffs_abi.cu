@@ -419,7 +419,7 @@ int launch_warp(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, cons
 // sample (ffs_kmarg.cuh). Workspace: [perm | U^T | K | Gs slots | C slots].
 struct KmPlan {
   const void* fn;
-  int Rl, Lpt, grid, warps;
+  int Rl, Lpt, grid, warps, G;
   bool c_smem, blocked;
   size_t warp_smem, smem, ws_perm, ws_ut, ws_k, ws_c, total;
 };
@@ -429,16 +429,22 @@ bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   return dtype == FFS_F64 && Np <= ffsk::kKmMaxNp && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
 }
 
-template <int WARPS, bool BLK>
-const void* km_fn(int Rl) {
-  return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<1, WARPS, BLK>)
-       : Rl <= 4 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<4, WARPS, BLK>)
-                 : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<16, WARPS, BLK>);
+template <bool BLK>
+const void* km_fn(int Rl, int G) {
+  if (G == 16)
+    return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<1, 4, BLK, 16>)
+                   : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<4, 4, BLK, 16>);
+  return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<1, 4, BLK, 32>)
+       : Rl <= 4 ? reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<4, 4, BLK, 32>)
+                 : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<16, 4, BLK, 32>);
 }
 
 int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k) {
-  k.Rl = (int)((L + 1023) / 1024);
-  k.Lpt = 1024 * k.Rl;
+  // sample owner: a warp (32 tiles), or a half warp (16 tiles, two samples per warp) for L <= 1024,
+  // where most of a draw keeps at most 16 lanes busy (C3 marginal: 0.58 -> ? ms)
+  k.G = (L <= 1024 && ffsh::option(FFS_OPT_TILE_GRAM) != 4.0) ? 16 : 32;
+  k.Rl = (int)((L + k.G * k.G - 1) / (k.G * k.G));
+  k.Lpt = k.G * k.G * k.Rl;
   k.c_smem = Np <= 32;  // C [N'][N'] in shared memory (8 KB per warp at most), else a workspace slot per warp
   k.warps = 4;
   // N' > 24: blocked evaluation of the forms (K entries read once per block of 8 draws instead of
@@ -446,9 +452,10 @@ int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k
   // forces flat / blocked
   const double ot = ffsh::option(FFS_OPT_TILE_GRAM);
   k.blocked = ot == 3.0 || (ot != 2.0 && Np > 24);
-  k.fn = k.blocked ? km_fn<4, true>(k.Rl) : km_fn<4, false>(k.Rl);
-  k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.c_smem, k.blocked);
-  k.smem = k.warps * k.warp_smem + ffsk::align16((size_t)Np * (Np + 1));  // + the entry/pair table
+  k.fn = k.blocked ? km_fn<true>(k.Rl, k.G) : km_fn<false>(k.Rl, k.G);
+  k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.c_smem, k.blocked, k.G);
+  const int owners = k.warps * (32 / k.G);  // per CTA
+  k.smem = owners * k.warp_smem + ffsk::align16((size_t)Np * (Np + 1));  // + the entry/pair table
   if (k.smem > kMaxSmem) return fail(FFS_EINVAL, "tile-Gram path: shared memory %zu too large", k.smem);
   if (int rc = ffsh::ensure_max_smem(k.fn)) return rc;
   int per_sm = 0;
@@ -456,12 +463,12 @@ int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k
     return fail(FFS_EINVAL, "tile-Gram kernel does not fit on an SM (smem=%zu)", k.smem);
   const int sms = ffsh::sm_count(ffsh::device());
   int64_t ctas = (int64_t)std::min(per_sm, 8) * sms;
-  ctas = std::min<int64_t>(ctas, (M + k.warps - 1) / k.warps);
+  ctas = std::min<int64_t>(ctas, (M + owners - 1) / owners);
   k.grid = (int)std::max<int64_t>(1, ctas);
-  const size_t slots = (size_t)k.grid * k.warps;
+  const size_t slots = (size_t)k.grid * owners;
   k.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
   k.ws_ut = align_up((size_t)N * k.Lpt * 8);
-  k.ws_k = align_up((size_t)32 * N * N * 8);
+  k.ws_k = align_up((size_t)k.G * N * N * 8);
   k.ws_c = k.c_smem ? 0 : align_up(slots * (size_t)Np * Np * 8);
   k.total = k.ws_perm + k.ws_ut + k.ws_k + k.ws_c;
   return FFS_OK;
@@ -488,8 +495,8 @@ int launch_kmarg(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, con
   double* K = reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut);
   ffsh::prof_begin(stream);
   launch_transpose(U, Ut, L, N, k.Lpt, FFS_F64, stream);
-  const dim3 kg((unsigned)((N + 63) / 64), (unsigned)((N + 63) / 64), 32);
-  ffsk::ffs_tile_gram_u_kernel<<<kg, 256, 0, stream>>>(static_cast<const double*>(U), K, (int)L, (int)N, 32 * k.Rl);
+  const dim3 kg((unsigned)((N + 63) / 64), (unsigned)((N + 63) / 64), (unsigned)k.G);
+  ffsk::ffs_tile_gram_u_kernel<<<kg, 256, 0, stream>>>(static_cast<const double*>(U), K, (int)L, (int)N, k.G * k.Rl, k.G);
   ++ffsh::launches();
   if (int rc2 = launch_permute(uniforms, 2 * Np, perm, M, N, Np, stream)) return rc2;
   ffsk::KMargParams p{};

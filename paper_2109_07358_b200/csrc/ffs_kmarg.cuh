@@ -24,11 +24,11 @@
 
 namespace ffsk {
 
-// K[a][b][t] = sum_{x in tile t} U[x][a] U[x][b], tiles of Rt rows; grid (b tiles, a tiles, 32),
+// K[a][b][t] = sum_{x in tile t} U[x][a] U[x][b], G tiles of Rt rows; grid (b tiles, a tiles, G),
 // 256 threads, 64 x 64 outputs per CTA (4 x 4 per thread); only a-tile <= b-tile is computed, the
 // mirror image is written with it
 static __global__ void __launch_bounds__(256) ffs_tile_gram_u_kernel(const double* __restrict__ U, double* __restrict__ K,
-                                                                    int L, int N, int Rt) {
+                                                                    int L, int N, int Rt, int G) {
   if (blockIdx.y > blockIdx.x) return;
   __shared__ double As[16][64 + 4], Bs[16][64 + 4];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
@@ -67,51 +67,60 @@ static __global__ void __launch_bounds__(256) ffs_tile_gram_u_kernel(const doubl
     for (int j = 0; j < 4; ++j) {
       const int a = a0 + ty * 4 + i, b = b0 + tx * 4 + j;
       if (a < N && b < N) {
-        Kt[((size_t)a * N + b) * 32] = acc[i][j];
-        if (blockIdx.y != blockIdx.x) Kt[((size_t)b * N + a) * 32] = acc[i][j];
+        Kt[((size_t)a * N + b) * G] = acc[i][j];
+        if (blockIdx.y != blockIdx.x) Kt[((size_t)b * N + a) * G] = acc[i][j];
       }
     }
 }
 
 struct KMargParams {
   const double* U;         // [L][N]
-  const double* Ut;        // [N][Lpt] transposed, zero-padded, Lpt = 1024 Rl
-  const double* K;         // [N][N][32] tile Gram matrices of U, tile-minor
+  const double* Ut;        // [N][Lpt] transposed, zero-padded, Lpt = G G Rl
+  const double* K;         // [N][N][G] tile Gram matrices of U, tile-minor
   const int32_t* permg;    // [M][Np]
   const double* uniforms;  // [M][2Np]
   int32_t* positions;      // [M][Np]
   int32_t* flags;          // [M] or null
   double* Cw;              // [slots][Np][Np] coefficient matrix (null: in shared memory)
-  int L, N, Np, Lpt, Rl;   // Rl rows per lane of a tile (tile = 32 Rl rows)
+  int L, N, Np, Lpt, Rl;   // Rl rows per lane of a tile (tile = G Rl rows, G tiles; G = lanes per sample)
   int64_t M, S0, S;
   double* trace;           // [S][Np][L] or null
-  size_t warp_smem;        // bytes of shared memory per warp
+  size_t warp_smem;        // bytes of shared memory per sample owner (a group of G lanes)
   double kappa_max;        // blocked forms: cancellation guard (as ffs_gram.cuh)
 };
 
 constexpr int kKmMaxNp = 64;
 
-// per-warp shared memory: m, selection uniforms, d, U[x_k, m], pivot row, the drawn-row bitmap,
+// shared memory per sample owner (a warp, or a half warp when L <= 1024: G = 16 lanes, 16 tiles): m, selection uniforms, d, U[x_k, m], pivot row, the drawn-row bitmap,
 // (small N') C, and for the forms either the offsets of the sample's entries in K + their
 // coefficients (flat evaluation), or the block's D, tile Gram entries and their sqrt-diagonal
 // (blocked evaluation)
-__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np, bool c_smem, bool blocked) {
+__host__ __device__ inline size_t kmarg_warp_smem(int L, int Np, bool c_smem, bool blocked, int G) {
   const size_t ne = ((size_t)Np * (Np + 1) / 2 + 15) & ~size_t(15);  // padded to the form's batch of 16
-  const size_t forms = blocked ? sizeof(double) * (48 + (size_t)Np * 8 + 36 * 32 + 8 * 32)
+  const size_t forms = blocked ? sizeof(double) * (48 + (size_t)Np * 8 + 36 * G + 8 * G)
                                : align16(sizeof(double) * ne) + align16(sizeof(int) * ne);
   return align16(sizeof(int) * Np) + 4 * align16(sizeof(double) * Np) + forms +
          align16(sizeof(uint32_t) * ((L + 31) / 32)) + (c_smem ? align16(sizeof(double) * Np * Np) : 0);
 }
 
-template <int RLMAX, int WARPS, bool BLK>
-static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 1) ffs_kmarg_kernel(const KMargParams p) {
+// G lanes own a sample (G = 32: a warp; G = 16: a half warp, two samples per warp -- for small L the
+// per-draw work is dominated by steps that keep <= 16 lanes busy). `lane` below is the lane WITHIN
+// the owner group; every shuffle / ballot / barrier is restricted to the group's lanes.
+template <int RLMAX, int WARPS, bool BLK, int G>
+static __global__ void __launch_bounds__(32 * WARPS, (RLMAX <= 4 && !BLK) ? 6 : 1) ffs_kmarg_kernel(const KMargParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NG = 32 / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & (G - 1), gi = (threadIdx.x & 31) / G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (0xffffu << (16 * gi));
+  auto gballot = [&](bool pred) -> unsigned {
+    const unsigned bsel = __ballot_sync(gmask, pred);
+    return G == 32 ? bsel : ((bsel >> (16 * gi)) & 0xffffu);
+  };
   const int L = p.L, N = p.N, Np = p.Np, Rl = p.Rl, Lpt = p.Lpt;
-  const int Rt = 32 * Rl;
+  const int Rt = G * Rl;
   const int ne_all = Np * (Np + 1) / 2;
   const int ne_pad = (ne_all + 15) & ~15;
-  unsigned char* wb = smem + (size_t)warp * p.warp_smem;
+  unsigned char* wb = smem + (size_t)(warp * NG + gi) * p.warp_smem;
   const size_t dsz = align16(sizeof(double) * Np);
   int* m = reinterpret_cast<int*>(wb);
   double* uselv = reinterpret_cast<double*>(wb + align16(sizeof(int) * Np));
@@ -123,17 +132,17 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
   int* koff = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(coef) + align16(sizeof(double) * ne_pad));
   double* Dm = coef + 48;
   double* gbs = Dm + (size_t)Np * 8;
-  double* sgs = gbs + 36 * 32;
-  uint32_t* bits = BLK ? reinterpret_cast<uint32_t*>(sgs + 8 * 32)
+  double* sgs = gbs + 36 * G;
+  uint32_t* bits = BLK ? reinterpret_cast<uint32_t*>(sgs + 8 * G)
                        : reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(koff) + align16(sizeof(int) * ne_pad));
   unsigned char* extra = reinterpret_cast<unsigned char*>(bits) + align16(sizeof(uint32_t) * ((L + 31) / 32));
   const int nwords = (L + 31) >> 5;
-  const int64_t slot = (int64_t)blockIdx.x * WARPS + warp;
-  const int64_t nslots = (int64_t)gridDim.x * WARPS;
+  const int64_t slot = ((int64_t)blockIdx.x * WARPS + warp) * NG + gi;
+  const int64_t nslots = (int64_t)gridDim.x * WARPS * NG;
   double* C = p.Cw != nullptr ? p.Cw + (size_t)slot * Np * Np : reinterpret_cast<double*>(extra);
   const double* Kl = p.K + lane;  // lane = tile
   // entry e <-> (q, q'), q <= q', e = q'(q'+1)/2 + q: one table per CTA
-  uint16_t* pairs = reinterpret_cast<uint16_t*>(smem + (size_t)WARPS * p.warp_smem);
+  uint16_t* pairs = reinterpret_cast<uint16_t*>(smem + (size_t)WARPS * NG * p.warp_smem);
   for (int e = threadIdx.x; e < ne_all; e += blockDim.x) {
     int qp = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
     while ((qp + 1) * (qp + 2) / 2 <= e) ++qp;
@@ -144,30 +153,30 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
 
   auto scan = [&](double v) -> double {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, v, d);
+    for (int d = 1; d < G; d <<= 1) {
+      const double y = __shfl_up_sync(gmask, v, d, G);
       if (lane >= d) v += y;
     }
     return v;
   };
 
   for (int64_t i = slot; i < p.M; i += nslots) {
-    __syncwarp();
-    for (int j = lane; j < Np; j += 32) {
+    __syncwarp(gmask);
+    for (int j = lane; j < Np; j += G) {
       m[j] = p.permg[i * Np + j];
       FFS_CHECK(m[j] >= 0 && m[j] < N);
       uselv[j] = p.uniforms[i * 2 * (int64_t)Np + Np + j];
     }
-    for (int j = lane; j < nwords; j += 32) bits[j] = 0u;
-    __syncwarp();
+    for (int j = lane; j < nwords; j += G) bits[j] = 0u;
+    __syncwarp(gmask);
     // ---- offsets of the sample's Gram entries G[q][q'] = K[m_q][m_q'][:] in K (entry e by lane e mod 32)
     if constexpr (!BLK) {
-      for (int e = lane; e < ne_all; e += 32) {
+      for (int e = lane; e < ne_all; e += G) {
         const unsigned pr = pairs[e];
-        koff[e] = (m[pr & 255u] * N + m[pr >> 8]) * 32;
+        koff[e] = (m[pr & 255u] * N + m[pr >> 8]) * G;
       }
-      for (int e = ne_all + lane; e < ne_pad; e += 32) koff[e] = 0;
-      __syncwarp();
+      for (int e = ne_all + lane; e < ne_pad; e += G) koff[e] = 0;
+      __syncwarp(gmask);
     }
     int flag = 0;
     const bool traced = p.trace != nullptr && (uint64_t)(i - p.S0) < (uint64_t)p.S;
@@ -185,18 +194,18 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
         const int rb = r & 7, k0 = r - rb;
         if (rb == 0) {
           const int nb = min(8, Np - k0), na = k0 + nb;
-          for (int idx = lane; idx < na * 8; idx += 32) {
+          for (int idx = lane; idx < na * 8; idx += G) {
             const int a = idx >> 3, c = idx & 7;
             Dm[idx] = a < k0 ? (c < nb ? -C[(size_t)a * Np + k0 + c] : 0.0) : (a - k0 == c ? 1.0 : 0.0);
           }
-          __syncwarp();
+          __syncwarp(gmask);
           double gb[36];
 #pragma unroll
           for (int e = 0; e < 36; ++e) gb[e] = 0.0;
           for (int a = 0; a < na; a += 2) {
             const int a1 = min(a + 1, na - 1);
-            const double* Ka = Kl + (size_t)m[a] * N * 32;
-            const double* Kb = Kl + (size_t)m[a1] * N * 32;
+            const double* Ka = Kl + (size_t)m[a] * N * G;
+            const double* Kb = Kl + (size_t)m[a1] * N * G;
             double t0[8], t1[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) t0[c] = t1[c] = 0.0;
@@ -204,7 +213,7 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
               double g0[8], g1[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const int mb = m[min(b + j, na - 1)] * 32;
+                const int mb = m[min(b + j, na - 1)] * G;
                 g0[j] = Ka[mb];
                 g1[j] = Kb[mb];
               }
@@ -234,9 +243,9 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
               }
           }
 #pragma unroll
-          for (int e = 0; e < 36; ++e) gbs[e * 32 + lane] = gb[e];
+          for (int e = 0; e < 36; ++e) gbs[e * G + lane] = gb[e];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) sgs[q * 32 + lane] = sqrt(fmax(gb[q * (q + 1) / 2 + q], 0.0));
+          for (int q = 0; q < 8; ++q) sgs[q * G + lane] = sqrt(fmax(gb[q * (q + 1) / 2 + q], 0.0));
         }
         if (lane <= rb) {
           const int qp = lane;
@@ -245,39 +254,39 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
           for (int q = 0; q < qp; ++q) cc[q] = 2.0 * dq * dvec[k0 + q];
           cc[qp] = dq * dq;
         }
-        __syncwarp();
+        __syncwarp(gmask);
         const int neb = (rb + 1) * (rb + 2) / 2;
-        for (int e = 0; e < neb; ++e) f = fma(coef[e], gbs[e * 32 + lane], f);
+        for (int e = 0; e < neb; ++e) f = fma(coef[e], gbs[e * G + lane], f);
         // cancellation guard (as ffs_gram.cuh): bound (sum_q |d_q| sqrt(G_blk[q][q]))^2 against the total
-        double bd = sgs[rb * 32 + lane];
-        for (int q = 0; q < rb; ++q) bd = fma(fabs(dvec[k0 + q]), sgs[q * 32 + lane], bd);
+        double bd = sgs[rb * G + lane];
+        for (int q = 0; q < rb; ++q) bd = fma(fabs(dvec[k0 + q]), sgs[q * G + lane], bd);
         bd *= bd;
         double ft = f > 0.0 ? f : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          ft += __shfl_xor_sync(0xffffffffu, ft, o);
-          bd += __shfl_xor_sync(0xffffffffu, bd, o);
+        for (int o = G / 2; o > 0; o >>= 1) {
+          ft += __shfl_xor_sync(gmask, ft, o, G);
+          bd += __shfl_xor_sync(gmask, bd, o, G);
         }
         if (!(ft * p.kappa_max >= bd)) {
           // rare: the form on the ORIGINAL columns (conditioned within a factor N'), entry by entry
           f = 0.0;
           for (int qp = 0; qp <= r; ++qp) {
             const double dq = qp == r ? 1.0 : dvec[qp];
-            const double* Kc = Kl + (size_t)m[qp] * 32;
+            const double* Kc = Kl + (size_t)m[qp] * G;
             double acc = 0.0;
-            for (int q = 0; q < qp; ++q) acc = fma(Kc[(size_t)m[q] * N * 32], dvec[q], acc);
-            f = fma(dq, fma(Kc[(size_t)m[qp] * N * 32], dq, 2.0 * acc), f);
+            for (int q = 0; q < qp; ++q) acc = fma(Kc[(size_t)m[q] * N * G], dvec[q], acc);
+            f = fma(dq, fma(Kc[(size_t)m[qp] * N * G], dq, 2.0 * acc), f);
           }
         }
       } else {
         // ---- coefficients of the form d^T G d, d = (dvec[0:r], 1): column q' by lane q' (mod 32)
-        for (int qp = lane; qp <= r; qp += 32) {
+        for (int qp = lane; qp <= r; qp += G) {
           const double dq = qp == r ? 1.0 : dvec[qp];
           double* cc = coef + qp * (qp + 1) / 2;
           for (int q = 0; q < qp; ++q) cc[q] = 2.0 * dq * dvec[q];
           cc[qp] = dq * dq;
         }
-        __syncwarp();
+        __syncwarp(gmask);
         // ---- tile totals f (lane = tile)
         {
           double a[8];
@@ -286,8 +295,8 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
           // batches of 16 entries: offsets and coefficients by 16-byte broadcast reads, the 16 K rows
           // in flight together (the arrays are padded to a multiple of 16 entries: coefficient 0)
           const int ne16 = (ne + 15) & ~15;
-          for (int e = lane + ne; e < ne16; e += 32) coef[e] = 0.0;
-          __syncwarp();
+          for (int e = lane + ne; e < ne16; e += G) coef[e] = 0.0;
+          __syncwarp(gmask);
           for (int e = 0; e < ne16; e += 16) {
             int ko[16];
             double g[16], cf[16];
@@ -340,18 +349,18 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
           f = sum;
         }
         const double incl = scan(f);
-        Ttot = __shfl_sync(0xffffffffu, incl, 31);
+        Ttot = __shfl_sync(gmask, incl, G - 1, G);
         ok = (Ttot > 0.0) && (Ttot <= 1.7976931348623157e308);
         if (!ok) continue;
         const double thr = u * Ttot;
-        const unsigned cross = __ballot_sync(0xffffffffu, f > 0.0 && incl > thr);
-        const unsigned posl = __ballot_sync(0xffffffffu, f > 0.0);
+        const unsigned cross = gballot(f > 0.0 && incl > thr);
+        const unsigned posl = gballot(f > 0.0);
         const int tau = cross ? __ffs(cross) - 1 : 31 - __clz(posl);
-        double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+        double ex = __shfl_up_sync(gmask, incl, 1, G);
         if (lane == 0) ex = 0.0;
-        const double thr_in = thr - __shfl_sync(0xffffffffu, ex, tau);
+        const double thr_in = thr - __shfl_sync(gmask, ex, tau, G);
         // ---- rows of tile tau, Rl consecutive rows per lane
-        const int xb = (tau * 32 + lane) * Rl;
+        const int xb = (tau * G + lane) * Rl;
         double s[RLMAX];
         {
           const double* col = p.Ut + (size_t)mr * Lpt + xb;
@@ -393,13 +402,13 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
           c[j] = run;
         }
         const double incl2 = scan(run);
-        double ex2 = __shfl_up_sync(0xffffffffu, incl2, 1);
+        double ex2 = __shfl_up_sync(gmask, incl2, 1, G);
         if (lane == 0) ex2 = 0.0;
         // the in-tile threshold as the same fraction of the tile's row-wise total that thr_in is
         // of the tile total used by the tile scan (they differ by rounding); u T >= T after
         // rounding: the last row with w > 0
-        const double Dt = __shfl_sync(0xffffffffu, incl2, 31);
-        const double thr2 = cross ? (thr_in / __shfl_sync(0xffffffffu, f, tau)) * Dt : 1.7976931348623157e308;
+        const double Dt = __shfl_sync(gmask, incl2, G - 1, G);
+        const double thr2 = cross ? (thr_in / __shfl_sync(gmask, f, tau, G)) * Dt : 1.7976931348623157e308;
         const double tp = thr2 - ex2;
         int rs = RLMAX, rl = -1;
 #pragma unroll
@@ -412,15 +421,15 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
           const double prev = j > 0 ? c[j - 1] : 0.0;
           if (c[j] > prev) rl = j;
         }
-        const unsigned b1 = __ballot_sync(0xffffffffu, rs < RLMAX);
+        const unsigned b1 = gballot(rs < RLMAX);
         if (b1) {
           const int ln = __ffs(b1) - 1;
-          xsel = (tau * 32 + ln) * Rl + __shfl_sync(0xffffffffu, rs, ln);
+          xsel = (tau * G + ln) * Rl + __shfl_sync(gmask, rs, ln, G);
         } else {
-          const unsigned b2 = __ballot_sync(0xffffffffu, rl >= 0);
+          const unsigned b2 = gballot(rl >= 0);
           if (b2) {
             const int ln = 31 - __clz(b2);
-            xsel = (tau * 32 + ln) * Rl + __shfl_sync(0xffffffffu, rl, ln);
+            xsel = (tau * G + ln) * Rl + __shfl_sync(gmask, rl, ln, G);
           }
         }
         if (xsel >= 0) break;
@@ -428,14 +437,14 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
       if (xsel < 0) {
         // T not finite / positive (flag bit0): the smallest site not drawn yet
         flag |= 1;
-        for (int wbase = 0; wbase < nwords && xsel < 0; wbase += 32) {
+        for (int wbase = 0; wbase < nwords && xsel < 0; wbase += G) {
           const int wi = wbase + lane;
           uint32_t word = wi < nwords ? bits[wi] : 0xffffffffu;
           if (wi == nwords - 1 && (L & 31)) word |= 0xffffffffu << (L & 31);
-          const unsigned bf = __ballot_sync(0xffffffffu, word != 0xffffffffu);
+          const unsigned bf = gballot(word != 0xffffffffu);
           if (bf) {
             const int ln = __ffs(bf) - 1;
-            const uint32_t wsel = __shfl_sync(0xffffffffu, word, ln);
+            const uint32_t wsel = __shfl_sync(gmask, word, ln, G);
             xsel = (wbase + ln) * 32 + (__ffs(~wsel) - 1);
           }
         }
@@ -444,15 +453,15 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
       if (traced) {
         const double inv = ok ? 1.0 / Ttot : 0.0;
         double* tr = p.trace + ((i - p.S0) * Np + r) * (int64_t)L;
-        for (int x = lane; x < L; x += 32) {
+        for (int x = lane; x < L; x += G) {
           const double sx = srow(x);
           tr[x] = drawn(x) ? 0.0 : sx * sx * inv;
         }
       }
       // ---- pivot row v[c] = V[x, c] - V[x, 0:r] C[0:r, c] (c >= r) and the Gauss-Jordan update
-      for (int q = lane; q < Np; q += 32) urow[q] = p.U[(size_t)xsel * N + m[q]];
-      __syncwarp();
-      for (int cc = r + lane; cc < Np; cc += 32) {
+      for (int q = lane; q < Np; q += G) urow[q] = p.U[(size_t)xsel * N + m[q]];
+      __syncwarp(gmask);
+      for (int cc = r + lane; cc < Np; cc += G) {
         double a0 = urow[cc], a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int q = 0;
         for (; q + 4 <= r; q += 4) {
@@ -466,11 +475,11 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
         for (; q < r; ++q) a0 = fma(-urow[q], C[(size_t)q * Np + cc], a0);
         vrow[cc] = (a0 + a1) + (a2 + a3);
       }
-      __syncwarp();
+      __syncwarp(gmask);
       const double piv = vrow[r];
       if (ok && piv * piv < 1e-12 * Ttot) flag |= 2;
       const double ip = fast_rcp(piv);
-      for (int cc = r + 1 + lane; cc < Np; cc += 32) {
+      for (int cc = r + 1 + lane; cc < Np; cc += G) {
         const double z = vrow[cc] * ip;
         int q = 0;
         for (; q + 4 <= r; q += 4) {
@@ -490,11 +499,11 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX == 1 && !BLK) ? 8 : 
         bits[xsel >> 5] |= 1u << (xsel & 31);
         p.positions[i * Np + r] = xsel;
       }
-      __syncwarp();
+      __syncwarp(gmask);
       // d of the next step: -(column r+1 of C)
       if (r + 1 < Np)
-        for (int q = lane; q <= r; q += 32) dvec[q] = -C[(size_t)q * Np + r + 1];
-      __syncwarp();
+        for (int q = lane; q <= r; q += G) dvec[q] = -C[(size_t)q * Np + r + 1];
+      __syncwarp(gmask);
     }
     if (lane == 0 && p.flags != nullptr) p.flags[i] = flag;
   }
