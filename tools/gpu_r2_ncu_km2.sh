@@ -3,7 +3,7 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out/ncu_km; mkdir -p $O
 python tools/run_once.py dpp:marginal 1 > /dev/null 2>&1
-for w in anderson:marginal dpp:marginal; do
+for w in anderson:marginal; do
   f=$(echo $w | tr ':' '_')
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffs_kmarg_kernel -s 1 -c 1 -o $O/src_$f \
     python tools/run_once.py $w 2 > $O/src_$f.log 2>&1
