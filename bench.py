@@ -158,6 +158,15 @@ def path_of(cfg, Np, cplx):
     return "ffs_sample_kernel (CTA owners)", dt
 
 
+def path_note(cfg, Np, cplx):
+    """What `frac` means where the path executes fewer flops than the paper's count."""
+    if (not cplx) and not (cfg.L <= 256 and Np <= 48) and Np <= 64 and 64 * Np <= 3 * cfg.L and cfg.N <= 2048:
+        return ("tile-Gram path: tile totals come from the tile Gram matrices of U, so the executed flops per sample "
+                "(~G N'^3/6 + N'^2 L/(2G), G = 16 or 32 tiles) are below the paper's L N'^2 + N'^3 that `achieved` "
+                "counts; frac is a throughput ratio against the FP64 peak, not a pipe utilisation")
+    return None
+
+
 def load_roofline_file():
     try:
         with open(ROOFLINE_FILE) as f:
@@ -330,6 +339,8 @@ def sweep_entry(r, cpu_budget, no_cpu):
          "effective_gflops": M * paper_flops(cfg.L, Np, cplx) / (r["ms"] * 1e-3) / 1e9,
          "frac": r["frac"], "clocks": r["clocks"], "e2e": r.get("e2e"), "gpu_launches": r["launches"],
          "sample_flags_nonzero": r["flags_bad"]}
+    if path_note(cfg, Np, cplx):
+        e["note"] = path_note(cfg, Np, cplx)
     if not no_cpu:
         rate, n, t, cores = cpu_oracle_rate(r["U"], r["uni"], Np, budget_s=cpu_budget)
         e["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": cores, "kind": "oracle",
@@ -545,6 +556,8 @@ def run_gpu(args):
         for k in ("traffic_source", "gemm"):
             if k in rf:
                 line["roofline"][k] = rf[k]
+        if path_note(cfg, Np, cplx):
+            line["roofline"]["note"] = path_note(cfg, Np, cplx)
         if world == 1 and not args.no_cpu:
             if sweep and wl_name(cfg.name, Np < cfg.N) in sweep and "cpu_baseline" in sweep[wl_name(cfg.name, Np < cfg.N)]:
                 line["cpu_baseline"] = sweep[wl_name(cfg.name, Np < cfg.N)]["cpu_baseline"]
