@@ -136,15 +136,20 @@ def config_of(cfg, Np, M):
             "l2": L2_NOTE}
 
 
+def km_np_max(L):
+    """Largest N' the tile-Gram path takes (ffs_abi.cu kmarg_eligible)."""
+    return 24 if L <= 1024 else 32 if L < 2048 else 64
+
+
 def path_of(cfg, Np, cplx):
     """Kernel (sequence) libffs dispatches this shape to (ffs_abi.cu launch()) and its arithmetic."""
     if (not cplx) and cfg.L <= 256 and Np <= 48:
         return "ffs_seg_kernel (warp-segment owners)", "f64"
     dt = "c128" if cplx else "f64"
-    if (not cplx) and Np <= 64 and 64 * Np <= 3 * cfg.L and cfg.N <= 2048:
+    if (not cplx) and Np <= km_np_max(cfg.L) and 64 * Np <= 3 * cfg.L and cfg.N <= 2048:
         return ("tile-Gram path: ffs_tile_gram_u_kernel (32 tile Gram matrices of U, once per call) + "
                 "ffs_kmarg_kernel (warp per sample, tile totals as quadratic forms"
-                + (", blocked)" if Np > 24 else ")")), dt
+                + (", blocked)" if Np > 32 else ")")), dt
     if cfg.L >= 2048 and cfg.N >= 256 and cfg.N % 2 == 0:
         if Np < cfg.N:
             return ("block-step path (marginal): ffs_cluster_kernel<STEP> with gathered contraction + "
@@ -160,7 +165,7 @@ def path_of(cfg, Np, cplx):
 
 def path_note(cfg, Np, cplx):
     """What `frac` means where the path executes fewer flops than the paper's count."""
-    if (not cplx) and not (cfg.L <= 256 and Np <= 48) and Np <= 64 and 64 * Np <= 3 * cfg.L and cfg.N <= 2048:
+    if (not cplx) and not (cfg.L <= 256 and Np <= 48) and Np <= km_np_max(cfg.L) and 64 * Np <= 3 * cfg.L and cfg.N <= 2048:
         return ("tile-Gram path: tile totals come from the tile Gram matrices of U, so the executed flops per sample "
                 "(~G N'^3/6 + N'^2 L/(2G), G = 16 or 32 tiles) are below the paper's L N'^2 + N'^3 that `achieved` "
                 "counts; frac is a throughput ratio against the FP64 peak, not a pipe utilisation")

@@ -426,7 +426,11 @@ struct KmPlan {
 
 bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   if (ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0 || ffsh::option(FFS_OPT_TILE_GRAM) == 0.0) return false;
-  return dtype == FFS_F64 && Np <= ffsk::kKmMaxNp && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
+  // measured against the panel kernels (tools/shape_time.py, profiles/r02/shape_times.log): below
+  // L = 2048 the CTA-owner kernel wins from N' ~ 26 on (L = 1024: N' = 32 3.5 vs 4.2 ms); from L = 2048
+  // the tile-Gram path wins up to N' = 64 by 3-5x
+  const int64_t np_max = L <= 1024 ? 24 : L < 2048 ? 32 : ffsk::kKmMaxNp;
+  return dtype == FFS_F64 && Np <= np_max && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
 }
 
 template <bool BLK>
@@ -447,11 +451,11 @@ int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k
   k.Lpt = k.G * k.G * k.Rl;
   k.c_smem = Np <= 32;  // C [N'][N'] in shared memory (8 KB per warp at most), else a workspace slot per warp
   k.warps = 4;
-  // N' > 24: blocked evaluation of the forms (K entries read once per block of 8 draws instead of
+  // N' > 32: blocked evaluation of the forms (K entries read once per block of 8 draws instead of
   // once per draw: C5 marginal 3.3 instead of 11.7 MB of K rows per sample); option value 2 / 3
   // forces flat / blocked
   const double ot = ffsh::option(FFS_OPT_TILE_GRAM);
-  k.blocked = ot == 3.0 || (ot != 2.0 && Np > 24);
+  k.blocked = ot == 3.0 || (ot != 2.0 && Np > 32);  // N' = 32: flat 1.91 vs blocked 2.25 ms; 48: 13.3 vs 6.9
   k.fn = k.blocked ? km_fn<true>(k.Rl, k.G) : km_fn<false>(k.Rl, k.G);
   k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.c_smem, k.blocked, k.G);
   const int owners = k.warps * (32 / k.G);  // per CTA

@@ -61,6 +61,23 @@ struct GramParams {
 
 __device__ unsigned long long g_gram_stats[2];
 
+// Sum of v[e] over the 32 lanes for 64 values by recursive halving: at the step with lane mask
+// 16, 8, .., 1 a lane keeps the half of its values selected by that lane bit and receives the
+// partner's sums of that half (32 + 16 + .. + 2 = 62 shuffles instead of 64 x 5); afterwards lane l
+// holds the totals of entries 2 l and 2 l + 1 in v[0], v[1].
+__device__ __forceinline__ void warp_reduce_scatter64(double (&v)[64], int lane) {
+#pragma unroll
+  for (int h = 32; h >= 2; h >>= 1) {
+    const bool up = (lane & (h >> 1)) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? v[j] : v[j + h];
+      const double keep = up ? v[j + h] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, h >> 1);
+    }
+  }
+}
+
 // one warp per (sample, tile): lane l takes rows l, l + 32, ... of the tile
 template <typename T, int B>
 static __global__ void __launch_bounds__(256) ffs_gram_kernel(const GramParams p) {
@@ -113,13 +130,12 @@ static __global__ void __launch_bounds__(256) ffs_gram_kernel(const GramParams p
     }
   }
   double* out = p.G + (size_t)sl * NE * 32 + tau;
+  double v64[64];
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    double a = acc[e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == (e & 31)) out[(size_t)e * 32] = a;
-  }
+  for (int e = 0; e < 64; ++e) v64[e] = e < NE ? acc[e] : 0.0;
+  warp_reduce_scatter64(v64, lane);
+  if (2 * lane < NE) out[(size_t)(2 * lane) * 32] = v64[0];
+  if (2 * lane + 1 < NE) out[(size_t)(2 * lane + 1) * 32] = v64[1];
 }
 
 template <typename T, int B>
