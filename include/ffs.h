@@ -212,7 +212,10 @@ typedef enum {
   FFS_OPT_TILE_GRAM = 14,       /* 1 (default): real U, 64 N' <= 3 L and N' <= 24 (L <= 1024), 32 (L < 2048), 64 (larger L): the tile-Gram
                                    path (ffs_kmarg.cuh): tile totals as quadratic forms of the 32 tile
                                    Gram matrices of U, one warp per sample; 0: the panel kernels */
-  FFS_OPT_LAST = 14
+  FFS_OPT_GJ_PAIR = 15,         /* 1 (default): real block-step paths update W for two consecutive blocks in
+                                   one pass (ffs_dense_gj2_kernel: half the W traffic); 2: complex too;
+                                   0: one pass per block */
+  FFS_OPT_LAST = 15
 } ffs_option;
 int ffs_set_option(int option, double value);
 double ffs_get_option(int option);

@@ -57,6 +57,7 @@ double default_option(int o) {
     case FFS_OPT_DENSE_MIN_L: return 2048.0;
     case FFS_OPT_DENSE_MIN_N: return 256.0;
     case FFS_OPT_TILE_GRAM: return 1.0;
+    case FFS_OPT_GJ_PAIR: return 1.0;
     default: return 0.0;
   }
 }
@@ -697,6 +698,7 @@ struct DensePlan {
   size_t ws_oza, ws_ea, ws_ozb, ws_eb;
   size_t ws_perm, ws_y, ws_p, ws_w, ws_ch, ws_row, ws_ut, ws_g, total;
   int k_gather;        // blocks with k0 < k_gather contract the gathered columns in the step kernel
+  int gj_pair;         // 1: the trailing Gauss-Jordan updates of two consecutive blocks in one pass
   int gram;            // 1: GEMM blocks draw on the tile Gram matrices (ffs_gram.cuh)
   int Rt;              // rows per Gram tile (32 tiles cover L)
 };
@@ -714,6 +716,10 @@ template <typename T>
 const void* dense_gj_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, gj_tj<T>()>); }
 template <typename T>
 size_t dense_gj_bytes(int k0) { return ffsk::dense_gj_smem<T, 8, gj_tj<T>()>(k0); }
+template <typename T>
+const void* dense_gj2_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj2_kernel<T, 8, gj_tj<T>()>); }
+template <typename T>
+size_t dense_gj2_bytes(int k0) { return ffsk::dense_gj2_smem<T, 8, gj_tj<T>()>(k0); }
 template <int NS>
 const void* ozaki_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel<NS>); }
 const void* ozaki2_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm2_kernel<8>); }
@@ -771,7 +777,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   d.ws_p = p_bytes;
   d.ws_w = align_up((size_t)d.S * Np * Np * es);
   d.ws_ch = align_up((size_t)d.S * (d.c.Lpt / 32) * 4);
-  d.ws_row = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * es);
+  d.ws_row = 2 * align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * es) + align_up((size_t)d.S * d.c.B * d.c.B * es);  // 2 x rowg, T21
   // hybrid: while k0 is small the gathered contraction (L k0 B per sample, from the transposed U)
   // costs less than the GEMM's full-N one (L N B); crossover measured on C4/C5.
   // Complex contractions do 2x the flops per gathered byte, so gathering pays longer.
@@ -813,6 +819,14 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
             d.ws_g;
   const size_t gjs = cx ? dense_gj_bytes<cplx>((int)Np) : dense_gj_bytes<double>((int)Np);
   if (gjs > kMaxSmem) return fail(FFS_EINVAL, "block-step path: N'=%lld too large for the GJ tile", (long long)Np);
+  const size_t gj2s = cx ? dense_gj2_bytes<cplx>((int)Np) : dense_gj2_bytes<double>((int)Np);
+  // measured: real C5 675.2 -> 659.9 ms (the pair kernel moves half the W bytes but doubles the per-CTA
+  // gathers of V[X, m_i]); complex C4 701 -> 773 ms (16 complex accumulators per column spill at 128
+  // registers), so complex keeps one pass per block unless the option is 2
+  const double gp = ffsh::option(FFS_OPT_GJ_PAIR);
+  d.gj_pair = ((gp == 2.0 || (gp != 0.0 && !cx)) && gj2s <= kMaxSmem) ? 1 : 0;
+  if (d.gj_pair)
+    if (int rc = ffsh::ensure_max_smem(cx ? dense_gj2_fn<cplx>() : dense_gj2_fn<double>())) return rc;
   return ffsh::ensure_max_smem(cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>());
 }
 
@@ -885,7 +899,10 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
   double* Y = d.ws_y ? reinterpret_cast<double*>(Yb) : nullptr;
   double* Pd = reinterpret_cast<double*>(Pb);
   double* Wd = reinterpret_cast<double*>(Wb);
-  double* rowg = reinterpret_cast<double*>(rowb);
+  const size_t rowg_bytes = align_up((size_t)d.S * (d.c.B * d.c.B + d.c.B) * es);
+  double* rowg2[2] = {reinterpret_cast<double*>(rowb), reinterpret_cast<double*>(rowb + rowg_bytes)};
+  double* t21 = reinterpret_cast<double*>(rowb + 2 * rowg_bytes);
+  const void* gj2f = cx ? dense_gj2_fn<cplx>() : dense_gj2_fn<double>();
   for (int64_t base = 0; base < M; base += d.S) {
     const int64_t nh = std::min<int64_t>(d.S, M - base);
     if (Y && cudaMemsetAsync(Y, 0, d.ws_y, stream) != cudaSuccess) return fail(FFS_ECUDA, "memset failed");
@@ -916,7 +933,7 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
     c.trace = S > 0 ? trace : nullptr;
     c.Pd = Pd;
     c.ldY = d.ldY;
-    c.rowg = rowg;
+    c.rowg = rowg2[0];
     c.permg = perm;
     c.chosen_g = ch;
     c.base = base;
@@ -937,7 +954,7 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
     q.U = static_cast<const double*>(U);
     q.perm = perm;
     q.positions = positions;
-    q.rowg = rowg;
+    q.rowg = rowg2[0];
     q.W = Wd;
     q.Y = Y;
     q.ldY = d.ldY;
@@ -946,6 +963,10 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
     q.base = base;
     const dim3 ggrid((unsigned)(f * d.ldY / ffsk::kGN), (unsigned)((L + ffsk::kGM - 1) / ffsk::kGM));
     for (int k0 = 0; k0 < Np; k0 += B) {
+      // this block's pivot rows go to rowg[(k0 / B) & 1]: the paired GJ update needs two blocks' factors
+      double* rowg = rowg2[(k0 / B) & 1];
+      c.rowg = rowg;
+      q.rowg = rowg;
       c.gather = k0 < d.k_gather ? 1 : 0;
       if (!c.gather) {
         if (ns) {
@@ -1021,9 +1042,45 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
         if (e != cudaSuccess) return fail(FFS_ECUDA, "step launch failed: %s", cudaGetErrorString(e));
         ++ffsh::launches();
       }
-      if (k0 + B < Np) {
+      // Gauss-Jordan update. Paired mode: an even block e (k0 = 2 B p) with later columns beyond the
+      // next block only updates that next block's B columns; after the odd block both blocks'
+      // trailing updates run in one pass over W (ffs_dense_gj2_kernel)
+      const bool even = ((k0 / B) & 1) == 0;
+      const bool pair_first = d.gj_pair && even && k0 + 2 * B < Np;
+      const bool pair_second = d.gj_pair && !even && k0 + B < Np;
+      if (pair_second) {
+        const int ke = k0 - B;  // the pair starts at the even block
+        if (cx)
+          ffsk::ffs_dense_t21_kernel<cplx, 8><<<(unsigned)nh, 256, 0, stream>>>(static_cast<const double*>(U), perm, positions, Wd,
+                                                                               t21, base, (int)N, (int)Np, ke);
+        else
+          ffsk::ffs_dense_t21_kernel<double, 8><<<(unsigned)nh, 256, 0, stream>>>(static_cast<const double*>(U), perm, positions,
+                                                                                 Wd, t21, base, (int)N, (int)Np, ke);
+        ffsk::DenseGj2Params q2{};
+        q2.U = static_cast<const double*>(U);
+        q2.perm = perm;
+        q2.positions = positions;
+        q2.rowg1 = rowg2[(ke / B) & 1];
+        q2.rowg2 = rowg;
+        q2.t21 = t21;
+        q2.W = Wd;
+        q2.Y = Y;
+        q2.ldY = d.ldY;
+        q2.base = base;
+        q2.N = (int)N;
+        q2.Np = (int)Np;
+        q2.k0 = ke;
+        const int nc = (int)Np - ke - 2 * B;
+        const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
+        const size_t gsm = cx ? dense_gj2_bytes<cplx>(ke) : dense_gj2_bytes<double>(ke);
+        void* qargs[] = {&q2};
+        e = cudaLaunchKernel(gj2f, jg, dim3(256), qargs, gsm, stream);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "gj2 launch failed: %s", cudaGetErrorString(e));
+        ffsh::launches() += 2;
+      } else if (k0 + B < Np) {
         q.k0 = k0;
-        const int nc = (int)Np - k0 - B;
+        q.jend = pair_first ? k0 + 2 * B : (int)Np;
+        const int nc = q.jend - k0 - B;
         const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
         const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
         void* qargs[] = {&q};

@@ -228,6 +228,8 @@ struct DenseGjParams {
   double* Y;                // [N][ldY] (complex: the real 2N x 2ldY expansion)
   int64_t ldY, base;        // ldY in scalars of T
   int N, Np, k0;
+  int jend;                 // columns k1 <= j < jend are updated (Np: all later columns; k1 + B: only the
+                            // next block's, when the rest follows in ffs_dense_gj2_kernel)
 };
 
 template <typename T, int B, int kGjTJ>
@@ -250,7 +252,8 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   const int t = threadIdx.x, jg = t % 64, part = t / 64;
   const int jl = jg * CPT;                        // first column of this thread within the tile
   const int j = k1 + blockIdx.x * kGjTJ + jl;     // first global column
-  const bool has = j < Np;
+  const int jend = q.jend;
+  const bool has = j < jend;
   T* Vn = reinterpret_cast<T*>(smem);   // [k0][B]   V[X_new, 0:k0] transposed (a row's B values contiguous)
   T* Zp = Vn + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
   T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
@@ -282,7 +285,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   __syncthreads();
   // 16-byte W accesses only when every row start is 16-byte aligned (N' even); the pair of
   // columns j, j+1 is loaded element-wise otherwise, and a pair past N' keeps its second slot 0
-  const bool two = j + 1 < Np;
+  const bool two = j + 1 < jend;
   const bool vec = two && (Np & 1) == 0;
   auto ldw = [&](int ii, T (&w)[CPT]) {
     const T* src = W + (size_t)ii * Np + j;
@@ -339,7 +342,7 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
   T* Wb = Vn;
   stage(Wb, k0 * B, [&](int idx) { return W[(size_t)(idx / B) * Np + k0 + idx % B]; });
   // (2) one thread per column: Z = S^{-1} (V[X_new, j] - sum)
-  if (t < kGjTJ && k1 + blockIdx.x * kGjTJ + t < Np) {
+  if (t < kGjTJ && k1 + blockIdx.x * kGjTJ + t < jend) {
     const int c = t, jc = k1 + blockIdx.x * kGjTJ + c;
     T z[B];
 #pragma unroll
@@ -422,6 +425,309 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
       dense_y_store<T>(q.Y, q.ldY, pm[ii], col0 + c, c < nb1 ? S::neg(W[(size_t)ii * Np + k1 + c]) : S::zero());
     }
     if (t < nb1) dense_y_store<T>(q.Y, q.ldY, pm[k1 + t], col0 + t, S::one());
+  }
+}
+
+
+// ---------------------------------------------------------------- paired Gauss-Jordan update
+// Two consecutive blocks' trailing updates in ONE pass over W (half the W traffic of two
+// ffs_dense_gj_kernel launches: the update is HBM-bound, 8 FMAs per element read twice and written
+// once). Blocks e = [k0, k0+8) and o = [k0+8, k0+16) with drawn rows X1, X2 and Schur factors
+// S1 = L1 U1, S2 = L2 U2 (rowg1, rowg2). After block e only its next 8 columns were updated (the
+// single-block kernel restricted to one 8-column tile), so for the later columns j >= k0+16 W still
+// holds the state W_old of block start k0, while W[0:k0, k0:k0+8] = Wb1 and W[0:k0+8, k0+8:k0+16] =
+// Wb2 are the two blocks' own coefficient panels. With a1 = V[X1, 0:k0] W_old[0:k0, j] and
+// a2 = V[X2, 0:k0] W_old[0:k0, j] (one pass, 16 accumulators per column):
+//   z1 = S1^{-1} (V[X1, j] - a1)
+//   z2 = S2^{-1} (V[X2, j] - a2 + (V[X2, 0:k0] Wb1) z1 - V[X2, k0:k0+8] z1)
+//   W[0:k0, j] = W_old - Wb1[0:k0] z1 - Wb2[0:k0] z2     (second pass)
+//   W[k0:k0+8, j] = z1 - Wb2[k0:k0+8] z2,   W[k0+8:k0+16, j] = z2
+// -- the same arithmetic as two single-block updates in a different association. T21 = V[X2, 0:k0] Wb1
+// (8 x 8) is formed per CTA from the staged operands. The tile holding columns k0+16 .. k0+23
+// scatters the next block's Y_s columns.
+struct DenseGj2Params {
+  const double* U;
+  const int32_t* perm;
+  const int32_t* positions;
+  const double* rowg1;      // [Sb][B*B + B] of block e
+  const double* rowg2;      // of block o
+  const double* t21;        // [Sb][B*B] T21 = V[X2, 0:k0] Wb1 (ffs_dense_t21_kernel)
+  double* W;
+  double* Y;
+  int64_t ldY, base;
+  int N, Np, k0;
+};
+
+// T21[r][c] = sum_{i<k0} V[X2[r], m_i] W[i][k0+c], one CTA of 256 threads per batch sample
+// (thread = (r, c) x 4 slices of i)
+template <typename T, int B>
+static __global__ void __launch_bounds__(256) ffs_dense_t21_kernel(const double* __restrict__ U, const int32_t* __restrict__ perm,
+                                                                  const int32_t* __restrict__ positions,
+                                                                  const double* __restrict__ Wg, double* __restrict__ t21,
+                                                                  int64_t base, int N, int Np, int k0) {
+  using S = Sc<T>;
+  static_assert(B * B * 4 == 256, "thread mapping");
+  __shared__ double red[4][B * B][2];
+  const int sl = blockIdx.x, t = threadIdx.x, e = t % (B * B), part = t / (B * B);
+  const int r = e / B, c = e % B;
+  const int64_t i_s = base + sl;
+  const int32_t* pm = perm + i_s * Np;
+  const T* Ug = reinterpret_cast<const T*>(U);
+  const T* W = reinterpret_cast<const T*>(Wg) + (size_t)sl * Np * Np;
+  const size_t xrow = (size_t)positions[i_s * Np + k0 + B + r] * N;
+  T a = S::zero();
+  int i = part;
+  for (; i + 12 < k0; i += 16) {
+    T v[4], w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = Ug[xrow + pm[i + 4 * u]];
+      w[u] = W[(size_t)(i + 4 * u) * Np + k0 + c];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a = S::fms(v[u], w[u], a);
+  }
+  for (; i < k0; i += 4) a = S::fms(Ug[xrow + pm[i]], W[(size_t)i * Np + k0 + c], a);
+  const T m = S::neg(a);
+  red[part][e][0] = reinterpret_cast<const double*>(&m)[0];
+  red[part][e][1] = S::kDoubles == 2 ? reinterpret_cast<const double*>(&m)[S::kDoubles - 1] : 0.0;
+  __syncthreads();
+  if (part == 0) {
+    double* out = t21 + ((size_t)sl * B * B + e) * S::kDoubles;
+    out[0] = (red[0][e][0] + red[1][e][0]) + (red[2][e][0] + red[3][e][0]);
+    if (S::kDoubles == 2) out[1] = (red[0][e][1] + red[1][e][1]) + (red[2][e][1] + red[3][e][1]);
+  }
+}
+
+constexpr int kGj2KC = 128;  // rows of V[X1 u X2, .] / of the coefficient panels staged per chunk
+
+template <typename T, int B, int kGjTJ>
+__host__ __device__ inline size_t dense_gj2_smem(int) {
+  // chunk [kGj2KC][2B], Zp [4][2B][TJ], Zs [2B][TJ], T21 + V2n + Wb2 rows k0..k0+B-1 ([B][B] each),
+  // Row/Pinv x 2, positions
+  return sizeof(T) * ((size_t)2 * B * kGj2KC + 4 * 2 * B * kGjTJ + 2 * B * kGjTJ + 3 * B * B + 2 * (B * B + B)) +
+         sizeof(int) * 2 * B + 16;
+}
+
+template <typename T, int B, int kGjTJ>
+static __global__ void __launch_bounds__(256, 2) ffs_dense_gj2_kernel(const DenseGj2Params q) {
+  using S = Sc<T>;
+  constexpr int CPT = kGjTJ / 64;
+  constexpr int UNR = 4;
+  constexpr int B2 = 2 * B;
+  static_assert(CPT == 1 || (CPT == 2 && sizeof(T) == 8), "two columns per thread only for real");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int k0 = q.k0, k1 = k0 + B, k2 = k0 + B2, Np = q.Np, N = q.N;
+  const int sl = blockIdx.y;
+  const int64_t i_s = q.base + sl;
+  const int t = threadIdx.x, jg = t % 64, part = t / 64;
+  const int jl = jg * CPT;
+  const int j = k2 + blockIdx.x * kGjTJ + jl;
+  const bool has = j < Np;
+  T* Ch = reinterpret_cast<T*>(smem);     // [kGj2KC][2B]: V[X1 u X2, m_i] (pass 1), W[i][k0:k2] (pass 2)
+  T* Zp = Ch + (size_t)B2 * kGj2KC;       // [4][2B][TJ]
+  T* Zs = Zp + 4 * B2 * kGjTJ;            // [2B][TJ]: z1 (rows 0..B-1), z2
+  T* T21 = Zs + B2 * kGjTJ;               // [B][B]
+  T* V2n = T21 + B * B;                   // [B][B] V[X2, m_{k0+c}]
+  T* W2r = V2n + B * B;                   // [B][B] Wb2 rows k0 .. k0+B-1
+  T* RP1 = W2r + B * B;                   // Row1 [B][B], Pinv1 [B]
+  T* RP2 = RP1 + B * B + B;
+  int* xn = reinterpret_cast<int*>(RP2 + B * B + B);  // X1 (0..B-1), X2 (B..2B-1)
+  const int32_t* pm = q.perm + i_s * Np;
+  const T* Ug = reinterpret_cast<const T*>(q.U);
+  T* W = reinterpret_cast<T*>(q.W) + (size_t)sl * Np * Np;
+  if (t < B2) xn[t] = q.positions[i_s * Np + k0 + t];
+  if (t < B * B + B) {
+    RP1[t] = reinterpret_cast<const T*>(q.rowg1)[(size_t)sl * (B * B + B) + t];
+    RP2[t] = reinterpret_cast<const T*>(q.rowg2)[(size_t)sl * (B * B + B) + t];
+  }
+  __syncthreads();
+  if (t < B * B) {
+    V2n[t] = Ug[(size_t)xn[B + t / B] * N + pm[k0 + t % B]];
+    W2r[t] = W[(size_t)(k0 + t / B) * Np + k1 + t % B];
+    T21[t] = reinterpret_cast<const T*>(q.t21)[(size_t)sl * B * B + t];
+  }
+  // one chunk of kc rows x 2B values: 8 independent loads per thread in flight
+  auto stage = [&](int n, auto&& src) {
+    for (int b0 = t; b0 < n; b0 += 8 * (int)blockDim.x) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = b0 + u * (int)blockDim.x;
+        if (idx < n) v[u] = src(idx);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = b0 + u * (int)blockDim.x;
+        if (idx < n) Ch[idx] = v[u];
+      }
+    }
+  };
+  const bool two = j + 1 < Np;
+  const bool vec = two && (Np & 1) == 0;
+  auto ldw = [&](int ii, T (&w)[CPT]) {
+    const T* src = W + (size_t)ii * Np + j;
+    if constexpr (CPT == 2) {
+      if (vec) {
+        const double2 v = *reinterpret_cast<const double2*>(src);
+        w[0] = v.x;
+        w[1] = v.y;
+      } else {
+        w[0] = src[0];
+        w[1] = two ? src[1] : S::zero();
+      }
+    } else {
+      w[0] = src[0];
+    }
+  };
+  // (1) minus the partial sums a1, a2 over this thread's slice of i (rows part, part + 4, ..)
+  T acc[CPT][B2];
+#pragma unroll
+  for (int e = 0; e < CPT; ++e)
+#pragma unroll
+    for (int tt = 0; tt < B2; ++tt) acc[e][tt] = S::zero();
+  for (int c0 = 0; c0 < k0; c0 += kGj2KC) {
+    const int kc = min(kGj2KC, k0 - c0);
+    __syncthreads();
+    stage(B2 * kc, [&](int idx) { return Ug[(size_t)xn[idx % B2] * N + pm[c0 + idx / B2]]; });
+    __syncthreads();
+    if (has) {
+      int il = part;  // kGj2KC is a multiple of 4: the slices stay aligned across chunks
+      for (; il + 4 * (UNR - 1) < kc; il += 4 * UNR) {
+        T w[UNR][CPT];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) ldw(c0 + il + 4 * u, w[u]);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int tt = 0; tt < B2; ++tt) {
+            const T vn = Ch[(il + 4 * u) * B2 + tt];
+#pragma unroll
+            for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(vn, w[u][e], acc[e][tt]);
+          }
+      }
+      for (; il < kc; il += 4) {
+        T w[CPT];
+        ldw(c0 + il, w);
+#pragma unroll
+        for (int tt = 0; tt < B2; ++tt)
+#pragma unroll
+          for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(Ch[il * B2 + tt], w[e], acc[e][tt]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < CPT; ++e)
+#pragma unroll
+    for (int tt = 0; tt < B2; ++tt) Zp[(part * B2 + tt) * kGjTJ + jl + e] = acc[e][tt];
+  __syncthreads();
+  // (2) one thread per column: z1, z2 and the 2B new rows
+  if (t < kGjTJ && k2 + blockIdx.x * kGjTJ + t < Np) {
+    const int c = t, jc = k2 + blockIdx.x * kGjTJ + c;
+    auto solve = [&](T (&z)[B], const T* Row, const T* Pinv) {
+#pragma unroll
+      for (int tt = 1; tt < B; ++tt)
+#pragma unroll
+        for (int s2 = 0; s2 < tt; ++s2) z[tt] = S::fms(S::mul(Row[tt * B + s2], Pinv[s2]), z[s2], z[tt]);
+#pragma unroll
+      for (int tt = B - 1; tt >= 0; --tt) {
+#pragma unroll
+        for (int s2 = tt + 1; s2 < B; ++s2) z[tt] = S::fms(Row[tt * B + s2], z[s2], z[tt]);
+        z[tt] = S::mul(z[tt], Pinv[tt]);
+      }
+    };
+    T z1[B], z2[B];
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt) {
+      const T a01 = S::add(Zp[(0 * B2 + tt) * kGjTJ + c], Zp[(1 * B2 + tt) * kGjTJ + c]);
+      const T a23 = S::add(Zp[(2 * B2 + tt) * kGjTJ + c], Zp[(3 * B2 + tt) * kGjTJ + c]);
+      z1[tt] = S::add(Ug[(size_t)xn[tt] * N + pm[jc]], S::add(a01, a23));
+      const T b01 = S::add(Zp[(0 * B2 + B + tt) * kGjTJ + c], Zp[(1 * B2 + B + tt) * kGjTJ + c]);
+      const T b23 = S::add(Zp[(2 * B2 + B + tt) * kGjTJ + c], Zp[(3 * B2 + B + tt) * kGjTJ + c]);
+      z2[tt] = S::add(Ug[(size_t)xn[B + tt] * N + pm[jc]], S::add(b01, b23));
+    }
+    solve(z1, RP1, RP1 + B * B);
+    // r2 += T21 z1 - V[X2, k0:k1] z1   (T21 = V[X2, 0:k0] Wb1)
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt)
+#pragma unroll
+      for (int cc = 0; cc < B; ++cc) {
+        z2[tt] = S::fms(S::neg(T21[tt * B + cc]), z1[cc], z2[tt]);
+        z2[tt] = S::fms(V2n[tt * B + cc], z1[cc], z2[tt]);
+      }
+    solve(z2, RP2, RP2 + B * B);
+#pragma unroll
+    for (int tt = 0; tt < B; ++tt) {
+      Zs[tt * kGjTJ + c] = z1[tt];
+      Zs[(B + tt) * kGjTJ + c] = z2[tt];
+      T w1 = z1[tt];
+#pragma unroll
+      for (int cc = 0; cc < B; ++cc) w1 = S::fms(W2r[tt * B + cc], z2[cc], w1);
+      W[(size_t)(k0 + tt) * Np + jc] = w1;
+      W[(size_t)(k1 + tt) * Np + jc] = z2[tt];
+    }
+  }
+  __syncthreads();
+  // (3) rank-2B update of the earlier rows, chunks in REVERSE order (the rows pass 1 read last are
+  // the ones most likely still in L2); Ch holds W[i][k0:k2] = (Wb1[i], Wb2[i])
+  T z[CPT][B2];
+#pragma unroll
+  for (int e = 0; e < CPT; ++e)
+#pragma unroll
+    for (int tt = 0; tt < B2; ++tt) z[e][tt] = has ? Zs[tt * kGjTJ + jl + e] : S::zero();
+  auto upd = [&](int ii, int il, T (&a)[CPT]) {
+    const T* wb = Ch + (size_t)il * B2;
+#pragma unroll
+    for (int tt = 0; tt < B2; ++tt) {
+      const T wv = wb[tt];
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) a[e] = S::fms(wv, z[e][tt], a[e]);
+    }
+    T* dst = W + (size_t)ii * Np + j;
+    if constexpr (CPT == 2) {
+      if (vec) {
+        *reinterpret_cast<double2*>(dst) = make_double2(a[0], a[1]);
+      } else {
+        dst[0] = a[0];
+        if (two) dst[1] = a[1];
+      }
+    } else {
+      dst[0] = a[0];
+    }
+  };
+  const int nchunks = (k0 + kGj2KC - 1) / kGj2KC;
+  for (int cb = nchunks - 1; cb >= 0; --cb) {
+    const int c0 = cb * kGj2KC;
+    const int kc = min(kGj2KC, k0 - c0);
+    __syncthreads();
+    stage(B2 * kc, [&](int idx) { return W[(size_t)(c0 + idx / B2) * Np + k0 + idx % B2]; });
+    __syncthreads();
+    if (has) {
+      int m = ((kc - part + 3) >> 2) - 1;
+      for (; m >= UNR - 1; m -= UNR) {
+        T a[UNR][CPT];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) ldw(c0 + part + 4 * (m - u), a[u]);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) upd(c0 + part + 4 * (m - u), part + 4 * (m - u), a[u]);
+      }
+      for (; m >= 0; --m) {
+        T a[CPT];
+        ldw(c0 + part + 4 * m, a);
+        upd(c0 + part + 4 * m, part + 4 * m, a);
+      }
+    }
+  }
+  // next block's Y_s columns (the tile holding columns k2 .. k2+B-1)
+  if (blockIdx.x == 0 && q.Y != nullptr) {
+    __syncthreads();
+    const int nb1 = min(B, Np - k2);
+    const int64_t col0 = (int64_t)sl * B;
+    for (int idx = t; idx < k2 * B; idx += blockDim.x) {
+      const int ii = idx / B, c = idx % B;
+      dense_y_store<T>(q.Y, q.ldY, pm[ii], col0 + c, c < nb1 ? S::neg(W[(size_t)ii * Np + k2 + c]) : S::zero());
+    }
+    if (t < nb1) dense_y_store<T>(q.Y, q.ldY, pm[k2 + t], col0 + t, S::one());
   }
 }
 

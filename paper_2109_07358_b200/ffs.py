@@ -33,6 +33,7 @@ OPTIONS = {
     "dense_min_l": 12,      # smallest L on the block-step paths (default 2048)
     "dense_min_n": 13,      # smallest N on the block-step paths (default 256)
     "tile_gram": 14,        # 1: small-N' real shapes on the tile-Gram path (default)
+    "gj_pair": 15,          # 1: two blocks' trailing Gauss-Jordan updates in one pass (default)
 }
 
 EXPORTED = (

@@ -1,6 +1,5 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-python tools/run_once.py peierls 1 > /dev/null 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ll_peierls.csv python tools/run_once.py peierls 1 > /dev/null 2>&1
-python tools/launch_share.py gpurun_out/ll_peierls.csv > gpurun_out/ll_peierls.txt; head -7 gpurun_out/ll_peierls.txt
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "dense_path or gram_draw or small_batches" 2>&1 | tail -3
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "dense_path or gram_draw or small_batches or graph_replay or panel_paths or odd_marginal or large_L" 2>&1 | tail -6
+timeout 600 python tools/theta_scan.py dpp - gj_pair=0 2>&1 | tail -2
+timeout 600 python tools/theta_scan.py peierls - gj_pair=0 2>&1 | tail -2
