@@ -202,7 +202,9 @@ typedef enum {
   FFS_OPT_GEMM_2SM = 9,         /* 1 (default): the 8-slice Ozaki GEMM runs as CTA pairs (tcgen05
                                    cta_group::2, 256 x 64 tiles); 0: one CTA per 128 x 64 tile */
   FFS_OPT_GRAM_DRAW = 10,       /* 1 (default): the draws of a GEMM block step run one warp per sample on
-                                   the tile Gram matrices of the panel (ffs_gram.cuh);
+                                   the tile Gram matrices of the panel (ffs_gram.cuh) -- also the
+                                   gathered blocks, whose panel the cluster kernel then only contracts
+                                   (3: gathered blocks draw in the cluster kernel);
                                    0: the cluster step kernel (panel in registers) */
   FFS_OPT_GRAM_KAPPA = 11,      /* Gram draws: recompute the tile totals directly from the panel when
                                    T < bound / kappa (cancellation guard); default 1e4 */

@@ -1005,7 +1005,17 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
       }
       c.k0 = k0;
       cudaError_t e;
-      if (!c.gather && d.gram) {
+      // gathered blocks of a full-sampling call with the Gram draws: the cluster kernel only contracts
+      // the panel (into the GEMM's output buffer), the draws run on the Gram path like a GEMM block
+      const bool panel_only = c.gather && d.gram && d.ws_p > 0 && ffsh::option(FFS_OPT_GRAM_DRAW) != 3.0;
+      c.panel_out = panel_only ? 1 : 0;
+      if (panel_only) {
+        void* args[] = {&c};
+        e = launch_cluster_kernel(d.c.fn, d.c.CS, (int)(nh * d.c.CS), d.c.threads, d.c.smem, stream, args);
+        if (e != cudaSuccess) return fail(FFS_ECUDA, "panel launch failed: %s", cudaGetErrorString(e));
+        ++ffsh::launches();
+      }
+      if ((!c.gather || panel_only) && d.gram) {
         // draws on the tile Gram matrices of the GEMM panel: one pass over P, then a warp per sample
         ffsk::GramParams g{};
         g.Pd = Pd;

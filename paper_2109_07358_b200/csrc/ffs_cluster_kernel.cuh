@@ -42,6 +42,8 @@ struct ClusterParams {
   uint32_t* chosen_g;      // [Sb][Lpt/32] rows drawn so far (bit per row)
   int k0, Sb;
   int gather;              // STEP: 1 = contract the gathered columns of Ut (no GEMM for this block)
+  int panel_out;           // STEP + gather: 1 = only write the contracted panel to Pd ([L][B] per sample);
+                           // the draws follow in ffs_gram_kernel + ffs_gram_draw_kernel (ffs_gram.cuh)
   int64_t base;
 };
 
@@ -243,6 +245,24 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
             for (int r = 0; r < R; ++r) P[r][c] = S::fms(v[r], wb[c], P[r][c]);
         }
       }
+      bool draws_here = true;
+      if constexpr (STEP) {
+        if (p.panel_out) {
+          // the gathered panel goes to global memory in the GEMM's layout; no draws in this kernel
+          double2* pb = reinterpret_cast<double2*>(const_cast<T*>(reinterpret_cast<const T*>(p.Pd)) + ((size_t)sl * L + row0) * B);
+          constexpr int kV = B * S::kDoubles / 2;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (row0 + r < L) {
+#pragma unroll
+              for (int v = 0; v < kV; ++v) {
+                if constexpr (S::kDoubles == 1) pb[r * kV + v] = make_double2(P[r][2 * v], P[r][2 * v + 1]);
+                else pb[r * kV + v] = make_double2(reinterpret_cast<double*>(&P[r][v])[0], reinterpret_cast<double*>(&P[r][v])[1]);
+              }
+            }
+          draws_here = false;
+        }
+      }
       // rows drawn earlier: exactly zero weight in the first column of this block
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -256,7 +276,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       // take an extra, cluster-uniform round (rare).
       static_for<0, B>([&](auto rrc) {
         constexpr int rr = decltype(rrc)::value;
-        if (rr < nb) {
+        if (rr < nb && draws_here) {
           const int k = k0 + rr;
           double w[R], c[R];
           double acc = 0.0;
@@ -444,7 +464,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
       if constexpr (STEP) {
         // the Gauss-Jordan update runs batched in ffs_dense_gj_kernel: hand it S = L U of this block
         __syncthreads();  // the last draw's Row / Pinv entries come from other warps
-        if (rank == 0 && t < B * B + B) {
+        if (draws_here && rank == 0 && t < B * B + B) {
           T* rg = reinterpret_cast<T*>(p.rowg) + sl * (B * B + B);
           rg[t] = t < B * B ? Row[t] : Pinv[t - B * B];
         }
@@ -543,6 +563,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
     // ---- a6: positions (rank 0) and flags (OR over the cluster, collected in rank 0)
     const int fcta = (__syncthreads_or(flag & 1) ? 1 : 0) | (__syncthreads_or(flag & 2) ? 2 : 0);
     if constexpr (STEP) {
+      if (p.panel_out) continue;  // no draws here: nothing to publish, no DSMEM traffic to fence
       const int nbs = min(B, Np - p.k0);
       if (rank == 0)
         for (int j = p.k0 + t; j < p.k0 + nbs; j += blockDim.x) p.positions[i * Np + j] = pos[j];

@@ -261,6 +261,8 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
                                   {"dense_theta": 0, "gram_kappa": 0},
                                   {"dense_theta": 0, "gj_pair": 0},
                                   {"dense_theta": 0.1, "gj_pair": 2},
+                                  {"dense_theta": 0.6, "gram_draw": 3},
+                                  {"dense_theta": 1, "gram_draw": 3, "dense_batch": 9},
                                   {"dense_theta": 0.4, "dense_batch": 5, "gj_pair": 0},
                                   {"dense_theta": 0, "gram_kappa": 1e30}])
 def test_dense_path_schedules(opts, cplx):
