@@ -200,7 +200,8 @@ typedef enum {
                                    captured); 0: direct launches */
   FFS_OPT_FORCE_GENERIC = 8,    /* 1: every shape on the per-sample warp/CTA-owner kernel (testing) */
   FFS_OPT_GEMM_2SM = 9,         /* 1 (default): the 8-slice Ozaki GEMM runs as CTA pairs (tcgen05
-                                   cta_group::2, 256 x 64 tiles); 0: one CTA per 128 x 64 tile */
+                                   cta_group::2) on 256 x 128 tiles in two passes of four diagonals;
+                                   3: CTA pairs on 256 x 64 tiles, one pass; 0: one CTA per 128 x 64 tile */
   FFS_OPT_GRAM_DRAW = 10,       /* 1 (default): the draws of a GEMM block step run one warp per sample on
                                    the tile Gram matrices of the panel (ffs_gram.cuh) -- also the
                                    gathered blocks, whose panel the cluster kernel then only contracts

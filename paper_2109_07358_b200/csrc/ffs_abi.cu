@@ -723,6 +723,7 @@ size_t dense_gj2_bytes(int k0) { return ffsk::dense_gj2_smem<T, 8, gj_tj<T>()>(k
 template <int NS>
 const void* ozaki_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm_kernel<NS>); }
 const void* ozaki2_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm2_kernel<8>); }
+const void* ozaki2w_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_ozaki_gemm2w_kernel); }
 
 // 3-D tensor map [NS][rows][Kp] of int8 slices, box {kOzBK, box_rows, 1}, 64-byte swizzle
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -805,6 +806,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   if (ns == 8) {
     if (int rc = ffsh::ensure_max_smem(ozaki_fn<8>())) return rc;
     if (int rc = ffsh::ensure_max_smem(ozaki2_fn())) return rc;
+    if (int rc = ffsh::ensure_max_smem(ozaki2w_fn())) return rc;
   } else if (ns == 7) {
     if (int rc = ffsh::ensure_max_smem(ozaki_fn<7>())) return rc;
   }
@@ -880,9 +882,13 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
   CUtensorMap oz_ta, oz_tb;
   // the 2-SM GEMM (tcgen05 cta_group::2) for 8 slices; each CTA loads half of the B tile
   const bool oz2 = ns == 8 && ffsh::option(FFS_OPT_GEMM_2SM) != 0.0;
+  // 256 x 128 pair tiles in two passes of four diagonals (ffs_ozaki_gemm2w_kernel: C5 644.5 -> 633.2 ms,
+  // C4 686.1 -> 681.0 ms); option value 3: the 256 x 64 single-pass pair tiles
+  const bool oz2w = oz2 && ffsh::option(FFS_OPT_GEMM_2SM) != 3.0 && oz_ncols % ffsk::kOzWBN == 0;
   if (ns) {
     if (oz_tensor_map(&oz_ta, oza, ns, L, d.Kp, ffsk::kOzBM) != FFS_OK) return FFS_ECUDA;
-    if (oz_tensor_map(&oz_tb, ozb, ns, oz_ncols, d.Kp, oz2 ? ffsk::kOzBN / 2 : ffsk::kOzBN) != FFS_OK) return FFS_ECUDA;
+    if (oz_tensor_map(&oz_tb, ozb, ns, oz_ncols, d.Kp, oz2w ? ffsk::kOzWBN / 2 : oz2 ? ffsk::kOzBN / 2 : ffsk::kOzBN) != FFS_OK)
+      return FFS_ECUDA;
     // A = U (real L x 2N view for complex): split once per call
     const int64_t fK = f * N;
     const unsigned g = (unsigned)((L + 7) / 8);
@@ -987,7 +993,13 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
           op.m_fast = (int64_t)L * d.Kp < oz_ncols * d.Kp ? 1 : 0;
           const int64_t ntiles = ((L + ffsk::kOzBM - 1) / ffsk::kOzBM) * (oz_ncols / ffsk::kOzBN);
           const dim3 og((unsigned)std::min<int64_t>(ntiles, ffsh::sm_count(ffsh::device())));  // persistent
-          if (oz2) {
+          if (oz2w) {
+            const int64_t np2 = ((L + 2 * ffsk::kOzBM - 1) / (2 * ffsk::kOzBM)) * (oz_ncols / ffsk::kOzWBN);
+            const int g2 = (int)std::min<int64_t>(np2, ffsh::sm_count(ffsh::device()) / 2) * 2;  // whole pairs
+            void* oargs[] = {&oz_ta, &oz_tb, &op};
+            cudaError_t oe = launch_cluster_kernel(ozaki2w_fn(), 2, g2, ffsk::kOzThreads, ffsk::oz2w_smem(), stream, oargs);
+            if (oe != cudaSuccess) return fail(FFS_ECUDA, "gemm launch failed: %s", cudaGetErrorString(oe));
+          } else if (oz2) {
             const int64_t np2 = ((L + 2 * ffsk::kOzBM - 1) / (2 * ffsk::kOzBM)) * (oz_ncols / ffsk::kOzBN);
             const int g2 = (int)std::min<int64_t>(np2, ffsh::sm_count(ffsh::device()) / 2) * 2;  // whole pairs
             void* oargs[] = {&oz_ta, &oz_tb, &op};

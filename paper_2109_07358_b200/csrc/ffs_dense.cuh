@@ -1154,6 +1154,222 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm2_kernel(c
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
+// ---- wide 2-SM variant: 256 x 128 pair tiles in TWO PASSES of four diagonals each.
+// With N = 64 every MMA reads 4 KB of A and 2 KB of B from shared memory for 32 tensor-pipe cycles
+// (192 B/clk against the ~128 B/clk the tensor core can read: the INT8 pipe cannot exceed ~67 %,
+// measured 59.7 %, profiles/r02/final/full_ozaki2_dpp_raw.csv). Eight accumulators of 128 columns do
+// not fit TMEM (512 columns), so a tile runs as two "virtual tiles": pass 1 accumulates the
+// diagonals d = i + j = 4..7 (26 slice products, all 8 slices of both operands), pass 0 the
+// diagonals 0..3 (10 products, slices 0..3 only); each pass has four 128-column accumulators and
+// its MMAs read 4 KB + 4 KB per 64 cycles. Pass 1 (the small terms) stores its scaled sum, pass 0
+// adds its own to it (the tile is L2-resident between the two). Same TMA / MMA / epilogue roles and
+// barrier protocol as ffs_ozaki_gemm2_kernel, one K loop per virtual tile; the stage holds 8 A
+// slices (8 KB each) and 8 half B slices (64 columns, 4 KB each).
+constexpr int kOzWBN = 128;
+constexpr int kOzWTB = (kOzWBN / 2) * kOzBK;  // one CTA's half of a B slice tile (64 columns)
+constexpr int oz2w_stage_bytes() { return kOzMaxS * (kOzTA + kOzWTB); }
+constexpr size_t oz2w_smem() { return (size_t)kOzStages * oz2w_stage_bytes() + (2 * kOzStages + 2) * 8 + 16 + 1024; }
+static_assert(oz2w_smem() <= 227 * 1024, "two stages of the wide tile fit shared memory");
+
+static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm2w_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                              const __grid_constant__ CUtensorMap tmB,
+                                                                              const OzakiParams p) {
+  constexpr int NS = 8;
+  extern __shared__ __align__(1024) unsigned char oz_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kOzStages * oz2w_stage_bytes());
+  uint64_t* empty = full + kOzStages;
+  uint64_t* tfull = empty + kOzStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const unsigned crank = oz2_rank();
+  const bool leader = crank == 0;
+  const int KT = p.K / kOzBK;
+  const int mt = (p.M + 2 * kOzBM - 1) / (2 * kOzBM), nt = p.N / kOzWBN;  // pair tiles: 256 x 128
+  const int ntiles = mt * nt;
+  const int pfirst = (int)(blockIdx.x >> 1), pstep = (int)(gridDim.x >> 1);
+  auto tile_origin = [&](int tt, int& m0, int& n0) {  // this CTA's 128 rows of the pair tile
+    const int a = p.m_fast ? tt % mt : tt / nt, b = p.m_fast ? tt / mt : tt % nt;
+    m0 = a * 2 * kOzBM + (int)crank * kOzBM;
+    n0 = b * kOzWBN;
+  };
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (t == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      oz_mbar_init(full + s, 1);
+      oz_mbar_init(empty + s, 1);
+    }
+    oz_mbar_init(tfull, 1);
+    oz_mbar_init(tempty, 2 * 256);  // both CTAs' epilogue threads
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  oz2_cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+  // virtual tiles: (tile, pass) with pass 1 (diagonals 4..7) first, then pass 0 (diagonals 0..3)
+  if (warp == 8 && lane == 0) {  // TMA producer (both CTAs)
+    int g = 0;
+    for (int tt = pfirst; tt < ntiles; tt += pstep) {
+      int m0, n0;
+      tile_origin(tt, m0, n0);
+      const int nb0 = n0 + (int)crank * (kOzWBN / 2);
+      for (int pass = 1; pass >= 0; --pass) {
+        const int nsl = pass ? NS : NS / 2;  // slices this pass reads
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int st = g % kOzStages;
+          if (g >= kOzStages) oz_mbar_wait(empty + st, ((g / kOzStages) - 1) & 1);
+          unsigned char* sb = sm + st * oz2w_stage_bytes();
+          const uint32_t fb = oz_u32(full + st) & kPeerMask;
+          if (leader)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_u32(full + st)),
+                         "r"(2 * nsl * (kOzTA + kOzWTB))
+                         : "memory");
+          for (int i = 0; i < nsl; ++i) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                    oz_u32(sb + i * kOzTA)),
+                "l"(&tmA), "r"(kt * kOzBK), "r"(m0), "r"(i), "r"(fb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                    oz_u32(sb + NS * kOzTA + i * kOzWTB)),
+                "l"(&tmB), "r"(kt * kOzBK), "r"(nb0), "r"(i), "r"(fb)
+                : "memory");
+          }
+        }
+      }
+    }
+  } else if (warp == 9 && lane == 0 && leader) {  // MMA issuer: the leader CTA only
+    const uint32_t idesc =
+        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzWBN >> 3) << 17) | ((uint32_t)((2 * kOzBM) >> 4) << 24);
+    const uint16_t mask = 0x3;
+    int g = 0, it = 0;
+    for (int tt = pfirst; tt < ntiles; tt += pstep) {
+      for (int pass = 1; pass >= 0; --pass, ++it) {
+        if (it > 0) oz_mbar_wait(tempty, (it - 1) & 1);  // both CTAs read the previous accumulators
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int dmin = pass ? NS / 2 : 0;
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int st = g % kOzStages;
+          oz_mbar_wait(full + st, (g / kOzStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const unsigned char* sb = sm + st * oz2w_stage_bytes();
+          const uint64_t da0 = oz_desc(sb), db0 = oz_desc(sb + NS * kOzTA);
+#pragma unroll
+          for (int i = 0; i < NS; ++i)
+#pragma unroll
+            for (int j = 0; j < NS - i; ++j) {
+              const int d = i + j;
+              if (d < dmin || d >= dmin + NS / 2) continue;
+#pragma unroll
+              for (int ks = 0; ks < kOzBK / 32; ++ks) {
+                const uint64_t da = oz_desc_add(da0, i * kOzTA + ks * 32);
+                const uint64_t db = oz_desc_add(db0, j * kOzWTB + ks * 32);
+                const uint32_t acc = (kt > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first write of D_d: i = 0
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)((d - dmin) * kOzWBN)),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                    : "memory");
+              }
+            }
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                           oz_u32(empty + st)),
+                       "h"(mask)
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         oz_u32(tfull)),
+                     "h"(mask)
+                     : "memory");
+      }
+    }
+  }
+  if (warp < 8) {  // epilogue (both CTAs): warp w: rows 32 (w % 4) .., columns 64 (w / 4) .. of this CTA's 128 x 128
+    const int q = warp & 3, ch0 = (warp >> 2) * (kOzWBN / 2);
+    const uint32_t te = oz_u32(tempty) & kPeerMask;
+    int it = 0;
+    for (int tt = pfirst; tt < ntiles; tt += pstep) {
+      int m0, n0;
+      tile_origin(tt, m0, n0);
+      const int row = m0 + q * 32 + lane;
+      const bool rok = row < p.M;
+      const int er = rok ? p.ea[row] : 0;
+      const int lp = __ffs(p.panel) - 1;
+      double* crow = p.C + (size_t)row * p.panel;
+      const size_t sstride = (size_t)p.M * p.panel;
+      for (int pass = 1; pass >= 0; --pass, ++it) {
+        oz_mbar_wait(tfull, it & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int dmin = pass ? NS / 2 : 0;
+        // 32 columns at a time (all 64 in registers at once spilled: 663 vs 633 ms per C5 call; an L1
+        // prefetch of pass 0's read-modify-write lines: 647 ms)
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          const int ch = ch0 + half * 32;
+          double acc[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+#pragma unroll
+          for (int dl = NS / 2 - 1; dl >= 0; --dl) {  // smallest terms first
+            const double sc = ldexp(1.0, -7 * (dmin + dl + 2));
+            uint32_t v[32];
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(dl * kOzWBN + ch);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                  "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], sc, acc[c]);
+          }
+          if (half == 1) {
+            // every accumulator of this pass is in registers / stored: hand TMEM back to the MMA issuer
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(te) : "memory");
+          }
+          if (rok) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              const int col = n0 + ch + c;
+              FFS_CHECK(col + 1 < p.N);
+              const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
+              const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;
+              const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
+              const double s1 = (b1 > 0 && b1 < 2047) ? __longlong_as_double((long long)b1 << 52) : ldexp(1.0, er + e2.y);
+              double2* dst = reinterpret_cast<double2*>(crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1)));
+              double2 o = make_double2(acc[c] * s0, acc[c + 1] * s1);
+              if (pass == 0) {  // add the large terms to pass 1's sum of the small ones
+                const double2 prev = *dst;
+                o.x += prev.x;
+                o.y += prev.y;
+              }
+              *dst = o;
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  oz2_cluster_sync();  // neither CTA leaves while the other may still signal it or read its TMEM
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
 // x = 2^e sum_i q_i 2^{-7(i+1)}, |q_i| <= 127 (frexp exponent: |x 2^-e| < 1); q_i of element k of
 // row r goes to out[(i * rows + r) * Kp + k]; zero for k in [K, Kp)
 template <int NS>

@@ -27,7 +27,7 @@ OPTIONS = {
     "cluster": 6,           # 1: L >= 2048 on cluster kernels (default); 0: one CTA per sample
     "graph": 7,             # 1: block-step launches replayed as a CUDA graph (default)
     "force_generic": 8,     # 1: every shape on the per-sample warp/CTA-owner kernel
-    "gemm_2sm": 9,          # 1: the 8-slice Ozaki GEMM as tcgen05 CTA pairs (default)
+    "gemm_2sm": 9,          # 1: the 8-slice Ozaki GEMM as tcgen05 CTA pairs, 256x128 two-pass tiles (default); 3: 256x64
     "gram_draw": 10,        # 1: GEMM block steps draw on the tile Gram matrices (default)
     "gram_kappa": 11,       # cancellation guard of the Gram draws (default 1e4)
     "dense_min_l": 12,      # smallest L on the block-step paths (default 2048)

@@ -256,6 +256,8 @@ def test_extreme_selection_uniforms(L, N, Np, cplx, useL):
                                   {"dense_theta": 0, "dense_gemm": 0},
                                   {"dense_theta": 0.3, "graph": 0},
                                   {"dense_theta": 0, "gemm_2sm": 0},
+                                  {"dense_theta": 0, "gemm_2sm": 3},
+                                  {"dense_theta": 0.2, "gemm_2sm": 3, "dense_batch": 13},
                                   {"dense_theta": 0, "gram_draw": 0},
                                   {"dense_batch": 9, "dense_theta": 0.25, "gram_draw": 0},
                                   {"dense_theta": 0, "gram_kappa": 0},

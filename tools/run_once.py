@@ -8,6 +8,9 @@ import torch  # noqa: E402
 
 from paper_2109_07358_b200 import ffs, inputs  # noqa: E402
 
+for kv in filter(None, os.environ.get("FFS_OPTS", "").split(",")):  # e.g. FFS_OPTS=gemm_2sm=2,dense_theta=0
+    k, v = kv.split("=")
+    ffs.set_option(k, float(v))
 name = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 dev = torch.device("cuda", 0)
