@@ -513,7 +513,7 @@ template <typename T, int B, int kGjTJ>
 static __global__ void __launch_bounds__(256, 2) ffs_dense_gj2_kernel(const DenseGj2Params q) {
   using S = Sc<T>;
   constexpr int CPT = kGjTJ / 64;
-  constexpr int UNR = 4;
+  constexpr int UNR = sizeof(T) == 8 ? 4 : 2;  // complex: 16 complex accumulators + 4 loads in flight spill at 128 registers
   constexpr int B2 = 2 * B;
   static_assert(CPT == 1 || (CPT == 2 && sizeof(T) == 8), "two columns per thread only for real");
   extern __shared__ __align__(16) unsigned char smem[];

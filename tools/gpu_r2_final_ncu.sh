@@ -17,12 +17,13 @@ full() {  # name workload kernel-regex skip
   ncu -i $O/full_$1.ncu-rep --page raw --csv > $O/full_$1_raw.csv 2>/dev/null
   rm -f $O/full_$1.ncu-rep
 }
-full ozaki2_dpp dpp ffs_ozaki_gemm2_kernel 60
+full ozaki2_dpp dpp ffs_ozaki_gemm2w_kernel 60
 full gram_dpp dpp "ffs_gram_kernel" 60
 full gramdraw_dpp dpp ffs_gram_draw_kernel 60
 full gj_dpp dpp ffs_dense_gj_kernel 100
+full gj2_dpp dpp ffs_dense_gj2_kernel 50
 full step_dpp dpp ffs_cluster_kernel 8
-full ozaki2_peierls peierls ffs_ozaki_gemm2_kernel 30
+full ozaki2_peierls peierls ffs_ozaki_gemm2w_kernel 30
 full gram_peierls peierls "ffs_gram_kernel" 30
 full gramdraw_peierls peierls ffs_gram_draw_kernel 30
 full seg_dw dw ffs_seg_kernel 1

@@ -59,7 +59,7 @@ for wl, cap in [("dw", "seg_dw"), ("anderson", "sample_anderson"), ("anderson:ma
         g = sum(v for k, v in sh.items() if "ozaki_gemm" in k)
         out[wl]["traffic_source"] += " (the dominant kernel of the path)"
         out[wl]["gemm"] = {
-            "kernel": "ffs_ozaki_gemm2_kernel<8> (tcgen05.mma.cta_group::2.kind::i8, TMEM accumulators, TMA)",
+            "kernel": "ffs_ozaki_gemm2w_kernel (tcgen05.mma.cta_group::2.kind::i8, 256 x 128 pair tiles in two passes, TMEM accumulators, TMA)",
             "share_of_path": round(g, 4),
             "int8_pipe_active": d.get("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", 0) / 100,
             "tensor_pipe_active": d.get("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
