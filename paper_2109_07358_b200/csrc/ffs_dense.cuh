@@ -1342,22 +1342,30 @@ static __global__ void __launch_bounds__(kOzThreads, 1) ffs_ozaki_gemm2w_kernel(
             asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(te) : "memory");
           }
           if (rok) {
+            // 32-byte stores (one full sector per lane and instruction; the lanes of a warp are 64 /
+            // 128 bytes apart in the panel layout, so 16-byte stores cost two half-filled sector
+            // writes each)
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
+            for (int c = 0; c < 32; c += 4) {
               const int col = n0 + ch + c;
-              FFS_CHECK(col + 1 < p.N);
-              const int2 e2 = *reinterpret_cast<const int2*>(p.eb + col);
-              const int b0 = 1023 + er + e2.x, b1 = 1023 + er + e2.y;
-              const double s0 = (b0 > 0 && b0 < 2047) ? __longlong_as_double((long long)b0 << 52) : ldexp(1.0, er + e2.x);
-              const double s1 = (b1 > 0 && b1 < 2047) ? __longlong_as_double((long long)b1 << 52) : ldexp(1.0, er + e2.y);
-              double2* dst = reinterpret_cast<double2*>(crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1)));
-              double2 o = make_double2(acc[c] * s0, acc[c + 1] * s1);
-              if (pass == 0) {  // add the large terms to pass 1's sum of the small ones
-                const double2 prev = *dst;
-                o.x += prev.x;
-                o.y += prev.y;
+              FFS_CHECK(col + 3 < p.N);
+              const int4 e4 = *reinterpret_cast<const int4*>(p.eb + col);
+              const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
+              double o[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int bb = 1023 + er + eb4[u];  // 2^(ea + eb) from its biased exponent
+                const double sf = (bb > 0 && bb < 2047) ? __longlong_as_double((long long)bb << 52) : ldexp(1.0, er + eb4[u]);
+                o[u] = acc[c + u] * sf;
               }
-              *dst = o;
+              double* dst = crow + (size_t)(col >> lp) * sstride + (col & (p.panel - 1));
+              if (pass == 0) {  // add the large terms to pass 1's sum of the small ones
+                double pv[4];
+                asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(pv[0]), "=d"(pv[1]), "=d"(pv[2]), "=d"(pv[3]) : "l"(dst));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) o[u] += pv[u];
+              }
+              asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "d"(o[0]), "d"(o[1]), "d"(o[2]), "d"(o[3]) : "memory");
             }
           }
         }

@@ -1,6 +1,5 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 300 python tools/theta_scan.py peierls - gj_pair=2 2>&1 | tail -2
-python tools/run_once.py peierls 1 > /dev/null 2>&1
-FFS_OPTS=gj_pair=2 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ll_peierls_pair.csv python tools/run_once.py peierls 1 > /dev/null 2>&1
-python tools/launch_share.py gpurun_out/ll_peierls_pair.csv > gpurun_out/ll_peierls_pair.txt; head -3 gpurun_out/ll_peierls_pair.txt
+timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "dense_path and (opts1 or opts3)" 2>&1 | tail -3
+timeout 300 python tools/theta_scan.py dpp - 2>&1 | tail -1
+timeout 300 python tools/theta_scan.py peierls - 2>&1 | tail -1
