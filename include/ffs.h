@@ -54,7 +54,10 @@ typedef enum { FFS_OK = 0, FFS_EINVAL = -1, FFS_ECUDA = -2, FFS_ENOWS = -3 } ffs
  * path) it holds, per batch of S samples (the most whose factors W [N'][N'] fit a
  * 24 GB budget, at least 1024 and at most 8192, at most M), every batch sample's W, the coefficient
  * and panel matrices Y [N][8 S] and P [L][8 S] of the dense GEMM, U^T and the permutations: e.g.
- * 9.4 GB for the C5 config (L=16384, N=1024, M=1024), 20 GB for C4 (L=4096, N=512, c128). */
+ * 9.4 GB for the C5 config (L=16384, N=1024, M=1024), 20 GB for C4 (L=4096, N=512, c128). On the
+ * tile-Gram path (real U, small N'; FFS_OPT_TILE_GRAM) it holds U^T, the tile Gram matrices of U
+ * (8 G N^2 bytes, G = 16 or 32 tiles), the permutations and, for N' > 32, one N' x N' coefficient
+ * matrix per resident sample owner: 0.4 GB for the C5 marginal (N' = 64). */
 size_t ffs_workspace_bytes(int64_t L, int64_t N, int64_t Nprime, ffs_dtype dtype, int64_t M);
 
 /* Full sampling (N' = N): Eq. 1-3. uniforms [M][2N], positions [M][N]. */
