@@ -152,11 +152,11 @@ def path_of(cfg, Np, cplx):
                 + (", blocked)" if Np > 32 else ")")), dt
     if cfg.L >= 2048 and cfg.N >= 256 and cfg.N % 2 == 0:
         if Np < cfg.N:
-            return ("block-step path (marginal): ffs_cluster_kernel<STEP> with gathered contraction + "
-                    "ffs_dense_gj_kernel per block, CUDA graph"), dt
-        return ("block-step path (hybrid dense): per block ffs_ozaki_gemm2_kernel<8> (P = U Y), ffs_gram_kernel + "
-                "ffs_gram_draw_kernel (draws on tile Gram matrices, warp per sample), ffs_dense_gj_kernel; "
-                "ffs_cluster_kernel<STEP> for k0 < theta N'; CUDA graph"), \
+            return ("block-step path (marginal): ffs_cluster_kernel<STEP> (gathered contraction, panel out) + "
+                    "ffs_gram_kernel + ffs_gram_draw_kernel + ffs_dense_gj(2)_kernel per block, CUDA graph"), dt
+        return ("block-step path (hybrid dense): per block ffs_ozaki_gemm2w_kernel (P = U Y; gathered contraction in "
+                "ffs_cluster_kernel<STEP> for k0 < theta N'), ffs_gram_kernel + ffs_gram_draw_kernel (draws on tile "
+                "Gram matrices, warp per sample), ffs_dense_gj_kernel / ffs_dense_gj2_kernel; CUDA graph"), \
             dt + " (dense GEMM: Ozaki FP64 emulation, int8 x 8 slices on tcgen05; fp64-level, <= 1.3e-15 normwise)"
     if cfg.L >= 2048:
         return "ffs_cluster_kernel", dt

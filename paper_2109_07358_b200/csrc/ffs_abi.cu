@@ -760,6 +760,10 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   // 8192 (marginals have no GEMM operands)
   const double wbytes = (double)Np * (double)Np * (cx ? 16.0 : 8.0);
   int64_t cap = std::max<int64_t>(1024, std::min<int64_t>(8192, (int64_t)(24e9 / wbytes)));
+  // marginals on the Gram path keep the panels P [L][8] of a batch: at most ~4 GB of them
+  const bool marg_gram = Np < N && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0 && ffsh::option(FFS_OPT_GRAM_DRAW) != 3.0 &&
+                         (L + 1023) / 1024 <= ffsk::kGramMaxRl;
+  if (marg_gram) cap = std::max<int64_t>(256, std::min<int64_t>(cap, (int64_t)(4e9 / ((double)L * 8 * (cx ? 16.0 : 8.0)))));
   const double ob = ffsh::option(FFS_OPT_DENSE_BATCH);
   if (ob >= 1.0) cap = (int64_t)ob;
   d.S = std::max<int64_t>(1, std::min<int64_t>(M, cap));
@@ -772,7 +776,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   if (gsel != 0 && gsel != 7 && gsel != 8) return fail(FFS_EINVAL, "FFS_OPT_DENSE_GEMM must be 0, 7 or 8");
   d.gemm = no_gemm ? -1 : gsel;
   const size_t y_bytes = no_gemm ? 0 : align_up((size_t)N * d.ldY * es * (cx ? 2 : 1));  // complex: 2N x 2ldY expansion
-  const size_t p_bytes = no_gemm ? 0 : align_up((size_t)L * d.ldY * es);
+  const size_t p_bytes = (no_gemm && !marg_gram) ? 0 : align_up((size_t)L * d.ldY * es);
   d.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
   d.ws_y = y_bytes;
   d.ws_p = p_bytes;
@@ -811,7 +815,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
     if (int rc = ffsh::ensure_max_smem(ozaki_fn<7>())) return rc;
   }
   // Gram draws for the GEMM blocks: 32 row tiles of Rt rows (a multiple of 32) per sample
-  d.gram = (!no_gemm && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0) ? 1 : 0;
+  d.gram = ((!no_gemm || marg_gram) && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0) ? 1 : 0;
   d.Rt = (int)(((L + 31) / 32 + 31) / 32 * 32);
   if (d.Rt / 32 > ffsk::kGramMaxRl) d.gram = 0;
   d.ws_g = d.gram ? align_up((size_t)d.S * (cx ? ffsk::GramIdx<cplx>::NE : ffsk::GramIdx<double>::NE) * 32 * 8) : 0;
