@@ -138,7 +138,7 @@ def config_of(cfg, Np, M):
 
 def km_np_max(L):
     """Largest N' the tile-Gram path takes (ffs_abi.cu kmarg_eligible)."""
-    return 24 if L <= 1024 else 32 if L < 2048 else 64
+    return 24 if L <= 1024 else 32 if L < 2048 else 64 if L < 4096 else 96
 
 
 def path_of(cfg, Np, cplx):

@@ -430,7 +430,9 @@ bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   // measured against the panel kernels (tools/shape_time.py, profiles/r02/shape_times.log): below
   // L = 2048 the CTA-owner kernel wins from N' ~ 26 on (L = 1024: N' = 32 3.5 vs 4.2 ms); from L = 2048
   // the tile-Gram path wins up to N' = 64 by 3-5x
-  const int64_t np_max = L <= 1024 ? 24 : L < 2048 ? 32 : ffsk::kKmMaxNp;
+  // (N' = 96: L = 4096 20.0 vs 24.3 ms, 8192: 25.8 vs 47.2, 16384: 29.9 vs 52.2; N' = 128 loses at
+  // L <= 8192 and wins by 12 % at 16384)
+  const int64_t np_max = L <= 1024 ? 24 : L < 2048 ? 32 : L < 4096 ? 64 : ffsk::kKmMaxNp;
   return dtype == FFS_F64 && Np <= np_max && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
 }
 

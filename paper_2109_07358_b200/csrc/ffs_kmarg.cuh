@@ -89,7 +89,7 @@ struct KMargParams {
   double kappa_max;        // blocked forms: cancellation guard (as ffs_gram.cuh)
 };
 
-constexpr int kKmMaxNp = 64;
+constexpr int kKmMaxNp = 96;
 
 // shared memory per sample owner (a warp, or a half warp when L <= 1024: G = 16 lanes, 16 tiles): m, selection uniforms, d, U[x_k, m], pivot row, the drawn-row bitmap,
 // (small N') C, and for the forms either the offsets of the sample's entries in K + their
