@@ -53,3 +53,30 @@ def test_no_cpu_fallback_in_product_path():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "ffs_ref" not in txt, f
+
+
+def test_option_table_matches_header():
+    """The binding's option names map to the values of include/ffs.h's ffs_option enum."""
+    pytest.importorskip("torch")
+    from paper_2109_07358_b200 import ffs
+    src = open(os.path.join(ROOT, "include", "ffs.h")).read()
+    enum = dict((n.lower(), int(v)) for n, v in re.findall(r"FFS_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", src))
+    last = enum.pop("last")
+    assert last == max(enum.values())
+    assert sorted(enum.values()) == list(range(1, last + 1))
+    assert {k: v for k, v in ffs.OPTIONS.items()} == enum
+
+
+def test_sass_has_the_blackwell_tensor_path():
+    """The Ozaki GEMM is tcgen05 code: UTCIMMA (tcgen05.mma.kind::i8), UTMALDG (TMA loads), LDTM
+    (tcgen05.ld) appear in the library's SASS."""
+    import shutil
+    import subprocess
+    from paper_2109_07358_b200 import build
+    so = build.build()
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("no cuobjdump")
+    sass = subprocess.run([exe, "-sass", so], capture_output=True, text=True).stdout
+    for mnem in ("UTCIMMA", "UTMALDG", "LDTM"):
+        assert mnem in sass, mnem
