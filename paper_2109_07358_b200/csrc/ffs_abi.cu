@@ -718,6 +718,9 @@ template <typename T>
 const void* dense_gj_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<T, 8, gj_tj<T>()>); }
 template <typename T>
 size_t dense_gj_bytes(int k0) { return ffsk::dense_gj_smem<T, 8, gj_tj<T>()>(k0); }
+// 8-column updates (the paired schedule's eager step, the last blocks): 64 slices of i x 4 column threads
+const void* dense_gj_narrow_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj_kernel<double, 8, 8, 64>); }
+size_t dense_gj_narrow_bytes(int k0) { return ffsk::dense_gj_smem<double, 8, 8, 64>(k0); }
 template <typename T>
 const void* dense_gj2_fn() { return reinterpret_cast<const void*>(&ffsk::ffs_dense_gj2_kernel<T, 8, gj_tj<T>()>); }
 template <typename T>
@@ -835,6 +838,7 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   d.gj_pair = ((gp == 2.0 || (gp != 0.0 && !cx)) && gj2s <= kMaxSmem) ? 1 : 0;
   if (d.gj_pair)
     if (int rc = ffsh::ensure_max_smem(cx ? dense_gj2_fn<cplx>() : dense_gj2_fn<double>())) return rc;
+  if (int rc = ffsh::ensure_max_smem(dense_gj_narrow_fn())) return rc;
   return ffsh::ensure_max_smem(cx ? dense_gj_fn<cplx>() : dense_gj_fn<double>());
 }
 
@@ -1109,10 +1113,11 @@ int issue_dense(const DensePlan& d, const void* U, int64_t L, int64_t N, int dty
         q.k0 = k0;
         q.jend = pair_first ? k0 + 2 * B : (int)Np;
         const int nc = q.jend - k0 - B;
-        const dim3 jg((unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
-        const size_t gsm = cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
+        const bool narrow = !cx && nc <= 8 && dense_gj_narrow_bytes(k0) <= kMaxSmem;
+        const dim3 jg(narrow ? 1u : (unsigned)((nc + gjt - 1) / gjt), (unsigned)nh);
+        const size_t gsm = narrow ? dense_gj_narrow_bytes(k0) : cx ? dense_gj_bytes<cplx>(k0) : dense_gj_bytes<double>(k0);
         void* qargs[] = {&q};
-        e = cudaLaunchKernel(gjf, jg, dim3(256), qargs, gsm, stream);
+        e = cudaLaunchKernel(narrow ? dense_gj_narrow_fn() : gjf, jg, dim3(256), qargs, gsm, stream);
         if (e != cudaSuccess) return fail(FFS_ECUDA, "gj launch failed: %s", cudaGetErrorString(e));
         ++ffsh::launches();
       }

@@ -232,31 +232,35 @@ struct DenseGjParams {
                             // next block's, when the rest follows in ffs_dense_gj2_kernel)
 };
 
-template <typename T, int B, int kGjTJ>
+template <typename T, int B, int kGjTJ, int PARTS = 4>
 __host__ __device__ inline size_t dense_gj_smem(int k0) {
-  return sizeof(T) * ((size_t)B * k0 + 4 * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
+  return sizeof(T) * ((size_t)B * k0 + PARTS * B * kGjTJ + B * kGjTJ + B * B + B) + sizeof(int) * 2 * B;
 }
 
-// CPT adjacent columns per thread (2 for real: 16-byte W accesses), kGjTJ = 64 * CPT columns per
-// CTA of 256 threads; the i loops keep UNR independent W loads in flight per thread.
-template <typename T, int B, int kGjTJ>
+// CPT adjacent columns per thread (2 for real: 16-byte W accesses), 256 / PARTS column threads x
+// PARTS slices of i per CTA of 256 threads (kGjTJ = 256 / PARTS * CPT columns); the i loops keep UNR
+// independent W loads in flight per thread. PARTS = 4 for wide updates; PARTS = 64 (8 columns per
+// CTA) for the 8-column updates of the paired schedule, where 4 slices left 16 threads walking k0 / 4
+// rows each (0.21 ms per launch at k0 ~ 500).
+template <typename T, int B, int kGjTJ, int PARTS = 4>
 static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjParams q) {
   using S = Sc<T>;
-  constexpr int CPT = kGjTJ / 64;
+  constexpr int CT = 256 / PARTS;  // column threads
+  constexpr int CPT = kGjTJ / CT;
   constexpr int UNR = 8;
   static_assert(CPT == 1 || (CPT == 2 && sizeof(T) == 8), "two columns per thread only for real");
   extern __shared__ __align__(16) unsigned char smem[];
   const int k0 = q.k0, k1 = k0 + B, Np = q.Np, N = q.N;
   const int sl = blockIdx.y;
   const int64_t i_s = q.base + sl;
-  const int t = threadIdx.x, jg = t % 64, part = t / 64;
+  const int t = threadIdx.x, jg = t % CT, part = t / CT;
   const int jl = jg * CPT;                        // first column of this thread within the tile
   const int j = k1 + blockIdx.x * kGjTJ + jl;     // first global column
   const int jend = q.jend;
   const bool has = j < jend;
   T* Vn = reinterpret_cast<T*>(smem);   // [k0][B]   V[X_new, 0:k0] transposed (a row's B values contiguous)
   T* Zp = Vn + (size_t)B * k0;          // [4][B][TJ] partial sums (negated)
-  T* Zs = Zp + 4 * B * kGjTJ;           // [B][TJ]
+  T* Zs = Zp + PARTS * B * kGjTJ;       // [B][TJ]
   T* RP = Zs + B * kGjTJ;               // Row [B][B], Pinv [B]
   int* xn = reinterpret_cast<int*>(RP + B * B + B);
   const int32_t* pm = q.perm + i_s * Np;
@@ -310,20 +314,20 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     for (int tt = 0; tt < B; ++tt) acc[e][tt] = S::zero();
   if (has) {
     int ii = part;
-    for (; ii + 4 * (UNR - 1) < k0; ii += 4 * UNR) {
+    for (; ii + PARTS * (UNR - 1) < k0; ii += PARTS * UNR) {
       T w[UNR][CPT];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) ldw(ii + 4 * u, w[u]);
+      for (int u = 0; u < UNR; ++u) ldw(ii + PARTS * u, w[u]);
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
 #pragma unroll
         for (int tt = 0; tt < B; ++tt) {
-          const T vn = Vn[(ii + 4 * u) * B + tt];
+          const T vn = Vn[(ii + PARTS * u) * B + tt];
 #pragma unroll
           for (int e = 0; e < CPT; ++e) acc[e][tt] = S::fms(vn, w[u][e], acc[e][tt]);
         }
     }
-    for (; ii < k0; ii += 4) {
+    for (; ii < k0; ii += PARTS) {
       T w[CPT];
       ldw(ii, w);
 #pragma unroll
@@ -347,8 +351,12 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     T z[B];
 #pragma unroll
     for (int tt = 0; tt < B; ++tt) {
-      const T a01 = S::add(Zp[(0 * B + tt) * kGjTJ + c], Zp[(1 * B + tt) * kGjTJ + c]);
-      const T a23 = S::add(Zp[(2 * B + tt) * kGjTJ + c], Zp[(3 * B + tt) * kGjTJ + c]);
+      T a01 = S::zero(), a23 = S::zero();  // pairwise over the slices
+#pragma unroll 4
+      for (int pp = 0; pp < PARTS; pp += 4) {
+        a01 = S::add(a01, S::add(Zp[((pp + 0) * B + tt) * kGjTJ + c], Zp[((pp + 1) * B + tt) * kGjTJ + c]));
+        a23 = S::add(a23, S::add(Zp[((pp + 2) * B + tt) * kGjTJ + c], Zp[((pp + 3) * B + tt) * kGjTJ + c]));
+      }
       z[tt] = S::add(Ug[(size_t)xn[tt] * N + pm[jc]], S::add(a01, a23));
     }
     const T* Row = RP;
@@ -400,18 +408,18 @@ static __global__ void __launch_bounds__(256) ffs_dense_gj_kernel(const DenseGjP
     // rows part, part + 4, ... < k0 in REVERSE order: step (1) streamed them upwards, so the rows
     // it read last are the ones most likely still in L2 (forward order re-reads a working set larger
     // than L2 in LRU's worst order)
-    int m = ((k0 - part + 3) >> 2) - 1;
+    int m = (k0 - part + PARTS - 1) / PARTS - 1;
     for (; m >= UNR - 1; m -= UNR) {
       T a[UNR][CPT];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) ldw(part + 4 * (m - u), a[u]);
+      for (int u = 0; u < UNR; ++u) ldw(part + PARTS * (m - u), a[u]);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) upd(part + 4 * (m - u), a[u]);
+      for (int u = 0; u < UNR; ++u) upd(part + PARTS * (m - u), a[u]);
     }
     for (; m >= 0; --m) {
       T a[CPT];
-      ldw(part + 4 * m, a);
-      upd(part + 4 * m, a);
+      ldw(part + PARTS * m, a);
+      upd(part + PARTS * m, a);
     }
   }
   // next block's Y_s columns (the tile holding columns k1 .. k1+B-1)
