@@ -444,7 +444,7 @@ def test_panel_paths_without_tile_gram(L, N, Np):
 # Tile-Gram path: tile sizes of 1, 3, 4 and 16 rows per lane (L = 1024 .. 16384, ragged last tiles),
 # N' from 1 to 64, full sampling (N' = N) and marginals, many samples per warp slot.
 @pytest.mark.parametrize("L,N,Np", [(600, 20, 20), (1024, 128, 16), (2500, 64, 48), (3000, 300, 57), (4096, 140, 64),
-                                   (16384, 96, 33), (7000, 12, 1), (8192, 200, 96)])
+                                   (16384, 96, 33), (7000, 12, 1), (8192, 200, 96), (200, 60, 5), (256, 90, 8)])
 @pytest.mark.parametrize("mode", [1, 2, 3, 4])  # default (flat forms for N' <= 24, else blocked; half-warp owners for L <= 1024), flat, blocked, warp owners
 def test_tile_gram_path(L, N, Np, mode):
     ffs = _ffs()

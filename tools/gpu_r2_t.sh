@@ -1,3 +1,3 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 300 python tools/theta_scan.py dpp - gj_pair=3 gj_pair=1 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "tile_gram_path" 2>&1 | tail -3
