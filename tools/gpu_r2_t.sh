@@ -1,3 +1,4 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "tile_gram_path" 2>&1 | tail -3
+for i in 1 2 3; do timeout 300 python tools/theta_scan.py dpp - 2>&1 | tail -1; done
+timeout 300 python tools/theta_scan.py peierls - 2>&1 | tail -1
