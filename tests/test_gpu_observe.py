@@ -71,3 +71,44 @@ def test_gutzwiller_matches_oracle(name, V):
     assert (dcount.cpu().numpy() == np.bincount(D, minlength=cfg.N + 1)).all()
     if V == 0.0:
         assert res[0] == 1.0
+
+
+# pair correlations of the GPU samples against the projection-DPP closed form
+# <n_x n_y> = K_xx K_yy - |K_xy|^2 (K = U U^dagger); for the marginal of N' < N particles the first N'
+# picks of an exchangeable order give the factor N'(N'-1) / (N(N-1)). Counted on the device
+# (ffs_pair_occupation) over the window of the W sites with the largest occupation; z-test with a
+# Bonferroni bound where the expected count is >= 50, pooled Poisson check for the rest.
+@pytest.mark.parametrize("name,marginal", [("dw", False), ("anderson", True), ("dpp", True)])
+def test_pair_correlations_full_size(name, marginal):
+    from scipy import stats
+    ffs = _ffs()
+    cfg = inputs.CONFIGS[name]
+    U = inputs.build_u(cfg)
+    Np = cfg.marginal_Np if marginal else cfg.N
+    M = cfg.marginal_M if marginal else cfg.M
+    uni = inputs.uniforms(M, Np, cfg.uniform_seed + 700)
+    pos = ffs.ffs_sample_marginal(torch.from_numpy(U).cuda(), torch.from_numpy(uni).cuda(), Np)
+    torch.cuda.synchronize()
+    Kd = np.sum(np.abs(U) ** 2, axis=1)
+    W = 64
+    sites = np.sort(np.argsort(-Kd)[:W])            # the W most occupied sites, relabelled 0..W-1
+    hp = pos.cpu().numpy()
+    relabel = np.full(cfg.L, -1, dtype=np.int32)
+    relabel[sites] = np.arange(W, dtype=np.int32)
+    sub = relabel[hp]                               # other sites become -1 (skipped by the observables)
+    pair = ffs.ffs_pair_occupation(torch.from_numpy(np.ascontiguousarray(sub)).cuda(), W).cpu().numpy().astype(np.float64)
+    Us = U[sites]
+    K = Us @ Us.conj().T
+    fac = Np * (Np - 1) / (cfg.N * (cfg.N - 1))
+    P = fac * (np.outer(np.diag(K).real, np.diag(K).real) - np.abs(K) ** 2)
+    iu = np.triu_indices(W, 1)
+    p, obs = np.clip(P[iu], 0.0, 1.0), pair[iu]
+    big = M * p * (1 - p) >= 50
+    if name != "dpp":  # (C5's marginal has no pair with an expected count >= 50 at M = 8192: pooled check only)
+        assert big.sum() >= 20, big.sum()
+    if big.any():
+        z = np.abs(obs[big] / M - p[big]) / np.sqrt(p[big] * (1 - p[big]) / M)
+        assert z.max() < stats.norm.isf(1e-3 / (2 * big.sum())), (z.max(), int(big.sum()))
+    lam, tot = M * p[~big].sum(), obs[~big].sum()
+    if lam > 0:
+        assert stats.poisson.sf(tot - 1, lam) > 1e-4 and stats.poisson.cdf(tot, lam) > 1e-4, (tot, lam)

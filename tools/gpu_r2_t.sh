@@ -1,4 +1,3 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-for i in 1 2 3; do timeout 300 python tools/theta_scan.py dpp - 2>&1 | tail -1; done
-timeout 300 python tools/theta_scan.py peierls - 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_observe.py -m gpu -x -q -k "pair_correlations" 2>&1 | tail -12
