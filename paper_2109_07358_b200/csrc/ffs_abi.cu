@@ -24,6 +24,7 @@
 #include "ffs_dense.cuh"
 #include "ffs_gram.cuh"
 #include "ffs_kmarg.cuh"
+#include "ffs_kmarg_c.cuh"
 #include "ffs_lens.cuh"
 #include "ffs_observe.cuh"
 #include "ffs_metro.cuh"
@@ -433,7 +434,21 @@ bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   // (N' = 96: L = 4096 20.0 vs 24.3 ms, 8192: 25.8 vs 47.2, 16384: 29.9 vs 52.2; N' = 128 loses at
   // L <= 8192 and wins by 12 % at 16384)
   const int64_t np_max = L <= 1024 ? 24 : L < 2048 ? 32 : L < 4096 ? 64 : ffsk::kKmMaxNp;
+  if (dtype == FFS_C128) {  // complex: flat forms only (ffs_kmarg_c.cuh), K is 16 G N^2 bytes
+    const int owners = L <= 1024 ? 8 : 4;
+    return Np <= std::min<int64_t>(np_max, ffsk::kKmcMaxNp) && 64 * Np <= 3 * L && L <= 8192 && N <= 1024 &&
+           owners * ffsk::kmargc_owner_smem((int)L, (int)Np) + ffsk::align16((size_t)Np * (Np + 1)) <= kMaxSmem;
+  }
   return dtype == FFS_F64 && Np <= np_max && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
+}
+
+const void* kmc_fn(int Rl, int G) {
+  if (G == 16)
+    return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmargc_kernel<1, 4, 16>)
+                   : reinterpret_cast<const void*>(&ffsk::ffs_kmargc_kernel<4, 4, 16>);
+  return Rl <= 1 ? reinterpret_cast<const void*>(&ffsk::ffs_kmargc_kernel<1, 4, 32>)
+       : Rl <= 4 ? reinterpret_cast<const void*>(&ffsk::ffs_kmargc_kernel<4, 4, 32>)
+                 : reinterpret_cast<const void*>(&ffsk::ffs_kmargc_kernel<16, 4, 32>);
 }
 
 template <bool BLK>
@@ -446,21 +461,22 @@ const void* km_fn(int Rl, int G) {
                  : reinterpret_cast<const void*>(&ffsk::ffs_kmarg_kernel<16, 4, BLK, 32>);
 }
 
-int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k) {
+int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, KmPlan& k) {
+  const bool cx = dtype == FFS_C128;
   // sample owner: a warp (32 tiles), or a half warp (16 tiles, two samples per warp) for L <= 1024,
   // where most of a draw keeps at most 16 lanes busy (C3 marginal: 0.58 -> ? ms)
   k.G = (L <= 1024 && ffsh::option(FFS_OPT_TILE_GRAM) != 4.0) ? 16 : 32;
   k.Rl = (int)((L + k.G * k.G - 1) / (k.G * k.G));
   k.Lpt = k.G * k.G * k.Rl;
-  k.c_smem = Np <= 32;  // C [N'][N'] in shared memory (8 KB per warp at most), else a workspace slot per warp
+  k.c_smem = Np <= 32 || cx;  // C [N'][N'] in shared memory (8 KB per warp at most), else a workspace slot per warp
   k.warps = 4;
   // N' > 32: blocked evaluation of the forms (K entries read once per block of 8 draws instead of
   // once per draw: C5 marginal 3.3 instead of 11.7 MB of K rows per sample); option value 2 / 3
   // forces flat / blocked
   const double ot = ffsh::option(FFS_OPT_TILE_GRAM);
-  k.blocked = ot == 3.0 || (ot != 2.0 && Np > 32);  // N' = 32: flat 1.91 vs blocked 2.25 ms; 48: 13.3 vs 6.9
-  k.fn = k.blocked ? km_fn<true>(k.Rl, k.G) : km_fn<false>(k.Rl, k.G);
-  k.warp_smem = ffsk::kmarg_warp_smem((int)L, (int)Np, k.c_smem, k.blocked, k.G);
+  k.blocked = !cx && (ot == 3.0 || (ot != 2.0 && Np > 32));  // N' = 32: flat 1.91 vs blocked 2.25 ms; 48: 13.3 vs 6.9
+  k.fn = cx ? kmc_fn(k.Rl, k.G) : k.blocked ? km_fn<true>(k.Rl, k.G) : km_fn<false>(k.Rl, k.G);
+  k.warp_smem = cx ? ffsk::kmargc_owner_smem((int)L, (int)Np) : ffsk::kmarg_warp_smem((int)L, (int)Np, k.c_smem, k.blocked, k.G);
   const int owners = k.warps * (32 / k.G);  // per CTA
   k.smem = owners * k.warp_smem + ffsk::align16((size_t)Np * (Np + 1));  // + the entry/pair table
   if (k.smem > kMaxSmem) return fail(FFS_EINVAL, "tile-Gram path: shared memory %zu too large", k.smem);
@@ -474,25 +490,27 @@ int make_km_plan_uncached(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k
   k.grid = (int)std::max<int64_t>(1, ctas);
   const size_t slots = (size_t)k.grid * owners;
   k.ws_perm = align_up((size_t)std::max<int64_t>(M, 1) * Np * 4);
-  k.ws_ut = align_up((size_t)N * k.Lpt * 8);
-  k.ws_k = align_up((size_t)k.G * N * N * 8);
+  k.ws_ut = align_up((size_t)N * k.Lpt * (cx ? 16 : 8));
+  k.ws_k = align_up((size_t)k.G * N * N * (cx ? 16 : 8));
   k.ws_c = k.c_smem ? 0 : align_up(slots * (size_t)Np * Np * 8);
   k.total = k.ws_perm + k.ws_ut + k.ws_k + k.ws_c;
   return FFS_OK;
 }
 
 PlanCache<KmPlan> g_km_plans;
-int make_km_plan(int64_t L, int64_t N, int64_t Np, int64_t M, KmPlan& k) {
-  return g_km_plans.get(plan_key(4, L, N, Np, M, FFS_F64), k,
-                        [&](KmPlan& p) { return make_km_plan_uncached(L, N, Np, M, p); });
+int make_km_plan(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, KmPlan& k) {
+  return g_km_plans.get(plan_key(4, L, N, Np, M, dtype), k,
+                        [&](KmPlan& p) { return make_km_plan_uncached(L, N, Np, dtype, M, p); });
 }
 
 void launch_transpose(const void* U, double* Ut, int64_t L, int64_t N, int Lpt, int dtype, cudaStream_t s);
 
-int launch_kmarg(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, const double* uniforms, int32_t* positions,
-                 int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S, double* trace) {
+int launch_kmarg(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np, const double* uniforms,
+                 int32_t* positions, int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t stream, int64_t S0, int64_t S,
+                 double* trace) {
+  const bool cx = dtype == FFS_C128;
   KmPlan k;
-  int rc = make_km_plan(L, N, Np, M, k);
+  int rc = make_km_plan(L, N, Np, dtype, M, k);
   if (rc != FFS_OK) return rc;
   if (!ws || ws_bytes < k.total) return fail(FFS_ENOWS, "workspace %zu bytes < required %zu", ws_bytes, k.total);
   if (((uintptr_t)ws & (kAlign - 1)) != 0) return fail(FFS_EINVAL, "workspace not 256-byte aligned");
@@ -501,9 +519,14 @@ int launch_kmarg(const void* U, int64_t L, int64_t N, int64_t M, int64_t Np, con
   double* Ut = reinterpret_cast<double*>(w + k.ws_perm);
   double* K = reinterpret_cast<double*>(w + k.ws_perm + k.ws_ut);
   ffsh::prof_begin(stream);
-  launch_transpose(U, Ut, L, N, k.Lpt, FFS_F64, stream);
-  const dim3 kg((unsigned)((N + 63) / 64), (unsigned)((N + 63) / 64), (unsigned)k.G);
-  ffsk::ffs_tile_gram_u_kernel<<<kg, 256, 0, stream>>>(static_cast<const double*>(U), K, (int)L, (int)N, k.G * k.Rl, k.G);
+  launch_transpose(U, Ut, L, N, k.Lpt, dtype, stream);
+  if (cx) {
+    const dim3 kg((unsigned)((N + 31) / 32), (unsigned)((N + 31) / 32), (unsigned)k.G);
+    ffsk::ffs_tile_gram_uc_kernel<<<kg, 256, 0, stream>>>(static_cast<const double*>(U), K, (int)L, (int)N, k.G * k.Rl, k.G);
+  } else {
+    const dim3 kg((unsigned)((N + 63) / 64), (unsigned)((N + 63) / 64), (unsigned)k.G);
+    ffsk::ffs_tile_gram_u_kernel<<<kg, 256, 0, stream>>>(static_cast<const double*>(U), K, (int)L, (int)N, k.G * k.Rl, k.G);
+  }
   ++ffsh::launches();
   if (int rc2 = launch_permute(uniforms, 2 * Np, perm, M, N, Np, stream)) return rc2;
   ffsk::KMargParams p{};
@@ -1282,7 +1305,7 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
   if (warp_eligible(L, N, Np, dtype))
     rc = launch_warp(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
   else if (kmarg_eligible(L, N, Np, dtype))
-    rc = launch_kmarg(U, L, N, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
+    rc = launch_kmarg(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
   else if (dense_eligible(L, N, Np, dtype))
     rc = launch_dense(U, L, N, dtype, M, Np, uniforms, positions, flags, ws, ws_bytes, stream, S0, S, trace);
   else if (cluster_eligible(L, dtype))
@@ -1305,7 +1328,7 @@ size_t workspace_bytes(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
   }
   if (kmarg_eligible(L, N, Np, dtype)) {
     KmPlan k;
-    return make_km_plan(L, N, Np, M, k) == FFS_OK ? k.total : 0;
+    return make_km_plan(L, N, Np, dtype, M, k) == FFS_OK ? k.total : 0;
   }
   if (dense_eligible(L, N, Np, dtype)) {
     DensePlan d;

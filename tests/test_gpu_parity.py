@@ -472,3 +472,32 @@ def test_tile_gram_path(L, N, Np, mode):
         gpos2, gfl2, _ = run_gpu(U, uni2, Np)
         assert (gpos2 == ref.sample(U, uni2, Np=Np)).all()
         assert not (gfl2 & 1).any()
+
+
+# Complex tile-Gram path (ffs_kmarg_c.cuh: Hermitian tile Gram matrices, flat forms, N' <= 32): half-warp
+# and warp owners, 1 / 3 / 4 rows per lane, marginals and full sampling, extreme selection uniforms;
+# and the same shapes on the panel kernels with the option off.
+@pytest.mark.parametrize("L,N,Np", [(600, 20, 20), (1024, 64, 16), (2500, 40, 32), (4096, 300, 24), (3000, 12, 1)])
+@pytest.mark.parametrize("mode", [1, 0])
+def test_tile_gram_path_complex(L, N, Np, mode):
+    ffs = _ffs()
+    ffs.set_option("tile_gram", mode)
+    U = inputs.random_orthonormal(L, N, 17 * L + N, complex_=True)
+    M = 2000 if (mode == 1 and L * Np <= 40000) else 64
+    uni = inputs.uniforms(M, Np, 3 * L + Np)
+    gpos, gflags, gw = run_gpu(U, uni, Np, trace_S=2, trace_S0=M - 2)
+    idx = np.array(_spread(M, min(M, 64)))
+    rpos = ref.sample(U, uni[idx], Np=Np)
+    r = compare_positions(U, uni[idx], gpos[idx], rpos, Np)
+    assert not r["failures"], r["failures"][:3]
+    assert (gflags == 0).all()
+    assert all(len(set(q)) == Np for q in gpos.tolist())
+    last = np.arange(M - 2, M)
+    rlast, rw = ref.weights(U, uni[last], Np=Np)
+    assert compare_weights(gw, rw, gpos[last], rlast) <= WEIGHT_TOL
+    for useL in (0.0, 1.0 - 2.0 ** -53):
+        uni2 = uni[:32].copy()
+        uni2[:, Np:] = useL
+        gpos2, gfl2, _ = run_gpu(U, uni2, Np)
+        assert (gpos2 == ref.sample(U, uni2, Np=Np)).all()
+        assert not (gfl2 & 1).any()

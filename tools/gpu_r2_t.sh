@@ -1,3 +1,6 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_observe.py -m gpu -x -q -k "pair_correlations" 2>&1 | tail -12
+export FFS_COMPLEX=1
+for s in "1024 64 16 8192" "1024 64 24 8192" "2048 256 32 4096" "4096 512 16 4096" "4096 512 32 4096" "8192 256 32 2048"; do
+  timeout 300 python tools/shape_time.py $s --- tile_gram=0 2>&1 | grep "L="
+done
