@@ -31,7 +31,8 @@
  * Errors (all synchronous, message in ffs_last_error()): FFS_EINVAL for null pointers when M > 0,
  * N < 1, N > L, N' not in [1, N], unknown dtype, or L beyond the supported range (L <= 16384 real,
  * L <= 8192 complex: one sample's L x 8 panel must fit the register files of one thread-block
- * cluster / one SM; larger L returns FFS_EINVAL, it is never truncated); FFS_ENOWS if the workspace
+ * cluster / one SM; real calls with small N' -- the tile-Gram path, FFS_OPT_TILE_GRAM -- keep no
+ * panel and go up to L = 262144; any other larger L returns FFS_EINVAL, it is never truncated); FFS_ENOWS if the workspace
  * is NULL or smaller than ffs_workspace_bytes(...); FFS_ECUDA for CUDA launch/runtime errors.
  * M == 0 is an OK no-op.
  */

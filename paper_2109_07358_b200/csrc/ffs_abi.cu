@@ -426,6 +426,7 @@ struct KmPlan {
   size_t warp_smem, smem, ws_perm, ws_ut, ws_k, ws_c, total;
 };
 
+constexpr int64_t kMaxLTileGram = 262144;
 bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   if (ffsh::option(FFS_OPT_FORCE_GENERIC) != 0.0 || ffsh::option(FFS_OPT_TILE_GRAM) == 0.0) return false;
   // measured against the panel kernels (tools/shape_time.py, profiles/r02/shape_times.log): below
@@ -439,7 +440,9 @@ bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
     return Np <= std::min<int64_t>(np_max, ffsk::kKmcMaxNp) && 64 * Np <= 3 * L && L <= 8192 && N <= 1024 &&
            owners * ffsk::kmargc_owner_smem((int)L, (int)Np) + ffsk::align16((size_t)Np * (Np + 1)) <= kMaxSmem;
   }
-  return dtype == FFS_F64 && Np <= np_max && 64 * Np <= 3 * L && L <= 16384 && N <= 2048;
+  // real: any L up to 2^18 (beyond 16384 the rows of a tile are scanned in chunks of 16 per lane)
+  return dtype == FFS_F64 && Np <= np_max && 64 * Np <= 3 * L && L <= kMaxLTileGram && N <= 2048 &&
+         4 * ffsk::kmarg_warp_smem((int)L, (int)Np, Np <= 32, Np > 32, 32) + ffsk::align16((size_t)Np * (Np + 1)) <= kMaxSmem;
 }
 
 const void* kmc_fn(int Rl, int G) {
@@ -1281,15 +1284,16 @@ int launch_generic(const void* U, int64_t L, int64_t N, int dtype, int64_t M, in
   return FFS_OK;
 }
 
-int check_shape(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
+int check_shape(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, bool tile_gram_ok = false) {
   if (L < 1 || N < 1 || N > L || Np < 1 || Np > N || L > INT32_MAX || M < 0)
     return fail(FFS_EINVAL, "invalid shape L=%lld N=%lld N'=%lld M=%lld", (long long)L, (long long)N, (long long)Np,
                 (long long)M);
   if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
   const int64_t maxL = dtype == FFS_C128 ? kMaxLComplex : kMaxLReal;
-  if (L > maxL)
+  if (L > maxL && !(tile_gram_ok && kmarg_eligible(L, N, Np, dtype)))  // (the tile-Gram path keeps no panel: real small-N' calls up to L = 2^18)
     return fail(FFS_EINVAL, "unsupported L=%lld for dtype %d: the per-sample panel must fit one SM's registers "
-                "(max L %lld); see include/ffs.h", (long long)L, dtype, (long long)maxL);
+                "(max L %lld; real U with small N' up to %lld on the tile-Gram path); see include/ffs.h", (long long)L, dtype,
+                (long long)maxL, (long long)kMaxLTileGram);
   return FFS_OK;
 }
 
@@ -1298,7 +1302,7 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
            double* trace) {
   ffsh::launches() = 0;
   if (M == 0) return FFS_OK;
-  if (int rc = check_shape(L, N, Np, dtype, M)) return rc;
+  if (int rc = check_shape(L, N, Np, dtype, M, true)) return rc;
   if (!U || !uniforms || !positions) return fail(FFS_EINVAL, "null U/uniforms/positions with M=%lld", (long long)M);
   if (S > 0 && !trace) return fail(FFS_EINVAL, "null trace buffer with S=%lld", (long long)S);
   int rc;
@@ -1320,7 +1324,7 @@ int launch(const void* U, int64_t L, int64_t N, int dtype, int64_t M, int64_t Np
 }
 
 size_t workspace_bytes(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M) {
-  if (check_shape(L, N, Np, dtype, std::max<int64_t>(M, 1)) != FFS_OK) return 0;
+  if (check_shape(L, N, Np, dtype, std::max<int64_t>(M, 1), true) != FFS_OK) return 0;
   M = std::max<int64_t>(M, 1);
   if (warp_eligible(L, N, Np, dtype)) {
     WarpPlan w;
@@ -1760,7 +1764,7 @@ int ffs_sample_host(const void* U, int64_t L, int64_t N, ffs_dtype dtype, int64_
                     const double* uniforms, int32_t* positions, int32_t* sample_flags, void* workspace,
                     size_t ws_bytes, void* stream) {
   if (M == 0) return FFS_OK;
-  if (int rc = check_shape(L, N, Nprime, dtype, M)) return rc;
+  if (int rc = check_shape(L, N, Nprime, dtype, M, true)) return rc;
   HostLayout h;
   if (!host_layout(L, N, Nprime, dtype, M, h)) return FFS_EINVAL;
   if (!U || !uniforms || !positions || !workspace || ws_bytes < h.total)

@@ -178,9 +178,12 @@ def test_edge_cases():
     assert L.ffs_sample(Ud.data_ptr(), 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == ffs.FFS_ENOWS
     assert L.ffs_sample(None, 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
     # L beyond the supported range (16384 real, 8192 complex): FFS_EINVAL, never truncated
-    assert L.ffs_workspace_bytes(16385, 8, 8, 0, 4) == 0
+    # (real calls with small N' go up to L = 2^18 on the tile-Gram path: test_tile_gram_path)
+    assert L.ffs_workspace_bytes(16385, 256, 200, 0, 4) == 0
+    assert L.ffs_workspace_bytes(16385, 8, 8, 0, 4) > 0
+    assert L.ffs_workspace_bytes(262145, 8, 8, 0, 4) == 0
     assert L.ffs_workspace_bytes(8193, 8, 8, 1, 4) == 0
-    assert L.ffs_sample(Ud.data_ptr(), 16385, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
+    assert L.ffs_sample(Ud.data_ptr(), 16385, 200, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
     assert "unsupported L" in L.ffs_last_error().decode()
     # trace range outside [0, M)
     assert L.ffs_debug_trace(Ud.data_ptr(), 10, 3, 0, 4, 3, ud.data_ptr(), pos.data_ptr(), None, None, 0, None,
@@ -444,7 +447,8 @@ def test_panel_paths_without_tile_gram(L, N, Np):
 # Tile-Gram path: tile sizes of 1, 3, 4 and 16 rows per lane (L = 1024 .. 16384, ragged last tiles),
 # N' from 1 to 64, full sampling (N' = N) and marginals, many samples per warp slot.
 @pytest.mark.parametrize("L,N,Np", [(600, 20, 20), (1024, 128, 16), (2500, 64, 48), (3000, 300, 57), (4096, 140, 64),
-                                   (16384, 96, 33), (7000, 12, 1), (8192, 200, 96), (200, 60, 5), (256, 90, 8)])
+                                   (16384, 96, 33), (7000, 12, 1), (8192, 200, 96), (200, 60, 5), (256, 90, 8),
+                                   (40000, 24, 8), (70001, 16, 5)])
 @pytest.mark.parametrize("mode", [1, 2, 3, 4])  # default (flat forms for N' <= 24, else blocked; half-warp owners for L <= 1024), flat, blocked, warp owners
 def test_tile_gram_path(L, N, Np, mode):
     ffs = _ffs()

@@ -1,6 +1,6 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-export FFS_COMPLEX=1
-for s in "1024 64 16 8192" "1024 64 24 8192" "2048 256 32 4096" "4096 512 16 4096" "4096 512 32 4096" "8192 256 32 2048"; do
-  timeout 300 python tools/shape_time.py $s --- tile_gram=0 2>&1 | grep "L="
-done
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "tile_gram_path or edge_cases or marginal" 2>&1 | tail -5
+timeout 300 python tools/theta_scan.py anderson:marginal - 2>&1 | tail -1
+timeout 300 python tools/theta_scan.py dpp:marginal - 2>&1 | tail -1
+timeout 300 python tools/shape_time.py 65536 64 16 4096 2>&1 | grep "L="
