@@ -31,7 +31,7 @@
  * Errors (all synchronous, message in ffs_last_error()): FFS_EINVAL for null pointers when M > 0,
  * N < 1, N > L, N' not in [1, N], unknown dtype, or L beyond the supported range (L <= 16384 real,
  * L <= 8192 complex: one sample's L x 8 panel must fit the register files of one thread-block
- * cluster / one SM; real calls with small N' -- the tile-Gram path, FFS_OPT_TILE_GRAM -- keep no
+ * cluster / one SM; calls with small N' -- the tile-Gram path, FFS_OPT_TILE_GRAM -- keep no
  * panel and go up to L = 262144; any other larger L returns FFS_EINVAL, it is never truncated); FFS_ENOWS if the workspace
  * is NULL or smaller than ffs_workspace_bytes(...); FFS_ECUDA for CUDA launch/runtime errors.
  * M == 0 is an OK no-op.
@@ -216,7 +216,7 @@ typedef enum {
   FFS_OPT_DENSE_MIN_L = 12,     /* smallest L on the block-step paths (default 2048); below 2048 every
                                    block of a full sampling call takes the GEMM + Gram draws */
   FFS_OPT_DENSE_MIN_N = 13,     /* smallest N on the block-step paths (default 256) */
-  FFS_OPT_TILE_GRAM = 14,       /* 1 (default): complex U with N' <= 32 (L <= 8192, N <= 1024) and real U, 64 N' <= 3 L and N' <= 24 (L <= 1024), 32 (L < 2048), 64 (L < 4096), 96 (larger L): the tile-Gram
+  FFS_OPT_TILE_GRAM = 14,       /* 1 (default): complex U with N' <= 32 (N <= 1024) and real U, L <= 262144, 64 N' <= 3 L and N' <= 24 (L <= 1024), 32 (L < 2048), 64 (L < 4096), 96 (larger L): the tile-Gram
                                    path (ffs_kmarg.cuh): tile totals as quadratic forms of the 32 tile
                                    Gram matrices of U, one warp per sample; 0: the panel kernels */
   FFS_OPT_GJ_PAIR = 15,         /* 1 (default): real block-step paths update W for two consecutive blocks in

@@ -435,9 +435,9 @@ bool kmarg_eligible(int64_t L, int64_t N, int64_t Np, int dtype) {
   // (N' = 96: L = 4096 20.0 vs 24.3 ms, 8192: 25.8 vs 47.2, 16384: 29.9 vs 52.2; N' = 128 loses at
   // L <= 8192 and wins by 12 % at 16384)
   const int64_t np_max = L <= 1024 ? 24 : L < 2048 ? 32 : L < 4096 ? 64 : ffsk::kKmMaxNp;
-  if (dtype == FFS_C128) {  // complex: flat forms only (ffs_kmarg_c.cuh), K is 16 G N^2 bytes
+  if (dtype == FFS_C128) {  // complex: flat forms only (ffs_kmarg_c.cuh), K is 16 G N^2 bytes; L as for real U
     const int owners = L <= 1024 ? 8 : 4;
-    return Np <= std::min<int64_t>(np_max, ffsk::kKmcMaxNp) && 64 * Np <= 3 * L && L <= 8192 && N <= 1024 &&
+    return Np <= std::min<int64_t>(np_max, ffsk::kKmcMaxNp) && 64 * Np <= 3 * L && L <= kMaxLTileGram && N <= 1024 &&
            owners * ffsk::kmargc_owner_smem((int)L, (int)Np) + ffsk::align16((size_t)Np * (Np + 1)) <= kMaxSmem;
   }
   // real: any L up to 2^18 (beyond 16384 the rows of a tile are scanned in chunks of 16 per lane)
@@ -1290,7 +1290,7 @@ int check_shape(int64_t L, int64_t N, int64_t Np, int dtype, int64_t M, bool til
                 (long long)M);
   if (dtype != FFS_F64 && dtype != FFS_C128) return fail(FFS_EINVAL, "unknown dtype %d", dtype);
   const int64_t maxL = dtype == FFS_C128 ? kMaxLComplex : kMaxLReal;
-  if (L > maxL && !(tile_gram_ok && kmarg_eligible(L, N, Np, dtype)))  // (the tile-Gram path keeps no panel: real small-N' calls up to L = 2^18)
+  if (L > maxL && !(tile_gram_ok && kmarg_eligible(L, N, Np, dtype)))  // (the tile-Gram path keeps no panel: small-N' calls up to L = 2^18)
     return fail(FFS_EINVAL, "unsupported L=%lld for dtype %d: the per-sample panel must fit one SM's registers "
                 "(max L %lld; real U with small N' up to %lld on the tile-Gram path); see include/ffs.h", (long long)L, dtype,
                 (long long)maxL, (long long)kMaxLTileGram);

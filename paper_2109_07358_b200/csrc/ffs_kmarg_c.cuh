@@ -208,28 +208,48 @@ static __global__ void __launch_bounds__(32 * WARPS) ffs_kmargc_kernel(const KMa
         double ex = __shfl_up_sync(gmask, incl, 1, G);
         if (lane == 0) ex = 0.0;
         const double thr_in = thr - __shfl_sync(gmask, ex, tau, G);
-        // ---- rows of tile tau, Rl consecutive rows per lane
+        // ---- rows of tile tau, Rl consecutive rows per lane, RLMAX at a time
         const int xb = (tau * G + lane) * Rl;
-        cplx s[RLMAX];
-        {
-          const cplx* col = Ut + (size_t)mr * Lpt + xb;
+        auto chunk = [&](int c0, cplx (&s)[RLMAX]) {  // s(x) of rows xb + c0 .. (those < xb + Rl)
+          const int nr = Rl - c0;
+          {
+            const cplx* col = Ut + (size_t)mr * Lpt + xb + c0;
 #pragma unroll
-          for (int j = 0; j < RLMAX; ++j) s[j] = j < Rl ? col[j] : S::zero();
-        }
-        for (int q = 0; q < r; ++q) {
-          const cplx dq = S::neg(dvec[q]);
-          const cplx* col = Ut + (size_t)m[q] * Lpt + xb;
+            for (int j = 0; j < RLMAX; ++j) s[j] = j < nr ? col[j] : S::zero();
+          }
+          for (int q = 0; q < r; ++q) {
+            const cplx dq = S::neg(dvec[q]);
+            const cplx* col = Ut + (size_t)m[q] * Lpt + xb + c0;
 #pragma unroll
-          for (int j = 0; j < RLMAX; ++j)
-            if (j < Rl) s[j] = S::fms(col[j], dq, s[j]);
-        }
+            for (int j = 0; j < RLMAX; ++j)
+              if (j < nr) s[j] = S::fms(col[j], dq, s[j]);
+          }
+        };
+        constexpr int kNoRow = 0x7fffffff;
+        const bool one_chunk = RLMAX < 16 || Rl <= RLMAX;  // L <= G G RLMAX: the lane's prefix stays in registers
         double c[RLMAX];
         double run = 0.0;
+        {
+          cplx s[RLMAX];
+          if constexpr (RLMAX < 16) {
+            chunk(0, s);
 #pragma unroll
-        for (int j = 0; j < RLMAX; ++j) {
-          const int x = xb + j;
-          if (j < Rl && x < L && !drawn(x)) run += S::abs2(s[j]);
-          c[j] = run;
+            for (int j = 0; j < RLMAX; ++j) {
+              const int x = xb + j;
+              if (j < Rl && x < L && !drawn(x)) run += S::abs2(s[j]);
+              c[j] = run;
+            }
+          } else {
+            for (int c0 = 0; c0 < Rl; c0 += RLMAX) {
+              chunk(c0, s);
+#pragma unroll
+              for (int j = 0; j < RLMAX; ++j) {
+                const int x = xb + c0 + j;
+                if (c0 + j < Rl && x < L && !drawn(x)) run += S::abs2(s[j]);
+                c[j] = run;
+              }
+            }
+          }
         }
         const double incl2 = scan(run);
         double ex2 = __shfl_up_sync(gmask, incl2, 1, G);
@@ -237,18 +257,39 @@ static __global__ void __launch_bounds__(32 * WARPS) ffs_kmargc_kernel(const KMa
         const double Dt = __shfl_sync(gmask, incl2, G - 1, G);
         const double thr2 = cross ? (thr_in / __shfl_sync(gmask, f, tau, G)) * Dt : 1.7976931348623157e308;
         const double tp = thr2 - ex2;
-        int rs = RLMAX, rl = -1;
+        int rs = kNoRow, rl = -1;  // first row of this lane past the threshold / its last row with w > 0
+        if (one_chunk) {
 #pragma unroll
-        for (int j = RLMAX - 1; j >= 0; --j) {
-          const double prev = j > 0 ? c[j - 1] : 0.0;
-          if (c[j] > prev && c[j] > tp) rs = j;
-        }
+          for (int j = RLMAX - 1; j >= 0; --j) {
+            const double prev = j > 0 ? c[j - 1] : 0.0;
+            if (c[j] > prev && c[j] > tp) rs = j;
+          }
 #pragma unroll
-        for (int j = 0; j < RLMAX; ++j) {
-          const double prev = j > 0 ? c[j - 1] : 0.0;
-          if (c[j] > prev) rl = j;
+          for (int j = 0; j < RLMAX; ++j) {
+            const double prev = j > 0 ? c[j - 1] : 0.0;
+            if (c[j] > prev) rl = j;
+          }
+        } else if constexpr (RLMAX >= 16) {
+          // large L: the same sums again, chunk by chunk (identical order, so the last prefix is `run`)
+          cplx s[RLMAX];
+          double pre = 0.0;
+          for (int c0 = 0; c0 < Rl; c0 += RLMAX) {
+            chunk(c0, s);
+#pragma unroll
+            for (int j = 0; j < RLMAX; ++j) {
+              const int x = xb + c0 + j;
+              if (c0 + j < Rl && x < L && !drawn(x)) {
+                const double prev = pre;
+                pre += S::abs2(s[j]);
+                if (pre > prev) {
+                  rl = c0 + j;
+                  if (rs == kNoRow && pre > tp) rs = c0 + j;
+                }
+              }
+            }
+          }
         }
-        const unsigned b1 = gballot(rs < RLMAX);
+        const unsigned b1 = gballot(rs != kNoRow);
         if (b1) {
           const int ln = __ffs(b1) - 1;
           xsel = (tau * G + ln) * Rl + __shfl_sync(gmask, rs, ln, G);

@@ -112,3 +112,39 @@ def test_pair_correlations_full_size(name, marginal):
     lam, tot = M * p[~big].sum(), obs[~big].sum()
     if lam > 0:
         assert stats.poisson.sf(tot - 1, lam) > 1e-4 and stats.poisson.cdf(tot, lam) > 1e-4, (tot, lam)
+
+
+# Large L on the tile-Gram path (L = 65536: 64 rows per lane of the crossing tile, scanned in four
+# chunks of 16): single-site occupations of the marginal against the closed form
+# <n_x> = (N'/N) K_xx (exchangeable column order). U has a localised envelope, so that a
+# few thousand rows around the maxima carry expected counts >= 50. n_x is 0 or 1 per sample and the
+# samples are independent, so the count of a site is exactly binomial(M, <n_x>).
+@pytest.mark.parametrize("complex_", [False, True])
+def test_large_L_marginal_occupations(complex_):
+    from scipy import stats
+    ffs = _ffs()
+    L, N, Np, M = 65536, 32, 8, 65536
+    rng = np.random.default_rng(4242 + int(complex_))
+    x = np.arange(L)
+    env = np.exp(-0.5 * ((x - 30011.0) / 700.0) ** 2) + 0.4 * np.exp(-0.5 * ((x - 51007.0) / 300.0) ** 2) + 1e-3
+    A = rng.standard_normal((L, N))
+    if complex_:
+        A = A + 1j * rng.standard_normal((L, N))
+    U, _ = np.linalg.qr(A * env[:, None])
+    U = np.ascontiguousarray(U)
+    uni = inputs.uniforms(M, Np, 90210 + int(complex_))
+    pos, flags = ffs.ffs_sample_marginal(torch.from_numpy(U).cuda(), torch.from_numpy(uni).cuda(), Np, with_flags=True)
+    torch.cuda.synchronize()
+    assert (flags.cpu().numpy() == 0).all()
+    hp = pos.cpu().numpy()
+    assert all(len(set(q)) == Np for q in hp[:: M // 512].tolist())
+    obs = np.bincount(hp.ravel(), minlength=L).astype(np.float64)
+    p = (Np / N) * np.sum(np.abs(U) ** 2, axis=1)
+    big = M * p >= 50
+    assert big.sum() >= 1000, big.sum()
+    z = np.abs(obs[big] - M * p[big]) / np.sqrt(M * p[big] * (1 - p[big]))
+    assert z.max() < stats.norm.isf(1e-3 / (2 * big.sum())), (z.max(), int(big.sum()))
+    lam, tot = M * p[~big].sum(), obs[~big].sum()
+    assert stats.poisson.sf(tot - 1, lam) > 1e-4 and stats.poisson.cdf(tot, lam) > 1e-4, (tot, lam)
+    # the z-scores as a whole: mean square 1 up to sampling noise
+    assert np.mean(z ** 2) < 1.15, np.mean(z ** 2)

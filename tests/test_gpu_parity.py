@@ -178,11 +178,13 @@ def test_edge_cases():
     assert L.ffs_sample(Ud.data_ptr(), 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == ffs.FFS_ENOWS
     assert L.ffs_sample(None, 10, 3, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
     # L beyond the supported range (16384 real, 8192 complex): FFS_EINVAL, never truncated
-    # (real calls with small N' go up to L = 2^18 on the tile-Gram path: test_tile_gram_path)
+    # (calls with small N' go up to L = 2^18 on the tile-Gram path: test_tile_gram_path[_complex])
     assert L.ffs_workspace_bytes(16385, 256, 200, 0, 4) == 0
     assert L.ffs_workspace_bytes(16385, 8, 8, 0, 4) > 0
     assert L.ffs_workspace_bytes(262145, 8, 8, 0, 4) == 0
-    assert L.ffs_workspace_bytes(8193, 8, 8, 1, 4) == 0
+    assert L.ffs_workspace_bytes(8193, 256, 200, 1, 4) == 0
+    assert L.ffs_workspace_bytes(8193, 8, 8, 1, 4) > 0
+    assert L.ffs_workspace_bytes(262145, 8, 8, 1, 4) == 0
     assert L.ffs_sample(Ud.data_ptr(), 16385, 200, 0, 4, ud.data_ptr(), pos.data_ptr(), None, None, 0, None) == -1
     assert "unsupported L" in L.ffs_last_error().decode()
     # trace range outside [0, M)
@@ -479,12 +481,15 @@ def test_tile_gram_path(L, N, Np, mode):
 
 
 # Complex tile-Gram path (ffs_kmarg_c.cuh: Hermitian tile Gram matrices, flat forms, N' <= 32): half-warp
-# and warp owners, 1 / 3 / 4 rows per lane, marginals and full sampling, extreme selection uniforms;
+# and warp owners, 1 / 3 / 4 / 6 rows per lane and the chunked row scan beyond L = 16384, marginals and full sampling, extreme selection uniforms;
 # and the same shapes on the panel kernels with the option off.
-@pytest.mark.parametrize("L,N,Np", [(600, 20, 20), (1024, 64, 16), (2500, 40, 32), (4096, 300, 24), (3000, 12, 1)])
+@pytest.mark.parametrize("L,N,Np", [(600, 20, 20), (1024, 64, 16), (2500, 40, 32), (4096, 300, 24), (3000, 12, 1),
+                                    (6000, 16, 8), (20000, 16, 8), (40001, 12, 5)])
 @pytest.mark.parametrize("mode", [1, 0])
 def test_tile_gram_path_complex(L, N, Np, mode):
     ffs = _ffs()
+    if mode == 0 and L > 8192:
+        pytest.skip("the complex panel kernels stop at L = 8192")
     ffs.set_option("tile_gram", mode)
     U = inputs.random_orthonormal(L, N, 17 * L + N, complex_=True)
     M = 2000 if (mode == 1 and L * Np <= 40000) else 64
