@@ -356,8 +356,9 @@ def sweep_entry(r, cpu_budget, no_cpu):
 def measure_extensions(dev, steps, no_cpu, cpu_budget):
     """The §8(f) rows beyond the BASELINE workloads, each timed like a sweep entry (device time
     with inputs resident, L2 flushed, kernel events, clocks, e2e where a host path exists):
-    the L-ensemble front end (`lens`), the Supp S7 Metropolis variant (`metro`), and the
-    Gutzwiller reweighting of C2 spinful samples (`gutzwiller`, HBM-bound)."""
+    the L-ensemble front end (`lens`), the Supp S7 Metropolis variant (`metro`), the
+    Gutzwiller reweighting of C2 spinful samples (`gutzwiller`, HBM-bound), small-N' marginals at
+    L = 65536 (`large_L`, `large_L_complex`) and the modified-HKPV comparator."""
     import torch
     from paper_2109_07358_b200 import ffs
 
@@ -469,6 +470,32 @@ def measure_extensions(dev, steps, no_cpu, cpu_budget):
                                       "unit": "GB/s", "frac": byts / (kms * 1e-3) / 1e9 / measured_hbm(),
                                       "bytes_def": "positions read once: 4 N' B per sample"},
                          "clocks": clocks, "gpu_launches": nl}
+    # L beyond the panel kernels' limits (16384 real / 8192 complex): small-N' marginals on the tile-Gram path
+    for cx in (False, True):
+        L, N, Np, M = 65536, 64, 16, 4096
+        U = inputs.random_orthonormal(L, N, 5000 + N, complex_=cx)
+        uni = inputs.uniforms(M, Np, 5100 + int(cx))
+        Ud, ud = torch.from_numpy(U).to(dev), torch.from_numpy(uni).to(dev)
+        ws = ffs.Workspace(dev)
+        ms, kms, clocks, nl = timed(lambda: ffs.ffs_sample_marginal(Ud, ud, Np, workspace=ws, stream=stream), steps)
+        fl = paper_flops(L, Np, cx)
+        key = "large_L_complex" if cx else "large_L"
+        out[key] = {"config": {"workload": key, "L": L, "N": N, "Nprime": Np, "M": M, "l2": L2_NOTE},
+                    "dtype": "c128" if cx else "f64", "value": M / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms,
+                    "kernel": "ffs_tile_gram_u%s_kernel + ffs_kmarg%s_kernel (chunked row scan)" % (("c", "c") if cx else ("", "")),
+                    "kernel_ms": kms, "effective_gflops": M * fl / (ms * 1e-3) / 1e9,
+                    "frac": M * fl / (kms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                    "note": "throughput ratio against the paper's flop count (the tile-Gram path executes fewer flops)",
+                    "clocks": clocks, "gpu_launches": nl}
+        if not no_cpu:
+            from oracle import ref
+            n = 64
+            t0 = time.perf_counter()
+            ref.sample(U, uni[:n], Np=Np)
+            t = time.perf_counter() - t0
+            out[key]["cpu_baseline"] = {"value": n / t, "unit": "samples/s", "cores": min(n, ref.num_threads()),
+                                        "kind": "oracle", "sample": f"first {n} of {M} samples ({t:.1f} s)"}
+        del Ud, ud, ws
     # the paper's comparator on the same GPU: modified HKPV (2 L N^2) vs FFS (L N^2 + N^3),
     # PAPER.md:81 "nearly the twice" / Fig. 3B (L = 1024 random U, N sweep); same uniforms layout
     hk = {}
