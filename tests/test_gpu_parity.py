@@ -206,16 +206,21 @@ def test_edge_cases():
             assert all(sorted(p) == list(range(l)) for p in gpos.tolist())
 
 
-def test_host_path_matches_device_path():
+@pytest.mark.parametrize("shape", ["dw", (40000, 24, 8, False), (20000, 16, 8, True)])
+def test_host_path_matches_device_path(shape):
     ffs = _ffs()
-    cfg = inputs.CONFIGS["dw"]
-    U = inputs.build_u(cfg)
+    if shape == "dw":
+        cfg = inputs.CONFIGS["dw"]
+        U, Np = inputs.build_u(cfg), cfg.N
+    else:  # beyond the panel kernels' L: the tile-Gram path through the host call
+        L, N, Np, cx = shape
+        U = inputs.random_orthonormal(L, N, L + N, complex_=cx)
     M = 20000  # > one host chunk
-    uni = inputs.uniforms(M, cfg.N, 77)
-    dev, _, _ = run_gpu(U, uni, cfg.N)
+    uni = inputs.uniforms(M, Np, 77)
+    dev, _, _ = run_gpu(U, uni, Np)
     hU = torch.from_numpy(U).pin_memory()
     hu = torch.from_numpy(uni).pin_memory()
-    hp = ffs.ffs_sample_host(hU, hu, cfg.N)
+    hp = ffs.ffs_sample_host(hU, hu, Np)
     assert (hp.numpy() == dev).all()
 
 
