@@ -363,21 +363,30 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX <= 4 && !BLK) ? 6 : 
         const int xb = (tau * G + lane) * Rl;
         auto chunk = [&](int c0, double (&s)[RLMAX]) {  // rows xb + c0 .. xb + c0 + RLMAX - 1 (those < xb + Rl)
           const int nr = Rl - c0;
-          {
-            const double* col = p.Ut + (size_t)mr * Lpt + xb + c0;
+          // a full chunk of an even number of rows per lane: 16-byte loads (xb + c0 is even)
+          const bool vec = RLMAX % 2 == 0 && nr >= RLMAX && (Rl & 1) == 0;
+          auto ldcol = [&](const double* col, double (&dst)[RLMAX]) {
+            if constexpr (RLMAX % 2 == 0) {
+              if (vec) {
 #pragma unroll
-            for (int j = 0; j < RLMAX; ++j) s[j] = j < nr ? col[j] : 0.0;
-          }
+                for (int j = 0; j < RLMAX / 2; ++j) {
+                  const double2 v = reinterpret_cast<const double2*>(col)[j];
+                  dst[2 * j] = v.x;
+                  dst[2 * j + 1] = v.y;
+                }
+                return;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < RLMAX; ++j) dst[j] = j < nr ? col[j] : 0.0;
+          };
+          ldcol(p.Ut + (size_t)mr * Lpt + xb + c0, s);
           constexpr int QB = RLMAX == 1 ? 8 : RLMAX <= 4 ? 4 : 2;  // columns in flight
           int q = 0;
           for (; q + QB <= r; q += QB) {
             double cv[QB][RLMAX];
 #pragma unroll
-            for (int b = 0; b < QB; ++b) {
-              const double* col = p.Ut + (size_t)m[q + b] * Lpt + xb + c0;
-#pragma unroll
-              for (int j = 0; j < RLMAX; ++j) cv[b][j] = j < nr ? col[j] : 0.0;
-            }
+            for (int b = 0; b < QB; ++b) ldcol(p.Ut + (size_t)m[q + b] * Lpt + xb + c0, cv[b]);
 #pragma unroll
             for (int b = 0; b < QB; ++b) {
               const double dq = dvec[q + b];
