@@ -366,6 +366,16 @@ static __global__ void __launch_bounds__(32 * WARPS, (RLMAX <= 4 && !BLK) ? 6 : 
           // a full chunk of an even number of rows per lane: 16-byte loads (xb + c0 is even)
           const bool vec = RLMAX % 2 == 0 && nr >= RLMAX && (Rl & 1) == 0;
           auto ldcol = [&](const double* col, double (&dst)[RLMAX]) {
+            if constexpr (RLMAX % 4 == 0) {
+              if (vec && (Rl & 3) == 0) {  // 32-byte loads
+#pragma unroll
+                for (int j = 0; j < RLMAX / 4; ++j)
+                  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                      : "=d"(dst[4 * j]), "=d"(dst[4 * j + 1]), "=d"(dst[4 * j + 2]), "=d"(dst[4 * j + 3])
+                      : "l"(col + 4 * j));
+                return;
+              }
+            }
             if constexpr (RLMAX % 2 == 0) {
               if (vec) {
 #pragma unroll
