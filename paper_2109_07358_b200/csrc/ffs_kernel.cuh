@@ -130,7 +130,13 @@ __device__ __forceinline__ void load_col(const Params& p, const T* __restrict__ 
     }
   } else {
     const T* base = reinterpret_cast<const T*>(p.Ut) + (size_t)col * p.Lp + t * R;
-    if constexpr (sizeof(T) == 8 && (R % 2) == 0) {
+    if constexpr (sizeof(T) == 8 && (R % 4) == 0) {  // 32-byte loads (Lp is a multiple of R)
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q)
+        asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+            : "=d"(v[4 * q]), "=d"(v[4 * q + 1]), "=d"(v[4 * q + 2]), "=d"(v[4 * q + 3])
+            : "l"(base + 4 * q));
+    } else if constexpr (sizeof(T) == 8 && (R % 2) == 0) {
 #pragma unroll
       for (int q = 0; q < R / 2; ++q) {
         const double2 d = __ldg(reinterpret_cast<const double2*>(base) + q);
