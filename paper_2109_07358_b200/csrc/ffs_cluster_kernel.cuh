@@ -102,6 +102,24 @@ __device__ __forceinline__ void st_remote_s32(void* local_ptr, unsigned rank, in
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
+// R consecutive rows of one U^T column (row0 and Lpt are multiples of R): 32-byte loads where they fit
+template <typename T, int R>
+__device__ __forceinline__ void ldrows(const T* __restrict__ base, T (&v)[R]) {
+  constexpr int kD = sizeof(T) / 8 * R;  // doubles
+  if constexpr (kD % 4 == 0 && (sizeof(T) == 8 ? R % 4 == 0 : R % 2 == 0)) {
+    double* d = reinterpret_cast<double*>(&v[0]);
+    const double* b = reinterpret_cast<const double*>(base);
+#pragma unroll
+    for (int q = 0; q < kD / 4; ++q)
+      asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+          : "=d"(d[4 * q]), "=d"(d[4 * q + 1]), "=d"(d[4 * q + 2]), "=d"(d[4 * q + 3])
+          : "l"(b + 4 * q));
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = base[r];
+  }
+}
+
 template <typename T, int R, int B, int MAXT, bool STEP = false>
 __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -217,8 +235,10 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
 #pragma unroll
       for (int c = 0; c < B; ++c) {
         const T* base = Utg + (size_t)perm[min(k0 + c, Np - 1)] * p.Lpt + row0;
+        T v[R];
+        ldrows(base, v);
 #pragma unroll
-        for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? base[r] : S::zero();
+        for (int r = 0; r < R; ++r) P[r][c] = (c < nb) ? v[r] : S::zero();
       }
       }
       // contraction over the k0 earlier columns; W rows are staged kKC at a time in shared memory
@@ -234,8 +254,7 @@ __global__ void __launch_bounds__(MAXT, 1) ffs_cluster_kernel(const ClusterParam
         for (int i2 = 0; i2 < kc; ++i2) {
           const T* base = Utg + (size_t)perm[c0 + i2] * p.Lpt + row0;
           T v[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) v[r] = base[r];
+          ldrows(base, v);
           T wb[B];
 #pragma unroll
           for (int c = 0; c < B; ++c) wb[c] = Wb[i2 * B + c];
