@@ -822,8 +822,9 @@ int make_dense_plan_uncached(int64_t L, int64_t N, int64_t Np, int dtype, int64_
   else if (d.gemm == 7) theta = cx ? 0.35 : 0.15;
   else theta = cx ? 0.3 : 0.15;  // 8 slices, 2-SM GEMM (tools/theta_scan.py: C5 0.1-0.25, C4 0.25-0.4)
   // with the Gram draws a GEMM block costs less than a cluster-step block sooner (C5 0.1: 691.9 ms,
-  // 0.15: 693.5, 0: 712.9; C4 0.2: 701.5, 0.3: 702.9, 0: 753.3)
-  if (d.gemm == 8 && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0) theta = cx ? 0.2 : 0.1;
+  // 0.15: 693.5, 0: 712.9; C4 0.2: 701.5, 0.3: 702.9, 0: 753.3; with the 32-byte U^T loads of the
+  // gathered blocks C4 0.2: 663.9-666.9, 0.25: 662.1, 0.3: 660.2, 0.35: 666.3)
+  if (d.gemm == 8 && ffsh::option(FFS_OPT_GRAM_DRAW) != 0.0) theta = cx ? 0.25 : 0.1;
   const double ot = ffsh::option(FFS_OPT_DENSE_THETA);
   if (ot >= 0.0) theta = ot;
   if (L < 2048) theta = 0.0;

@@ -212,17 +212,29 @@ static __global__ void __launch_bounds__(32 * WARPS) ffs_kmargc_kernel(const KMa
         const int xb = (tau * G + lane) * Rl;
         auto chunk = [&](int c0, cplx (&s)[RLMAX]) {  // s(x) of rows xb + c0 .. (those < xb + Rl)
           const int nr = Rl - c0;
-          {
-            const cplx* col = Ut + (size_t)mr * Lpt + xb + c0;
+          // a full chunk of an even number of rows per lane: 32-byte loads (xb + c0 is even)
+          const bool vec = RLMAX % 2 == 0 && nr >= RLMAX && (Rl & 1) == 0;
+          auto ldcol = [&](const cplx* col, cplx (&dst)[RLMAX]) {
+            if constexpr (RLMAX % 2 == 0) {
+              if (vec) {
 #pragma unroll
-            for (int j = 0; j < RLMAX; ++j) s[j] = j < nr ? col[j] : S::zero();
-          }
+                for (int j = 0; j < RLMAX / 2; ++j)
+                  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                      : "=d"(dst[2 * j].re), "=d"(dst[2 * j].im), "=d"(dst[2 * j + 1].re), "=d"(dst[2 * j + 1].im)
+                      : "l"(col + 2 * j));
+                return;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < RLMAX; ++j) dst[j] = j < nr ? col[j] : S::zero();
+          };
+          ldcol(Ut + (size_t)mr * Lpt + xb + c0, s);
           for (int q = 0; q < r; ++q) {
             const cplx dq = S::neg(dvec[q]);
-            const cplx* col = Ut + (size_t)m[q] * Lpt + xb + c0;
+            cplx cv[RLMAX];
+            ldcol(Ut + (size_t)m[q] * Lpt + xb + c0, cv);
 #pragma unroll
-            for (int j = 0; j < RLMAX; ++j)
-              if (j < nr) s[j] = S::fms(col[j], dq, s[j]);
+            for (int j = 0; j < RLMAX; ++j) s[j] = S::fms(cv[j], dq, s[j]);
           }
         };
         constexpr int kNoRow = 0x7fffffff;
